@@ -1,0 +1,266 @@
+// K2 (split-K decode attention over the compressed paged cache) and K3 (LSE combine).
+//
+// Reference: pkg/src/tadakv/attention.py attend_streaming (103-151): per KV head,
+// tiles over compressed then residual tokens (94-100); logits = (K̂ @ q) * F32(1/sqrt(D));
+// running max / normalizer / weighted sum; out = acc / norm.  K̂ = mean - deq(dev)
+// (cache.py:193-200) with deq = fmaf(code, scale, min), bit-identical to the
+// reference's f32(f64 min + code * f64 scale) (SURVEY §8a "Dequant").
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "tada_common.cuh"
+
+namespace tada {
+
+struct AttnArgs {
+  tada_page_layout L;
+  const uint8_t* pool;
+  const void* q;
+  int Hq;
+  const int32_t* page_table;
+  int pt_stride;
+  const int32_t* comp_len;
+  const int32_t* res_len;
+  const float* res_k;
+  const float* res_v;
+  int64_t res_seq_stride;
+  float scale;
+  int splits;
+  float* part_acc;  // [B][Hq][S][D]
+  float* part_ml;   // [B][Hq][S][2]
+  void* out;
+  int out_dtype;
+};
+
+__device__ __forceinline__ void store_any(void* out, int dtype, int64_t i, float v) {
+  if (dtype == TADA_F32) reinterpret_cast<float*>(out)[i] = v;
+  else reinterpret_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(v);
+}
+
+// Token range [t_begin, t_end) of split `s` for a sequence of n tokens; chunks are
+// multiples of `align` so split boundaries fall on tile boundaries.
+__device__ __forceinline__ void split_range(int n, int splits, int s, int align, int& t0, int& t1) {
+  int chunk = (n + splits - 1) / splits;
+  chunk = (chunk + align - 1) / align * align;
+  t0 = min(n, s * chunk);
+  t1 = min(n, t0 + chunk);
+}
+
+template <int BITS>
+__device__ __forceinline__ float khat_elem(const float* mean, const uint8_t* grp, float s, float mn, int d) {
+  if (BITS == 16) return __fsub_rn(mean[d], reinterpret_cast<const float*>(grp)[d]);
+  return __fsub_rn(mean[d], __fmaf_rn(float(get_code(grp, d, BITS)), s, mn));
+}
+
+// ------------------------------------------------------------------ generic exact kernel
+// Any (H, Hq, D, bits).  CTA = (split, sequence); f32 reconstruct-then-dot.
+constexpr int kGenTile = 32;
+
+template <typename QT, int BITS>
+__global__ void __launch_bounds__(256) attn_generic_kernel(AttnArgs a) {
+  extern __shared__ __align__(16) float sm[];
+  const int H = a.L.heads, D = a.L.head_dim, Hq = a.Hq, G = Hq / H, P = a.L.page_tokens, gb = a.L.group_bytes;
+  const int b = blockIdx.y, split = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
+  float* qs = sm;                 // [Hq][D]
+  float* acc = qs + Hq * D;       // [Hq][D]
+  float* lg = acc + Hq * D;       // [Hq][kGenTile]
+  float* mrow = lg + Hq * kGenTile;
+  float* lrow = mrow + Hq;
+  float* crow = lrow + Hq;
+  const int C = a.comp_len[b], n = C + a.res_len[b];
+  int t_begin, t_end;
+  split_range(n, a.splits, split, kGenTile, t_begin, t_end);
+  const QT* q = reinterpret_cast<const QT*>(a.q) + int64_t(b) * Hq * D;
+  for (int i = tid; i < Hq * D; i += bd) {
+    qs[i] = to_f32(q[i]);
+    acc[i] = 0.f;
+  }
+  for (int g = tid; g < Hq; g += bd) {
+    mrow[g] = -__int_as_float(0x7f800000);
+    lrow[g] = 0.f;
+  }
+  __syncthreads();
+  const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
+  const int64_t res_base = int64_t(b) * a.res_seq_stride;
+
+  for (int t0 = t_begin; t0 < t_end; t0 += kGenTile) {
+    const int nt = min(kGenTile, t_end - t0);
+    for (int pair = tid; pair < Hq * nt; pair += bd) {
+      const int g = pair / nt, j = pair - g * nt, t = t0 + j, h = g / G;
+      const float* qg = qs + g * D;
+      float dot = 0.f;
+      if (t < C) {
+        const uint8_t* page = a.pool + int64_t(pt[t / P]) * a.L.page_bytes;
+        const int r = t % P;
+        const float* mean = reinterpret_cast<const float*>(page + a.L.off_mean[0]) + r * D;
+        const uint8_t* grp = page + a.L.off_codes[0] + (int64_t(r) * H + h) * gb;
+        const float2 sm2 = reinterpret_cast<const float2*>(page + a.L.off_meta[0])[r * H + h];
+        for (int d = 0; d < D; ++d) dot = __fmaf_rn(qg[d], khat_elem<BITS>(mean, grp, sm2.x, sm2.y, d), dot);
+      } else {
+        const float* kr = a.res_k + ((res_base + (t - C)) * H + h) * D;
+        for (int d = 0; d < D; ++d) dot = __fmaf_rn(qg[d], kr[d], dot);
+      }
+      lg[g * kGenTile + j] = __fmul_rn(dot, a.scale);
+    }
+    __syncthreads();
+    for (int g = tid; g < Hq; g += bd) {
+      float tmax = lg[g * kGenTile];
+      for (int j = 1; j < nt; ++j) tmax = fmaxf(tmax, lg[g * kGenTile + j]);
+      const float m_new = fmaxf(mrow[g], tmax);
+      const float corr = expf(mrow[g] - m_new);
+      float sum = 0.f;
+      for (int j = 0; j < nt; ++j) {
+        const float p = expf(lg[g * kGenTile + j] - m_new);
+        lg[g * kGenTile + j] = p;
+        sum += p;
+      }
+      lrow[g] = lrow[g] * corr + sum;
+      mrow[g] = m_new;
+      crow[g] = corr;
+    }
+    __syncthreads();
+    for (int pair = tid; pair < Hq * D; pair += bd) {
+      const int g = pair / D, d = pair - g * D, h = g / G;
+      float av = acc[pair] * crow[g];
+      for (int j = 0; j < nt; ++j) {
+        const int t = t0 + j;
+        float v;
+        if (t < C) {
+          const uint8_t* page = a.pool + int64_t(pt[t / P]) * a.L.page_bytes;
+          const int r = t % P;
+          const float* mean = reinterpret_cast<const float*>(page + a.L.off_mean[1]) + r * D;
+          const uint8_t* grp = page + a.L.off_codes[1] + (int64_t(r) * H + h) * gb;
+          const float2 sm2 = reinterpret_cast<const float2*>(page + a.L.off_meta[1])[r * H + h];
+          v = khat_elem<BITS>(mean, grp, sm2.x, sm2.y, d);
+        } else {
+          v = a.res_v[((res_base + (t - C)) * H + h) * D + d];
+        }
+        av = __fmaf_rn(lg[g * kGenTile + j], v, av);
+      }
+      acc[pair] = av;
+    }
+    __syncthreads();
+  }
+  if (a.splits == 1) {
+    for (int pair = tid; pair < Hq * D; pair += bd) {
+      const int g = pair / D;
+      store_any(a.out, a.out_dtype, int64_t(b) * Hq * D + pair, acc[pair] / lrow[g]);
+    }
+  } else {
+    for (int pair = tid; pair < Hq * D; pair += bd) {
+      const int g = pair / D, d = pair - g * D;
+      a.part_acc[((int64_t(b) * Hq + g) * a.splits + split) * D + d] = acc[pair];
+    }
+    for (int g = tid; g < Hq; g += bd) {
+      float* ml = a.part_ml + ((int64_t(b) * Hq + g) * a.splits + split) * 2;
+      ml[0] = mrow[g];
+      ml[1] = lrow[g];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K3: split combine
+// out = sum_s acc_s * e^{m_s - M} / sum_s l_s * e^{m_s - M}   (log-sum-exp merge)
+__global__ void combine_kernel(const float* __restrict__ part_acc, const float* __restrict__ part_ml, int S, int D,
+                               void* out, int out_dtype) {
+  const int64_t bg = blockIdx.x;  // b * Hq + g
+  const float* ml = part_ml + bg * S * 2;
+  float M = -__int_as_float(0x7f800000);
+  for (int s = 0; s < S; ++s) M = fmaxf(M, ml[2 * s]);
+  float L = 0.f;
+  for (int s = 0; s < S; ++s)
+    if (ml[2 * s + 1] > 0.f) L += ml[2 * s + 1] * expf(ml[2 * s] - M);
+  const float inv = 1.f / L;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    float o = 0.f;
+    for (int s = 0; s < S; ++s)
+      if (ml[2 * s + 1] > 0.f) o += part_acc[(bg * S + s) * D + d] * expf(ml[2 * s] - M);
+    store_any(out, out_dtype, bg * D + d, o * inv);
+  }
+}
+
+template <typename QT>
+static int launch_generic(const AttnArgs& a, int batch, cudaStream_t st) {
+  const int Hq = a.Hq, D = a.L.head_dim;
+  const size_t smem = (size_t(2) * Hq * D + size_t(Hq) * kGenTile + 3 * Hq) * 4;
+  void (*kern)(AttnArgs) = nullptr;
+  switch (a.L.bits) {
+    case 2: kern = attn_generic_kernel<QT, 2>; break;
+    case 4: kern = attn_generic_kernel<QT, 4>; break;
+    case 8: kern = attn_generic_kernel<QT, 8>; break;
+    default: kern = attn_generic_kernel<QT, 16>; break;
+  }
+  if (smem > 48 * 1024) {
+    if (smem > 220 * 1024) return fail(TADA_ERR_CONFIG, "num_q_heads*head_dim too large for decode attention");
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string("attn smem: ") + cudaGetErrorString(e));
+  }
+  kern<<<dim3(a.splits, batch), 256, smem, st>>>(a);
+  return check_launch("decode_attn_generic");
+}
+
+}  // namespace tada
+
+using namespace tada;
+
+extern "C" {
+
+int64_t tada_decode_attn_workspace_bytes(int32_t batch, int32_t num_q_heads, int32_t head_dim, int32_t num_splits) {
+  if (num_splits <= 1) return 0;
+  return int64_t(batch) * num_q_heads * num_splits * (int64_t(head_dim) + 2) * 4;
+}
+
+int32_t tada_decode_attn_suggest_splits(int32_t batch, int64_t max_tokens, int32_t page_tokens) {
+  if (batch <= 0 || max_tokens <= 0) return 1;
+  const int64_t target_ctas = 148 * 4;
+  int64_t s = (target_ctas + batch - 1) / batch;
+  const int64_t max_s = (max_tokens + 255) / 256;  // keep >= ~256 tokens per split
+  if (s > max_s) s = max_s;
+  if (s < 1) s = 1;
+  (void)page_tokens;
+  return int32_t(s);
+}
+
+int tada_decode_attn(const tada_page_layout* layout, const uint8_t* pool, const void* q, int32_t q_dtype, int32_t batch,
+                     int32_t num_q_heads, const int32_t* page_table, int32_t pt_stride, const int32_t* comp_len,
+                     const int32_t* res_len, const float* res_k, const float* res_v, int64_t res_seq_stride,
+                     float scale, int32_t num_splits, void* workspace, void* out, int32_t out_dtype, int32_t mode,
+                     void* stream) {
+  if (!layout) return fail(TADA_ERR_CONFIG, "null layout");
+  if (q_dtype != TADA_F32 && q_dtype != TADA_BF16) return fail(TADA_ERR_CONFIG, "q dtype must be f32 or bf16");
+  if (out_dtype != TADA_F32 && out_dtype != TADA_BF16) return fail(TADA_ERR_CONFIG, "out dtype must be f32 or bf16");
+  if (batch < 0 || num_q_heads <= 0 || num_q_heads % layout->heads != 0)
+    return fail(TADA_ERR_CONFIG, "num_q_heads must be a positive multiple of num_kv_heads");
+  if (num_splits < 1 || num_splits > 4096) return fail(TADA_ERR_CONFIG, "num_splits out of range");
+  if (batch == 0) return TADA_OK;
+  if (!q || !out || !comp_len || !res_len) return fail(TADA_ERR_SHAPE, "null buffer");
+  if (num_splits > 1 && !workspace) return fail(TADA_ERR_SHAPE, "workspace required for num_splits > 1");
+  AttnArgs a{};
+  a.L = *layout;
+  a.pool = pool;
+  a.q = q;
+  a.Hq = num_q_heads;
+  a.page_table = page_table;
+  a.pt_stride = pt_stride;
+  a.comp_len = comp_len;
+  a.res_len = res_len;
+  a.res_k = res_k;
+  a.res_v = res_v;
+  a.res_seq_stride = res_seq_stride;
+  a.scale = scale;
+  a.splits = num_splits;
+  a.part_acc = reinterpret_cast<float*>(workspace);
+  a.part_ml = a.part_acc + int64_t(batch) * num_q_heads * num_splits * layout->head_dim;
+  a.out = out;
+  a.out_dtype = out_dtype;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  (void)mode;
+  int rc = q_dtype == TADA_F32 ? launch_generic<float>(a, batch, st) : launch_generic<__nv_bfloat16>(a, batch, st);
+  if (rc != TADA_OK || num_splits == 1) return rc;
+  combine_kernel<<<unsigned(int64_t(batch) * num_q_heads), 128, 0, st>>>(a.part_acc, a.part_ml, num_splits,
+                                                                          layout->head_dim, out, out_dtype);
+  return check_launch("decode_attn_combine");
+}
+
+}  // extern "C"

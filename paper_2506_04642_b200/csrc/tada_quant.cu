@@ -1,0 +1,614 @@
+// Quantizer, packer, mean-centering and K1 (fused quantize-on-append) for sm_100a.
+//
+// Reference: pkg/src/tadakv/quant.py (quantize_tensor 200-229, _quantize_rows 143-174,
+// pack_codes 93-111, unpack_codes 114-140, _dequantize_rows 177-180) and
+// pkg/src/tadakv/cache.py (mean_center 98-111, append_tokens 154-180,
+// _compress_block 182-188).  Codes, scales, mins and means are bit-exact.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <mutex>
+#include <string>
+
+#include "tada_common.cuh"
+
+namespace tada {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return TADA_OK;
+}
+
+static bool valid_bits(int b) { return b == 2 || b == 4 || b == 8 || b == 16; }
+static bool valid_dtype(int t) { return t == TADA_F32 || t == TADA_BF16; }
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+static inline int grid_for(int64_t work, int per_block) {
+  int64_t g = (work + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > 148 * 64) g = 148 * 64;
+  return int(g);
+}
+
+// ------------------------------------------------------------------ warp group quantizer
+//
+// One warp quantizes one group of D elements.  Lane l owns elements
+// c*128 + 4l .. +3 of chunk c (NCH chunks cover D <= 128*NCH), so each lane packs
+// 4 codes = 4*bits bits = whole bytes for every width, exactly like pack_codes'
+// zero-padded byte layout (quant.py:101-111).
+template <int NCH, typename Load>
+__device__ __forceinline__ void quantize_group_warp(Load load, int D, int bits, uint8_t* __restrict__ out,
+                                                    float* scale_out, float* min_out, int32_t* err, int lane,
+                                                    bool vec_ok) {
+  float v[NCH][4];
+  float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000);
+  bool bad = false;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int e0 = c * 128 + lane * 4;
+    if (vec_ok && e0 + 3 < D) {
+      load.vec4(e0, v[c]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[c][k] = (e0 + k < D) ? load(e0 + k) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (e0 + k < D) {
+        bad |= !finite(v[c][k]);
+        mn = fminf(mn, v[c][k]);
+        mx = fmaxf(mx, v[c][k]);
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad)) {
+    if (lane == 0 && err) atomicOr(err, 1);  // host raises DataError (quant.py:151-152)
+  }
+  if (bits == 16) {  // raw f32 pass-through (quant.py:208-219)
+    float* o = reinterpret_cast<float*>(out);
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      const int e0 = c * 128 + lane * 4;
+      if (vec_ok && e0 + 3 < D) {
+        *reinterpret_cast<float4*>(o + e0) = make_float4(v[c][0], v[c][1], v[c][2], v[c][3]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (e0 + k < D) o[e0 + k] = v[c][k];
+      }
+    }
+    if (lane == 0) {
+      *scale_out = 0.f;
+      *min_out = 0.f;
+    }
+    return;
+  }
+  mn = warp_min(mn);
+  mx = warp_max(mx);
+  const float s = group_scale(mn, mx, bits);
+  const int cmax = (1 << bits) - 1;
+  const bool fast = s >= 0x1p-100f && s <= 0x1p100f;
+  const float inv_s = fast ? __frcp_rn(s) : 0.f;
+  const int gb = int(group_bytes(D, bits));
+  const int nbytes = bits / 2;  // bytes produced by 4 codes
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int e0 = c * 128 + lane * 4;
+    if (e0 >= D) continue;
+    uint32_t word = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t code = 0;
+      if (e0 + k < D && s != 0.f) code = quant_code(v[c][k], mn, s, inv_s, fast, cmax);
+      word |= code << (bits * k);
+    }
+    const int off = (e0 * bits) >> 3;
+    if (vec_ok && off + nbytes <= gb) {
+      if (bits == 2) out[off] = uint8_t(word);
+      else if (bits == 4) *reinterpret_cast<uint16_t*>(out + off) = uint16_t(word);
+      else *reinterpret_cast<uint32_t*>(out + off) = word;
+    } else {
+      for (int j = 0; j < nbytes; ++j)
+        if (off + j < gb) out[off + j] = uint8_t(word >> (8 * j));
+    }
+  }
+  if (lane == 0) {
+    *scale_out = s;
+    *min_out = mn;
+  }
+}
+
+template <typename T>
+struct GlobalRow {
+  const T* p;
+  __device__ float operator()(int e) const { return to_f32(p[e]); }
+  __device__ void vec4(int e, float (&v)[4]) const { load4(p + e, v); }
+};
+
+// dev = mean - x, read from shared memory (cache.py:110)
+struct CenteredRow {
+  const float* mean;
+  const float* x;
+  __device__ float operator()(int e) const { return __fsub_rn(mean[e], x[e]); }
+  __device__ void vec4(int e, float (&v)[4]) const {
+    const float4 m = *reinterpret_cast<const float4*>(mean + e);
+    const float4 a = *reinterpret_cast<const float4*>(x + e);
+    v[0] = __fsub_rn(m.x, a.x);
+    v[1] = __fsub_rn(m.y, a.y);
+    v[2] = __fsub_rn(m.z, a.z);
+    v[3] = __fsub_rn(m.w, a.w);
+  }
+};
+
+// ------------------------------------------------------------------ quantize_tensor
+template <typename T, int NCH>
+__global__ void __launch_bounds__(256) quantize_groups_kernel(const T* __restrict__ rows, int64_t n_groups, int D,
+                                                              int bits, uint8_t* __restrict__ codes,
+                                                              float* __restrict__ scales, float* __restrict__ mins,
+                                                              int32_t* err, bool vec_ok) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  const int64_t gb = group_bytes(D, bits);
+  for (int64_t g = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); g < n_groups; g += warps) {
+    GlobalRow<T> ld{rows + g * D};
+    quantize_group_warp<NCH>(ld, D, bits, codes + g * gb, scales + g, mins + g, err, lane, vec_ok);
+  }
+}
+
+// ------------------------------------------------------------------ dequantize / (un)pack
+__global__ void dequant_kernel(const uint8_t* __restrict__ codes, const float* __restrict__ scales,
+                               const float* __restrict__ mins, int D, int bits, const int64_t* __restrict__ sel,
+                               int64_t n_out, float* __restrict__ out) {
+  const int64_t gb = group_bytes(D, bits);
+  const int64_t total = n_out * D;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = i / D;
+    const int e = int(i - j * D);
+    const int64_t g = sel ? sel[j] : j;
+    const uint8_t* grp = codes + g * gb;
+    if (bits == 16) {
+      out[i] = reinterpret_cast<const float*>(grp)[e];
+    } else {
+      out[i] = dequant_exact(get_code(grp, e, bits), scales[g], mins[g]);
+    }
+  }
+}
+
+__global__ void pack_kernel(const uint8_t* __restrict__ codes, int64_t n_groups, int D, int bits,
+                            uint8_t* __restrict__ packed) {
+  const int gb = int(group_bytes(D, bits));
+  const int per = 8 / bits;
+  const int64_t total = n_groups * gb;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t g = i / gb;
+    const int byte = int(i - g * gb);
+    uint32_t w = 0;
+    for (int k = 0; k < per; ++k) {
+      const int e = byte * per + k;
+      if (e < D) w |= (uint32_t(codes[g * D + e]) & ((1u << bits) - 1u)) << (bits * k);
+    }
+    packed[i] = uint8_t(w);
+  }
+}
+
+__global__ void unpack_kernel(const uint8_t* __restrict__ packed, int D, int bits, const int64_t* __restrict__ sel,
+                              int64_t n_out, uint8_t* __restrict__ codes) {
+  const int64_t gb = group_bytes(D, bits);
+  const int64_t total = n_out * D;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = i / D;
+    const int e = int(i - j * D);
+    const int64_t g = sel ? sel[j] : j;
+    codes[i] = uint8_t(get_code(packed + g * gb, e, bits));
+  }
+}
+
+// ------------------------------------------------------------------ mean_center
+// mean[t][d] = f32((((0 + x0) + x1) + ... ) / H) with an fp64 sequential head sum
+// (numpy reduces the non-contiguous head axis in order).
+__device__ __forceinline__ float head_mean(const float* col, int stride, int H) {
+  double acc = 0.0;
+  for (int h = 0; h < H; ++h) acc = __dadd_rn(acc, double(col[h * stride]));
+  return __double2float_rn(__ddiv_rn(acc, double(H)));
+}
+
+template <typename T>
+__global__ void mean_center_kernel(const T* __restrict__ x, int64_t tokens, int H, int D, float* __restrict__ mean,
+                                   float* __restrict__ dev, int32_t* err) {
+  const int64_t total = tokens * D;
+  bool bad = false;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = i / D;
+    const int d = int(i - t * D);
+    const T* col = x + t * H * D + d;
+    double acc = 0.0;
+    for (int h = 0; h < H; ++h) {
+      const float xv = to_f32(col[h * D]);
+      bad |= !finite(xv);
+      acc = __dadd_rn(acc, double(xv));
+    }
+    const float m = __double2float_rn(__ddiv_rn(acc, double(H)));
+    mean[i] = m;
+    for (int h = 0; h < H; ++h) dev[(t * H + h) * D + d] = __fsub_rn(m, to_f32(col[h * D]));
+  }
+  if (bad && err) atomicOr(err, 1);
+}
+
+// ------------------------------------------------------------------ K1: quantize-on-append
+//
+// CTA = a tile of TT consecutive tokens of one sequence, both sides (blockIdx.y).
+//  A: tile [TT][H][D] -> smem (f32), 16B vector loads.
+//  B: per (t, d) fp64 head-sum mean -> smem + paged mean block.
+//  C: warp per (t, h) group: dev = mean - x, warp-shuffle min/max, fp64 scale +
+//     fixed-point refinement, half-up codes, LSB-first pack -> paged codes/meta.
+struct AppendArgs {
+  tada_page_layout L;
+  uint8_t* pool;
+  const void* src[2];
+  int64_t n_tok;
+  int64_t src_seq_stride;
+  const int32_t* page_table;
+  int pt_stride;
+  const int32_t* dst_start;
+  int64_t dst_offset;
+  int32_t* err;
+  int tt;  // tokens per tile
+  int tiles_per_seq;
+  bool vec_ok;
+};
+
+template <typename T, int NCH>
+__global__ void __launch_bounds__(256) quant_append_kernel(AppendArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  const int H = a.L.heads, D = a.L.head_dim, bits = a.L.bits, P = a.L.page_tokens;
+  const int side = blockIdx.y;
+  const int b = blockIdx.x / a.tiles_per_seq;
+  const int64_t i0 = int64_t(blockIdx.x % a.tiles_per_seq) * a.tt;
+  const int64_t rem = a.n_tok - i0;
+  const int nt = int(rem < a.tt ? rem : a.tt);
+  if (nt <= 0) return;
+  const int row = H * D;
+  float* xs = smem;                  // [tt][H*D]
+  float* ms = smem + a.tt * row;     // [tt][D]
+  const T* src = reinterpret_cast<const T*>(a.src[side]) + (int64_t(b) * a.src_seq_stride + i0) * row;
+
+  // A: load tile
+  const int n_el = nt * row;
+  bool bad = false;
+  if (a.vec_ok) {
+    for (int e = threadIdx.x * 4; e < n_el; e += blockDim.x * 4) {
+      float v[4];
+      load4(src + e, v);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) bad |= !finite(v[k]);
+      *reinterpret_cast<float4*>(xs + e) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+  } else {
+    for (int e = threadIdx.x; e < n_el; e += blockDim.x) {
+      xs[e] = to_f32(src[e]);
+      bad |= !finite(xs[e]);
+    }
+  }
+  if (bad && a.err) atomicOr(a.err, 1);
+  __syncthreads();
+
+  const int64_t c0 = a.dst_start[b] + a.dst_offset;
+  const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
+  // B: means
+  for (int e = threadIdx.x; e < nt * D; e += blockDim.x) {
+    const int t = e / D, d = e - t * D;
+    const float m = head_mean(xs + t * row + d, D, H);
+    ms[t * D + d] = m;
+    const int64_t c = c0 + i0 + t;
+    uint8_t* page = a.pool + int64_t(pt[c / P]) * a.L.page_bytes;
+    reinterpret_cast<float*>(page + a.L.off_mean[side])[(c % P) * D + d] = m;
+  }
+  __syncthreads();
+
+  // C: groups
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int gb = a.L.group_bytes;
+  for (int g = warp; g < nt * H; g += nw) {
+    const int t = g / H, h = g - t * H;
+    const int64_t c = c0 + i0 + t;
+    uint8_t* page = a.pool + int64_t(pt[c / P]) * a.L.page_bytes;
+    const int64_t grp = (c % P) * H + h;
+    float* meta = reinterpret_cast<float*>(page + a.L.off_meta[side]) + 2 * grp;
+    CenteredRow ld{ms + t * D, xs + t * row + h * D};
+    quantize_group_warp<NCH>(ld, D, bits, page + a.L.off_codes[side] + grp * gb, meta, meta + 1, a.err, lane,
+                             a.vec_ok);
+  }
+}
+
+// ------------------------------------------------------------------ residual write / lengths
+template <typename T>
+__global__ void residual_write_kernel(float* __restrict__ rk, float* __restrict__ rv, int64_t res_seq_stride, int row,
+                                      const T* __restrict__ sk, const T* __restrict__ sv, int64_t n_tok,
+                                      int64_t src_seq_stride, const int32_t* __restrict__ pos, int pos_offset,
+                                      int batch) {
+  const int64_t per_seq = n_tok * row;
+  const int64_t total = per_seq * batch * 2;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int side = int(i / (per_seq * batch));
+    const int64_t r = i - side * per_seq * batch;
+    const int b = int(r / per_seq);
+    const int64_t e = r - b * per_seq;
+    const T* s = side ? sv : sk;
+    float* d = side ? rv : rk;
+    const int64_t dst_tok = int64_t(b) * res_seq_stride + pos[b] + pos_offset;
+    d[dst_tok * row + e] = to_f32(s[int64_t(b) * src_seq_stride * row + e]);
+  }
+}
+
+__global__ void lengths_add_kernel(int32_t* arr, int batch, int32_t delta) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < batch) arr[i] += delta;
+}
+
+// ------------------------------------------------------------------ paged <-> dense (TADAKV1 export/import)
+template <bool kGather>
+__global__ void move_compressed_kernel(tada_page_layout L, uint8_t* pool, const int32_t* __restrict__ page_row,
+                                       int64_t n_tok, int side, float* mean, uint8_t* codes, float* scales,
+                                       float* mins) {
+  const int H = L.heads, D = L.head_dim, P = L.page_tokens, gb = L.group_bytes;
+  const int64_t per_tok = int64_t(D) + int64_t(H) * gb + 2 * H;  // work items per token
+  const int64_t total = n_tok * per_tok;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = i / per_tok;
+    int64_t k = i - t * per_tok;
+    uint8_t* page = pool + int64_t(page_row[t / P]) * L.page_bytes;
+    const int64_t r = t % P;
+    if (k < D) {
+      float* pm = reinterpret_cast<float*>(page + L.off_mean[side]) + r * D + k;
+      if (kGather) mean[t * D + k] = *pm; else *pm = mean[t * D + k];
+      continue;
+    }
+    k -= D;
+    if (k < int64_t(H) * gb) {
+      uint8_t* pc = page + L.off_codes[side] + r * H * gb + k;
+      if (kGather) codes[t * H * gb + k] = *pc; else *pc = codes[t * H * gb + k];
+      continue;
+    }
+    k -= int64_t(H) * gb;
+    const int h = int(k >> 1);
+    float* pmeta = reinterpret_cast<float*>(page + L.off_meta[side]) + 2 * (r * H + h) + (k & 1);
+    float* dense = (k & 1) ? mins : scales;
+    if (kGather) dense[t * H + h] = *pmeta; else *pmeta = dense[t * H + h];
+  }
+}
+
+// ------------------------------------------------------------------ host dispatch helpers
+template <typename T>
+static int launch_quantize(const void* rows, int64_t n, int D, int bits, uint8_t* codes, float* scales, float* mins,
+                           int32_t* err, cudaStream_t st) {
+  const int wpb = 8;
+  const int grid = grid_for(n, wpb);
+  const bool vec = (D % 4 == 0) && (reinterpret_cast<uintptr_t>(rows) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(codes) % 4 == 0);
+  const T* r = reinterpret_cast<const T*>(rows);
+  if (D <= 128)
+    quantize_groups_kernel<T, 1><<<grid, 256, 0, st>>>(r, n, D, bits, codes, scales, mins, err, vec);
+  else if (D <= 256)
+    quantize_groups_kernel<T, 2><<<grid, 256, 0, st>>>(r, n, D, bits, codes, scales, mins, err, vec);
+  else if (D <= 512)
+    quantize_groups_kernel<T, 4><<<grid, 256, 0, st>>>(r, n, D, bits, codes, scales, mins, err, vec);
+  else
+    quantize_groups_kernel<T, 8><<<grid, 256, 0, st>>>(r, n, D, bits, codes, scales, mins, err, vec);
+  return check_launch("quantize_groups");
+}
+
+template <typename T, int NCH>
+static int launch_append_n(const AppendArgs& a, int batch, size_t smem, cudaStream_t st) {
+  auto kern = quant_append_kernel<T, NCH>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string("quant_append smem: ") + cudaGetErrorString(e));
+  }
+  dim3 grid(unsigned(int64_t(batch) * a.tiles_per_seq), 2);
+  kern<<<grid, 256, smem, st>>>(a);
+  return check_launch("quant_append");
+}
+
+template <typename T>
+static int launch_append(const AppendArgs& a, int batch, size_t smem, cudaStream_t st) {
+  const int D = a.L.head_dim;
+  if (D <= 128) return launch_append_n<T, 1>(a, batch, smem, st);
+  if (D <= 256) return launch_append_n<T, 2>(a, batch, smem, st);
+  if (D <= 512) return launch_append_n<T, 4>(a, batch, smem, st);
+  return launch_append_n<T, 8>(a, batch, smem, st);
+}
+
+}  // namespace tada
+
+using namespace tada;
+
+// ====================================================================== C ABI
+extern "C" {
+
+int tada_abi_version(void) { return TADA_ABI_VERSION; }
+const char* tada_last_error(void) { return g_err.c_str(); }
+
+int64_t tada_bytes_per_group(int32_t group_size, int32_t bits) {
+  if (!valid_bits(bits) || group_size < 0) return -1;
+  return group_bytes(group_size, bits);
+}
+
+int tada_page_layout_init(int32_t page_tokens, int32_t heads, int32_t head_dim, int32_t bits, tada_page_layout* out) {
+  if (!out) return fail(TADA_ERR_CONFIG, "null layout");
+  if (!valid_bits(bits)) return fail(TADA_ERR_CONFIG, "bit width must be one of (2, 4, 8, 16), got " + std::to_string(bits));
+  if (page_tokens <= 0 || heads <= 0 || head_dim <= 0)
+    return fail(TADA_ERR_CONFIG, "page_tokens, heads and head_dim must be positive");
+  if (head_dim > 1024) return fail(TADA_ERR_CONFIG, "head_dim > 1024 is not supported");
+  auto up = [](int64_t x, int64_t a) { return (x + a - 1) / a * a; };
+  tada_page_layout L{};
+  L.page_tokens = page_tokens;
+  L.heads = heads;
+  L.head_dim = head_dim;
+  L.bits = bits;
+  L.group_bytes = int32_t(group_bytes(head_dim, bits));
+  int64_t off = 0;
+  for (int side = 0; side < 2; ++side) {
+    L.off_mean[side] = off;
+    off = up(off + int64_t(page_tokens) * head_dim * 4, 128);
+    L.off_codes[side] = off;
+    off = up(off + int64_t(page_tokens) * heads * L.group_bytes, 128);
+    L.off_meta[side] = off;
+    off = up(off + int64_t(page_tokens) * heads * 8, 128);
+  }
+  L.page_bytes = up(off, 256);
+  *out = L;
+  return TADA_OK;
+}
+
+int tada_quantize_groups(const void* rows, int32_t dtype, int64_t n_groups, int32_t group_size, int32_t bits,
+                         uint8_t* codes, float* scales, float* mins, int32_t* err_flag, void* stream) {
+  if (!valid_bits(bits)) return fail(TADA_ERR_CONFIG, "bit width must be one of (2, 4, 8, 16)");
+  if (!valid_dtype(dtype)) return fail(TADA_ERR_CONFIG, "dtype must be f32 or bf16");
+  if (n_groups < 0 || group_size <= 0 || group_size > 1024) return fail(TADA_ERR_SHAPE, "bad group geometry");
+  if (n_groups == 0) return TADA_OK;
+  if (!rows || !codes || !scales || !mins) return fail(TADA_ERR_SHAPE, "null buffer");
+  return dtype == TADA_F32
+             ? launch_quantize<float>(rows, n_groups, group_size, bits, codes, scales, mins, err_flag, S(stream))
+             : launch_quantize<__nv_bfloat16>(rows, n_groups, group_size, bits, codes, scales, mins, err_flag, S(stream));
+}
+
+int tada_dequantize_groups(const uint8_t* codes, const float* scales, const float* mins, int64_t n_groups,
+                           int32_t group_size, int32_t bits, const int64_t* select, int64_t n_select, float* out,
+                           void* stream) {
+  if (!valid_bits(bits)) return fail(TADA_ERR_CONFIG, "bit width must be one of (2, 4, 8, 16)");
+  if (group_size <= 0 || n_groups < 0) return fail(TADA_ERR_SHAPE, "bad group geometry");
+  const int64_t n_out = select ? n_select : n_groups;
+  if (n_out <= 0) return TADA_OK;
+  dequant_kernel<<<grid_for(n_out * group_size, 256), 256, 0, S(stream)>>>(codes, scales, mins, group_size, bits,
+                                                                           select, n_out, out);
+  return check_launch("dequantize_groups");
+}
+
+int tada_pack_codes(const uint8_t* codes, int64_t n_groups, int32_t group_size, int32_t bits, uint8_t* packed,
+                    void* stream) {
+  if (bits != 2 && bits != 4 && bits != 8) return fail(TADA_ERR_CONFIG, "packing supports widths (2, 4, 8)");
+  if (group_size <= 0 || n_groups < 0) return fail(TADA_ERR_SHAPE, "bad group geometry");
+  if (n_groups == 0) return TADA_OK;
+  pack_kernel<<<grid_for(n_groups * group_bytes(group_size, bits), 256), 256, 0, S(stream)>>>(codes, n_groups,
+                                                                                               group_size, bits, packed);
+  return check_launch("pack_codes");
+}
+
+int tada_unpack_codes(const uint8_t* packed, int64_t n_groups, int32_t group_size, int32_t bits, const int64_t* select,
+                      int64_t n_select, uint8_t* codes, void* stream) {
+  if (bits != 2 && bits != 4 && bits != 8) return fail(TADA_ERR_CONFIG, "unpacking supports widths (2, 4, 8)");
+  if (group_size <= 0 || n_groups < 0) return fail(TADA_ERR_SHAPE, "bad group geometry");
+  const int64_t n_out = select ? n_select : n_groups;
+  if (n_out <= 0) return TADA_OK;
+  unpack_kernel<<<grid_for(n_out * group_size, 256), 256, 0, S(stream)>>>(packed, group_size, bits, select, n_out,
+                                                                          codes);
+  return check_launch("unpack_codes");
+}
+
+int tada_mean_center(const void* x, int32_t dtype, int64_t tokens, int32_t heads, int32_t head_dim, float* mean,
+                     float* dev, int32_t* err_flag, void* stream) {
+  if (!valid_dtype(dtype)) return fail(TADA_ERR_CONFIG, "dtype must be f32 or bf16");
+  if (tokens < 0 || heads <= 0 || head_dim <= 0) return fail(TADA_ERR_SHAPE, "bad (tokens, heads, head_dim)");
+  if (tokens == 0) return TADA_OK;
+  const int grid = grid_for(tokens * head_dim, 256);
+  if (dtype == TADA_F32)
+    mean_center_kernel<float><<<grid, 256, 0, S(stream)>>>(reinterpret_cast<const float*>(x), tokens, heads, head_dim,
+                                                             mean, dev, err_flag);
+  else
+    mean_center_kernel<__nv_bfloat16><<<grid, 256, 0, S(stream)>>>(reinterpret_cast<const __nv_bfloat16*>(x), tokens,
+                                                                     heads, head_dim, mean, dev, err_flag);
+  return check_launch("mean_center");
+}
+
+int tada_quant_append(const tada_page_layout* layout, uint8_t* pool, const void* src_k, const void* src_v,
+                      int32_t dtype, int32_t batch, int64_t n_tok, int64_t src_seq_stride, const int32_t* page_table,
+                      int32_t pt_stride, const int32_t* dst_start, int64_t dst_offset, int32_t* err_flag,
+                      void* stream) {
+  if (!layout) return fail(TADA_ERR_CONFIG, "null layout");
+  if (!valid_dtype(dtype)) return fail(TADA_ERR_CONFIG, "dtype must be f32 or bf16");
+  if (batch < 0 || n_tok < 0 || src_seq_stride < n_tok) return fail(TADA_ERR_SHAPE, "bad batch/token geometry");
+  if (batch == 0 || n_tok == 0) return TADA_OK;
+  if (!pool || !src_k || !src_v || !page_table || !dst_start) return fail(TADA_ERR_SHAPE, "null buffer");
+  AppendArgs a{};
+  a.L = *layout;
+  a.pool = pool;
+  a.src[0] = src_k;
+  a.src[1] = src_v;
+  a.n_tok = n_tok;
+  a.src_seq_stride = src_seq_stride;
+  a.page_table = page_table;
+  a.pt_stride = pt_stride;
+  a.dst_start = dst_start;
+  a.dst_offset = dst_offset;
+  a.err = err_flag;
+  const int row = layout->heads * layout->head_dim;
+  const size_t per_tok = size_t(row + layout->head_dim) * 4;
+  int tt = int((32 * 1024) / per_tok);
+  tt = tt < 1 ? 1 : (tt > 16 ? 16 : tt);
+  if (tt > n_tok) tt = int(n_tok);
+  const size_t smem = per_tok * tt;
+  if (smem > 200 * 1024) return fail(TADA_ERR_CONFIG, "heads*head_dim too large for quant_append");
+  a.tt = tt;
+  a.tiles_per_seq = int((n_tok + tt - 1) / tt);
+  const size_t esz = dtype == TADA_F32 ? 4 : 2;
+  a.vec_ok = (layout->head_dim % 4 == 0) && (reinterpret_cast<uintptr_t>(src_k) % 16 == 0) &&
+             (reinterpret_cast<uintptr_t>(src_v) % 16 == 0) && ((src_seq_stride * row * esz) % 16 == 0) &&
+             (layout->group_bytes % 4 == 0 || layout->bits <= 4);
+  return dtype == TADA_F32 ? launch_append<float>(a, batch, smem, S(stream))
+                           : launch_append<__nv_bfloat16>(a, batch, smem, S(stream));
+}
+
+int tada_residual_write(float* res_k, float* res_v, int64_t res_seq_stride, int32_t heads, int32_t head_dim,
+                        const void* src_k, const void* src_v, int32_t dtype, int32_t batch, int64_t n_tok,
+                        int64_t src_seq_stride, const int32_t* pos, int32_t pos_offset, void* stream) {
+  if (!valid_dtype(dtype)) return fail(TADA_ERR_CONFIG, "dtype must be f32 or bf16");
+  if (batch < 0 || n_tok < 0) return fail(TADA_ERR_SHAPE, "bad batch/token geometry");
+  if (batch == 0 || n_tok == 0) return TADA_OK;
+  const int row = heads * head_dim;
+  const int grid = grid_for(int64_t(batch) * n_tok * row * 2, 256);
+  if (dtype == TADA_F32)
+    residual_write_kernel<float><<<grid, 256, 0, S(stream)>>>(
+        res_k, res_v, res_seq_stride, row, reinterpret_cast<const float*>(src_k), reinterpret_cast<const float*>(src_v),
+        n_tok, src_seq_stride, pos, pos_offset, batch);
+  else
+    residual_write_kernel<__nv_bfloat16><<<grid, 256, 0, S(stream)>>>(
+        res_k, res_v, res_seq_stride, row, reinterpret_cast<const __nv_bfloat16*>(src_k),
+        reinterpret_cast<const __nv_bfloat16*>(src_v), n_tok, src_seq_stride, pos, pos_offset, batch);
+  return check_launch("residual_write");
+}
+
+int tada_lengths_add(int32_t* arr, int32_t batch, int32_t delta, void* stream) {
+  if (batch <= 0) return TADA_OK;
+  lengths_add_kernel<<<(batch + 127) / 128, 128, 0, S(stream)>>>(arr, batch, delta);
+  return check_launch("lengths_add");
+}
+
+int tada_gather_compressed(const tada_page_layout* layout, const uint8_t* pool, const int32_t* page_row, int64_t n_tok,
+                           int32_t side, float* mean, uint8_t* codes, float* scales, float* mins, void* stream) {
+  if (!layout || side < 0 || side > 1) return fail(TADA_ERR_CONFIG, "bad layout/side");
+  if (n_tok <= 0) return TADA_OK;
+  const int64_t per = layout->head_dim + int64_t(layout->heads) * layout->group_bytes + 2 * layout->heads;
+  move_compressed_kernel<true><<<grid_for(n_tok * per, 256), 256, 0, S(stream)>>>(
+      *layout, const_cast<uint8_t*>(pool), page_row, n_tok, side, mean, codes, scales, mins);
+  return check_launch("gather_compressed");
+}
+
+int tada_scatter_compressed(const tada_page_layout* layout, uint8_t* pool, const int32_t* page_row, int64_t n_tok,
+                            int32_t side, const float* mean, const uint8_t* codes, const float* scales,
+                            const float* mins, void* stream) {
+  if (!layout || side < 0 || side > 1) return fail(TADA_ERR_CONFIG, "bad layout/side");
+  if (n_tok <= 0) return TADA_OK;
+  const int64_t per = layout->head_dim + int64_t(layout->heads) * layout->group_bytes + 2 * layout->heads;
+  move_compressed_kernel<false><<<grid_for(n_tok * per, 256), 256, 0, S(stream)>>>(
+      *layout, pool, page_row, n_tok, side, const_cast<float*>(mean), const_cast<uint8_t*>(codes),
+      const_cast<float*>(scales), const_cast<float*>(mins));
+  return check_launch("scatter_compressed");
+}
+
+}  // extern "C"

@@ -1,0 +1,139 @@
+"""GPU parity of decode attention (K2 split-K + K3 combine) vs the reference.
+
+Bars: exact generic kernel (f32 out) within 1e-5 of the reference's
+attend_streaming (the reference's own streaming-vs-naive tolerance,
+test_acceptance.py:150-178); the tensor-core kernel (bf16 out) within the
+north_star's 2e-3 max-abs.  Mirrors pkg/tests/test_attention.py (hot-path subset).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import golden_io as gio
+from oracle import tada_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+ARR, CASES = gio.load()
+
+
+def tk():
+    import paper_2506_04642_b200 as m
+
+    return m
+
+
+def cfg_for(hq, h, d, R, bits):
+    m = tk()
+    return m.ModelConfig(1, hq, h, d, R, m.RopeParams(d), m.PrecisionPlan((bits,)))
+
+
+def replay(key):
+    c = CASES[key]
+    k, v, q = gio.kv_inputs(c["seed"], c["schedule"], c["hq"], c["h"], c["d"])
+    cache = tk().CompressedLayerCache(c["h"], c["d"], c["bits"], c["R"])
+    for a, b in zip(gio.split_schedule(k, c["schedule"]), gio.split_schedule(v, c["schedule"])):
+        cache.append_tokens(a, b)
+    return cache, q, cfg_for(c["hq"], c["h"], c["d"], c["R"], c["bits"])
+
+
+@pytest.mark.parametrize("key", [k for k in gio.keys("kv") if sum(CASES[k]["schedule"]) > 0])
+def test_attend_streaming_golden(key):
+    cache, q, cfg = replay(key)
+    out = tk().attend_streaming(q, cache, cfg).output
+    assert np.abs(out - ARR[f"{key}/attn_stream64"]).max() <= 1e-5
+    naive = tk().attend_naive(q, cache, cfg).output
+    assert np.abs(naive - ARR[f"{key}/attn_naive"]).max() <= 1e-5
+
+
+@pytest.mark.parametrize("key", gio.keys("c1"))
+def test_config1_attention_golden(key):
+    c = CASES[key]
+    k, v, q = gio.c1_inputs(c["hq"])
+    cache = tk().CompressedLayerCache(8, 128, 4, c["R"])
+    cache.append_tokens(k, v)
+    out = tk().attend_streaming(q, cache, cfg_for(c["hq"], 8, 128, c["R"], 4)).output
+    assert np.abs(out - ARR[f"{key}/attn_stream64"]).max() <= 1e-5
+
+
+def test_single_token_returns_value_and_empty_cache():
+    m = tk()
+    cfg = cfg_for(4, 2, 16, 4, 4)
+    rng = np.random.default_rng(0)
+    cache = m.CompressedLayerCache(2, 16, 4, 4)
+    with pytest.raises(m.StateError):
+        m.attend_streaming(np.zeros((4, 16), np.float32), cache, cfg)
+    k = rng.normal(size=(1, 2, 16)).astype(np.float32)
+    v = rng.normal(size=(1, 2, 16)).astype(np.float32)
+    cache.append_tokens(k, v)
+    out = m.attend_streaming(rng.normal(size=(4, 16)).astype(np.float32), cache, cfg).output
+    for g in range(4):
+        assert np.allclose(out[g], v[0, m.kv_head_index(g, 4, 2)], atol=1e-6)
+    with pytest.raises(m.ShapeError):
+        m.attend_streaming(np.zeros((3, 16), np.float32), cache, cfg)
+
+
+def test_scores_normalized():
+    m = tk()
+    cfg = cfg_for(4, 2, 16, 4, 4)
+    rng = np.random.default_rng(4)
+    cache = m.CompressedLayerCache(2, 16, 4, 4)
+    cache.append_tokens(rng.normal(size=(7, 2, 16)).astype(np.float32), rng.normal(size=(7, 2, 16)).astype(np.float32))
+    out = m.attend_naive(rng.normal(size=(4, 16)).astype(np.float32), cache, cfg, return_scores=True)
+    assert len(out.scores) == 4
+    for row in out.scores:
+        assert row.shape == (7,) and abs(float(row.sum()) - 1.0) < 1e-5
+
+
+def _paged_case(B, H, hq, D, bits, T, R, seed, page_tokens=64):
+    m = tk()
+    rng = np.random.default_rng(seed)
+    k = orc.bf16_round(rng.normal(size=(B, T, H, D)).astype(np.float32))
+    v = orc.bf16_round(rng.normal(size=(B, T, H, D)).astype(np.float32))
+    q = orc.bf16_round(rng.normal(size=(B, hq, D)).astype(np.float32))
+    store = m.PagedKVCache(1, H, D, (bits,), R, batch=B, page_tokens=page_tokens, max_tokens=T + 1,
+                           shuffle_pages=True, seed=seed)
+    store.append(0, torch.from_numpy(k).cuda().bfloat16(), torch.from_numpy(v).cuda().bfloat16())
+    want = []
+    for b in range(B):
+        st = orc.LayerState(H, D, bits, R)
+        orc.append(st, k[b], v[b])
+        want.append(orc.attend(q[b], st, hq)[0])
+    return store, torch.from_numpy(q).cuda(), np.stack(want)
+
+
+@pytest.mark.parametrize("bits", [2, 4, 8, 16])
+@pytest.mark.parametrize("splits", [1, 3, 16])
+def test_paged_batched_exact(bits, splits):
+    store, q, want = _paged_case(B=3, H=8, hq=32, D=128, bits=bits, T=700, R=128, seed=bits)
+    out = store.attend(0, q, num_splits=splits, mode=1)
+    assert np.abs(out.cpu().numpy() - want).max() <= 1e-5
+
+
+@pytest.mark.parametrize("bits", [2, 4, 8])
+@pytest.mark.parametrize("hq", [8, 32, 64])
+def test_paged_batched_fast_bf16(bits, hq):
+    store, q, want = _paged_case(B=4, H=8, hq=hq, D=128, bits=bits, T=1500, R=128, seed=10 + bits)
+    out = store.attend(0, q.bfloat16(), out_dtype=torch.bfloat16, mode=2)
+    assert np.abs(out.float().cpu().numpy() - want).max() <= 2e-3
+    out32 = store.attend(0, q, out_dtype=torch.float32, mode=2)
+    assert np.abs(out32.cpu().numpy() - want).max() <= 2e-3
+
+
+def test_precision_ordering():
+    """test_attention.py:158-176: median error vs the raw-K/V f64 oracle shrinks with width."""
+    m = tk()
+    errs = {b: [] for b in (2, 4, 8, 16)}
+    for seed in range(20):
+        rng = np.random.default_rng(seed)
+        k = rng.normal(size=(12, 2, 16)).astype(np.float32)
+        v = rng.normal(size=(12, 2, 16)).astype(np.float32)
+        q = rng.normal(size=(4, 16)).astype(np.float32)
+        exact = orc.attend_f64(q, k, v, 4)
+        for b in errs:
+            cache = m.CompressedLayerCache(2, 16, b, 0)
+            cache.append_tokens(k, v)
+            errs[b].append(float(np.linalg.norm(m.attend_naive(q, cache, cfg_for(4, 2, 16, 0, b)).output - exact)))
+    med = [float(np.median(errs[b])) for b in (2, 4, 8, 16)]
+    assert med[0] >= med[1] >= med[2] >= med[3]

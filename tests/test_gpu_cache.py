@@ -1,0 +1,160 @@
+"""GPU parity of the compressed cache: K1 quantize-on-append into the paged layout.
+
+Every cache is exported back to the reference layout and compared byte-for-byte
+through TADAKV1 (serialize_cache) against the golden blobs the reference wrote,
+or against the oracle.  Mirrors pkg/tests/test_cache.py (hot-path subset).
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+import golden_io as gio
+from oracle import tada_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+ARR, CASES = gio.load()
+
+
+def tk():
+    import paper_2506_04642_b200 as m
+
+    return m
+
+
+def replay(key):
+    c = CASES[key]
+    k, v, q = gio.kv_inputs(c["seed"], c["schedule"], c["hq"], c["h"], c["d"])
+    cache = tk().CompressedLayerCache(c["h"], c["d"], c["bits"], c["R"])
+    for a, b in zip(gio.split_schedule(k, c["schedule"]), gio.split_schedule(v, c["schedule"])):
+        cache.append_tokens(a, b)
+    return cache, k, v, q
+
+
+@pytest.mark.parametrize("key", gio.keys("kv"))
+def test_append_schedule_blob_golden(key):
+    cache, *_ = replay(key)
+    blob = tk().serialize_cache(cache)
+    assert len(blob) == CASES[key]["blob_len"]
+    assert hashlib.sha256(blob).hexdigest() == CASES[key]["blob_sha256"]
+
+
+@pytest.mark.parametrize("key", gio.keys("kv")[::3])
+def test_deserialize_round_trip(key):
+    cache, *_ = replay(key)
+    blob = tk().serialize_cache(cache)
+    restored = tk().deserialize_cache(blob)
+    assert tk().serialize_cache(restored) == blob
+    assert restored.total_tokens == cache.total_tokens
+
+
+@pytest.mark.parametrize("key", gio.keys("c1"))
+def test_config1_blob_golden(key):
+    c = CASES[key]
+    k, v, q = gio.c1_inputs(c["hq"])
+    cache = tk().CompressedLayerCache(8, 128, 4, c["R"])
+    cache.append_tokens(k, v)
+    blob = tk().serialize_cache(cache)
+    assert hashlib.sha256(blob).hexdigest() == c["blob_sha256"]
+    # bf16 device input (production dtype) lands on the same bytes
+    cache2 = tk().CompressedLayerCache(8, 128, 4, c["R"])
+    cache2.append_tokens(torch.from_numpy(k).cuda().bfloat16(), torch.from_numpy(v).cuda().bfloat16())
+    assert tk().serialize_cache(cache2) == blob
+
+
+def test_flush_trace_one_at_a_time():
+    """test_cache.py:96-105."""
+    cache = tk().CompressedLayerCache(2, 16, 4, 4)
+    rng = np.random.default_rng(2)
+    counts = []
+    for _ in range(5):
+        k = rng.normal(size=(1, 2, 16)).astype(np.float32)
+        cache.append_tokens(k, k.copy())
+        counts.append((cache.compressed_tokens, cache.r))
+    assert counts == [(0, 1), (0, 2), (0, 3), (4, 0), (4, 1)]
+
+
+@pytest.mark.parametrize("bits", [2, 4, 8, 16])
+@pytest.mark.parametrize("R", [0, 3, 128])
+def test_bulk_equals_incremental(bits, R):
+    """test_cache.py:107-117, at decode granularity and the paper's R."""
+    rng = np.random.default_rng(3 + bits)
+    k = rng.normal(size=(300, 4, 32)).astype(np.float32)
+    v = rng.normal(size=(300, 4, 32)).astype(np.float32)
+    bulk = tk().CompressedLayerCache(4, 32, bits, R)
+    bulk.append_tokens(k, v)
+    step = tk().CompressedLayerCache(4, 32, bits, R)
+    for t in range(0, 300, 7):
+        step.append_tokens(k[t: t + 7], v[t: t + 7])
+    ref = orc.LayerState(4, 32, bits, R)
+    orc.append(ref, k, v)
+    assert tk().serialize_cache(bulk) == tk().serialize_cache(step) == orc.dump(ref)
+
+
+@pytest.mark.parametrize("bits", [2, 4, 8, 16])
+def test_identical_heads_bit_exact(bits):
+    """test_cache.py:159-173: identical heads reconstruct losslessly."""
+    cache = tk().CompressedLayerCache(2, 16, bits, 3)
+    rng = np.random.default_rng(6)
+    k = np.repeat(rng.normal(size=(10, 1, 16)).astype(np.float32), 2, axis=1)
+    v = np.repeat(rng.normal(size=(10, 1, 16)).astype(np.float32), 2, axis=1)
+    cache.append_tokens(k, v)
+    assert cache.compressed_tokens == 9
+    for head in range(2):
+        k_hat, v_hat = cache.reconstruct(head)
+        assert np.array_equal(k_hat, k[:, head, :]) and np.array_equal(v_hat, v[:, head, :])
+
+
+def test_outlier_regime_and_errors():
+    m = tk()
+    rng = np.random.default_rng(5)
+    x = orc.outlier_activations(rng, 256, 8, 128)
+    y = orc.outlier_activations(rng, 256, 8, 128)
+    cache = m.CompressedLayerCache(8, 128, 2, 0)
+    cache.append_tokens(x, y)
+    ref = orc.LayerState(8, 128, 2, 0)
+    orc.append(ref, x, y)
+    assert m.serialize_cache(cache) == orc.dump(ref)
+    with pytest.raises(m.ShapeError):
+        cache.append_tokens(np.zeros((1, 3, 128), np.float32), np.zeros((1, 3, 128), np.float32))
+    bad = x[:2].copy()
+    bad[1, 3, 7] = np.nan
+    before = m.serialize_cache(cache)
+    with pytest.raises(m.DataError):
+        cache.append_tokens(bad, bad)
+    assert m.serialize_cache(cache) == before  # no mutation on error
+
+
+@pytest.mark.parametrize("plan", [(8, 4, 2, 16), (4, 4, 4, 4)])
+def test_paged_multilayer_batched_vs_oracle(plan):
+    """PagedKVCache: B sequences x L layers, shuffled pages, mixed widths; each (layer, seq) == oracle."""
+    m = tk()
+    B, H, D, R = 3, 8, 128, 16
+    store = m.PagedKVCache(len(plan), H, D, plan, R, batch=B, page_tokens=16, max_tokens=200, shuffle_pages=True)
+    rng = np.random.default_rng(11)
+    chunks = [37, 1, 1, 60, 5]
+    data = {}
+    for layer in range(len(plan)):
+        ks = orc.bf16_round(rng.normal(size=(B, sum(chunks), H, D)).astype(np.float32))
+        vs = orc.bf16_round(rng.normal(size=(B, sum(chunks), H, D)).astype(np.float32))
+        data[layer] = (ks, vs)
+        off = 0
+        for n in chunks:
+            kt = torch.from_numpy(ks[:, off: off + n]).cuda().bfloat16()
+            vt = torch.from_numpy(vs[:, off: off + n]).cuda().bfloat16()
+            store.append(layer, kt, vt)
+            off += n
+    store.check_errors()
+    for layer, bits in enumerate(plan):
+        for b in range(B):
+            ref = orc.LayerState(H, D, bits, R)
+            orc.append(ref, data[layer][0][b], data[layer][1][b])
+            ex = store.export(layer, b)
+            kd = ex["k_dev"].to_host()
+            assert kd.codes == ref.kdev.payload
+            assert np.array_equal(ex["k_mean"].cpu().numpy(), ref.kmean)
+            assert ex["v_dev"].to_host().codes == ref.vdev.payload
+            assert np.array_equal(ex["residual_v"].cpu().numpy(), ref.rv)
