@@ -1,0 +1,376 @@
+"""Benchmark of the TaDA KV hot path on B200 (BASELINE.json metric / config 2).
+
+Workload (``config.workload``): Llama-3-8B-shaped decode — 32 layers, 32 q / 8 kv
+heads, head_dim 128, 32k context, batch 16 per GPU, searched-style per-layer
+plan [8]*2 + [4]*22 + [2]*8, residual_length 128.  One STEP = one decode
+token for every sequence through every layer: K1 append of the new token's K/V
+(residual write; block flush every 128 steps) + K2/K3 split-K decode attention
+over the compressed cache, then one NCCL all-gather of the step's attention
+outputs when N > 1.  Multi-GPU: sequences are sharded by rank (weak scaling:
+16 sequences per GPU), no collective inside the hot loop.
+
+``value``  = decode tokens/s (whole job) with inputs resident in HBM.
+``e2e``    = the same through the public API with pinned-host q / K / V copied in
+             and attention outputs copied out every step.
+``roofline`` = decode attention (K2+K3) algorithmic bytes / its CUDA-event time.
+``quant_append`` = config 3's metric (prefill bulk quantize-append GB/s), measured
+             while the 32k-token cache is built.
+``cpu_baseline`` = the CPU oracle port (oracle/tada_oracle.py, numpy) timed on this
+             host on a bounded sample, extrapolated to the same step.
+
+``--impl reference`` times that CPU implementation alone on this host's cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode attn tokens/s + HBM GB/s vs roofline (Llama-3-8B, 32k ctx); quant-append GB/s"
+PLAN = [8] * 2 + [4] * 22 + [2] * 8
+L, HQ, H, D, T, B_PER_GPU, R = 32, 32, 8, 128, 32768, 16, 128
+WORKLOAD = "llama3-8b decode, 32 layers, 32q/8kv heads, head_dim 128, 32k ctx, batch 16/GPU, plan [8]*2+[4]*22+[2]*8"
+
+
+def tok_bytes(bits: int) -> int:
+    """Algorithmic bytes per compressed context token per side: f32 mean + codes + f32 (scale, min)."""
+    gb = D * 4 if bits == 16 else D * bits // 8
+    return 4 * D + H * gb + 8 * H
+
+
+def attn_alg_bytes(bits: int, batch: int, ctx_c: int, ctx_r: int) -> int:
+    """One decode-attention launch (one layer, `batch` sequences): both sides + residual (bf16-accounted) + q/out."""
+    return batch * (2 * ctx_c * tok_bytes(bits) + 2 * ctx_r * H * D * 2 + 2 * HQ * D * 2)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        busy = [s for s in sm if s > 0.5 * mx] if mx else sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------ CPU oracle leg
+def _cpu_worker(args):
+    """One host core: build oracle caches at T=32768 for widths 8/4/2, then time attend on each `reps` times."""
+    seed, tokens, reps = args
+    os.environ["OMP_NUM_THREADS"] = os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from oracle import tada_oracle as orc
+
+    rng = np.random.default_rng(seed)
+    times = {}
+    for bits in (8, 4, 2):
+        st = orc.LayerState(H, D, bits, R)
+        k = orc.bf16_round(rng.normal(size=(tokens, H, D)).astype(np.float32))
+        v = orc.bf16_round(rng.normal(size=(tokens, H, D)).astype(np.float32))
+        orc.append(st, k, v)
+        del k, v
+        q = orc.bf16_round(rng.normal(size=(HQ, D)).astype(np.float32))
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            orc.attend(q, st, HQ, block=64)
+            ts.append(time.perf_counter() - t0)
+        times[bits] = ts
+    return times
+
+
+def cpu_oracle_leg(reps: int, tokens: int = T, workers: int | None = None):
+    """Per-unit (1 sequence x 1 layer) attend times on `workers` cores in parallel -> C2 decode tokens/s."""
+    cores = os.cpu_count() or 1
+    workers = workers or min(cores, 32)
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(workers) as pool:
+        res = pool.map(_cpu_worker, [(1000 + i, tokens, reps) for i in range(workers)])
+    per = {b: [t for r in res for t in r[b]] for b in (8, 4, 2)}
+    med = {b: statistics.median(per[b]) for b in per}
+    unit_mix = sum(med[b] for b in PLAN)  # one sequence through all 32 layers, one core
+    step_s = unit_mix * B_PER_GPU / workers  # 16 sequences spread over `workers` cores
+    alg = sum(attn_alg_bytes(b, 1, tokens, 0) for b in PLAN) * B_PER_GPU
+    return {
+        "tokens_per_s": B_PER_GPU / step_s, "step_s": step_s, "alg_gbs": alg / step_s / 1e9, "workers": workers,
+        "unit_s": {str(b): med[b] for b in med}, "per_step_samples": workers * 3,
+        "sample": f"{workers} workers x 1 (seq, layer) unit per width {{8,4,2}} at T={tokens} x {reps} reps; "
+                  f"step = 16 seqs x 32 layers extrapolated linearly from the per-width medians",
+    }
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    reps = 1
+    warm = cpu_oracle_leg(reps=max(1, args.warmup // 3))  # builds + warms; counts toward warmup
+    times = []
+    last = warm
+    for _ in range(max(1, args.steps // 5)):
+        last = cpu_oracle_leg(reps=reps)
+        times.append(last["step_s"])
+    step_s = statistics.median(times)
+    v = B_PER_GPU / step_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD + " (CPU oracle port, numpy)", "global_batch": B_PER_GPU, "seq_len": T,
+                   "parallelism": f"{last['workers']} host processes"},
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": last["workers"], "kind": "port",
+                         "sample": last["sample"]},
+        "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "hbm_gbs_equiv": last["alg_gbs"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------ GPU arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2506_04642_b200 as tk
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    B = B_PER_GPU
+    steps, warm = args.steps, args.warmup
+    max_tokens = T + R + steps + warm + 8
+    store = tk.PagedKVCache(L, H, D, PLAN, R, batch=B, page_tokens=64, max_tokens=max_tokens, shuffle_pages=True,
+                            seed=rank)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1002 + rank)
+
+    # ---- prefill: bulk quantize-append of 32k tokens into every layer (config 3's quant-append GB/s)
+    qa_ms, qa_bytes = [], 0
+    for layer in range(L):
+        k = torch.randn((B, T, H, D), generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
+        v = torch.randn((B, T, H, D), generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        store.append(layer, k, v)
+        e1.record()
+        e1.synchronize()
+        qa_ms.append(e0.elapsed_time(e1))
+        qa_bytes += 2 * B * T * H * D * 2 + B * T * 2 * tok_bytes(PLAN[layer])
+        del k, v
+    store.check_errors()
+    quant_append_gbs = qa_bytes / (sum(qa_ms) / 1e3) / 1e9
+
+    # ---- per-step synthetic inputs (a few sets, cycled; the 35 GB cache is the traffic, >> L2)
+    nsets = 4
+    qs = [torch.randn((L, B, HQ, D), generator=gen, device=dev).to(torch.bfloat16) for _ in range(nsets)]
+    ks = [torch.randn((L, B, 1, H, D), generator=gen, device=dev).to(torch.bfloat16) for _ in range(nsets)]
+    vs = [torch.randn((L, B, 1, H, D), generator=gen, device=dev).to(torch.bfloat16) for _ in range(nsets)]
+    outs = torch.empty((L, B, HQ, D), dtype=torch.bfloat16, device=dev)
+    gathered = torch.empty((world, L, B, HQ, D), dtype=torch.bfloat16, device=dev) if world > 1 else None
+    splits = store.suggest_splits(0)
+    attn_events = []
+
+    def step(i, q_in=None, k_in=None, v_in=None, record=False):
+        s = i % nsets
+        q_all = qs[s] if q_in is None else q_in
+        k_all = ks[s] if k_in is None else k_in
+        v_all = vs[s] if v_in is None else v_in
+        for layer in range(L):
+            store.append(layer, k_all[layer], v_all[layer])
+            if record:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+            store.attend(layer, q_all[layer], out=outs[layer], num_splits=splits, mode=args.mode)
+            if record:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record()
+                c, r = store.lengths(layer)
+                attn_events.append((e0, e1, attn_alg_bytes(PLAN[layer], B, c, r)))
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, outs)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(warm):
+        step(i)
+    barrier()
+    launches_before = None
+    with ClockSampler(local) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for i in range(steps):
+            step(warm + i, record=True)
+        t1.record()
+        barrier()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_per_step = ms / steps
+    value = B * world * steps / (ms / 1e3)
+    attn_ms = sum(e0.elapsed_time(e1) for e0, e1, _ in attn_events)
+    attn_bytes = sum(b for _, _, b in attn_events)
+    achieved = attn_bytes / (attn_ms / 1e3) / 1e9
+    step_bytes = attn_bytes / steps
+    peak, peak_kind = peaks()
+
+    # ---- e2e through the public API: pinned host q/K/V in, outputs out, every step
+    qh = [t.cpu().pin_memory() for t in qs[:2]]
+    kh = [t.cpu().pin_memory() for t in ks[:2]]
+    vh = [t.cpu().pin_memory() for t in vs[:2]]
+    out_h = torch.empty(outs.shape, dtype=outs.dtype).pin_memory()
+    q_d = torch.empty_like(qs[0])
+    k_d = torch.empty_like(ks[0])
+    v_d = torch.empty_like(vs[0])
+    e2e_steps = max(3, steps // 2)
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for i in range(e2e_steps):
+        q_d.copy_(qh[i % 2], non_blocking=True)
+        k_d.copy_(kh[i % 2], non_blocking=True)
+        v_d.copy_(vh[i % 2], non_blocking=True)
+        step(i, q_d, k_d, v_d)
+        out_h.copy_(outs, non_blocking=True)
+    t1.record()
+    barrier()
+    e2e_ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_value = B * world * e2e_steps / (e2e_ms / 1e3)
+    h2d = (qh[0].numel() + kh[0].numel() + vh[0].numel()) * 2
+    d2h = out_h.numel() * 2
+    store.check_errors()
+
+    launches_per_step = L * (2 + (1 if splits > 1 else 0) + 1)  # residual write, length add, attn (+combine)
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "attn_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("traffic_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            c = cpu_oracle_leg(reps=1)
+            cpu = {"value": c["tokens_per_s"], "unit": "tokens/s", "cores": c["workers"], "kind": "port",
+                   "sample": c["sample"], "alg_gbs": c["alg_gbs"]}
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": steps, "warmup": warm,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u8 codes / f32 means+scales, bf16 q/out", "data": "synthetic (torch.randn bf16, seeded)",
+            "config": {"workload": WORKLOAD, "global_batch": B * world, "seq_len": T, "layers": L,
+                       "parallelism": f"seq-shard x{world}", "num_splits": splits, "page_tokens": 64,
+                       "kernel_mode": args.mode, "l2": "cache 35 GB/GPU >> 126 MB L2 (no flush needed)"},
+            "hbm_gbs": step_bytes / (ms_per_step / 1e3) / 1e9,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "kernel": "decode attention K2+K3 (tada_decode_attn)",
+                         "peak_source": peak_kind, "frac_of_8tbs_spec": achieved / 8000.0,
+                         "alg_bytes_per_step": step_bytes, "attn_ms_per_step": attn_ms / steps},
+            "quant_append": {"value": quant_append_gbs, "unit": "GB/s", "frac": quant_append_gbs / peak,
+                             "workload": f"prefill bulk quantize-append 32k tokens x batch {B} x 32 layers (config 3 "
+                                         f"shape per sequence)", "ms_per_layer": statistics.median(qa_ms)},
+            "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches_per_step * steps,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", type=int, default=0, help="attention kernel: 0 auto, 1 exact generic, 2 tensor-core")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
