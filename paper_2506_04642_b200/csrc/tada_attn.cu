@@ -9,43 +9,9 @@
 
 #include <string>
 
-#include "tada_common.cuh"
+#include "tada_attn.cuh"
 
 namespace tada {
-
-struct AttnArgs {
-  tada_page_layout L;
-  const uint8_t* pool;
-  const void* q;
-  int Hq;
-  const int32_t* page_table;
-  int pt_stride;
-  const int32_t* comp_len;
-  const int32_t* res_len;
-  const float* res_k;
-  const float* res_v;
-  int64_t res_seq_stride;
-  float scale;
-  int splits;
-  float* part_acc;  // [B][Hq][S][D]
-  float* part_ml;   // [B][Hq][S][2]
-  void* out;
-  int out_dtype;
-};
-
-__device__ __forceinline__ void store_any(void* out, int dtype, int64_t i, float v) {
-  if (dtype == TADA_F32) reinterpret_cast<float*>(out)[i] = v;
-  else reinterpret_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(v);
-}
-
-// Token range [t_begin, t_end) of split `s` for a sequence of n tokens; chunks are
-// multiples of `align` so split boundaries fall on tile boundaries.
-__device__ __forceinline__ void split_range(int n, int splits, int s, int align, int& t0, int& t1) {
-  int chunk = (n + splits - 1) / splits;
-  chunk = (chunk + align - 1) / align * align;
-  t0 = min(n, s * chunk);
-  t1 = min(n, t0 + chunk);
-}
 
 template <int BITS>
 __device__ __forceinline__ float khat_elem(const float* mean, const uint8_t* grp, float s, float mn, int d) {
@@ -150,10 +116,10 @@ __global__ void __launch_bounds__(256) attn_generic_kernel(AttnArgs a) {
   } else {
     for (int pair = tid; pair < Hq * D; pair += bd) {
       const int g = pair / D, d = pair - g * D;
-      a.part_acc[((int64_t(b) * Hq + g) * a.splits + split) * D + d] = acc[pair];
+      a.part_acc[((int64_t(b) * Hq + g) * a.slots + split) * D + d] = acc[pair];
     }
     for (int g = tid; g < Hq; g += bd) {
-      float* ml = a.part_ml + ((int64_t(b) * Hq + g) * a.splits + split) * 2;
+      float* ml = a.part_ml + ((int64_t(b) * Hq + g) * a.slots + split) * 2;
       ml[0] = mrow[g];
       ml[1] = lrow[g];
     }
@@ -207,19 +173,28 @@ using namespace tada;
 extern "C" {
 
 int64_t tada_decode_attn_workspace_bytes(int32_t batch, int32_t num_q_heads, int32_t head_dim, int32_t num_splits) {
-  if (num_splits <= 1) return 0;
-  return int64_t(batch) * num_q_heads * num_splits * (int64_t(head_dim) + 2) * 4;
+  // slots = splits + 1 (the tensor-core path puts the residual rows in an extra slot)
+  return int64_t(batch) * num_q_heads * (num_splits + 1) * (int64_t(head_dim) + 2) * 4;
 }
 
 int32_t tada_decode_attn_suggest_splits(int32_t batch, int64_t max_tokens, int32_t page_tokens) {
   if (batch <= 0 || max_tokens <= 0) return 1;
-  const int64_t target_ctas = 148 * 4;
-  int64_t s = (target_ctas + batch - 1) / batch;
-  const int64_t max_s = (max_tokens + 255) / 256;  // keep >= ~256 tokens per split
-  if (s > max_s) s = max_s;
-  if (s < 1) s = 1;
+  // One CTA per SM (the tensor-core kernel uses ~150-220 KB of smem): pick the smallest
+  // number of whole waves (<= 4) that keeps >= 256 tokens per split.
+  const int64_t sms = 148;
+  const int64_t max_s = (max_tokens + 255) / 256;
+  int64_t best = 1;
+  for (int64_t waves = 4; waves >= 1; --waves) {
+    const int64_t s = (sms * waves + batch - 1) / batch;
+    if (s <= max_s) {
+      best = s;
+      break;
+    }
+  }
+  if (best > max_s) best = max_s;
+  if (best < 1) best = 1;
   (void)page_tokens;
-  return int32_t(s);
+  return int32_t(best);
 }
 
 int tada_decode_attn(const tada_page_layout* layout, const uint8_t* pool, const void* q, int32_t q_dtype, int32_t batch,
@@ -235,7 +210,12 @@ int tada_decode_attn(const tada_page_layout* layout, const uint8_t* pool, const 
   if (num_splits < 1 || num_splits > 4096) return fail(TADA_ERR_CONFIG, "num_splits out of range");
   if (batch == 0) return TADA_OK;
   if (!q || !out || !comp_len || !res_len) return fail(TADA_ERR_SHAPE, "null buffer");
-  if (num_splits > 1 && !workspace) return fail(TADA_ERR_SHAPE, "workspace required for num_splits > 1");
+  if (mode < 0 || mode > 2) return fail(TADA_ERR_CONFIG, "mode must be 0 (auto), 1 (exact) or 2 (fast)");
+  const bool fast = mode == 2 || (mode == 0 && fast_supported(*layout, num_q_heads));
+  if (mode == 2 && !fast_supported(*layout, num_q_heads))
+    return fail(TADA_ERR_CONFIG, "fast decode attention needs head_dim 128, bits 2/4/8, num_q_heads in {8,16,32,64}, "
+                                 "group size in {1,2,4,8} and page_tokens % 32 == 0");
+  if ((num_splits > 1 || fast) && !workspace) return fail(TADA_ERR_SHAPE, "workspace required");
   AttnArgs a{};
   a.L = *layout;
   a.pool = pool;
@@ -250,15 +230,23 @@ int tada_decode_attn(const tada_page_layout* layout, const uint8_t* pool, const 
   a.res_seq_stride = res_seq_stride;
   a.scale = scale;
   a.splits = num_splits;
+  a.slots = fast ? num_splits + 1 : num_splits;
   a.part_acc = reinterpret_cast<float*>(workspace);
-  a.part_ml = a.part_acc + int64_t(batch) * num_q_heads * num_splits * layout->head_dim;
+  a.part_ml = a.part_acc + int64_t(batch) * num_q_heads * a.slots * layout->head_dim;
   a.out = out;
   a.out_dtype = out_dtype;
+  a.q_dtype = q_dtype;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  (void)mode;
-  int rc = q_dtype == TADA_F32 ? launch_generic<float>(a, batch, st) : launch_generic<__nv_bfloat16>(a, batch, st);
-  if (rc != TADA_OK || num_splits == 1) return rc;
-  combine_kernel<<<unsigned(int64_t(batch) * num_q_heads), 128, 0, st>>>(a.part_acc, a.part_ml, num_splits,
+  int rc;
+  if (fast) {
+    rc = launch_fast(a, batch, st);
+    if (rc == TADA_OK) rc = launch_residual(a, batch, st);
+  } else {
+    rc = q_dtype == TADA_F32 ? launch_generic<float>(a, batch, st) : launch_generic<__nv_bfloat16>(a, batch, st);
+    if (rc != TADA_OK || num_splits == 1) return rc;
+  }
+  if (rc != TADA_OK) return rc;
+  combine_kernel<<<unsigned(int64_t(batch) * num_q_heads), 128, 0, st>>>(a.part_acc, a.part_ml, a.slots,
                                                                           layout->head_dim, out, out_dtype);
   return check_launch("decode_attn_combine");
 }

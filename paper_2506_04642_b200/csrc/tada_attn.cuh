@@ -1,0 +1,49 @@
+// Shared declarations between the decode-attention translation units.
+#pragma once
+
+#include "tada_common.cuh"
+
+namespace tada {
+
+struct AttnArgs {
+  tada_page_layout L;
+  const uint8_t* pool;
+  const void* q;
+  int Hq;
+  const int32_t* page_table;
+  int pt_stride;
+  const int32_t* comp_len;
+  const int32_t* res_len;
+  const float* res_k;
+  const float* res_v;
+  int64_t res_seq_stride;
+  float scale;
+  int splits;       // splits over the compressed tokens (fast path) or all tokens (generic)
+  int slots;        // partial slots per (b, g) in the workspace (fast path: splits + 1 for the residual)
+  float* part_acc;  // [B][Hq][slots][D]
+  float* part_ml;   // [B][Hq][slots][2]
+  void* out;
+  int out_dtype;
+  int q_dtype;
+};
+
+__device__ __forceinline__ void store_any(void* out, int dtype, int64_t i, float v) {
+  if (dtype == TADA_F32) reinterpret_cast<float*>(out)[i] = v;
+  else reinterpret_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(v);
+}
+
+// Token range [t0, t1) of split s out of n tokens; chunk boundaries are multiples of `align`.
+__device__ __forceinline__ void split_range(int n, int splits, int s, int align, int& t0, int& t1) {
+  int chunk = (n + splits - 1) / splits;
+  chunk = (chunk + align - 1) / align * align;
+  t0 = min(n, s * chunk);
+  t1 = min(n, t0 + chunk);
+}
+
+// Fast path (tensor-core grouped-head contraction); returns TADA_ERR_CONFIG if the
+// geometry is unsupported so the caller can fall back to the generic kernel.
+bool fast_supported(const tada_page_layout& L, int Hq);
+int launch_fast(const AttnArgs& a, int batch, cudaStream_t st);
+int launch_residual(const AttnArgs& a, int batch, cudaStream_t st);
+
+}  // namespace tada

@@ -86,7 +86,8 @@ class PagedKVCache:
             return
         cap = max(need, 2 * self._cap_pages, 4)
         for i, lay in enumerate(self.layouts):
-            new = torch.empty((cap, lay.page_bytes), dtype=torch.uint8, device=self.dev)
+            # one spare page: 16-byte-rounded bulk copies of a tile tail may read a few bytes past a page
+            new = torch.empty((cap + 1, lay.page_bytes), dtype=torch.uint8, device=self.dev)
             if self._n_pages:
                 new[: self._n_pages].copy_(self.pools[i][: self._n_pages])
             self.pools[i] = new
