@@ -10,13 +10,13 @@
 // as an f16 hi + lo pair (≈22-bit); accumulation is f32.  Residual (uncompressed) rows
 // are handled by attn_residual_kernel into an extra split slot; K3 merges the slots.
 //
-// CTA = (split, sequence): 8 consumer warps + 1 producer warp.  The producer streams
-// 32-token tiles (K/V means, packed codes, scale/min) with cp.async.bulk (TMA bulk
-// copies, UBLKCP) into a 2-stage mbarrier ring; each tile the consumers
-//   1. convert the f32 means to f16 hi/lo in place (swizzled for ldmatrix),
-//   2. QK: S[tok, head] = mean-term + per-kv-head code-term MMAs, fold min/scale,
-//   3. online softmax (running max / normaliser per q head), P and P' = -p*vscale to smem,
-//   4. PV: O^T[d, head] += vmean^T·P^T + vcode^T·P'^T (one f32 accumulator).
+// CTA = (split, sequence): 8 consumer warps + 1 producer warp.  The producer warp streams
+// 32-token tiles with cp.async.bulk (TMA bulk copies, UBLKCP), one copy per token row into
+// bank-shifted padded rows, through a 2-3 stage mbarrier ring.  Per tile the consumers
+//   1. QK (warp = 8 tokens x half of head_dim): S[g, t] = Q·mean (f16 hi/lo, converted in
+//      registers) - min*sum(q) - scale*(Q·codes), q heads on the MMA M dimension;
+//   2. online softmax per q head (exp2 domain); P and P' = -p*vscale to smem (f16);
+//   3. PV (warp = 16 of head_dim): O[g, d] += P·vmean + P'_h·vcode_h, one f32 accumulator.
 #include <cuda_runtime.h>
 
 #include <string>
@@ -141,10 +141,14 @@ __device__ __forceinline__ void qk_code_pair(const uint32_t* w, int s, uint32_t&
 }
 
 // ------------------------------------------------------------------ shared memory plan
+// One bulk copy per token row, with bank-shifting pads so every fragment load below is
+// (near) conflict-free: mean rows D*4 + 16 B (4-bank shift per token), code rows
+// H*gb + 32 B (8-bank shift), scale/min rows up16(H*8) + 16 B.
 struct Plan {
   int H, gb;
-  int mean_bytes, codes_bytes, meta_bytes, side_bytes, stage_bytes;
-  int off_sbuf, off_pbuf, off_p2buf, off_qsum, off_corr, off_stats, off_bar, total;
+  int mrow, crow, trow, tcopy;  // row strides (bytes) and the meta copy size
+  int mean_bytes, codes_bytes, meta_bytes, side_bytes, stage_bytes, stages;
+  int off_work, off_sbuf, off_pbuf, off_p2buf, off_qsum, off_corr, off_stats, off_bar, total;
 };
 
 __host__ __device__ inline int up128(int x) { return (x + 127) / 128 * 128; }
@@ -153,24 +157,36 @@ __host__ __device__ inline Plan make_plan(int H, int gb, int HQ) {
   Plan p{};
   p.H = H;
   p.gb = gb;
-  p.mean_bytes = TT * D * 4;
-  p.codes_bytes = up128(TT * H * gb);
-  p.meta_bytes = up128(TT * H * 8);
+  p.mrow = D * 4 + 16;
+  p.crow = H * gb + 32;
+  p.tcopy = (H * 8 + 15) / 16 * 16;
+  p.trow = p.tcopy + 16;
+  p.mean_bytes = up128(TT * p.mrow);
+  p.codes_bytes = up128(TT * p.crow);
+  p.meta_bytes = up128(TT * p.trow);
   p.side_bytes = p.mean_bytes + p.codes_bytes + p.meta_bytes;
   p.stage_bytes = 2 * p.side_bytes;
-  int off = STAGES * p.stage_bytes;
+  // work area: logits (2 k-halves) + P + P'; doubles as the f16 q staging area in the prologue
+  const int work0 = up128(2 * HQ * SROW * 4) + 2 * up128(HQ * PROW * 2);
+  const int q16 = ((HQ + 15) / 16) * 16 * D * 2;  // f16 q staging (prologue only)
+  const int work = work0 > q16 ? work0 : q16;
+  const int tail = work + up128(HQ * 4) * 2 + up128(HQ * 16) + 128;
+  p.stages = (3 * p.stage_bytes + tail <= 227 * 1024) ? 3 : STAGES;
+  int off = p.stages * p.stage_bytes;
+  p.off_work = off;
   p.off_sbuf = off;
-  off += up128(HQ * SROW * 4);
+  off += up128(2 * HQ * SROW * 4);
   p.off_pbuf = off;
   off += up128(HQ * PROW * 2);
   p.off_p2buf = off;
   off += up128(HQ * PROW * 2);
+  off = p.off_work + work;
   p.off_qsum = off;
   off += up128(HQ * 4);
   p.off_corr = off;
   off += up128(HQ * 4);
   p.off_stats = off;
-  off += up128(HQ * 4 * 4);
+  off += up128(HQ * 16);
   p.off_bar = off;
   off += 128;
   p.total = off;
@@ -178,27 +194,31 @@ __host__ __device__ inline Plan make_plan(int H, int gb, int HQ) {
 }
 
 // ------------------------------------------------------------------ the kernel
+// Fragment orientation: q heads on M for both products.
+//   QK: S[g, t] = Q[g, d] · K̂^T[d, t]    A = Q (registers, f16), B = K-mean / K-codes tiles
+//   PV: O[g, d] = P[g, t] · V̂[t, d]      A = P, P' (smem, ldmatrix), B = V-mean / V-codes tiles
+// so every mean and code byte of a tile is read from smem by exactly one warp.
 template <int BITS, int HQ>
 __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  constexpr int NT = HQ / 8;  // n-tiles of 8 q heads
-  constexpr int NQK = 2 * NT;  // QK work items (m-tile x n-tile)
-  constexpr int IPW = (NQK + NCW - 1) / NCW;  // items per warp (QK and PV alike)
+  constexpr int MT = (HQ + 15) / 16;    // m-tiles of 16 q heads
   constexpr int TPH = (NCW * 32) / HQ;  // softmax threads per q head
   constexpr int TPT = TT / TPH;         // tokens per softmax thread
+  constexpr int MROWF = (D * 4 + 16) / 4;  // mean row stride in floats
   const int H = a.L.heads, G = HQ / H, gb = a.L.group_bytes, P = a.L.page_tokens;
   const Plan pl = make_plan(H, gb, HQ);
   const int b = blockIdx.y, split = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r = lane >> 2, qi = lane & 3;
 
-  float* sbuf = reinterpret_cast<float*>(smem + pl.off_sbuf);
+  float* sbuf = reinterpret_cast<float*>(smem + pl.off_sbuf);  // [2][HQ][SROW]
   __half* pbuf = reinterpret_cast<__half*>(smem + pl.off_pbuf);
   __half* p2buf = reinterpret_cast<__half*>(smem + pl.off_p2buf);
   float* qsum = reinterpret_cast<float*>(smem + pl.off_qsum);
   float* corr_s = reinterpret_cast<float*>(smem + pl.off_corr);
   float* stats = reinterpret_cast<float*>(smem + pl.off_stats);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + pl.off_bar);
-  uint64_t* empty = full + STAGES;
+  uint64_t* empty = full + 3;
+  const int S = pl.stages;
 
   const int C = a.comp_len[b];
   int t_begin, t_end;
@@ -206,240 +226,207 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a) {
   const int ntiles = (t_end - t_begin + TT - 1) / TT;
 
   if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // q row sums (f32, for the min term)
-  const float* qf = reinterpret_cast<const float*>(a.q) + int64_t(b) * HQ * D;
-  const __nv_bfloat16* qb = reinterpret_cast<const __nv_bfloat16*>(a.q) + int64_t(b) * HQ * D;
-  auto qload = [&](int g, int d) -> float { return a.q_dtype == TADA_F32 ? qf[g * D + d] : __bfloat162float(qb[g * D + d]); };
-  for (int g = warp; g < HQ; g += NCW + 1) {
-    float sacc = 0.f;
-    for (int d = lane; d < D; d += 32) sacc += qload(g, d);
-    sacc = warp_sum(sacc);
-    if (lane == 0) qsum[g] = sacc;
-  }
   __syncthreads();
 
   if (warp == NCW) {
-    // ================================================================ producer
-    if (lane == 0) {
-      const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
-      const uint32_t row_bytes_mean = D * 4, row_bytes_codes = H * gb, row_bytes_meta = H * 8;
-      for (int it = 0; it < ntiles; ++it) {
-        const int stg = it % STAGES;
-        if (it >= STAGES) mbar_wait(&empty[stg], ((it / STAGES) - 1) & 1);
-        const int t0 = t_begin + it * TT;
-        const int nv = min(TT, t_end - t0);
-        const uint8_t* page = a.pool + int64_t(pt[t0 / P]) * a.L.page_bytes;
-        const int row = t0 % P;
-        uint8_t* dst = smem + stg * pl.stage_bytes;
-        const uint32_t bm = nv * row_bytes_mean;
-        const uint32_t bc = (nv * row_bytes_codes + 15) & ~15u;
-        const uint32_t bt = (nv * row_bytes_meta + 15) & ~15u;
-        mbar_expect_tx(&full[stg], 2 * (bm + bc + bt));
-        for (int side = 0; side < 2; ++side) {
-          uint8_t* d0 = dst + side * pl.side_bytes;
-          bulk_g2s(d0, page + a.L.off_mean[side] + int64_t(row) * row_bytes_mean, bm, &full[stg]);
-          bulk_g2s(d0 + pl.mean_bytes, page + a.L.off_codes[side] + int64_t(row) * row_bytes_codes, bc, &full[stg]);
-          bulk_g2s(d0 + pl.mean_bytes + pl.codes_bytes, page + a.L.off_meta[side] + int64_t(row) * row_bytes_meta, bt,
-                   &full[stg]);
-        }
+    // ================================================================ producer: one bulk copy per row
+    const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
+    const uint32_t cbytes = H * gb;
+    for (int it = 0; it < ntiles; ++it) {
+      const int stg = it % S;
+      if (it >= S) mbar_wait(&empty[stg], ((it / S) - 1) & 1);
+      const int t0 = t_begin + it * TT;
+      const int nv = min(TT, t_end - t0);
+      const uint8_t* page = a.pool + int64_t(pt[t0 / P]) * a.L.page_bytes;
+      const int row0 = t0 % P;
+      uint8_t* dst = smem + stg * pl.stage_bytes;
+      if (lane == 0) mbar_expect_tx(&full[stg], uint32_t(nv) * 2u * (D * 4 + cbytes + pl.tcopy));
+      __syncwarp();
+      for (int j = lane; j < 6 * nv; j += 32) {
+        const int side = j / (3 * nv), rem = j - side * 3 * nv, reg = rem / nv, tk = rem - reg * nv;
+        uint8_t* d0 = dst + side * pl.side_bytes;
+        const int64_t row = row0 + tk;
+        if (reg == 0)
+          bulk_g2s(d0 + tk * pl.mrow, page + a.L.off_mean[side] + row * (D * 4), D * 4, &full[stg]);
+        else if (reg == 1)
+          bulk_g2s(d0 + pl.mean_bytes + tk * pl.crow, page + a.L.off_codes[side] + row * cbytes, cbytes, &full[stg]);
+        else
+          bulk_g2s(d0 + pl.mean_bytes + pl.codes_bytes + tk * pl.trow, page + a.L.off_meta[side] + row * (H * 8),
+                   pl.tcopy, &full[stg]);
       }
     }
     return;
   }
 
   // ================================================================== consumers
-  // Q B-fragments (k = d slot, n = q head) for this warp's QK n-tiles, f16.
-  uint32_t bq[IPW][8][2];
-  int qk_mt[IPW], qk_nt[IPW];
-#pragma unroll
-  for (int j = 0; j < IPW; ++j) {
-    const int item = warp + j * NCW;
-    qk_mt[j] = item % 2;
-    qk_nt[j] = item / 2;
-    if (item < NQK) {
-      const int g = 8 * qk_nt[j] + r;
-#pragma unroll
-      for (int s = 0; s < 8; ++s) {
-        const int dbase = 32 * qi;
-        bq[j][s][0] = pack_h2(qload(g, dbase + slot_d<BITS>(s, 0)), qload(g, dbase + slot_d<BITS>(s, 1)));
-        bq[j][s][1] = pack_h2(qload(g, dbase + slot_d<BITS>(s, 2)), qload(g, dbase + slot_d<BITS>(s, 3)));
+  // prologue: q rows -> f32 row sums (min term) + f16 copy in the work area
+  {
+    __half* q16 = reinterpret_cast<__half*>(smem + pl.off_work);
+    for (int g = warp; g < MT * 16; g += NCW) {
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      if (g < HQ) {
+        if (a.q_dtype == TADA_F32) load4(reinterpret_cast<const float*>(a.q) + (int64_t(b) * HQ + g) * D + 4 * lane, v);
+        else load4(reinterpret_cast<const __nv_bfloat16*>(a.q) + (int64_t(b) * HQ + g) * D + 4 * lane, v);
       }
+      const float ssum = warp_sum(v[0] + v[1] + v[2] + v[3]);
+      if (lane == 0 && g < HQ) qsum[g] = ssum;
+      *reinterpret_cast<uint2*>(q16 + g * D + 4 * lane) = make_uint2(pack_h2(v[0], v[1]), pack_h2(v[2], v[3]));
     }
   }
-  // PV accumulators O^T[d, head]: item -> (d-half dh, n-tile nt), 4 m-tiles of 16 d-rows.
-  float oacc[IPW][4][4];
+  consumer_sync();
+  const int kh = warp & 1, tq = 8 * (warp >> 1) + r;  // QK: k-half and this thread's B column (token)
+  uint32_t qa[MT][4][4];
+  {
+    const __half* q16 = reinterpret_cast<const __half*>(smem + pl.off_work);
 #pragma unroll
-  for (int j = 0; j < IPW; ++j)
+    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+      for (int k4 = 0; k4 < 4; ++k4) {
+        const int s = 4 * kh + k4, dq = 32 * qi;
+        const int g0 = 16 * mt + r, g1 = g0 + 8;
+        auto q2 = [&](int g, int w0, int w1) -> uint32_t {
+          const __half2 h = __halves2half2(q16[g * D + dq + slot_d<BITS>(s, w0)], q16[g * D + dq + slot_d<BITS>(s, w1)]);
+          return *reinterpret_cast<const uint32_t*>(&h);
+        };
+        qa[mt][k4][0] = q2(g0, 0, 1);
+        qa[mt][k4][1] = q2(g1, 0, 1);
+        qa[mt][k4][2] = q2(g0, 2, 3);
+        qa[mt][k4][3] = q2(g1, 2, 3);
+      }
+  }
+  float oacc[MT][2][4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) oacc[j][k][e] = 0.f;
-
-  // softmax ownership: thread -> (q head sg, token part)
-  const int sg = tid / TPH, spart = tid % TPH;
-  const int sh = sg / G;  // its kv head
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int n2 = 0; n2 < 2; ++n2)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) oacc[mt][n2][e] = 0.f;
+  const int sg = tid / TPH, spart = tid % TPH, sh = sg / G;  // softmax ownership
   float m_run = -__int_as_float(0x7f800000), l_part = 0.f, bp_part = 0.f;
-  const float scale = a.scale;
-  const float LOG2E = 1.4426950408889634f;
+  const float scale_log2 = a.scale * 1.4426950408889634f;
+  consumer_sync();  // q16 (work area) is dead from here on
 
   for (int it = 0; it < ntiles; ++it) {
-    const int stg = it % STAGES;
+    const int stg = it % S;
     const int t0 = t_begin + it * TT;
     const int nv = min(TT, t_end - t0);
-    mbar_wait(&full[stg], (it / STAGES) & 1);
-    uint8_t* base = smem + stg * pl.stage_bytes;
-    float* kmean = reinterpret_cast<float*>(base);
+    mbar_wait(&full[stg], (it / S) & 1);
+    const uint8_t* base = smem + stg * pl.stage_bytes;
+    const float* kmean = reinterpret_cast<const float*>(base);
     const uint8_t* kcodes = base + pl.mean_bytes;
-    const float2* kmeta = reinterpret_cast<const float2*>(base + pl.mean_bytes + pl.codes_bytes);
-    float* vmean = reinterpret_cast<float*>(base + pl.side_bytes);
+    const uint8_t* kmeta = base + pl.mean_bytes + pl.codes_bytes;
+    const float* vmean = reinterpret_cast<const float*>(base + pl.side_bytes);
     const uint8_t* vcodes = base + pl.side_bytes + pl.mean_bytes;
-    const float2* vmeta = reinterpret_cast<const float2*>(base + pl.side_bytes + pl.mean_bytes + pl.codes_bytes);
+    const uint8_t* vmeta = base + pl.side_bytes + pl.mean_bytes + pl.codes_bytes;
 
-    // ---------------------------------------------------------------- 1. mean f32 -> f16 hi/lo, in place
+    // ---------------------------------------------------------------- QK (warp = token octet x k-half)
     {
-      // K: item (t, s, i): slots (2i,2i+1) -> chunk 2s word i, slots (2i+8,2i+9) -> chunk 2s+1 word i
-      float2 ka[4], kb[4];
-      float va[2][8];
+      float acc[MT][4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int item = tid + u * NCW * 32;  // 0..1023
-        const int t = item >> 5, s = (item >> 2) & 7, i = item & 3;
-        const float* row = kmean + t * D + 32 * i + slot_base<BITS>(s);
-        ka[u] = *reinterpret_cast<const float2*>(row);
-        kb[u] = *reinterpret_cast<const float2*>(row + slot_off1<BITS>());
-      }
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int item = tid + u * NCW * 32;  // 0..511: (t, q8)
-        const int t = item >> 4, q8 = item & 15;
-        const float4 x0 = *reinterpret_cast<const float4*>(vmean + t * D + 8 * q8);
-        const float4 x1 = *reinterpret_cast<const float4*>(vmean + t * D + 8 * q8 + 4);
-        const bool ok = t < nv;
-        va[u][0] = ok ? x0.x : 0.f; va[u][1] = ok ? x0.y : 0.f; va[u][2] = ok ? x0.z : 0.f; va[u][3] = ok ? x0.w : 0.f;
-        va[u][4] = ok ? x1.x : 0.f; va[u][5] = ok ? x1.y : 0.f; va[u][6] = ok ? x1.z : 0.f; va[u][7] = ok ? x1.w : 0.f;
-      }
-      consumer_sync();
-      uint32_t* khi = reinterpret_cast<uint32_t*>(kmean);          // [TT][64 words] swizzled chunks
-      uint32_t* klo = reinterpret_cast<uint32_t*>(kmean) + TT * 64;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int item = tid + u * NCW * 32;
-        const int t = item >> 5, s = (item >> 2) & 7, i = item & 3;
-        uint32_t h0, l0, h1, l1;
-        split_h2(ka[u].x, kb[u].x, h0, l0);
-        split_h2(ka[u].y, kb[u].y, h1, l1);
-        const int c0 = (2 * s) ^ (t & 7), c1 = (2 * s + 1) ^ (t & 7);
-        khi[t * 64 + c0 * 4 + i] = h0;
-        klo[t * 64 + c0 * 4 + i] = l0;
-        khi[t * 64 + c1 * 4 + i] = h1;
-        klo[t * 64 + c1 * 4 + i] = l1;
-      }
-      __half* vhi = reinterpret_cast<__half*>(vmean);  // [TT][16 chunks][8]
-      __half* vlo = vhi + TT * D;
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int item = tid + u * NCW * 32;
-        const int t = item >> 4, q8 = item & 15, dh = q8 >> 3, rr = q8 & 7;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int c = (8 * dh + j) ^ (t & 7);
-          const __half h = __float2half_rn(va[u][j]);
-          vhi[t * D + c * 8 + rr] = h;
-          vlo[t * D + c * 8 + rr] = __float2half_rn(va[u][j] - __half2float(h));
-        }
-      }
-      consumer_sync();
-    }
-
-    // ---------------------------------------------------------------- 2. QK
-#pragma unroll
-    for (int j = 0; j < IPW; ++j) {
-      const int item = warp + j * NCW;
-      if (item >= NQK) break;
-      const int mt = qk_mt[j], nt = qk_nt[j];
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
+      // mean term: this thread's 16 contiguous d of token tq, converted to f16 hi/lo B fragments
+      float x[16];
       {
-        const int tok = 16 * mt + (lane & 7) + 8 * ((lane >> 3) & 1);
-        const int sub = lane >> 4;
-        const uint32_t rowhi = su32(kmean) + tok * 256, rowlo = rowhi + TT * 256;
+        const float4* src = reinterpret_cast<const float4*>(kmean + tq * MROWF + 32 * qi + 16 * kh);
 #pragma unroll
-        for (int s = 0; s < 8; ++s) {
-          const int c = (2 * s + sub) ^ (tok & 7);
-          uint32_t ah[4], al[4];
-          ldsm_x4(ah, rowhi + c * 16);
-          ldsm_x4(al, rowlo + c * 16);
-          mma(acc, ah, bq[j][s][0], bq[j][s][1]);
-          mma(acc, al, bq[j][s][0], bq[j][s][1]);
+        for (int u = 0; u < 4; ++u) {
+          const float4 v = src[u];
+          x[4 * u] = v.x; x[4 * u + 1] = v.y; x[4 * u + 2] = v.z; x[4 * u + 3] = v.w;
         }
       }
-      const int t_r = 16 * mt + r, t_r8 = t_r + 8;
-      const int g0 = 8 * nt + 2 * qi, g1 = g0 + 1;
-      const int h0 = g0 / G, h1 = g1 / G;
-      const float qs0 = qsum[g0], qs1 = qsum[g1];
-      const int hfirst = (8 * nt) / G, hlast = (8 * nt + 7) / G;
-      constexpr int WPR = BITS == 8 ? 8 : (BITS == 4 ? 4 : 2);  // code words per (token, head) per thread
-      for (int h = hfirst; h <= hlast; ++h) {
-        uint32_t wr[WPR], wr8[WPR];
-        const uint8_t* cr = kcodes + (t_r * H + h) * gb + (32 * qi * BITS) / 8;
-        const uint8_t* cr8 = kcodes + (t_r8 * H + h) * gb + (32 * qi * BITS) / 8;
 #pragma unroll
-        for (int w = 0; w < WPR; w += 2) {
-          const uint2 x = *reinterpret_cast<const uint2*>(cr + 4 * w);
-          const uint2 y = *reinterpret_cast<const uint2*>(cr8 + 4 * w);
-          wr[w] = x.x; wr[w + 1] = x.y; wr8[w] = y.x; wr8[w + 1] = y.y;
+      for (int k4 = 0; k4 < 4; ++k4) {
+        const int rb = slot_base<BITS>(k4), o1 = slot_off1<BITS>();  // == slot_base(4kh+k4) - 16kh
+        uint32_t h0, l0, h1, l1;
+        split_h2(x[rb], x[rb + o1], h0, l0);
+        split_h2(x[rb + 1], x[rb + o1 + 1], h1, l1);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          mma(acc[mt], qa[mt][k4], h0, h1);
+          mma(acc[mt], qa[mt][k4], l0, l1);
         }
+      }
+      // code term, one kv head at a time; fold -scale*C (and -min*sum(q) once, k-half 0)
+      const int tc0 = 8 * (warp >> 1) + 2 * qi;  // accumulator columns (tokens) tc0, tc0+1
+      for (int h = 0; h < H; ++h) {
+        constexpr int NW = BITS == 8 ? 4 : (BITS == 4 ? 2 : 1);
+        uint32_t w[NW];
+        const uint8_t* cp = kcodes + tq * pl.crow + h * gb + ((32 * qi + 16 * kh) * BITS) / 8;
+        if (NW == 4) {
+          const uint4 v = *reinterpret_cast<const uint4*>(cp);
+          w[0] = v.x; w[1] = v.y; w[2 % NW] = v.z; w[3 % NW] = v.w;
+        } else if (NW == 2) {
+          const uint2 v = *reinterpret_cast<const uint2*>(cp);
+          w[0] = v.x; w[1 % NW] = v.y;
+        } else {
+          w[0] = *reinterpret_cast<const uint32_t*>(cp);
+        }
+        const int mth = (h * G) / 16;
         float cacc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int s = 0; s < 8; ++s) {
-          uint32_t af[4];
-          qk_code_pair<BITS>(wr, s, af[0], af[2]);
-          qk_code_pair<BITS>(wr8, s, af[1], af[3]);
-          mma(cacc, af, bq[j][s][0], bq[j][s][1]);
+        for (int k4 = 0; k4 < 4; ++k4) {
+          uint32_t b0, b1;
+          qk_code_pair<BITS>(w, k4, b0, b1);
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt)
+            if (mt == mth) mma(cacc, qa[mt][k4], b0, b1);
         }
-        const float2 m_r = kmeta[t_r * H + h], m_r8 = kmeta[t_r8 * H + h];
-        if (h0 == h) {
-          acc[0] = fmaf(-m_r.x, cacc[0], fmaf(-m_r.y, qs0, acc[0]));
-          acc[2] = fmaf(-m_r8.x, cacc[2], fmaf(-m_r8.y, qs0, acc[2]));
-        }
-        if (h1 == h) {
-          acc[1] = fmaf(-m_r.x, cacc[1], fmaf(-m_r.y, qs1, acc[1]));
-          acc[3] = fmaf(-m_r8.x, cacc[3], fmaf(-m_r8.y, qs1, acc[3]));
+        const float2 ma = *reinterpret_cast<const float2*>(kmeta + tc0 * pl.trow + h * 8);
+        const float2 mb = *reinterpret_cast<const float2*>(kmeta + (tc0 + 1) * pl.trow + h * 8);
+        const int g0 = 16 * mth + r, g1 = g0 + 8;
+        const float mna = kh == 0 ? ma.y : 0.f, mnb = kh == 0 ? mb.y : 0.f;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          if (mt != mth) continue;
+          if (g0 < HQ && g0 / G == h) {
+            const float qs = qsum[g0];
+            acc[mt][0] = fmaf(-ma.x, cacc[0], fmaf(-mna, qs, acc[mt][0]));
+            acc[mt][1] = fmaf(-mb.x, cacc[1], fmaf(-mnb, qs, acc[mt][1]));
+          }
+          if (g1 < HQ && g1 / G == h) {
+            const float qs = qsum[g1];
+            acc[mt][2] = fmaf(-ma.x, cacc[2], fmaf(-mna, qs, acc[mt][2]));
+            acc[mt][3] = fmaf(-mb.x, cacc[3], fmaf(-mnb, qs, acc[mt][3]));
+          }
         }
       }
-      const float ninf = -__int_as_float(0x7f800000);
-      sbuf[g0 * SROW + t_r] = t_r < nv ? acc[0] * scale : ninf;
-      sbuf[g1 * SROW + t_r] = t_r < nv ? acc[1] * scale : ninf;
-      sbuf[g0 * SROW + t_r8] = t_r8 < nv ? acc[2] * scale : ninf;
-      sbuf[g1 * SROW + t_r8] = t_r8 < nv ? acc[3] * scale : ninf;
+      float* sb = sbuf + kh * HQ * SROW;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int g0 = 16 * mt + r, g1 = g0 + 8;
+        if (g0 < HQ) *reinterpret_cast<float2*>(sb + g0 * SROW + tc0) = make_float2(acc[mt][0], acc[mt][1]);
+        if (g1 < HQ) *reinterpret_cast<float2*>(sb + g1 * SROW + tc0) = make_float2(acc[mt][2], acc[mt][3]);
+      }
     }
     consumer_sync();
 
-    // ---------------------------------------------------------------- 3. online softmax
+    // ---------------------------------------------------------------- online softmax
     {
       float x[TPT];
       float tmax = -__int_as_float(0x7f800000);
 #pragma unroll
       for (int u = 0; u < TPT; ++u) {
-        x[u] = sbuf[sg * SROW + spart * TPT + u];
+        const int t = spart + TPH * u;
+        x[u] = t < nv ? (sbuf[sg * SROW + t] + sbuf[(HQ + sg) * SROW + t]) * scale_log2 : -__int_as_float(0x7f800000);
         tmax = fmaxf(tmax, x[u]);
       }
 #pragma unroll
       for (int o = TPH / 2; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
-      const float m_new = fmaxf(m_run, tmax);
-      const float corr = exp2f((m_run - m_new) * LOG2E);
+      const float m_new = fmaxf(m_run, tmax);  // in log2 units
+      const float corr = exp2f(m_run - m_new);
       m_run = m_new;
       float lsum = 0.f, bsum = 0.f;
 #pragma unroll
       for (int u = 0; u < TPT; ++u) {
-        const int t = spart * TPT + u;
-        const float p = exp2f((x[u] - m_new) * LOG2E);
-        const float2 vm = t < nv ? vmeta[t * H + sh] : make_float2(0.f, 0.f);
+        const int t = spart + TPH * u;
+        const float p = exp2f(x[u] - m_new);
+        const float2 vm = t < nv ? *reinterpret_cast<const float2*>(vmeta + t * pl.trow + sh * 8) : make_float2(0.f, 0.f);
         lsum += p;
         bsum = fmaf(p, vm.y, bsum);
         pbuf[sg * PROW + t] = __float2half_rn(p);
@@ -451,151 +438,134 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a) {
     }
     consumer_sync();
 
-    // ---------------------------------------------------------------- 4. PV
+    // ---------------------------------------------------------------- PV (warp = 16-wide d slice)
+    {
 #pragma unroll
-    for (int j = 0; j < IPW; ++j) {
-      const int item = warp + j * NCW;
-      if (item >= NQK) break;
-      const int dh = item % 2, nt = item / 2;
-      const int gc0 = 8 * nt + 2 * qi;
-      const float c0 = corr_s[gc0], c1 = corr_s[gc0 + 1];
+      for (int mt = 0; mt < MT; ++mt) {
+        const int g0 = 16 * mt + r, g1 = g0 + 8;
+        const float c0 = g0 < HQ ? corr_s[g0] : 0.f, c1 = g1 < HQ ? corr_s[g1] : 0.f;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        oacc[j][k][0] *= c0;
-        oacc[j][k][1] *= c1;
-        oacc[j][k][2] *= c0;
-        oacc[j][k][3] *= c1;
+        for (int n2 = 0; n2 < 2; ++n2) {
+          oacc[mt][n2][0] *= c0;
+          oacc[mt][n2][1] *= c0;
+          oacc[mt][n2][2] *= c1;
+          oacc[mt][n2][3] *= c1;
+        }
       }
-      const int gb_row = 8 * nt + r;  // B column (q head) of this thread
-      const int hcol = gb_row / G;
-      const int hfirst = (8 * nt) / G, hlast = (8 * nt + 7) / G;
+      const int dcol = 16 * warp + 2 * r;  // B column r <-> d = dcol (n-tile 0), dcol + 1 (n-tile 1)
 #pragma unroll
-      for (int ks = 0; ks < TT / 16; ++ks) {
-        const uint32_t bp0 = *reinterpret_cast<const uint32_t*>(pbuf + gb_row * PROW + 16 * ks + 2 * qi);
-        const uint32_t bp1 = *reinterpret_cast<const uint32_t*>(pbuf + gb_row * PROW + 16 * ks + 2 * qi + 8);
-        const uint32_t bq0 = *reinterpret_cast<const uint32_t*>(p2buf + gb_row * PROW + 16 * ks + 2 * qi);
-        const uint32_t bq1 = *reinterpret_cast<const uint32_t*>(p2buf + gb_row * PROW + 16 * ks + 2 * qi + 8);
-        // mean term: ldmatrix.trans of the converted vmean (rows = d, cols = tokens)
+      for (int k2 = 0; k2 < TT / 16; ++k2) {
+        const int ta = 16 * k2 + 2 * qi;  // this thread's B rows: tokens ta, ta+1, ta+8, ta+9
+        // mean term
+        uint32_t bh[2][2], bl[2][2];
         {
-          const int mat = lane >> 3;
-          const int tok = 16 * ks + (lane & 7) + 8 * (mat >> 1);
-          const uint32_t rowhi = su32(vmean) + tok * 256, rowlo = rowhi + TT * 256;
+          const float2 xa = *reinterpret_cast<const float2*>(vmean + ta * MROWF + dcol);
+          const float2 xb = *reinterpret_cast<const float2*>(vmean + (ta + 1) * MROWF + dcol);
+          const float2 xc = *reinterpret_cast<const float2*>(vmean + (ta + 8) * MROWF + dcol);
+          const float2 xd = *reinterpret_cast<const float2*>(vmean + (ta + 9) * MROWF + dcol);
+          split_h2(xa.x, xb.x, bh[0][0], bl[0][0]);
+          split_h2(xc.x, xd.x, bh[0][1], bl[0][1]);
+          split_h2(xa.y, xb.y, bh[1][0], bl[1][0]);
+          split_h2(xc.y, xd.y, bh[1][1], bl[1][1]);
+        }
+        uint32_t pa[MT][4], p2[MT][4];
+        {
+          const int mrow = (lane & 7) + 8 * ((lane >> 3) & 1), tcol = 16 * k2 + 8 * (lane >> 4);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int c = (8 * dh + 2 * k + (mat & 1)) ^ (tok & 7);
-            uint32_t ah[4], al[4];
-            ldsm_x4_t(ah, rowhi + c * 16);
-            ldsm_x4_t(al, rowlo + c * 16);
-            mma(oacc[j][k], ah, bp0, bp1);
-            mma(oacc[j][k], al, bp0, bp1);
+          for (int mt = 0; mt < MT; ++mt) {
+            const int g = 16 * mt + mrow;
+            ldsm_x4(pa[mt], su32(pbuf + g * PROW + tcol));
+            ldsm_x4(p2[mt], su32(p2buf + g * PROW + tcol));
           }
         }
-        // code term, one kv head at a time, B = -p*vscale masked to that head's columns
-        const int ta = 16 * ks + 2 * qi, tb = ta + 1, tc = ta + 8, td = ta + 9;
-        for (int h = hfirst; h <= hlast; ++h) {
-          const uint32_t m0 = hcol == h ? bq0 : 0u, m1 = hcol == h ? bq1 : 0u;
-          uint32_t af[4][4];
-          if (BITS == 4) {
-            const int off = 32 * dh + 4 * r;
-            const uint32_t wa = *reinterpret_cast<const uint32_t*>(vcodes + (ta * H + h) * gb + off);
-            const uint32_t wb = *reinterpret_cast<const uint32_t*>(vcodes + (tb * H + h) * gb + off);
-            const uint32_t wc = *reinterpret_cast<const uint32_t*>(vcodes + (tc * H + h) * gb + off);
-            const uint32_t wd = *reinterpret_cast<const uint32_t*>(vcodes + (td * H + h) * gb + off);
-            const uint32_t x01 = prmt(wa, wb, 0x5410u), y01 = prmt(wa, wb, 0x7632u);
-            const uint32_t x23 = prmt(wc, wd, 0x5410u), y23 = prmt(wc, wd, 0x7632u);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint32_t u01 = k < 2 ? x01 : y01, u23 = k < 2 ? x23 : y23;
-              const int shf = 8 * (k & 1);
-              af[k][0] = ints_to_h2((u01 >> shf) & 0x000F000Fu);
-              af[k][1] = ints_to_h2((u01 >> (shf + 4)) & 0x000F000Fu);
-              af[k][2] = ints_to_h2((u23 >> shf) & 0x000F000Fu);
-              af[k][3] = ints_to_h2((u23 >> (shf + 4)) & 0x000F000Fu);
-            }
-          } else if (BITS == 2) {
-            const int off = 16 * dh + 2 * r;
-            const uint32_t wa = *reinterpret_cast<const uint16_t*>(vcodes + (ta * H + h) * gb + off);
-            const uint32_t wb = *reinterpret_cast<const uint16_t*>(vcodes + (tb * H + h) * gb + off);
-            const uint32_t wc = *reinterpret_cast<const uint16_t*>(vcodes + (tc * H + h) * gb + off);
-            const uint32_t wd = *reinterpret_cast<const uint16_t*>(vcodes + (td * H + h) * gb + off);
-            const uint32_t x01 = wa | (wb << 16), x23 = wc | (wd << 16);
+        for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              af[k][0] = ints_to_h2((x01 >> (4 * k)) & 0x00030003u);
-              af[k][1] = ints_to_h2((x01 >> (4 * k + 2)) & 0x00030003u);
-              af[k][2] = ints_to_h2((x23 >> (4 * k)) & 0x00030003u);
-              af[k][3] = ints_to_h2((x23 >> (4 * k + 2)) & 0x00030003u);
-            }
-          } else {
-            const int off = 64 * dh + 8 * r;
-            const uint2 wa = *reinterpret_cast<const uint2*>(vcodes + (ta * H + h) * gb + off);
-            const uint2 wb = *reinterpret_cast<const uint2*>(vcodes + (tb * H + h) * gb + off);
-            const uint2 wc = *reinterpret_cast<const uint2*>(vcodes + (tc * H + h) * gb + off);
-            const uint2 wd = *reinterpret_cast<const uint2*>(vcodes + (td * H + h) * gb + off);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              // offsets 2k (row r) and 2k+1 (row r+8) live in word k/2, bytes (2k)%4 and (2k+1)%4
-              const uint32_t a01 = k < 2 ? wa.x : wa.y, b01 = k < 2 ? wb.x : wb.y;
-              const uint32_t a23 = k < 2 ? wc.x : wc.y, b23 = k < 2 ? wd.x : wd.y;
-              const uint32_t n0 = (2 * k) & 3, n1 = n0 + 1;
-              const uint32_t s0 = n0 | (n0 << 4) | ((4 + n0) << 8) | ((4 + n0) << 12);
-              const uint32_t s1 = n1 | (n1 << 4) | ((4 + n1) << 8) | ((4 + n1) << 12);
-              af[k][0] = ints_to_h2(prmt(a01, b01, s0) & 0x00FF00FFu);
-              af[k][1] = ints_to_h2(prmt(a01, b01, s1) & 0x00FF00FFu);
-              af[k][2] = ints_to_h2(prmt(a23, b23, s0) & 0x00FF00FFu);
-              af[k][3] = ints_to_h2(prmt(a23, b23, s1) & 0x00FF00FFu);
+          for (int n2 = 0; n2 < 2; ++n2) {
+            mma(oacc[mt][n2], pa[mt], bh[n2][0], bh[n2][1]);
+            mma(oacc[mt][n2], pa[mt], bl[n2][0], bl[n2][1]);
+          }
+        // code term per kv head, A = P' restricted to that head's rows
+        for (int h = 0; h < H; ++h) {
+          const int mth = (h * G) / 16;
+          uint32_t bc[2][2];
+          {
+            const uint8_t* ca = vcodes + ta * pl.crow + h * gb;
+            const int cs = pl.crow;
+            uint32_t xa, xb, xc, xd;
+            if (BITS == 4) {  // d = dcol, dcol+1 -> one byte (lo, hi nibble)
+              const int off = dcol >> 1;
+              xa = ca[off]; xb = ca[cs + off]; xc = ca[8 * cs + off]; xd = ca[9 * cs + off];
+              const uint32_t u = xa | (xb << 16), v = xc | (xd << 16);
+              bc[0][0] = ints_to_h2(u & 0x000F000Fu);
+              bc[1][0] = ints_to_h2((u >> 4) & 0x000F000Fu);
+              bc[0][1] = ints_to_h2(v & 0x000F000Fu);
+              bc[1][1] = ints_to_h2((v >> 4) & 0x000F000Fu);
+            } else if (BITS == 2) {  // d = dcol, dcol+1 -> 4 bits at bit 2*dcol
+              const int off = dcol >> 2, sft = (dcol & 3) * 2;
+              xa = ca[off] >> sft; xb = ca[cs + off] >> sft; xc = ca[8 * cs + off] >> sft; xd = ca[9 * cs + off] >> sft;
+              const uint32_t u = (xa & 0xFu) | ((xb & 0xFu) << 16), v = (xc & 0xFu) | ((xd & 0xFu) << 16);
+              bc[0][0] = ints_to_h2(u & 0x00030003u);
+              bc[1][0] = ints_to_h2((u >> 2) & 0x00030003u);
+              bc[0][1] = ints_to_h2(v & 0x00030003u);
+              bc[1][1] = ints_to_h2((v >> 2) & 0x00030003u);
+            } else {  // two bytes
+              xa = *reinterpret_cast<const uint16_t*>(ca + dcol);
+              xb = *reinterpret_cast<const uint16_t*>(ca + cs + dcol);
+              xc = *reinterpret_cast<const uint16_t*>(ca + 8 * cs + dcol);
+              xd = *reinterpret_cast<const uint16_t*>(ca + 9 * cs + dcol);
+              const uint32_t u = xa | (xb << 16), v = xc | (xd << 16);
+              bc[0][0] = ints_to_h2(u & 0x00FF00FFu);
+              bc[1][0] = ints_to_h2((u >> 8) & 0x00FF00FFu);
+              bc[0][1] = ints_to_h2(v & 0x00FF00FFu);
+              bc[1][1] = ints_to_h2((v >> 8) & 0x00FF00FFu);
             }
           }
 #pragma unroll
-          for (int k = 0; k < 4; ++k) mma(oacc[j][k], af[k], m0, m1);
+          for (int mt = 0; mt < MT; ++mt) {
+            if (mt != mth) continue;
+            const int g0 = 16 * mt + r, g1 = g0 + 8;
+            const bool k0 = g0 < HQ && g0 / G == h, k1 = g1 < HQ && g1 / G == h;
+            uint32_t am[4] = {k0 ? p2[mt][0] : 0u, k1 ? p2[mt][1] : 0u, k0 ? p2[mt][2] : 0u, k1 ? p2[mt][3] : 0u};
+            mma(oacc[mt][0], am, bc[0][0], bc[0][1]);
+            mma(oacc[mt][1], am, bc[1][0], bc[1][1]);
+          }
         }
       }
     }
-    // release the stage: generic-proxy writes (in-place conversion) must be ordered
-    // before the next async-proxy bulk copy into this buffer.
-    fence_proxy_async();
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stg]);
   }
 
   // ------------------------------------------------------------------ epilogue
-  {
 #pragma unroll
-    for (int o = TPH / 2; o > 0; o >>= 1) {
-      l_part += __shfl_xor_sync(0xffffffffu, l_part, o);
-      bp_part += __shfl_xor_sync(0xffffffffu, bp_part, o);
-    }
-    if (spart == 0) {
-      stats[4 * sg + 0] = m_run;
-      stats[4 * sg + 1] = l_part;
-      stats[4 * sg + 2] = bp_part;
-    }
+  for (int o = TPH / 2; o > 0; o >>= 1) {
+    l_part += __shfl_xor_sync(0xffffffffu, l_part, o);
+    bp_part += __shfl_xor_sync(0xffffffffu, bp_part, o);
+  }
+  if (spart == 0) {
+    stats[4 * sg + 0] = m_run;
+    stats[4 * sg + 1] = l_part;
+    stats[4 * sg + 2] = bp_part;
   }
   consumer_sync();
+  const float LN2 = 0.6931471805599453f;
 #pragma unroll
-  for (int j = 0; j < IPW; ++j) {
-    const int item = warp + j * NCW;
-    if (item >= NQK) break;
-    const int dh = item % 2, nt = item / 2;
-    const int g0 = 8 * nt + 2 * qi;
+  for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      const int g = g0 + e;
+      const int g = 16 * mt + r + 8 * e;
+      if (g >= HQ) continue;
       const float m = stats[4 * g], l = stats[4 * g + 1], bp = stats[4 * g + 2];
-      float* pa = a.part_acc + ((int64_t(b) * HQ + g) * a.slots + split) * D;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int d = 64 * dh + 8 * r + 2 * k;
-        // rows r (d) and r+8 (d+1): elements e and e+2 of the accumulator
-        *reinterpret_cast<float2*>(pa + d) = make_float2(oacc[j][k][e] - bp, oacc[j][k][e + 2] - bp);
-      }
-      if (dh == 0 && r == 0) {
+      float* pa = a.part_acc + ((int64_t(b) * HQ + g) * a.slots + split) * D + 16 * warp + 4 * qi;
+      *reinterpret_cast<float4*>(pa) = make_float4(oacc[mt][0][2 * e] - bp, oacc[mt][1][2 * e] - bp,
+                                                   oacc[mt][0][2 * e + 1] - bp, oacc[mt][1][2 * e + 1] - bp);
+      if (warp == 0 && qi == 0) {
         float* ml = a.part_ml + ((int64_t(b) * HQ + g) * a.slots + split) * 2;
-        ml[0] = l > 0.f ? m : -__int_as_float(0x7f800000);
+        ml[0] = l > 0.f ? m * LN2 : -__int_as_float(0x7f800000);  // back to natural-log units for K3
         ml[1] = l;
       }
     }
-  }
 }
 
 }  // namespace fast
@@ -677,7 +647,7 @@ bool fast_supported(const tada_page_layout& L, int Hq) {
   if (!(Hq == 8 || Hq == 16 || Hq == 32 || Hq == 64) || Hq % L.heads) return false;
   const int G = Hq / L.heads;
   if (!(G == 1 || G == 2 || G == 4 || G == 8)) return false;
-  if (L.page_tokens % fast::TT) return false;
+  if (L.page_tokens % fast::TT || L.heads > 32) return false;
   return fast::make_plan(L.heads, L.group_bytes, Hq).total <= 227 * 1024;
 }
 
