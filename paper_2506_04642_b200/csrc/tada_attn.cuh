@@ -1,6 +1,8 @@
 // Shared declarations between the decode-attention translation units.
 #pragma once
 
+#include <cuda.h>
+
 #include "tada_common.cuh"
 
 namespace tada {
@@ -39,6 +41,11 @@ __device__ __forceinline__ void split_range(int n, int splits, int s, int align,
   t0 = min(n, s * chunk);
   t1 = min(n, t0 + chunk);
 }
+
+// TMA descriptors of one layer pool: [side][region] with region 0 = means, 1 = codes, 2 = scale/min.
+struct alignas(64) TmaMaps {
+  CUtensorMap m[2][3];
+};
 
 // Fast path (tensor-core grouped-head contraction); returns TADA_ERR_CONFIG if the
 // geometry is unsupported so the caller can fall back to the generic kernel.

@@ -19,7 +19,11 @@
 //   3. PV (warp = 16 of head_dim): O[g, d] += P·vmean + P'_h·vcode_h, one f32 accumulator.
 #include <cuda_runtime.h>
 
+#include <cudaTypedefs.h>
+
+#include <mutex>
 #include <string>
+#include <unordered_map>
 
 #include "tada_attn.cuh"
 
@@ -141,37 +145,41 @@ __device__ __forceinline__ void qk_code_pair(const uint32_t* w, int s, uint32_t&
 }
 
 // ------------------------------------------------------------------ shared memory plan
-// One bulk copy per token row, with bank-shifting pads so every fragment load below is
-// (near) conflict-free: mean rows D*4 + 16 B (4-bank shift per token), code rows
-// H*gb + 32 B (8-bank shift), scale/min rows up16(H*8) + 16 B.
+// A stage holds one 32-token tile of both sides, loaded with 3-D TMA tensor copies
+// (cp.async.bulk.tensor, UTMALDG) from the paged pool:
+//   mean  : 4 bands of [32 rows x 128 B], 128B-swizzled  (D*4 = 512 B per row)
+//   codes : H*gb/128 bands of [32 rows x 128 B], 128B-swizzled
+//   meta  : one box [32 rows x TROW B] (TROW = H*8 + 16: the 16 B past the row are the
+//           TMA's out-of-bounds zero fill, which shifts banks by 4 per row)
+// so every fragment load below is bank-conflict free or at the minimum wavefront count.
+constexpr int BAND = TT * 128;  // bytes per 128-byte-wide band of a tile
+
 struct Plan {
-  int H, gb;
-  int mrow, crow, trow, tcopy;  // row strides (bytes) and the meta copy size
+  int H, gb, trow, nbands_c;
   int mean_bytes, codes_bytes, meta_bytes, side_bytes, stage_bytes, stages;
   int off_work, off_sbuf, off_pbuf, off_p2buf, off_qsum, off_corr, off_stats, off_bar, total;
 };
 
 __host__ __device__ inline int up128(int x) { return (x + 127) / 128 * 128; }
+__host__ __device__ inline int up1k(int x) { return (x + 1023) / 1024 * 1024; }
 
 __host__ __device__ inline Plan make_plan(int H, int gb, int HQ) {
   Plan p{};
   p.H = H;
   p.gb = gb;
-  p.mrow = D * 4 + 16;
-  p.crow = H * gb + 32;
-  p.tcopy = (H * 8 + 15) / 16 * 16;
-  p.trow = p.tcopy + 16;
-  p.mean_bytes = up128(TT * p.mrow);
-  p.codes_bytes = up128(TT * p.crow);
-  p.meta_bytes = up128(TT * p.trow);
+  p.trow = H * 8 + 16;
+  p.nbands_c = (H * gb) / 128;
+  p.mean_bytes = (D * 4 / 128) * BAND;
+  p.codes_bytes = p.nbands_c * BAND;
+  p.meta_bytes = up1k(TT * p.trow);
   p.side_bytes = p.mean_bytes + p.codes_bytes + p.meta_bytes;
   p.stage_bytes = 2 * p.side_bytes;
-  // work area: logits (2 k-halves) + P + P'; doubles as the f16 q staging area in the prologue
   const int work0 = up128(2 * HQ * SROW * 4) + 2 * up128(HQ * PROW * 2);
   const int q16 = ((HQ + 15) / 16) * 16 * D * 2;  // f16 q staging (prologue only)
   const int work = work0 > q16 ? work0 : q16;
-  const int tail = work + up128(HQ * 4) * 2 + up128(HQ * 16) + 128;
-  p.stages = (3 * p.stage_bytes + tail <= 227 * 1024) ? 3 : STAGES;
+  const int tail = work + up128(HQ * 4) * 2 + up128(HQ * 16) + 128 + 1024;  // + 1 KB alignment slack
+  const int budget = 227 * 1024;
+  p.stages = (3 * p.stage_bytes + tail <= budget) ? 3 : ((2 * p.stage_bytes + tail <= budget) ? 2 : 1);
   int off = p.stages * p.stage_bytes;
   p.off_work = off;
   p.off_sbuf = off;
@@ -179,7 +187,6 @@ __host__ __device__ inline Plan make_plan(int H, int gb, int HQ) {
   p.off_pbuf = off;
   off += up128(HQ * PROW * 2);
   p.off_p2buf = off;
-  off += up128(HQ * PROW * 2);
   off = p.off_work + work;
   p.off_qsum = off;
   off += up128(HQ * 4);
@@ -189,8 +196,19 @@ __host__ __device__ inline Plan make_plan(int H, int gb, int HQ) {
   off += up128(HQ * 16);
   p.off_bar = off;
   off += 128;
-  p.total = off;
+  p.total = off + 1024;
   return p;
+}
+
+// byte offset of (row t, byte o) inside a 128B-swizzled [TT x 128 B] band
+__device__ __forceinline__ int swz(int t, int o) { return t * 128 + ((((o >> 4) ^ t) & 7) << 4) + (o & 15); }
+
+__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
+      : "memory");
 }
 
 // ------------------------------------------------------------------ the kernel
@@ -199,12 +217,12 @@ __host__ __device__ inline Plan make_plan(int H, int gb, int HQ) {
 //   PV: O[g, d] = P[g, t] · V̂[t, d]      A = P, P' (smem, ldmatrix), B = V-mean / V-codes tiles
 // so every mean and code byte of a tile is read from smem by exactly one warp.
 template <int BITS, int HQ>
-__global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem[];
+__global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __grid_constant__ TmaMaps maps) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int MT = (HQ + 15) / 16;    // m-tiles of 16 q heads
   constexpr int TPH = (NCW * 32) / HQ;  // softmax threads per q head
   constexpr int TPT = TT / TPH;         // tokens per softmax thread
-  constexpr int MROWF = (D * 4 + 16) / 4;  // mean row stride in floats
   const int H = a.L.heads, G = HQ / H, gb = a.L.group_bytes, P = a.L.page_tokens;
   const Plan pl = make_plan(H, gb, HQ);
   const int b = blockIdx.y, split = blockIdx.x;
@@ -235,30 +253,29 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a) {
   __syncthreads();
 
   if (warp == NCW) {
-    // ================================================================ producer: one bulk copy per row
-    const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
-    const uint32_t cbytes = H * gb;
-    for (int it = 0; it < ntiles; ++it) {
-      const int stg = it % S;
-      if (it >= S) mbar_wait(&empty[stg], ((it / S) - 1) & 1);
-      const int t0 = t_begin + it * TT;
-      const int nv = min(TT, t_end - t0);
-      const uint8_t* page = a.pool + int64_t(pt[t0 / P]) * a.L.page_bytes;
-      const int row0 = t0 % P;
-      uint8_t* dst = smem + stg * pl.stage_bytes;
-      if (lane == 0) mbar_expect_tx(&full[stg], uint32_t(nv) * 2u * (D * 4 + cbytes + pl.tcopy));
-      __syncwarp();
-      for (int j = lane; j < 6 * nv; j += 32) {
-        const int side = j / (3 * nv), rem = j - side * 3 * nv, reg = rem / nv, tk = rem - reg * nv;
-        uint8_t* d0 = dst + side * pl.side_bytes;
-        const int64_t row = row0 + tk;
-        if (reg == 0)
-          bulk_g2s(d0 + tk * pl.mrow, page + a.L.off_mean[side] + row * (D * 4), D * 4, &full[stg]);
-        else if (reg == 1)
-          bulk_g2s(d0 + pl.mean_bytes + tk * pl.crow, page + a.L.off_codes[side] + row * cbytes, cbytes, &full[stg]);
-        else
-          bulk_g2s(d0 + pl.mean_bytes + pl.codes_bytes + tk * pl.trow, page + a.L.off_meta[side] + row * (H * 8),
-                   pl.tcopy, &full[stg]);
+    // ================================================================ producer: TMA tensor copies
+    if (lane == 0) {
+      const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
+      for (int s = 0; s < 2; ++s)
+        for (int k = 0; k < 3; ++k)
+          asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[s][k])) : "memory");
+      const uint32_t tx = 2u * uint32_t(pl.mean_bytes + pl.codes_bytes + TT * pl.trow);
+      for (int it = 0; it < ntiles; ++it) {
+        const int stg = it % S;
+        if (it >= S) mbar_wait(&empty[stg], ((it / S) - 1) & 1);
+        const int t0 = t_begin + it * TT;
+        const int page = pt[t0 / P];
+        const int row0 = t0 % P;
+        uint8_t* dst = smem + stg * pl.stage_bytes;
+        mbar_expect_tx(&full[stg], tx);
+        for (int side = 0; side < 2; ++side) {
+          uint8_t* d0 = dst + side * pl.side_bytes;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) tma_3d(d0 + j * BAND, &maps.m[side][0], 128 * j, row0, page, &full[stg]);
+          for (int j = 0; j < pl.nbands_c; ++j)
+            tma_3d(d0 + pl.mean_bytes + j * BAND, &maps.m[side][1], 128 * j, row0, page, &full[stg]);
+          tma_3d(d0 + pl.mean_bytes + pl.codes_bytes, &maps.m[side][2], 0, row0, page, &full[stg]);
+        }
       }
     }
     return;
@@ -300,6 +317,13 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a) {
         qa[mt][k4][3] = q2(g1, 2, 3);
       }
   }
+  // kv head of this thread's accumulator rows (16mt + r, 16mt + r + 8); -1 = padding row
+  int kvr[MT][2];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    kvr[mt][0] = 16 * mt + r < HQ ? (16 * mt + r) / G : -1;
+    kvr[mt][1] = 16 * mt + r + 8 < HQ ? (16 * mt + r + 8) / G : -1;
+  }
   float oacc[MT][2][4];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt)
@@ -318,27 +342,25 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a) {
     const int nv = min(TT, t_end - t0);
     mbar_wait(&full[stg], (it / S) & 1);
     const uint8_t* base = smem + stg * pl.stage_bytes;
-    const float* kmean = reinterpret_cast<const float*>(base);
+    const uint8_t* kmean = base;
     const uint8_t* kcodes = base + pl.mean_bytes;
     const uint8_t* kmeta = base + pl.mean_bytes + pl.codes_bytes;
-    const float* vmean = reinterpret_cast<const float*>(base + pl.side_bytes);
-    const uint8_t* vcodes = base + pl.side_bytes + pl.mean_bytes;
-    const uint8_t* vmeta = base + pl.side_bytes + pl.mean_bytes + pl.codes_bytes;
+    const uint8_t* vmean = base + pl.side_bytes;
+    const uint8_t* vcodes = vmean + pl.mean_bytes;
+    const uint8_t* vmeta = vmean + pl.mean_bytes + pl.codes_bytes;
 
     // ---------------------------------------------------------------- QK (warp = token octet x k-half)
+    const int tc0 = 8 * (warp >> 1) + 2 * qi;  // accumulator columns (tokens) tc0, tc0+1
     {
       float acc[MT][4];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
-      // mean term: this thread's 16 contiguous d of token tq, converted to f16 hi/lo B fragments
+      // mean term: d = 32qi + 16kh + [0,16) of token tq = band qi, bytes 64kh + [0,64)
       float x[16];
-      {
-        const float4* src = reinterpret_cast<const float4*>(kmean + tq * MROWF + 32 * qi + 16 * kh);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float4 v = src[u];
-          x[4 * u] = v.x; x[4 * u + 1] = v.y; x[4 * u + 2] = v.z; x[4 * u + 3] = v.w;
-        }
+      for (int u = 0; u < 4; ++u) {
+        const float4 v = *reinterpret_cast<const float4*>(kmean + qi * BAND + swz(tq, 64 * kh + 16 * u));
+        x[4 * u] = v.x; x[4 * u + 1] = v.y; x[4 * u + 2] = v.z; x[4 * u + 3] = v.w;
       }
 #pragma unroll
       for (int k4 = 0; k4 < 4; ++k4) {
@@ -353,11 +375,11 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a) {
         }
       }
       // code term, one kv head at a time; fold -scale*C (and -min*sum(q) once, k-half 0)
-      const int tc0 = 8 * (warp >> 1) + 2 * qi;  // accumulator columns (tokens) tc0, tc0+1
       for (int h = 0; h < H; ++h) {
         constexpr int NW = BITS == 8 ? 4 : (BITS == 4 ? 2 : 1);
         uint32_t w[NW];
-        const uint8_t* cp = kcodes + tq * pl.crow + h * gb + ((32 * qi + 16 * kh) * BITS) / 8;
+        const int cb = h * gb + ((32 * qi + 16 * kh) * BITS) / 8;
+        const uint8_t* cp = kcodes + (cb >> 7) * BAND + swz(tq, cb & 127);
         if (NW == 4) {
           const uint4 v = *reinterpret_cast<const uint4*>(cp);
           w[0] = v.x; w[1] = v.y; w[2 % NW] = v.z; w[3 % NW] = v.w;
@@ -367,7 +389,7 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a) {
         } else {
           w[0] = *reinterpret_cast<const uint32_t*>(cp);
         }
-        const int mth = (h * G) / 16;
+        const int mth = (h * G) >> 4;
         float cacc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int k4 = 0; k4 < 4; ++k4) {
@@ -379,18 +401,17 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a) {
         }
         const float2 ma = *reinterpret_cast<const float2*>(kmeta + tc0 * pl.trow + h * 8);
         const float2 mb = *reinterpret_cast<const float2*>(kmeta + (tc0 + 1) * pl.trow + h * 8);
-        const int g0 = 16 * mth + r, g1 = g0 + 8;
         const float mna = kh == 0 ? ma.y : 0.f, mnb = kh == 0 ? mb.y : 0.f;
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
           if (mt != mth) continue;
-          if (g0 < HQ && g0 / G == h) {
-            const float qs = qsum[g0];
+          if (kvr[mt][0] == h) {
+            const float qs = qsum[16 * mt + r];
             acc[mt][0] = fmaf(-ma.x, cacc[0], fmaf(-mna, qs, acc[mt][0]));
             acc[mt][1] = fmaf(-mb.x, cacc[1], fmaf(-mnb, qs, acc[mt][1]));
           }
-          if (g1 < HQ && g1 / G == h) {
-            const float qs = qsum[g1];
+          if (kvr[mt][1] == h) {
+            const float qs = qsum[16 * mt + r + 8];
             acc[mt][2] = fmaf(-ma.x, cacc[2], fmaf(-mna, qs, acc[mt][2]));
             acc[mt][3] = fmaf(-mb.x, cacc[3], fmaf(-mnb, qs, acc[mt][3]));
           }
@@ -442,8 +463,8 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a) {
     {
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
-        const int g0 = 16 * mt + r, g1 = g0 + 8;
-        const float c0 = g0 < HQ ? corr_s[g0] : 0.f, c1 = g1 < HQ ? corr_s[g1] : 0.f;
+        const float c0 = kvr[mt][0] >= 0 ? corr_s[16 * mt + r] : 0.f;
+        const float c1 = kvr[mt][1] >= 0 ? corr_s[16 * mt + r + 8] : 0.f;
 #pragma unroll
         for (int n2 = 0; n2 < 2; ++n2) {
           oacc[mt][n2][0] *= c0;
@@ -453,16 +474,17 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a) {
         }
       }
       const int dcol = 16 * warp + 2 * r;  // B column r <-> d = dcol (n-tile 0), dcol + 1 (n-tile 1)
+      const int mband = (4 * dcol) >> 7, mo = (4 * dcol) & 127;
 #pragma unroll
       for (int k2 = 0; k2 < TT / 16; ++k2) {
         const int ta = 16 * k2 + 2 * qi;  // this thread's B rows: tokens ta, ta+1, ta+8, ta+9
-        // mean term
         uint32_t bh[2][2], bl[2][2];
         {
-          const float2 xa = *reinterpret_cast<const float2*>(vmean + ta * MROWF + dcol);
-          const float2 xb = *reinterpret_cast<const float2*>(vmean + (ta + 1) * MROWF + dcol);
-          const float2 xc = *reinterpret_cast<const float2*>(vmean + (ta + 8) * MROWF + dcol);
-          const float2 xd = *reinterpret_cast<const float2*>(vmean + (ta + 9) * MROWF + dcol);
+          const uint8_t* vb = vmean + mband * BAND;
+          const float2 xa = *reinterpret_cast<const float2*>(vb + swz(ta, mo));
+          const float2 xb = *reinterpret_cast<const float2*>(vb + swz(ta + 1, mo));
+          const float2 xc = *reinterpret_cast<const float2*>(vb + swz(ta + 8, mo));
+          const float2 xd = *reinterpret_cast<const float2*>(vb + swz(ta + 9, mo));
           split_h2(xa.x, xb.x, bh[0][0], bl[0][0]);
           split_h2(xc.x, xd.x, bh[0][1], bl[0][1]);
           split_h2(xa.y, xb.y, bh[1][0], bl[1][0]);
@@ -487,45 +509,38 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a) {
           }
         // code term per kv head, A = P' restricted to that head's rows
         for (int h = 0; h < H; ++h) {
-          const int mth = (h * G) / 16;
+          const int mth = (h * G) >> 4;
           uint32_t bc[2][2];
           {
-            const uint8_t* ca = vcodes + ta * pl.crow + h * gb;
-            const int cs = pl.crow;
+            // byte holding codes d = dcol, dcol+1 of row (t, h)
+            const int cbyte = h * gb + ((dcol * BITS) >> 3);
+            const uint8_t* cband = vcodes + (cbyte >> 7) * BAND;
+            const int co = cbyte & 127;
             uint32_t xa, xb, xc, xd;
-            if (BITS == 4) {  // d = dcol, dcol+1 -> one byte (lo, hi nibble)
-              const int off = dcol >> 1;
-              xa = ca[off]; xb = ca[cs + off]; xc = ca[8 * cs + off]; xd = ca[9 * cs + off];
-              const uint32_t u = xa | (xb << 16), v = xc | (xd << 16);
-              bc[0][0] = ints_to_h2(u & 0x000F000Fu);
-              bc[1][0] = ints_to_h2((u >> 4) & 0x000F000Fu);
-              bc[0][1] = ints_to_h2(v & 0x000F000Fu);
-              bc[1][1] = ints_to_h2((v >> 4) & 0x000F000Fu);
-            } else if (BITS == 2) {  // d = dcol, dcol+1 -> 4 bits at bit 2*dcol
-              const int off = dcol >> 2, sft = (dcol & 3) * 2;
-              xa = ca[off] >> sft; xb = ca[cs + off] >> sft; xc = ca[8 * cs + off] >> sft; xd = ca[9 * cs + off] >> sft;
-              const uint32_t u = (xa & 0xFu) | ((xb & 0xFu) << 16), v = (xc & 0xFu) | ((xd & 0xFu) << 16);
-              bc[0][0] = ints_to_h2(u & 0x00030003u);
-              bc[1][0] = ints_to_h2((u >> 2) & 0x00030003u);
-              bc[0][1] = ints_to_h2(v & 0x00030003u);
-              bc[1][1] = ints_to_h2((v >> 2) & 0x00030003u);
-            } else {  // two bytes
-              xa = *reinterpret_cast<const uint16_t*>(ca + dcol);
-              xb = *reinterpret_cast<const uint16_t*>(ca + cs + dcol);
-              xc = *reinterpret_cast<const uint16_t*>(ca + 8 * cs + dcol);
-              xd = *reinterpret_cast<const uint16_t*>(ca + 9 * cs + dcol);
-              const uint32_t u = xa | (xb << 16), v = xc | (xd << 16);
-              bc[0][0] = ints_to_h2(u & 0x00FF00FFu);
-              bc[1][0] = ints_to_h2((u >> 8) & 0x00FF00FFu);
-              bc[0][1] = ints_to_h2(v & 0x00FF00FFu);
-              bc[1][1] = ints_to_h2((v >> 8) & 0x00FF00FFu);
+            if (BITS == 8) {
+              xa = *reinterpret_cast<const uint16_t*>(cband + swz(ta, co));
+              xb = *reinterpret_cast<const uint16_t*>(cband + swz(ta + 1, co));
+              xc = *reinterpret_cast<const uint16_t*>(cband + swz(ta + 8, co));
+              xd = *reinterpret_cast<const uint16_t*>(cband + swz(ta + 9, co));
+            } else {
+              const int sft = BITS == 2 ? (dcol & 3) * 2 : 0;
+              xa = cband[swz(ta, co)] >> sft;
+              xb = cband[swz(ta + 1, co)] >> sft;
+              xc = cband[swz(ta + 8, co)] >> sft;
+              xd = cband[swz(ta + 9, co)] >> sft;
             }
+            constexpr uint32_t M = BITS == 8 ? 0x00FF00FFu : (BITS == 4 ? 0x000F000Fu : 0x00030003u);
+            constexpr uint32_t LO = BITS == 8 ? 0xFFFFu : (BITS == 4 ? 0xFFu : 0xFu);
+            const uint32_t u = (xa & LO) | ((xb & LO) << 16), v = (xc & LO) | ((xd & LO) << 16);
+            bc[0][0] = ints_to_h2(u & M);
+            bc[1][0] = ints_to_h2((u >> BITS) & M);
+            bc[0][1] = ints_to_h2(v & M);
+            bc[1][1] = ints_to_h2((v >> BITS) & M);
           }
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) {
             if (mt != mth) continue;
-            const int g0 = 16 * mt + r, g1 = g0 + 8;
-            const bool k0 = g0 < HQ && g0 / G == h, k1 = g1 < HQ && g1 / G == h;
+            const bool k0 = kvr[mt][0] == h, k1 = kvr[mt][1] == h;
             uint32_t am[4] = {k0 ? p2[mt][0] : 0u, k1 ? p2[mt][1] : 0u, k0 ? p2[mt][2] : 0u, k1 ? p2[mt][3] : 0u};
             mma(oacc[mt][0], am, bc[0][0], bc[0][1]);
             mma(oacc[mt][1], am, bc[1][0], bc[1][1]);
@@ -647,8 +662,78 @@ bool fast_supported(const tada_page_layout& L, int Hq) {
   if (!(Hq == 8 || Hq == 16 || Hq == 32 || Hq == 64) || Hq % L.heads) return false;
   const int G = Hq / L.heads;
   if (!(G == 1 || G == 2 || G == 4 || G == 8)) return false;
-  if (L.page_tokens % fast::TT || L.heads > 32) return false;
+  if (L.page_tokens % fast::TT || (L.heads * L.group_bytes) % 128 || (L.heads * 8) % 16) return false;
   return fast::make_plan(L.heads, L.group_bytes, Hq).total <= 227 * 1024;
+}
+
+// ---------------------------------------------------------------- TMA descriptors
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 3-D byte tensor over the pool: (byte in row, row in page, page); box = [box0 B, 32 rows, 1 page].
+static bool encode_region(CUtensorMap* m, const uint8_t* base, uint64_t row_bytes, uint64_t rows, uint64_t page_bytes,
+                          uint32_t box0, bool swizzle) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {row_bytes, rows, uint64_t(1) << 20};
+  const cuuint64_t strides[2] = {row_bytes, page_bytes};
+  const cuuint32_t box[3] = {box0, uint32_t(fast::TT), 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int get_maps(const AttnArgs& a, TmaMaps* out) {
+  struct Key {
+    const uint8_t* pool;
+    int64_t page_bytes;
+    int bits, heads, page_tokens;
+    bool operator==(const Key& o) const {
+      return pool == o.pool && page_bytes == o.page_bytes && bits == o.bits && heads == o.heads &&
+             page_tokens == o.page_tokens;
+    }
+  };
+  struct Hash {
+    size_t operator()(const Key& k) const {
+      return std::hash<const void*>()(k.pool) ^ (std::hash<int64_t>()(k.page_bytes) << 1) ^ size_t(k.bits * 131 + k.heads);
+    }
+  };
+  static std::mutex mu;
+  static std::unordered_map<Key, TmaMaps, Hash> cache;
+  const Key key{a.pool, a.L.page_bytes, a.L.bits, a.L.heads, a.L.page_tokens};
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return TADA_OK;
+  }
+  TmaMaps m{};
+  const tada_page_layout& L = a.L;
+  const uint32_t trow = uint32_t(L.heads * 8 + 16);
+  for (int side = 0; side < 2; ++side) {
+    if (!encode_region(&m.m[side][0], a.pool + L.off_mean[side], uint64_t(L.head_dim) * 4, L.page_tokens, L.page_bytes,
+                       128, true) ||
+        !encode_region(&m.m[side][1], a.pool + L.off_codes[side], uint64_t(L.heads) * L.group_bytes, L.page_tokens,
+                       L.page_bytes, 128, true) ||
+        !encode_region(&m.m[side][2], a.pool + L.off_meta[side], uint64_t(L.heads) * 8, L.page_tokens, L.page_bytes,
+                       trow, false))
+      return fail(TADA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the decode-attention pool");
+  }
+  if (cache.size() > 256) cache.clear();
+  cache.emplace(key, m);
+  *out = m;
+  return TADA_OK;
 }
 
 template <int BITS, int HQ>
@@ -661,7 +746,10 @@ static int launch_fast_t(const AttnArgs& a, int batch, cudaStream_t st) {
     if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string("attn_fast smem: ") + cudaGetErrorString(e));
     attr_set = true;
   }
-  kern<<<dim3(a.splits, batch), fast::NTHR, pl.total, st>>>(a);
+  TmaMaps maps;
+  const int rc = get_maps(a, &maps);
+  if (rc != TADA_OK) return rc;
+  kern<<<dim3(a.splits, batch), fast::NTHR, pl.total, st>>>(a, maps);
   return check_launch("decode_attn_fast");
 }
 
