@@ -219,7 +219,9 @@ __device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, int c0
 template <int BITS, int HQ>
 __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __grid_constant__ TmaMaps maps) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1 KB alignment (128B-swizzle atoms) by pointer arithmetic on the __shared__ array, so the
+  // compiler keeps the shared state space (LDS, 32-bit addressing) for every access below
+  uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   constexpr int MT = (HQ + 15) / 16;    // m-tiles of 16 q heads
   constexpr int TPH = (NCW * 32) / HQ;  // softmax threads per q head
   constexpr int TPT = TT / TPH;         // tokens per softmax thread
