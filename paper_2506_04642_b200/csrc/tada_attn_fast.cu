@@ -33,7 +33,7 @@ namespace fast {
 constexpr int D = 128;
 constexpr int TT = 32;    // tokens per tile
 constexpr int NCW = 8;    // consumer warps
-constexpr int NTHR = (NCW + 1) * 32;
+constexpr int NTHR = NCW * 32;  // no dedicated producer warp: thread 0 issues the TMA copies
 constexpr int SROW = TT + 4;  // logits row stride (floats): conflict-free fragment stores
 constexpr int PROW = TT + 8;  // P row stride (halves): conflict-free B-fragment loads
 constexpr int STAGES = 2;
@@ -66,7 +66,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NCW * 32) : "memory"); }
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NCW * 32) : "memory"); }  // all warps
 
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -151,13 +151,12 @@ __device__ __forceinline__ void qk_code_pair(const uint32_t* w, int s, uint32_t&
 //   codes : H*gb/128 bands of [32 rows x 128 B], 128B-swizzled
 //   meta  : one box [32 rows x TROW B] (TROW = H*8 + 16: the 16 B past the row are the
 //           TMA's out-of-bounds zero fill, which shifts banks by 4 per row)
-// so every fragment load below is bank-conflict free or at the minimum wavefront count.
 constexpr int BAND = TT * 128;  // bytes per 128-byte-wide band of a tile
 
 struct Plan {
   int H, gb, trow, nbands_c;
   int mean_bytes, codes_bytes, meta_bytes, side_bytes, stage_bytes, stages;
-  int off_work, off_sbuf, off_pbuf, off_p2buf, off_qsum, off_corr, off_stats, off_bar, total;
+  int off_sbuf, off_pbuf, off_p2m, off_qsum, off_corr, off_stats, off_bar, total;
 };
 
 __host__ __device__ inline int up128(int x) { return (x + 127) / 128 * 128; }
@@ -165,6 +164,7 @@ __host__ __device__ inline int up1k(int x) { return (x + 1023) / 1024 * 1024; }
 
 __host__ __device__ inline Plan make_plan(int H, int gb, int HQ) {
   Plan p{};
+  const int MT = (HQ + 15) / 16;
   p.H = H;
   p.gb = gb;
   p.trow = H * 8 + 16;
@@ -174,20 +174,21 @@ __host__ __device__ inline Plan make_plan(int H, int gb, int HQ) {
   p.meta_bytes = up1k(TT * p.trow);
   p.side_bytes = p.mean_bytes + p.codes_bytes + p.meta_bytes;
   p.stage_bytes = 2 * p.side_bytes;
-  const int work0 = up128(2 * HQ * SROW * 4) + 2 * up128(HQ * PROW * 2);
-  const int q16 = ((HQ + 15) / 16) * 16 * D * 2;  // f16 q staging (prologue only)
-  const int work = work0 > q16 ? work0 : q16;
-  const int tail = work + up128(HQ * 4) * 2 + up128(HQ * 16) + 128 + 1024;  // + 1 KB alignment slack
+  // sbuf doubles as the f16 q staging area (prologue) and the PV partial-sum area (epilogue)
+  const int sbuf = up128(2 * HQ * SROW * 4);
+  const int stage_q = MT * 16 * D * 2;
+  const int sb = sbuf > stage_q ? sbuf : stage_q;
+  const int tail = sb + up128(MT * 16 * PROW * 2) + up128(H * 16 * PROW * 2) + 2 * up128(HQ * 4) + up128(HQ * 16) +
+                   128 + 1024;
   const int budget = 227 * 1024;
   p.stages = (3 * p.stage_bytes + tail <= budget) ? 3 : ((2 * p.stage_bytes + tail <= budget) ? 2 : 1);
   int off = p.stages * p.stage_bytes;
-  p.off_work = off;
   p.off_sbuf = off;
-  off += up128(2 * HQ * SROW * 4);
+  off += sb;
   p.off_pbuf = off;
-  off += up128(HQ * PROW * 2);
-  p.off_p2buf = off;
-  off = p.off_work + work;
+  off += up128(MT * 16 * PROW * 2);
+  p.off_p2m = off;
+  off += up128(H * 16 * PROW * 2);
   p.off_qsum = off;
   off += up128(HQ * 4);
   p.off_corr = off;
@@ -210,34 +211,48 @@ __device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, int c0
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
       : "memory");
 }
+// Wait with a suspend-time hint: the thread sleeps in hardware instead of spinning.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "TADA_WAITS_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra TADA_WAITS_%=;\n}\n" ::"r"(su32(bar)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
 
 // ------------------------------------------------------------------ the kernel
 // Fragment orientation: q heads on M for both products.
 //   QK: S[g, t] = Q[g, d] · K̂^T[d, t]    A = Q (registers, f16), B = K-mean / K-codes tiles
-//   PV: O[g, d] = P[g, t] · V̂[t, d]      A = P, P' (smem, ldmatrix), B = V-mean / V-codes tiles
+//       warp = (token octet, half of head_dim)
+//   PV: O[g, d] = P[g, t] · V̂[t, d]      A = P, P'_h (smem, ldmatrix), B = V-mean / V-codes tiles
+//       warp = (32-wide d slice, 16-token half of the tile)
 // so every mean and code byte of a tile is read from smem by exactly one warp.
-template <int BITS, int HQ>
+template <int BITS, int HQ, int H>
 __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __grid_constant__ TmaMaps maps) {
   extern __shared__ uint8_t smem_raw[];
   // 1 KB alignment (128B-swizzle atoms) by pointer arithmetic on the __shared__ array, so the
   // compiler keeps the shared state space (LDS, 32-bit addressing) for every access below
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+  constexpr int G = HQ / H;
   constexpr int MT = (HQ + 15) / 16;    // m-tiles of 16 q heads
+  constexpr int HPM = 16 / G < H ? 16 / G : H;  // kv heads per m-tile
   constexpr int TPH = (NCW * 32) / HQ;  // softmax threads per q head
   constexpr int TPT = TT / TPH;         // tokens per softmax thread
-  const int H = a.L.heads, G = HQ / H, gb = a.L.group_bytes, P = a.L.page_tokens;
-  const Plan pl = make_plan(H, gb, HQ);
+  constexpr int GB = BITS * D / 8;      // code bytes per (token, head)
+  const int P = a.L.page_tokens;
+  const Plan pl = make_plan(H, GB, HQ);
   const int b = blockIdx.y, split = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r = lane >> 2, qi = lane & 3;
 
   float* sbuf = reinterpret_cast<float*>(smem + pl.off_sbuf);  // [2][HQ][SROW]
-  __half* pbuf = reinterpret_cast<__half*>(smem + pl.off_pbuf);
-  __half* p2buf = reinterpret_cast<__half*>(smem + pl.off_p2buf);
+  __half* pbuf = reinterpret_cast<__half*>(smem + pl.off_pbuf);  // [MT*16][PROW]
+  __half* p2m = reinterpret_cast<__half*>(smem + pl.off_p2m);    // [H][16][PROW]: -p*vscale, rows of kv head h only
   float* qsum = reinterpret_cast<float*>(smem + pl.off_qsum);
   float* corr_s = reinterpret_cast<float*>(smem + pl.off_corr);
   float* stats = reinterpret_cast<float*>(smem + pl.off_stats);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + pl.off_bar);
-  uint64_t* empty = full + 3;
   const int S = pl.stages;
 
   const int C = a.comp_len[b];
@@ -246,47 +261,47 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
   const int ntiles = (t_end - t_begin + TT - 1) / TT;
 
   if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NCW);
-    }
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // zero P'_h (rows not belonging to head h stay zero forever) and the padded P rows
+  for (int i = tid; i < (H * 16 * PROW) / 2; i += NTHR) reinterpret_cast<uint32_t*>(p2m)[i] = 0u;
+  for (int i = tid; i < (MT * 16 * PROW) / 2; i += NTHR) reinterpret_cast<uint32_t*>(pbuf)[i] = 0u;
   __syncthreads();
 
-  if (warp == NCW) {
-    // ================================================================ producer: TMA tensor copies
-    if (lane == 0) {
-      const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
-      for (int s = 0; s < 2; ++s)
-        for (int k = 0; k < 3; ++k)
-          asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[s][k])) : "memory");
-      const uint32_t tx = 2u * uint32_t(pl.mean_bytes + pl.codes_bytes + TT * pl.trow);
-      for (int it = 0; it < ntiles; ++it) {
-        const int stg = it % S;
-        if (it >= S) mbar_wait(&empty[stg], ((it / S) - 1) & 1);
-        const int t0 = t_begin + it * TT;
-        const int page = pt[t0 / P];
-        const int row0 = t0 % P;
-        uint8_t* dst = smem + stg * pl.stage_bytes;
-        mbar_expect_tx(&full[stg], tx);
-        for (int side = 0; side < 2; ++side) {
-          uint8_t* d0 = dst + side * pl.side_bytes;
+  // TMA producer (thread 0): tile `it` -> stage it % S.  A stage is refilled only after a
+  // consumer barrier that every warp reaches after finishing the stage's previous tile.
+  const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
+  const uint32_t tx = 2u * uint32_t(pl.mean_bytes + pl.codes_bytes + TT * pl.trow);
+  auto issue = [&](int it) {
+    const int stg = it % S;
+    const int t0 = t_begin + it * TT;
+    const int page = pt[t0 / P];
+    const int row0 = t0 % P;
+    uint8_t* dst = smem + stg * pl.stage_bytes;
+    mbar_expect_tx(&full[stg], tx);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) tma_3d(d0 + j * BAND, &maps.m[side][0], 128 * j, row0, page, &full[stg]);
-          for (int j = 0; j < pl.nbands_c; ++j)
-            tma_3d(d0 + pl.mean_bytes + j * BAND, &maps.m[side][1], 128 * j, row0, page, &full[stg]);
-          tma_3d(d0 + pl.mean_bytes + pl.codes_bytes, &maps.m[side][2], 0, row0, page, &full[stg]);
-        }
-      }
+    for (int side = 0; side < 2; ++side) {
+      uint8_t* d0 = dst + side * pl.side_bytes;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) tma_3d(d0 + j * BAND, &maps.m[side][0], 128 * j, row0, page, &full[stg]);
+#pragma unroll
+      for (int j = 0; j < (H * GB) / 128; ++j)
+        tma_3d(d0 + pl.mean_bytes + j * BAND, &maps.m[side][1], 128 * j, row0, page, &full[stg]);
+      tma_3d(d0 + pl.mean_bytes + pl.codes_bytes, &maps.m[side][2], 0, row0, page, &full[stg]);
     }
-    return;
+  };
+  if (tid == 0) {
+    for (int s2 = 0; s2 < 2; ++s2)
+      for (int k = 0; k < 3; ++k)
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[s2][k])) : "memory");
+    for (int it = 0; it < S - 1 && it < ntiles; ++it) issue(it);
   }
 
   // ================================================================== consumers
-  // prologue: q rows -> f32 row sums (min term) + f16 copy in the work area
+  // prologue: q rows -> f32 row sums (min term) + f16 copy (staged in sbuf)
   {
-    __half* q16 = reinterpret_cast<__half*>(smem + pl.off_work);
+    __half* q16 = reinterpret_cast<__half*>(sbuf);
     for (int g = warp; g < MT * 16; g += NCW) {
       float v[4] = {0.f, 0.f, 0.f, 0.f};
       if (g < HQ) {
@@ -300,9 +315,10 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
   }
   consumer_sync();
   const int kh = warp & 1, tq = 8 * (warp >> 1) + r;  // QK: k-half and this thread's B column (token)
+  const int tc0 = 8 * (warp >> 1) + 2 * qi;           // QK accumulator columns (tokens) tc0, tc0+1
   uint32_t qa[MT][4][4];
   {
-    const __half* q16 = reinterpret_cast<const __half*>(smem + pl.off_work);
+    const __half* q16 = reinterpret_cast<const __half*>(sbuf);
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -321,22 +337,31 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
   }
   // kv head of this thread's accumulator rows (16mt + r, 16mt + r + 8); -1 = padding row
   int kvr[MT][2];
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt) {
-    kvr[mt][0] = 16 * mt + r < HQ ? (16 * mt + r) / G : -1;
-    kvr[mt][1] = 16 * mt + r + 8 < HQ ? (16 * mt + r + 8) / G : -1;
-  }
-  float oacc[MT][2][4];
+  float qsr[MT][2];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-    for (int n2 = 0; n2 < 2; ++n2)
+    for (int e = 0; e < 2; ++e) {
+      const int g = 16 * mt + r + 8 * e;
+      kvr[mt][e] = g < HQ ? g / G : -1;
+      qsr[mt][e] = g < HQ ? qsum[g] : 0.f;
+    }
+  // QK code addresses: (row tq, byte h*GB + off) with off = (32qi + 16kh)*BITS/8 < 128
+  constexpr int CW = BITS == 8 ? 4 : (BITS == 4 ? 2 : 1);  // code words per (token, head) per thread
+  const int qk_c0 = swz(tq, ((32 * qi + 16 * kh) * BITS) / 8);
+  // PV: warp = (d slice dq of 32, token half kk); B column r <-> d = 32dq + 4r + n (n-tile n = 0..3)
+  const int dq = warp & 3, kk = warp >> 2;
+  float oacc[MT][4][4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) oacc[mt][n2][e] = 0.f;
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) oacc[mt][n][e] = 0.f;
   const int sg = tid / TPH, spart = tid % TPH, sh = sg / G;  // softmax ownership
   float m_run = -__int_as_float(0x7f800000), l_part = 0.f, bp_part = 0.f;
   const float scale_log2 = a.scale * 1.4426950408889634f;
-  consumer_sync();  // q16 (work area) is dead from here on
+  consumer_sync();  // q16 staging area is dead from here on
 
   for (int it = 0; it < ntiles; ++it) {
     const int stg = it % S;
@@ -352,7 +377,6 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
     const uint8_t* vmeta = vmean + pl.mean_bytes + pl.codes_bytes;
 
     // ---------------------------------------------------------------- QK (warp = token octet x k-half)
-    const int tc0 = 8 * (warp >> 1) + 2 * qi;  // accumulator columns (tokens) tc0, tc0+1
     {
       float acc[MT][4];
 #pragma unroll
@@ -376,46 +400,48 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
           mma(acc[mt], qa[mt][k4], l0, l1);
         }
       }
-      // code term, one kv head at a time; fold -scale*C (and -min*sum(q) once, k-half 0)
-      for (int h = 0; h < H; ++h) {
-        constexpr int NW = BITS == 8 ? 4 : (BITS == 4 ? 2 : 1);
-        uint32_t w[NW];
-        const int cb = h * gb + ((32 * qi + 16 * kh) * BITS) / 8;
-        const uint8_t* cp = kcodes + (cb >> 7) * BAND + swz(tq, cb & 127);
-        if (NW == 4) {
-          const uint4 v = *reinterpret_cast<const uint4*>(cp);
-          w[0] = v.x; w[1] = v.y; w[2 % NW] = v.z; w[3 % NW] = v.w;
-        } else if (NW == 2) {
-          const uint2 v = *reinterpret_cast<const uint2*>(cp);
-          w[0] = v.x; w[1 % NW] = v.y;
-        } else {
-          w[0] = *reinterpret_cast<const uint32_t*>(cp);
+      // code term: per m-tile, its HPM kv heads as independent accumulation chains
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        uint32_t w[HPM][CW];
+        float cacc[HPM][4];
+#pragma unroll
+        for (int j = 0; j < HPM; ++j) {
+          const int h = mt * HPM + j;
+          const int hb = h * GB;
+          const uint8_t* cp = kcodes + (hb >> 7) * BAND + (qk_c0 ^ (hb & 127));
+          if (CW == 4) {
+            const uint4 v = *reinterpret_cast<const uint4*>(cp);
+            w[j][0] = v.x; w[j][1 % CW] = v.y; w[j][2 % CW] = v.z; w[j][3 % CW] = v.w;
+          } else if (CW == 2) {
+            const uint2 v = *reinterpret_cast<const uint2*>(cp);
+            w[j][0] = v.x; w[j][1 % CW] = v.y;
+          } else {
+            w[j][0] = *reinterpret_cast<const uint32_t*>(cp);
+          }
+          cacc[j][0] = cacc[j][1] = cacc[j][2] = cacc[j][3] = 0.f;
         }
-        const int mth = (h * G) >> 4;
-        float cacc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int k4 = 0; k4 < 4; ++k4) {
-          uint32_t b0, b1;
-          qk_code_pair<BITS>(w, k4, b0, b1);
+        for (int k4 = 0; k4 < 4; ++k4)
 #pragma unroll
-          for (int mt = 0; mt < MT; ++mt)
-            if (mt == mth) mma(cacc, qa[mt][k4], b0, b1);
-        }
-        const float2 ma = *reinterpret_cast<const float2*>(kmeta + tc0 * pl.trow + h * 8);
-        const float2 mb = *reinterpret_cast<const float2*>(kmeta + (tc0 + 1) * pl.trow + h * 8);
-        const float mna = kh == 0 ? ma.y : 0.f, mnb = kh == 0 ? mb.y : 0.f;
+          for (int j = 0; j < HPM; ++j) {
+            uint32_t b0, b1;
+            qk_code_pair<BITS>(w[j], k4, b0, b1);
+            mma(cacc[j], qa[mt][k4], b0, b1);
+          }
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          if (mt != mth) continue;
+        for (int j = 0; j < HPM; ++j) {
+          const int h = mt * HPM + j;
+          const float2 ma = *reinterpret_cast<const float2*>(kmeta + tc0 * pl.trow + h * 8);
+          const float2 mb = *reinterpret_cast<const float2*>(kmeta + (tc0 + 1) * pl.trow + h * 8);
+          const float mna = kh == 0 ? ma.y : 0.f, mnb = kh == 0 ? mb.y : 0.f;
           if (kvr[mt][0] == h) {
-            const float qs = qsum[16 * mt + r];
-            acc[mt][0] = fmaf(-ma.x, cacc[0], fmaf(-mna, qs, acc[mt][0]));
-            acc[mt][1] = fmaf(-mb.x, cacc[1], fmaf(-mnb, qs, acc[mt][1]));
+            acc[mt][0] = fmaf(-ma.x, cacc[j][0], fmaf(-mna, qsr[mt][0], acc[mt][0]));
+            acc[mt][1] = fmaf(-mb.x, cacc[j][1], fmaf(-mnb, qsr[mt][0], acc[mt][1]));
           }
           if (kvr[mt][1] == h) {
-            const float qs = qsum[16 * mt + r + 8];
-            acc[mt][2] = fmaf(-ma.x, cacc[2], fmaf(-mna, qs, acc[mt][2]));
-            acc[mt][3] = fmaf(-mb.x, cacc[3], fmaf(-mnb, qs, acc[mt][3]));
+            acc[mt][2] = fmaf(-ma.x, cacc[j][2], fmaf(-mna, qsr[mt][1], acc[mt][2]));
+            acc[mt][3] = fmaf(-mb.x, cacc[j][3], fmaf(-mnb, qsr[mt][1], acc[mt][3]));
           }
         }
       }
@@ -429,6 +455,8 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
     }
     consumer_sync();
 
+    // every warp has finished tile it-1 (its PV) -> refill that stage with tile it+S-1
+    if (tid == 0 && it + S - 1 < ntiles) issue(it + S - 1);
     // ---------------------------------------------------------------- online softmax
     {
       float x[TPT];
@@ -445,6 +473,7 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
       const float corr = exp2f(m_run - m_new);
       m_run = m_new;
       float lsum = 0.f, bsum = 0.f;
+      __half* p2row = p2m + (sh * 16 + (sg & 15)) * PROW;
 #pragma unroll
       for (int u = 0; u < TPT; ++u) {
         const int t = spart + TPH * u;
@@ -453,7 +482,7 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
         lsum += p;
         bsum = fmaf(p, vm.y, bsum);
         pbuf[sg * PROW + t] = __float2half_rn(p);
-        p2buf[sg * PROW + t] = __float2half_rn(-p * vm.x);
+        p2row[t] = __float2half_rn(-p * vm.x);
       }
       l_part = l_part * corr + lsum;
       bp_part = bp_part * corr + bsum;
@@ -461,97 +490,103 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
     }
     consumer_sync();
 
-    // ---------------------------------------------------------------- PV (warp = 16-wide d slice)
+    // ---------------------------------------------------------------- PV (warp = 32-wide d slice x 16 tokens)
     {
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         const float c0 = kvr[mt][0] >= 0 ? corr_s[16 * mt + r] : 0.f;
         const float c1 = kvr[mt][1] >= 0 ? corr_s[16 * mt + r + 8] : 0.f;
 #pragma unroll
-        for (int n2 = 0; n2 < 2; ++n2) {
-          oacc[mt][n2][0] *= c0;
-          oacc[mt][n2][1] *= c0;
-          oacc[mt][n2][2] *= c1;
-          oacc[mt][n2][3] *= c1;
+        for (int n = 0; n < 4; ++n) {
+          oacc[mt][n][0] *= c0;
+          oacc[mt][n][1] *= c0;
+          oacc[mt][n][2] *= c1;
+          oacc[mt][n][3] *= c1;
         }
       }
-      const int dcol = 16 * warp + 2 * r;  // B column r <-> d = dcol (n-tile 0), dcol + 1 (n-tile 1)
-      const int mband = (4 * dcol) >> 7, mo = (4 * dcol) & 127;
+      const int ta = 16 * kk + 2 * qi;  // this thread's B rows: tokens ta, ta+1, ta+8, ta+9
+      // mean term: float4 of d = 32dq + 4r .. +3 for each of the 4 tokens
+      uint32_t bh[4][2], bl[4][2];
+      {
+        const uint8_t* vb = vmean + dq * BAND;
+        const float4 xa = *reinterpret_cast<const float4*>(vb + swz(ta, 16 * r));
+        const float4 xb = *reinterpret_cast<const float4*>(vb + swz(ta + 1, 16 * r));
+        const float4 xc = *reinterpret_cast<const float4*>(vb + swz(ta + 8, 16 * r));
+        const float4 xd = *reinterpret_cast<const float4*>(vb + swz(ta + 9, 16 * r));
+        split_h2(xa.x, xb.x, bh[0][0], bl[0][0]);
+        split_h2(xc.x, xd.x, bh[0][1], bl[0][1]);
+        split_h2(xa.y, xb.y, bh[1][0], bl[1][0]);
+        split_h2(xc.y, xd.y, bh[1][1], bl[1][1]);
+        split_h2(xa.z, xb.z, bh[2][0], bl[2][0]);
+        split_h2(xc.z, xd.z, bh[2][1], bl[2][1]);
+        split_h2(xa.w, xb.w, bh[3][0], bl[3][0]);
+        split_h2(xc.w, xd.w, bh[3][1], bl[3][1]);
+      }
+      const int mrow = (lane & 7) + 8 * ((lane >> 3) & 1), tcol = 16 * kk + 8 * (lane >> 4);
 #pragma unroll
-      for (int k2 = 0; k2 < TT / 16; ++k2) {
-        const int ta = 16 * k2 + 2 * qi;  // this thread's B rows: tokens ta, ta+1, ta+8, ta+9
-        uint32_t bh[2][2], bl[2][2];
-        {
-          const uint8_t* vb = vmean + mband * BAND;
-          const float2 xa = *reinterpret_cast<const float2*>(vb + swz(ta, mo));
-          const float2 xb = *reinterpret_cast<const float2*>(vb + swz(ta + 1, mo));
-          const float2 xc = *reinterpret_cast<const float2*>(vb + swz(ta + 8, mo));
-          const float2 xd = *reinterpret_cast<const float2*>(vb + swz(ta + 9, mo));
-          split_h2(xa.x, xb.x, bh[0][0], bl[0][0]);
-          split_h2(xc.x, xd.x, bh[0][1], bl[0][1]);
-          split_h2(xa.y, xb.y, bh[1][0], bl[1][0]);
-          split_h2(xc.y, xd.y, bh[1][1], bl[1][1]);
+      for (int mt = 0; mt < MT; ++mt) {
+        uint32_t pa[4];
+        ldsm_x4(pa, su32(pbuf + (16 * mt + mrow) * PROW + tcol));
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+          mma(oacc[mt][n], pa, bh[n][0], bh[n][1]);
+          mma(oacc[mt][n], pa, bl[n][0], bl[n][1]);
         }
-        uint32_t pa[MT][4], p2[MT][4];
-        {
-          const int mrow = (lane & 7) + 8 * ((lane >> 3) & 1), tcol = 16 * k2 + 8 * (lane >> 4);
+      }
+      // code term: per kv head, A = P'_h (pre-masked rows), B = its codes of d = 32dq + 4r .. +3
+      constexpr int CB = BITS * 4 / 8;  // code bytes per token for the thread's 4 d
+      const int pv_c = (32 * dq + 4 * r) * BITS / 8;
 #pragma unroll
-          for (int mt = 0; mt < MT; ++mt) {
-            const int g = 16 * mt + mrow;
-            ldsm_x4(pa[mt], su32(pbuf + g * PROW + tcol));
-            ldsm_x4(p2[mt], su32(p2buf + g * PROW + tcol));
+      for (int h = 0; h < H; ++h) {
+        const int hb = h * GB + pv_c;
+        const uint8_t* cband = vcodes + (hb >> 7) * BAND;
+        const int co = hb & 127;
+        uint32_t xa, xb, xc, xd;
+        if (CB == 4) {
+          xa = *reinterpret_cast<const uint32_t*>(cband + swz(ta, co));
+          xb = *reinterpret_cast<const uint32_t*>(cband + swz(ta + 1, co));
+          xc = *reinterpret_cast<const uint32_t*>(cband + swz(ta + 8, co));
+          xd = *reinterpret_cast<const uint32_t*>(cband + swz(ta + 9, co));
+        } else if (CB == 2) {
+          xa = *reinterpret_cast<const uint16_t*>(cband + swz(ta, co));
+          xb = *reinterpret_cast<const uint16_t*>(cband + swz(ta + 1, co));
+          xc = *reinterpret_cast<const uint16_t*>(cband + swz(ta + 8, co));
+          xd = *reinterpret_cast<const uint16_t*>(cband + swz(ta + 9, co));
+        } else {
+          xa = cband[swz(ta, co)];
+          xb = cband[swz(ta + 1, co)];
+          xc = cband[swz(ta + 8, co)];
+          xd = cband[swz(ta + 9, co)];
+        }
+        uint32_t bc[4][2];
+        if (BITS == 8) {
+#pragma unroll
+          for (int n = 0; n < 4; ++n) {
+            const uint32_t sel = n | (n << 4) | ((4 + n) << 8) | ((4 + n) << 12);
+            bc[n][0] = ints_to_h2(prmt(xa, xb, sel) & 0x00FF00FFu);
+            bc[n][1] = ints_to_h2(prmt(xc, xd, sel) & 0x00FF00FFu);
+          }
+        } else {
+          constexpr uint32_t M = BITS == 4 ? 0x000F000Fu : 0x00030003u;
+          const uint32_t u = xa | (xb << 16), v = xc | (xd << 16);
+#pragma unroll
+          for (int n = 0; n < 4; ++n) {
+            bc[n][0] = ints_to_h2((u >> (BITS * n)) & M);
+            bc[n][1] = ints_to_h2((v >> (BITS * n)) & M);
           }
         }
+        constexpr int mth_div = 16 / G;
+        const int mth = h / (mth_div < 1 ? 1 : mth_div);
+        uint32_t am[4];
+        ldsm_x4(am, su32(p2m + (h * 16 + mrow) * PROW + tcol));
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
+        for (int mt = 0; mt < MT; ++mt) {
+          if (mt != mth) continue;
 #pragma unroll
-          for (int n2 = 0; n2 < 2; ++n2) {
-            mma(oacc[mt][n2], pa[mt], bh[n2][0], bh[n2][1]);
-            mma(oacc[mt][n2], pa[mt], bl[n2][0], bl[n2][1]);
-          }
-        // code term per kv head, A = P' restricted to that head's rows
-        for (int h = 0; h < H; ++h) {
-          const int mth = (h * G) >> 4;
-          uint32_t bc[2][2];
-          {
-            // byte holding codes d = dcol, dcol+1 of row (t, h)
-            const int cbyte = h * gb + ((dcol * BITS) >> 3);
-            const uint8_t* cband = vcodes + (cbyte >> 7) * BAND;
-            const int co = cbyte & 127;
-            uint32_t xa, xb, xc, xd;
-            if (BITS == 8) {
-              xa = *reinterpret_cast<const uint16_t*>(cband + swz(ta, co));
-              xb = *reinterpret_cast<const uint16_t*>(cband + swz(ta + 1, co));
-              xc = *reinterpret_cast<const uint16_t*>(cband + swz(ta + 8, co));
-              xd = *reinterpret_cast<const uint16_t*>(cband + swz(ta + 9, co));
-            } else {
-              const int sft = BITS == 2 ? (dcol & 3) * 2 : 0;
-              xa = cband[swz(ta, co)] >> sft;
-              xb = cband[swz(ta + 1, co)] >> sft;
-              xc = cband[swz(ta + 8, co)] >> sft;
-              xd = cband[swz(ta + 9, co)] >> sft;
-            }
-            constexpr uint32_t M = BITS == 8 ? 0x00FF00FFu : (BITS == 4 ? 0x000F000Fu : 0x00030003u);
-            constexpr uint32_t LO = BITS == 8 ? 0xFFFFu : (BITS == 4 ? 0xFFu : 0xFu);
-            const uint32_t u = (xa & LO) | ((xb & LO) << 16), v = (xc & LO) | ((xd & LO) << 16);
-            bc[0][0] = ints_to_h2(u & M);
-            bc[1][0] = ints_to_h2((u >> BITS) & M);
-            bc[0][1] = ints_to_h2(v & M);
-            bc[1][1] = ints_to_h2((v >> BITS) & M);
-          }
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt) {
-            if (mt != mth) continue;
-            const bool k0 = kvr[mt][0] == h, k1 = kvr[mt][1] == h;
-            uint32_t am[4] = {k0 ? p2[mt][0] : 0u, k1 ? p2[mt][1] : 0u, k0 ? p2[mt][2] : 0u, k1 ? p2[mt][3] : 0u};
-            mma(oacc[mt][0], am, bc[0][0], bc[0][1]);
-            mma(oacc[mt][1], am, bc[1][0], bc[1][1]);
-          }
+          for (int n = 0; n < 4; ++n) mma(oacc[mt][n], am, bc[n][0], bc[n][1]);
         }
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stg]);
   }
 
   // ------------------------------------------------------------------ epilogue
@@ -565,24 +600,49 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
     stats[4 * sg + 1] = l_part;
     stats[4 * sg + 2] = bp_part;
   }
+  // the two token halves (kk) hold partial O: kk = 1 parks its half in smem, kk = 0 adds it
+  float* park = reinterpret_cast<float*>(smem);  // stages are idle now: [MT*16][D] floats
   consumer_sync();
-  const float LN2 = 0.6931471805599453f;
+  // thread rows g = 16mt + r (+8); cols: n-tile n, col 2qi / 2qi+1 <-> d = 32dq + 8qi + n / + 4 + n
+  if (kk == 1) {
 #pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
+    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int g = 16 * mt + r + 8 * e;
-      if (g >= HQ) continue;
-      const float m = stats[4 * g], l = stats[4 * g + 1], bp = stats[4 * g + 2];
-      float* pa = a.part_acc + ((int64_t(b) * HQ + g) * a.slots + split) * D + 16 * warp + 4 * qi;
-      *reinterpret_cast<float4*>(pa) = make_float4(oacc[mt][0][2 * e] - bp, oacc[mt][1][2 * e] - bp,
-                                                   oacc[mt][0][2 * e + 1] - bp, oacc[mt][1][2 * e + 1] - bp);
-      if (warp == 0 && qi == 0) {
-        float* ml = a.part_ml + ((int64_t(b) * HQ + g) * a.slots + split) * 2;
-        ml[0] = l > 0.f ? m * LN2 : -__int_as_float(0x7f800000);  // back to natural-log units for K3
-        ml[1] = l;
+      for (int e = 0; e < 2; ++e) {
+        float* row = park + (16 * mt + r + 8 * e) * D + 32 * dq + 8 * qi;
+        *reinterpret_cast<float4*>(row) =
+            make_float4(oacc[mt][0][2 * e], oacc[mt][1][2 * e], oacc[mt][2][2 * e], oacc[mt][3][2 * e]);
+        *reinterpret_cast<float4*>(row + 4) =
+            make_float4(oacc[mt][0][2 * e + 1], oacc[mt][1][2 * e + 1], oacc[mt][2][2 * e + 1], oacc[mt][3][2 * e + 1]);
       }
-    }
+  }
+  consumer_sync();
+  if (kk == 0) {
+    const float LN2 = 0.6931471805599453f;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int g = 16 * mt + r + 8 * e;
+        if (g >= HQ) continue;
+        const float m = stats[4 * g], l = stats[4 * g + 1], bp = stats[4 * g + 2];
+        const float* row = park + g * D + 32 * dq + 8 * qi;
+        const float4 p0 = *reinterpret_cast<const float4*>(row);
+        const float4 p1 = *reinterpret_cast<const float4*>(row + 4);
+        float* pa = a.part_acc + ((int64_t(b) * HQ + g) * a.slots + split) * D + 32 * dq + 8 * qi;
+        *reinterpret_cast<float4*>(pa) =
+            make_float4(oacc[mt][0][2 * e] + p0.x - bp, oacc[mt][1][2 * e] + p0.y - bp, oacc[mt][2][2 * e] + p0.z - bp,
+                        oacc[mt][3][2 * e] + p0.w - bp);
+        *reinterpret_cast<float4*>(pa + 4) =
+            make_float4(oacc[mt][0][2 * e + 1] + p1.x - bp, oacc[mt][1][2 * e + 1] + p1.y - bp,
+                        oacc[mt][2][2 * e + 1] + p1.z - bp, oacc[mt][3][2 * e + 1] + p1.w - bp);
+        if (dq == 0 && qi == 0) {
+          float* ml = a.part_ml + ((int64_t(b) * HQ + g) * a.slots + split) * 2;
+          ml[0] = l > 0.f ? m * LN2 : -__int_as_float(0x7f800000);  // back to natural-log units for K3
+          ml[1] = l;
+        }
+      }
+  }
 }
 
 }  // namespace fast
@@ -660,11 +720,10 @@ __global__ void __launch_bounds__(256) attn_residual_kernel(AttnArgs a) {
 }
 
 bool fast_supported(const tada_page_layout& L, int Hq) {
-  if (L.head_dim != 128 || !(L.bits == 2 || L.bits == 4 || L.bits == 8)) return false;
-  if (!(Hq == 8 || Hq == 16 || Hq == 32 || Hq == 64) || Hq % L.heads) return false;
-  const int G = Hq / L.heads;
-  if (!(G == 1 || G == 2 || G == 4 || G == 8)) return false;
-  if (L.page_tokens % fast::TT || (L.heads * L.group_bytes) % 128 || (L.heads * 8) % 16) return false;
+  // compiled geometries: 8 KV heads (the Llama-3 family) with 8/16/32/64 q heads
+  if (L.head_dim != 128 || !(L.bits == 2 || L.bits == 4 || L.bits == 8) || L.heads != 8) return false;
+  if (!(Hq == 8 || Hq == 16 || Hq == 32 || Hq == 64)) return false;
+  if (L.page_tokens % fast::TT) return false;
   return fast::make_plan(L.heads, L.group_bytes, Hq).total <= 227 * 1024;
 }
 
@@ -741,7 +800,7 @@ static int get_maps(const AttnArgs& a, TmaMaps* out) {
 template <int BITS, int HQ>
 static int launch_fast_t(const AttnArgs& a, int batch, cudaStream_t st) {
   const fast::Plan pl = fast::make_plan(a.L.heads, a.L.group_bytes, HQ);
-  auto kern = fast::attn_fast_kernel<BITS, HQ>;
+  auto kern = fast::attn_fast_kernel<BITS, HQ, 8>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
