@@ -1,0 +1,31 @@
+#!/usr/bin/env bash
+# One gpurun session: GPU tests, smoke, micro-benches, bench line, ncu launch list.
+# Usage (from this container):
+#   gpurun --timeout 1500 -- 'bash tools/gpu_session.sh [tests|bench|ncu|all]'
+# Everything lands in gpurun_out/; each step has its own timeout so one hang cannot eat the call.
+set -u
+what=${1:-all}
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/gpu.txt 2>&1
+if [[ ! -f paper_2506_04642_b200/libtadakv_b200.so ]]; then make -j8 > gpurun_out/make.log 2>&1; fi
+
+if [[ $what == tests || $what == all ]]; then
+  timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+  timeout 300 python -c 'import __graft_entry__ as g; g.smoke()' > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+fi
+if [[ $what == micro || $what == all ]]; then
+  : > gpurun_out/micro.log
+  for bits in 2 4 8; do
+    for mode in 1 2; do
+      timeout 300 python tools/attn_bench.py --bits $bits --mode $mode >> gpurun_out/micro.log 2>&1
+    done
+  done
+fi
+if [[ $what == bench || $what == all ]]; then
+  timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+fi
+if [[ $what == ncu || $what == all ]]; then
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
+    --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_bench.log 2>&1
+  echo "ncu rc=$?" >> gpurun_out/ncu_bench.log
+fi
