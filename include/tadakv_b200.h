@@ -163,6 +163,25 @@ int tada_decode_attn(const tada_page_layout* layout, const uint8_t* pool, const 
                      int32_t num_splits, void* workspace, void* out, int32_t out_dtype, int32_t mode,
                      void* stream);
 
+/* Same as tada_decode_attn, and also writes lse_out[b][g] = log sum_t exp(scale * q.k_t) (natural
+ * log) so that attention over disjoint token sets held by different ranks can be merged exactly
+ * (the sequence-axis shard of SURVEY §8e; attend_streaming's online-softmax state,
+ * attention.py:139-147, expressed as (out, lse)). */
+int tada_decode_attn_lse(const tada_page_layout* layout, const uint8_t* pool, const void* q,
+                         int32_t q_dtype, int32_t batch, int32_t num_q_heads,
+                         const int32_t* page_table, int32_t pt_stride, const int32_t* comp_len,
+                         const int32_t* res_len, const float* res_k, const float* res_v,
+                         int64_t res_seq_stride, float scale, int32_t num_splits, void* workspace,
+                         void* out, int32_t out_dtype, int32_t mode, float* lse_out, void* stream);
+
+/* Merge n_parts normalised partial attentions: o_parts [n_parts][rows][head_dim] f32 and
+ * lse_parts [n_parts][rows] f32 (-inf = the part had no tokens) ->
+ * out[rows][head_dim] = sum_p o_p e^(lse_p - M) / sum_p e^(lse_p - M); lse_out (optional) gets the
+ * merged log-sum-exp.  This is the online-softmax merge of attention.py:139-147 applied across
+ * ranks after the NCCL all-gather of partials. */
+int tada_combine_lse(const float* o_parts, const float* lse_parts, int32_t n_parts, int64_t rows,
+                     int32_t head_dim, void* out, int32_t out_dtype, float* lse_out, void* stream);
+
 /* Suggested split count for a batch/context on this device (fills ~4 waves of SMs). */
 int32_t tada_decode_attn_suggest_splits(int32_t batch, int64_t max_tokens, int32_t page_tokens);
 

@@ -113,6 +113,8 @@ __global__ void __launch_bounds__(256) attn_generic_kernel(AttnArgs a) {
       const int g = pair / D;
       store_any(a.out, a.out_dtype, int64_t(b) * Hq * D + pair, acc[pair] / lrow[g]);
     }
+    if (a.lse_out)
+      for (int g = tid; g < Hq; g += bd) a.lse_out[int64_t(b) * Hq + g] = mrow[g] + logf(lrow[g]);
   } else {
     for (int pair = tid; pair < Hq * D; pair += bd) {
       const int g = pair / D, d = pair - g * D;
@@ -129,7 +131,7 @@ __global__ void __launch_bounds__(256) attn_generic_kernel(AttnArgs a) {
 // ------------------------------------------------------------------ K3: split combine
 // out = sum_s acc_s * e^{m_s - M} / sum_s l_s * e^{m_s - M}   (log-sum-exp merge)
 __global__ void combine_kernel(const float* __restrict__ part_acc, const float* __restrict__ part_ml, int S, int D,
-                               void* out, int out_dtype) {
+                               void* out, int out_dtype, float* lse_out) {
   const int64_t bg = blockIdx.x;  // b * Hq + g
   const float* ml = part_ml + bg * S * 2;
   float M = -__int_as_float(0x7f800000);
@@ -138,11 +140,37 @@ __global__ void combine_kernel(const float* __restrict__ part_acc, const float* 
   for (int s = 0; s < S; ++s)
     if (ml[2 * s + 1] > 0.f) L += ml[2 * s + 1] * expf(ml[2 * s] - M);
   const float inv = 1.f / L;
+  if (lse_out && threadIdx.x == 0) lse_out[bg] = M + logf(L);
   for (int d = threadIdx.x; d < D; d += blockDim.x) {
     float o = 0.f;
     for (int s = 0; s < S; ++s)
       if (ml[2 * s + 1] > 0.f) o += part_acc[(bg * S + s) * D + d] * expf(ml[2 * s] - M);
     store_any(out, out_dtype, bg * D + d, o * inv);
+  }
+}
+
+// ------------------------------------------------------------------ cross-rank merge of normalised partials
+// Each part p holds o_p = softmax-weighted mean over its own tokens and lse_p = log sum exp of its
+// logits (-inf: part saw no tokens).  out = sum_p o_p e^{lse_p - M} / sum_p e^{lse_p - M}.
+__global__ void combine_lse_kernel(const float* __restrict__ o, const float* __restrict__ lse, int n, int64_t rows,
+                                   int D, void* out, int out_dtype, float* lse_out) {
+  const int64_t row = blockIdx.x;
+  float M = -__int_as_float(0x7f800000);
+  for (int p = 0; p < n; ++p) M = fmaxf(M, lse[p * rows + row]);
+  float W = 0.f;
+  for (int p = 0; p < n; ++p) {
+    const float l = lse[p * rows + row];
+    if (l > -__int_as_float(0x7f800000)) W += expf(l - M);
+  }
+  const float inv = 1.f / W;
+  if (lse_out && threadIdx.x == 0) lse_out[row] = M + logf(W);
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    float acc = 0.f;
+    for (int p = 0; p < n; ++p) {
+      const float l = lse[p * rows + row];
+      if (l > -__int_as_float(0x7f800000)) acc += o[(p * rows + row) * D + d] * expf(l - M);
+    }
+    store_any(out, out_dtype, row * D + d, acc * inv);
   }
 }
 
@@ -197,11 +225,11 @@ int32_t tada_decode_attn_suggest_splits(int32_t batch, int64_t max_tokens, int32
   return int32_t(best);
 }
 
-int tada_decode_attn(const tada_page_layout* layout, const uint8_t* pool, const void* q, int32_t q_dtype, int32_t batch,
-                     int32_t num_q_heads, const int32_t* page_table, int32_t pt_stride, const int32_t* comp_len,
-                     const int32_t* res_len, const float* res_k, const float* res_v, int64_t res_seq_stride,
-                     float scale, int32_t num_splits, void* workspace, void* out, int32_t out_dtype, int32_t mode,
-                     void* stream) {
+static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool, const void* q, int32_t q_dtype,
+                            int32_t batch, int32_t num_q_heads, const int32_t* page_table, int32_t pt_stride,
+                            const int32_t* comp_len, const int32_t* res_len, const float* res_k, const float* res_v,
+                            int64_t res_seq_stride, float scale, int32_t num_splits, void* workspace, void* out,
+                            int32_t out_dtype, int32_t mode, float* lse_out, void* stream) {
   if (!layout) return fail(TADA_ERR_CONFIG, "null layout");
   if (q_dtype != TADA_F32 && q_dtype != TADA_BF16) return fail(TADA_ERR_CONFIG, "q dtype must be f32 or bf16");
   if (out_dtype != TADA_F32 && out_dtype != TADA_BF16) return fail(TADA_ERR_CONFIG, "out dtype must be f32 or bf16");
@@ -236,6 +264,7 @@ int tada_decode_attn(const tada_page_layout* layout, const uint8_t* pool, const 
   a.out = out;
   a.out_dtype = out_dtype;
   a.q_dtype = q_dtype;
+  a.lse_out = lse_out;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int rc;
   if (fast) {
@@ -247,8 +276,38 @@ int tada_decode_attn(const tada_page_layout* layout, const uint8_t* pool, const 
   }
   if (rc != TADA_OK) return rc;
   combine_kernel<<<unsigned(int64_t(batch) * num_q_heads), 128, 0, st>>>(a.part_acc, a.part_ml, a.slots,
-                                                                          layout->head_dim, out, out_dtype);
+                                                                          layout->head_dim, out, out_dtype, a.lse_out);
   return check_launch("decode_attn_combine");
+}
+
+int tada_decode_attn(const tada_page_layout* layout, const uint8_t* pool, const void* q, int32_t q_dtype, int32_t batch,
+                     int32_t num_q_heads, const int32_t* page_table, int32_t pt_stride, const int32_t* comp_len,
+                     const int32_t* res_len, const float* res_k, const float* res_v, int64_t res_seq_stride,
+                     float scale, int32_t num_splits, void* workspace, void* out, int32_t out_dtype, int32_t mode,
+                     void* stream) {
+  return decode_attn_impl(layout, pool, q, q_dtype, batch, num_q_heads, page_table, pt_stride, comp_len, res_len, res_k,
+                          res_v, res_seq_stride, scale, num_splits, workspace, out, out_dtype, mode, nullptr, stream);
+}
+
+int tada_decode_attn_lse(const tada_page_layout* layout, const uint8_t* pool, const void* q, int32_t q_dtype,
+                         int32_t batch, int32_t num_q_heads, const int32_t* page_table, int32_t pt_stride,
+                         const int32_t* comp_len, const int32_t* res_len, const float* res_k, const float* res_v,
+                         int64_t res_seq_stride, float scale, int32_t num_splits, void* workspace, void* out,
+                         int32_t out_dtype, int32_t mode, float* lse_out, void* stream) {
+  if (!lse_out) return fail(TADA_ERR_SHAPE, "null lse buffer");
+  return decode_attn_impl(layout, pool, q, q_dtype, batch, num_q_heads, page_table, pt_stride, comp_len, res_len, res_k,
+                          res_v, res_seq_stride, scale, num_splits, workspace, out, out_dtype, mode, lse_out, stream);
+}
+
+int tada_combine_lse(const float* o_parts, const float* lse_parts, int32_t n_parts, int64_t rows, int32_t head_dim,
+                     void* out, int32_t out_dtype, float* lse_out, void* stream) {
+  if (n_parts < 1 || rows < 0 || head_dim <= 0) return fail(TADA_ERR_CONFIG, "bad combine geometry");
+  if (out_dtype != TADA_F32 && out_dtype != TADA_BF16) return fail(TADA_ERR_CONFIG, "out dtype must be f32 or bf16");
+  if (rows == 0) return TADA_OK;
+  if (!o_parts || !lse_parts || !out) return fail(TADA_ERR_SHAPE, "null buffer");
+  combine_lse_kernel<<<unsigned(rows), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      o_parts, lse_parts, n_parts, rows, head_dim, out, out_dtype, lse_out);
+  return check_launch("combine_lse");
 }
 
 }  // extern "C"

@@ -27,6 +27,7 @@ struct AttnArgs {
   void* out;
   int out_dtype;
   int q_dtype;
+  float* lse_out;  // optional [B][Hq]: natural-log sum-exp of the scaled logits (cross-rank merge)
 };
 
 __device__ __forceinline__ void store_any(void* out, int dtype, int64_t i, float v) {

@@ -245,6 +245,33 @@ class PagedKVCache:
              out.data_ptr(), _dev.dtype_code(out), mode, _dev.stream())
         return out
 
+    def attend_lse(self, layer: int, q: torch.Tensor, num_splits: int | None = None, mode: int = 0,
+                   scale: float | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+        """Like :meth:`attend` (f32 out) and also the log-sum-exp ``[batch, Hq]`` of the scaled logits.
+
+        ``(out, lse)`` pairs over disjoint token sets merge exactly (shard.merge_partials).
+        """
+        if q.ndim != 3 or q.shape[0] != self.B or q.shape[2] != self.D or q.shape[1] % self.H:
+            raise ShapeError(f"query must be ({self.B}, Hq, {self.D}) with Hq a multiple of {self.H}, got "
+                             f"{tuple(q.shape)}")
+        if ((self.comp_host[layer] + self.res_host[layer]) == 0).any():
+            raise StateError("cannot attend over an empty cache")
+        hq = int(q.shape[1])
+        if q.dtype not in (torch.float32, torch.bfloat16):
+            q = q.float()
+        q = q.contiguous()
+        splits = num_splits or self.suggest_splits(layer)
+        ws = self.workspace(hq, splits)
+        out = torch.empty((self.B, hq, self.D), dtype=torch.float32, device=self.dev)
+        lse = torch.empty((self.B, hq), dtype=torch.float32, device=self.dev)
+        sc = np.float32(1.0 / math.sqrt(self.D)) if scale is None else np.float32(scale)
+        call("tada_decode_attn_lse", self._layout_ptr(layer), self.pools[layer].data_ptr(), q.data_ptr(),
+             _dev.dtype_code(q), self.B, hq, self.page_table.data_ptr(), self.page_table.shape[1],
+             self.comp_len[layer].data_ptr(), self.res_len[layer].data_ptr(), self.res_k[layer].data_ptr(),
+             self.res_v[layer].data_ptr(), self.res_k[layer].shape[1], float(sc), splits, _dev.ptr(ws),
+             out.data_ptr(), _dev.dtype_code(out), mode, lse.data_ptr(), _dev.stream())
+        return out, lse
+
     # ------------------------------------------------------------------ export / import (TADAKV1 parity vehicle)
     def export(self, layer: int, b: int = 0) -> dict:
         """Dense reference-layout tensors of one (layer, sequence): means, deviation records, residual rows."""
