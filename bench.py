@@ -262,7 +262,9 @@ def run_ours(args):
     for i in range(warm):
         step(i)
     barrier()
-    launches_before = None
+    from paper_2506_04642_b200._lib import launch_count
+
+    launches_before = launch_count()
     with ClockSampler(local) as clk:
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
@@ -271,6 +273,7 @@ def run_ours(args):
             step(warm + i, record=True)
         t1.record()
         barrier()
+    gpu_launches = launch_count() - launches_before
     ms = t0.elapsed_time(t1)
     if world > 1:
         tt = torch.tensor([ms], device=dev)
@@ -315,7 +318,6 @@ def run_ours(args):
     d2h = out_h.numel() * 2
     store.check_errors()
 
-    launches_per_step = L * (2 + (1 if splits > 1 else 0) + 1)  # residual write, length add, attn (+combine)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "attn_traffic.json")
     if os.path.exists(prof):
@@ -346,7 +348,7 @@ def run_ours(args):
                              "workload": f"prefill bulk quantize-append 32k tokens x batch {B} x 32 layers (config 3 "
                                          f"shape per sequence)", "ms_per_layer": statistics.median(qa_ms)},
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-            "gpu_launches": launches_per_step * steps,
+            "gpu_launches": gpu_launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }

@@ -75,6 +75,8 @@ typedef struct tada_page_layout {
 
 /* ---------------------------------------------------------------- library */
 int tada_abi_version(void);
+/* Kernels this library has launched so far in this process (all entry points, all streams). */
+int64_t tada_launch_count(void);
 const char* tada_last_error(void);
 /* bytes_per_group (quant.py:34-38); -1 on bad width. */
 int64_t tada_bytes_per_group(int32_t group_size, int32_t bits);

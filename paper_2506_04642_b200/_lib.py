@@ -49,6 +49,7 @@ F = C.c_float
 # name -> (restype, argtypes); every symbol declared in include/tadakv_b200.h
 SIGNATURES = {
     "tada_abi_version": (I32, []),
+    "tada_launch_count": (I64, []),
     "tada_last_error": (C.c_char_p, []),
     "tada_bytes_per_group": (I64, [I32, I32]),
     "tada_page_layout_init": (I32, [I32, I32, I32, I32, C.POINTER(PageLayout)]),
@@ -109,3 +110,8 @@ def page_layout(page_tokens: int, heads: int, head_dim: int, bits: int) -> PageL
     lay = PageLayout()
     call("tada_page_layout_init", page_tokens, heads, head_dim, bits, C.byref(lay))
     return lay
+
+
+def launch_count() -> int:
+    """Kernels launched by libtadakv_b200.so so far in this process."""
+    return int(load().tada_launch_count())

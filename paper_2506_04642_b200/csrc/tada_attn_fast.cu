@@ -171,9 +171,11 @@ __host__ __device__ inline Plan make_plan(int H, int gb, int HQ) {
   p.nbands_c = (H * gb) / 128;
   p.mean_bytes = (D * 4 / 128) * BAND;
   p.codes_bytes = p.nbands_c * BAND;
-  p.meta_bytes = up1k(TT * p.trow);
-  p.side_bytes = p.mean_bytes + p.codes_bytes + p.meta_bytes;
-  p.stage_bytes = 2 * p.side_bytes;
+  // stage = [K mean][K codes][V mean][V codes][K meta][V meta]: the swizzled regions stay 1 KB
+  // aligned while the two small meta boxes share the tail (8-bit then fits two stages)
+  p.meta_bytes = up128(TT * p.trow);
+  p.side_bytes = p.mean_bytes + p.codes_bytes;
+  p.stage_bytes = up1k(2 * p.side_bytes + 2 * p.meta_bytes);
   // sbuf doubles as the f16 q staging area (prologue) and the PV partial-sum area (epilogue)
   const int sbuf = up128(2 * HQ * SROW * 4);
   const int stage_q = MT * 16 * D * 2;
@@ -288,7 +290,7 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
 #pragma unroll
       for (int j = 0; j < (H * GB) / 128; ++j)
         tma_3d(d0 + pl.mean_bytes + j * BAND, &maps.m[side][1], 128 * j, row0, page, &full[stg]);
-      tma_3d(d0 + pl.mean_bytes + pl.codes_bytes, &maps.m[side][2], 0, row0, page, &full[stg]);
+      tma_3d(dst + 2 * pl.side_bytes + side * pl.meta_bytes, &maps.m[side][2], 0, row0, page, &full[stg]);
     }
   };
   if (tid == 0) {
@@ -371,10 +373,10 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
     const uint8_t* base = smem + stg * pl.stage_bytes;
     const uint8_t* kmean = base;
     const uint8_t* kcodes = base + pl.mean_bytes;
-    const uint8_t* kmeta = base + pl.mean_bytes + pl.codes_bytes;
+    const uint8_t* kmeta = base + 2 * pl.side_bytes;
     const uint8_t* vmean = base + pl.side_bytes;
     const uint8_t* vcodes = vmean + pl.mean_bytes;
-    const uint8_t* vmeta = vmean + pl.mean_bytes + pl.codes_bytes;
+    const uint8_t* vmeta = kmeta + pl.meta_bytes;
 
     // ---------------------------------------------------------------- QK (warp = token octet x k-half)
     {
@@ -724,7 +726,8 @@ bool fast_supported(const tada_page_layout& L, int Hq) {
   if (L.head_dim != 128 || !(L.bits == 2 || L.bits == 4 || L.bits == 8) || L.heads != 8) return false;
   if (!(Hq == 8 || Hq == 16 || Hq == 32 || Hq == 64)) return false;
   if (L.page_tokens % fast::TT) return false;
-  return fast::make_plan(L.heads, L.group_bytes, Hq).total <= 227 * 1024;
+  const fast::Plan pl = fast::make_plan(L.heads, L.group_bytes, Hq);
+  return pl.stages >= 2 && pl.total <= 227 * 1024;  // one stage cannot overlap load and compute
 }
 
 // ---------------------------------------------------------------- TMA descriptors

@@ -6,6 +6,7 @@
 // _compress_block 182-188).  Codes, scales, mins and means are bit-exact.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdio>
 #include <mutex>
 #include <string>
@@ -20,7 +21,11 @@ int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
+// Every kernel launch in the library is followed by exactly one check_launch, so this counts
+// launches (tada_launch_count; the bench reports it as gpu_launches).
+static std::atomic<int64_t> g_launches{0};
 int check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
   return TADA_OK;
@@ -430,6 +435,8 @@ using namespace tada;
 
 // ====================================================================== C ABI
 extern "C" {
+
+int64_t tada_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int tada_abi_version(void) { return TADA_ABI_VERSION; }
 const char* tada_last_error(void) { return g_err.c_str(); }

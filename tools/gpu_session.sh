@@ -10,13 +10,13 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > 
 if [[ ! -f paper_2506_04642_b200/libtadakv_b200.so ]]; then make -j8 > gpurun_out/make.log 2>&1; fi
 
 if [[ $what == tests || $what == all ]]; then
-  timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+  timeout 900 python -m pytest tests -m gpu -q -rA --timeout 120 --durations 25 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
   timeout 300 python -c 'import __graft_entry__ as g; g.smoke()' > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 fi
 if [[ $what == micro || $what == all ]]; then
   : > gpurun_out/micro.log
   for bits in 2 4 8; do
-    for mode in 1 2; do
+    for mode in ${MODES:-2}; do
       timeout 300 python tools/attn_bench.py --bits $bits --mode $mode >> gpurun_out/micro.log 2>&1
     done
   done
@@ -24,8 +24,15 @@ fi
 if [[ $what == bench || $what == all ]]; then
   timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 fi
+if [[ $what == prof || $what == all ]]; then
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_fast -s 3 -c 1 \
+    -o gpurun_out/attn4 -f python tools/attn_bench.py --bits ${PROF_BITS:-4} --iters 2 > gpurun_out/prof.log 2>&1
+  echo "prof rc=$?" >> gpurun_out/prof.log
+fi
 if [[ $what == ncu || $what == all ]]; then
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
+  # skip prefill (2 launches/layer) + 3 warm-up steps (5 launches/layer/step), list 2 steps
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'attn|combine|residual|lengths|quant' \
+    -s 544 -c 320 --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_bench.log 2>&1
   echo "ncu rc=$?" >> gpurun_out/ncu_bench.log
 fi
