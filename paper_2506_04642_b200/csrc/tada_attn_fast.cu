@@ -1,22 +1,29 @@
-// K2-fast: split-K flash-decoding over the compressed paged cache with the grouped-head
-// contraction on tensor cores (mma.sync m16n8k16, f16 in / f32 accumulate), sm_100a.
+// K2-fast: split-K flash-decoding over the compressed paged cache, sm_100a.
 //
 // Reference semantics: attend_streaming (pkg/src/tadakv/attention.py:103-151) with
-// K̂ = mean - (min + scale*code) (cache.py:193-200, quant.py:177-180).  The kernel uses
-// the algebraically identical factored form (SURVEY §7 hard part 2):
-//   q·k̂      = q·mean − min·Σq − scale·(q·code)
-//   Σ p·v̂    = p·vmean − Σ(p·vmin) − (p∘vscale)·vcode
-// Codes (≤255) are exact in f16, so q·code is exact per product; the f32 means enter
-// as an f16 hi + lo pair (≈22-bit); accumulation is f32.  Residual (uncompressed) rows
-// are handled by attn_residual_kernel into an extra split slot; K3 merges the slots.
+// K̂ = mean - (min + scale*code) (cache.py:193-200, quant.py:177-180).  The kernel uses the
+// algebraically identical factored form (SURVEY §7 hard part 2):
+//   q·k̂   = q·mean − min·Σq − scale·(q·code)
+//   Σ p·v̂ = p·vmean − Σ(p·vmin) + p'·vcode,      p' = −p·vscale
+// and runs both contractions on tensor cores (mma.sync m16n8k16, f16 × f16 → f32).  Codes
+// (≤ 255) are exact in f16; the f32 means enter as an f16 hi + lo pair (≈ 22-bit).
 //
-// CTA = (split, sequence): 8 consumer warps + 1 producer warp.  The producer warp streams
-// 32-token tiles with cp.async.bulk (TMA bulk copies, UBLKCP), one copy per token row into
-// bank-shifted padded rows, through a 2-3 stage mbarrier ring.  Per tile the consumers
-//   1. QK (warp = 8 tokens x half of head_dim): S[g, t] = Q·mean (f16 hi/lo, converted in
-//      registers) - min*sum(q) - scale*(Q·codes), q heads on the MMA M dimension;
-//   2. online softmax per q head (exp2 domain); P and P' = -p*vscale to smem (f16);
-//   3. PV (warp = 16 of head_dim): O[g, d] += P·vmean + P'_h·vcode_h, one f32 accumulator.
+// Why mma.sync and not tcgen05: every operand here is produced in registers (packed codes
+// → f16 by a LOP3 + HSUB2 per pair, means split hi/lo), N is the GQA group (≤ 8), and the
+// kernel is HBM-bound.  tcgen05 would need the dequantised operands written back to shared
+// memory in the UMMA layout first (an extra 64 KB of STS per 32-token tile per side).
+//
+// CTA = (split, sequence), 16 warps.  Warp w owns KV head h = w & 7 and token half
+// hf = w >> 3 of every 32-token tile:
+//   * QK code term, token-on-M: S_h^T[tok, n] = codes_h[tok, d] · Q_h^T[d, n], n = the G q
+//     heads of h (N = 8 columns, G used);
+//   * its own online softmax over its 16 tokens (m, l per q head and half);
+//   * PV code term, d-on-M: O_h^T[d, n] += codes_h^T[d, tok] · P'_h^T[tok, n].
+// The mean terms are shared by all KV heads and are split across the 16 warps as pieces:
+//   * QK: S_mean[q, tok] = Q[q, d] · mean^T[d, tok]     (q-tile, token octet, d half)
+//   * PV: O_mean[q, d]  += P_hf[q, tok] · vmean[tok, d]  (token half, q-tile, 32-wide d block)
+// Tiles stream in with 3-D TMA tensor copies (cp.async.bulk.tensor, 128B swizzle) through a
+// 2-3 stage mbarrier ring; two CTA barriers per tile.
 #include <cuda_runtime.h>
 
 #include <cudaTypedefs.h>
@@ -31,12 +38,13 @@ namespace tada {
 namespace fast {
 
 constexpr int D = 128;
-constexpr int TT = 32;    // tokens per tile
-constexpr int NCW = 8;    // consumer warps
-constexpr int NTHR = NCW * 32;  // no dedicated producer warp: thread 0 issues the TMA copies
-constexpr int SROW = TT + 4;  // logits row stride (floats): conflict-free fragment stores
-constexpr int PROW = TT + 8;  // P row stride (halves): conflict-free B-fragment loads
-constexpr int STAGES = 2;
+constexpr int TT = 32;              // tokens per tile
+constexpr int HT = TT / 2;          // tokens per warp half
+constexpr int NW = 16;              // warps
+constexpr int NTHR = NW * 32;
+constexpr int SROW = TT + 4;        // S_mean row stride (floats)
+constexpr int PROW = HT + 8;        // P / P' row stride (halves): 48-byte rows, conflict-free ldmatrix
+constexpr int BAND = TT * 128;      // bytes of one 128-byte-wide swizzled band of a tile
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -47,9 +55,6 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
-}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n.reg .pred p;\n"
@@ -59,22 +64,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   su32(dst)),
-               "l"(src), "r"(bytes), "r"(su32(bar))
-               : "memory");
-}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NCW * 32) : "memory"); }  // all warps
-
+__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], uint32_t addr) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(addr));
 }
@@ -89,74 +88,68 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
   return r;
 }
-// Masked integer pair (v in the low bits of each 16-bit half) -> exact f16x2 (v0, v1):
-// (0x6400 | v) is the f16 1024 + v; subtracting 1024 is exact.
-__device__ __forceinline__ uint32_t ints_to_h2(uint32_t x) {
+__device__ __forceinline__ uint32_t lop_and_or(uint32_t x, uint32_t m, uint32_t o) {  // (x & m) | o, one LOP3
   uint32_t r;
-  asm("sub.f16x2 %0, %1, %2;" : "=r"(r) : "r"(x | 0x64006400u), "r"(0x64006400u));
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(x), "r"(m), "r"(o));
   return r;
+}
+__device__ __forceinline__ uint32_t hsub2(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("sub.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+// Integer code field (value v at bit position pos of each 16-bit half) -> exact f16x2 (v, v):
+// OR-ing the f16 exponent of 2^(10-pos) makes the half read 2^(10-pos) + v; subtracting the
+// bias is exact.  pos in {0, 2, 4, 6} (bits 0-7 of a half are mantissa bits).
+template <int POS>
+__device__ __forceinline__ uint32_t field_h2(uint32_t x, uint32_t mask_at_0) {
+  constexpr uint32_t bias = POS == 0 ? 0x64006400u : (POS == 2 ? 0x5C005C00u : (POS == 4 ? 0x54005400u : 0x4C004C00u));
+  return hsub2(lop_and_or(x, mask_at_0 << POS, bias), bias);
 }
 __device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
   const __half2 h = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<const uint32_t*>(&h);
 }
+// f32 pair -> f16 hi pair + f16 residual pair (≈ 22 significant bits together)
 __device__ __forceinline__ void split_h2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
   const __half2 h = __floats2half2_rn(x0, x1);
   const float2 back = __half22float2(h);
   hi = *reinterpret_cast<const uint32_t*>(&h);
   lo = pack_h2(x0 - back.x, x1 - back.y);
 }
+// byte offset of (row t, byte o) inside a 128B-swizzled [TT x 128 B] band
+__device__ __forceinline__ int swz(int t, int o) { return t * 128 + ((((o >> 4) ^ t) & 7) << 4) + (o & 15); }
 
-// ------------------------------------------------------------------ k-slot <-> d maps (QK)
-// Thread quad-index i owns d in [32i, 32i+32) of every token; within k-step s its slots
-// (2i, 2i+1, 2i+8, 2i+9) map to d = 32i + base(s) + off[which] so that each f16x2
-// operand is one masked shift of a packed code word (see file header).
+// ------------------------------------------------------------------ QK code operand (token-on-M)
+// Thread quad-index c owns d in [32c, 32c+32) of every token row; k-step s takes 4 of them
+// (slots 2c, 2c+1 | 2c+8, 2c+9).  dq() is the d of each slot, used to lay out Q to match.
 template <int BITS>
-__device__ __forceinline__ int slot_base(int s) {
-  return BITS == 4 ? 8 * (s >> 1) + 2 * (s & 1) : (BITS == 2 ? 16 * (s >> 2) + 2 * (s & 3) : 4 * s);
+__host__ __device__ __forceinline__ int dq(int s, int c, int slot) {
+  const int lo = slot & 1, hi = slot >> 1;  // slot: 0 = (2c), 1 = (2c+1), 2 = (2c+8), 3 = (2c+9)
+  if (BITS == 4) return 32 * c + 8 * (s >> 1) + 2 * (s & 1) + hi + 4 * lo;
+  if (BITS == 2) return 32 * c + 16 * (s >> 2) + 2 * (s & 3) + hi + 8 * lo;
+  return 32 * c + 4 * s + hi + 2 * lo;
 }
+// f16x2 of (slot 2c, 2c+1) [which = 0] or (2c+8, 2c+9) [which = 1] of k-step s from the row's words
 template <int BITS>
-__device__ __forceinline__ int slot_off1() {
-  return BITS == 4 ? 4 : (BITS == 2 ? 8 : 2);
-}
-// slot 'which' (0: 2i, 1: 2i+1, 2: 2i+8, 3: 2i+9) -> d offset within the thread's 32-d block
-template <int BITS>
-__device__ __forceinline__ int slot_d(int s, int which) {
-  const int o1 = slot_off1<BITS>();
-  const int off = which == 0 ? 0 : (which == 1 ? o1 : (which == 2 ? 1 : o1 + 1));
-  return slot_base<BITS>(s) + off;
-}
-
-// Code A-fragment regs for one token row (QK): from the thread's packed words of that row.
-template <int BITS>
-__device__ __forceinline__ void qk_code_pair(const uint32_t* w, int s, uint32_t& lo, uint32_t& hi) {
+__device__ __forceinline__ uint32_t qk_pair(const uint32_t* w, int s, int which) {
   if (BITS == 4) {
-    const uint32_t x = w[s >> 1] >> (8 * (s & 1));
-    lo = ints_to_h2(x & 0x000F000Fu);
-    hi = ints_to_h2((x >> 4) & 0x000F000Fu);
+    const uint32_t x = (s & 1) ? (w[s >> 1] >> 8) : w[s >> 1];
+    return which ? field_h2<4>(x, 0x000F000Fu) : field_h2<0>(x, 0x000F000Fu);
   } else if (BITS == 2) {
-    const uint32_t x = w[s >> 2] >> (4 * (s & 3));
-    lo = ints_to_h2(x & 0x00030003u);
-    hi = ints_to_h2((x >> 2) & 0x00030003u);
+    const uint32_t x = (s & 2) ? (w[s >> 2] >> 8) : w[s >> 2];
+    if (s & 1) return which ? field_h2<6>(x, 0x00030003u) : field_h2<4>(x, 0x00030003u);
+    return which ? field_h2<2>(x, 0x00030003u) : field_h2<0>(x, 0x00030003u);
   } else {
-    lo = ints_to_h2(prmt(w[s], 0, 0x4240u) & 0x00FF00FFu);
-    hi = ints_to_h2(prmt(w[s], 0, 0x4341u) & 0x00FF00FFu);
+    return hsub2(prmt(w[s], 0x64646464u, which ? 0x4341u : 0x4240u), 0x64006400u);
   }
 }
 
 // ------------------------------------------------------------------ shared memory plan
-// A stage holds one 32-token tile of both sides, loaded with 3-D TMA tensor copies
-// (cp.async.bulk.tensor, UTMALDG) from the paged pool:
-//   mean  : 4 bands of [32 rows x 128 B], 128B-swizzled  (D*4 = 512 B per row)
-//   codes : H*gb/128 bands of [32 rows x 128 B], 128B-swizzled
-//   meta  : one box [32 rows x TROW B] (TROW = H*8 + 16: the 16 B past the row are the
-//           TMA's out-of-bounds zero fill, which shifts banks by 4 per row)
-constexpr int BAND = TT * 128;  // bytes per 128-byte-wide band of a tile
-
 struct Plan {
-  int H, gb, trow, nbands_c;
   int mean_bytes, codes_bytes, meta_bytes, side_bytes, stage_bytes, stages;
-  int off_sbuf, off_pbuf, off_p2m, off_qsum, off_corr, off_stats, off_bar, total;
+  int trow;
+  int off_smean, off_pbuf, off_p2, off_corr, off_stats, off_qsum, off_bar, total;
 };
 
 __host__ __device__ inline int up128(int x) { return (x + 127) / 128 * 128; }
@@ -164,115 +157,84 @@ __host__ __device__ inline int up1k(int x) { return (x + 1023) / 1024 * 1024; }
 
 __host__ __device__ inline Plan make_plan(int H, int gb, int HQ) {
   Plan p{};
-  const int MT = (HQ + 15) / 16;
-  p.H = H;
-  p.gb = gb;
-  p.trow = H * 8 + 16;
-  p.nbands_c = (H * gb) / 128;
+  const int mrows = HQ >= 16 ? HQ : 16;
+  p.trow = H * 8 + 16;  // meta box row: the 16 B past the row are TMA zero fill (shifts banks by 4 per row)
   p.mean_bytes = (D * 4 / 128) * BAND;
-  p.codes_bytes = p.nbands_c * BAND;
-  // stage = [K mean][K codes][V mean][V codes][K meta][V meta]: the swizzled regions stay 1 KB
-  // aligned while the two small meta boxes share the tail (8-bit then fits two stages)
+  p.codes_bytes = (H * gb / 128) * BAND;
+  // stage = [K mean][K codes][V mean][V codes][K meta][V meta]: swizzled regions stay 1 KB aligned
   p.meta_bytes = up128(TT * p.trow);
   p.side_bytes = p.mean_bytes + p.codes_bytes;
   p.stage_bytes = up1k(2 * p.side_bytes + 2 * p.meta_bytes);
-  // sbuf doubles as the f16 q staging area (prologue) and the PV partial-sum area (epilogue)
-  const int sbuf = up128(2 * HQ * SROW * 4);
-  const int stage_q = MT * 16 * D * 2;
-  const int sb = sbuf > stage_q ? sbuf : stage_q;
-  const int tail = sb + up128(MT * 16 * PROW * 2) + up128(H * 16 * PROW * 2) + 2 * up128(HQ * 4) + up128(HQ * 16) +
-                   128 + 1024;
+  const int smean = up128(2 * mrows * SROW * 4);  // also the f16 q staging area of the prologue
+  const int tail = smean + up128(2 * mrows * PROW * 2) + up128(NW * 8 * PROW * 2) + up128(2 * mrows * 4) +
+                   up128(2 * HQ * 16) + up128(HQ * 4) + 128 + 1024;
   const int budget = 227 * 1024;
   p.stages = (3 * p.stage_bytes + tail <= budget) ? 3 : ((2 * p.stage_bytes + tail <= budget) ? 2 : 1);
   int off = p.stages * p.stage_bytes;
-  p.off_sbuf = off;
-  off += sb;
+  // the epilogue parks both halves' partial outputs [2][HQ][D] f32 in the (idle) stages
+  if (off < 2 * HQ * D * 4) p.stages = 0;
+  p.off_smean = off;
+  off += smean;
   p.off_pbuf = off;
-  off += up128(MT * 16 * PROW * 2);
-  p.off_p2m = off;
-  off += up128(H * 16 * PROW * 2);
+  off += up128(2 * mrows * PROW * 2);
+  p.off_p2 = off;
+  off += up128(NW * 8 * PROW * 2);
+  p.off_corr = off;
+  off += up128(2 * mrows * 4);
+  p.off_stats = off;
+  off += up128(2 * HQ * 16);
   p.off_qsum = off;
   off += up128(HQ * 4);
-  p.off_corr = off;
-  off += up128(HQ * 4);
-  p.off_stats = off;
-  off += up128(HQ * 16);
   p.off_bar = off;
   off += 128;
   p.total = off + 1024;
   return p;
 }
 
-// byte offset of (row t, byte o) inside a 128B-swizzled [TT x 128 B] band
-__device__ __forceinline__ int swz(int t, int o) { return t * 128 + ((((o >> 4) ^ t) & 7) << 4) + (o & 15); }
-
-__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
-          "r"(su32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
-      : "memory");
-}
-// Wait with a suspend-time hint: the thread sleeps in hardware instead of spinning.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n.reg .pred p;\n"
-      "TADA_WAITS_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-      "@!p bra TADA_WAITS_%=;\n}\n" ::"r"(su32(bar)),
-      "r"(parity), "r"(1000000u)
-      : "memory");
-}
-
 // ------------------------------------------------------------------ the kernel
-// Fragment orientation: q heads on M for both products.
-//   QK: S[g, t] = Q[g, d] · K̂^T[d, t]    A = Q (registers, f16), B = K-mean / K-codes tiles
-//       warp = (token octet, half of head_dim)
-//   PV: O[g, d] = P[g, t] · V̂[t, d]      A = P, P'_h (smem, ldmatrix), B = V-mean / V-codes tiles
-//       warp = (32-wide d slice, 16-token half of the tile)
-// so every mean and code byte of a tile is read from smem by exactly one warp.
-template <int BITS, int HQ, int H>
+template <int BITS, int HQ>
 __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __grid_constant__ TmaMaps maps) {
   extern __shared__ uint8_t smem_raw[];
   // 1 KB alignment (128B-swizzle atoms) by pointer arithmetic on the __shared__ array, so the
   // compiler keeps the shared state space (LDS, 32-bit addressing) for every access below
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
-  constexpr int G = HQ / H;
-  constexpr int MT = (HQ + 15) / 16;    // m-tiles of 16 q heads
-  constexpr int HPM = 16 / G < H ? 16 / G : H;  // kv heads per m-tile
-  constexpr int TPH = (NCW * 32) / HQ;  // softmax threads per q head
-  constexpr int TPT = TT / TPH;         // tokens per softmax thread
-  constexpr int GB = BITS * D / 8;      // code bytes per (token, head)
+  constexpr int H = 8;
+  constexpr int G = HQ / H;                     // q heads per KV head (N columns used)
+  constexpr int MT = HQ >= 16 ? HQ / 16 : 1;    // 16-row q tiles
+  constexpr int MROWS = MT * 16;
+  constexpr int GB = BITS * D / 8;              // code bytes per (token, head)
+  constexpr int NPIECE = 8 * MT;                // mean-term pieces per tile (each of QK and PV)
+  constexpr int NPW = (NPIECE + NW - 1) / NW;   // pieces per warp
   const int P = a.L.page_tokens;
   const Plan pl = make_plan(H, GB, HQ);
-  const int b = blockIdx.y, split = blockIdx.x;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r = lane >> 2, qi = lane & 3;
-
-  float* sbuf = reinterpret_cast<float*>(smem + pl.off_sbuf);  // [2][HQ][SROW]
-  __half* pbuf = reinterpret_cast<__half*>(smem + pl.off_pbuf);  // [MT*16][PROW]
-  __half* p2m = reinterpret_cast<__half*>(smem + pl.off_p2m);    // [H][16][PROW]: -p*vscale, rows of kv head h only
-  float* qsum = reinterpret_cast<float*>(smem + pl.off_qsum);
-  float* corr_s = reinterpret_cast<float*>(smem + pl.off_corr);
-  float* stats = reinterpret_cast<float*>(smem + pl.off_stats);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + pl.off_bar);
   const int S = pl.stages;
+  const int b = blockIdx.y, split = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r = lane >> 2, c = lane & 3;
+  const int h = warp & 7, half = warp >> 3;
+
+  float* smean = reinterpret_cast<float*>(smem + pl.off_smean);  // [2 d-halves][MROWS][SROW]
+  __half* pbuf = reinterpret_cast<__half*>(smem + pl.off_pbuf);  // [2 token halves][MROWS][PROW]
+  __half* p2 = reinterpret_cast<__half*>(smem + pl.off_p2) + warp * 8 * PROW;  // this warp's P'^T [8 n][PROW]
+  float* corrb = reinterpret_cast<float*>(smem + pl.off_corr);   // [2][MROWS]
+  float* stats = reinterpret_cast<float*>(smem + pl.off_stats);  // [2][HQ][4] = (m, l, bp, -)
+  float* qsum = reinterpret_cast<float*>(smem + pl.off_qsum);    // [HQ]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + pl.off_bar);
 
   const int C = a.comp_len[b];
   int t_begin, t_end;
   split_range(C, a.splits, split, TT, t_begin, t_end);
-  const int ntiles = (t_end - t_begin + TT - 1) / TT;
+  const int ntiles = t_end > t_begin ? (t_end - t_begin + TT - 1) / TT : 0;
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // zero P'_h (rows not belonging to head h stay zero forever) and the padded P rows
-  for (int i = tid; i < (H * 16 * PROW) / 2; i += NTHR) reinterpret_cast<uint32_t*>(p2m)[i] = 0u;
-  for (int i = tid; i < (MT * 16 * PROW) / 2; i += NTHR) reinterpret_cast<uint32_t*>(pbuf)[i] = 0u;
+  // padded P rows (q >= HQ) must read as zero forever
+  for (int i = tid; i < (2 * MROWS * PROW) / 2; i += NTHR) reinterpret_cast<uint32_t*>(pbuf)[i] = 0u;
   __syncthreads();
 
-  // TMA producer (thread 0): tile `it` -> stage it % S.  A stage is refilled only after a
-  // consumer barrier that every warp reaches after finishing the stage's previous tile.
+  // TMA producer (thread 0): tile `it` -> stage it % S.  A stage is refilled only after the CTA
+  // barrier that every warp reaches once it has finished the stage's previous tile.
   const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
   const uint32_t tx = 2u * uint32_t(pl.mean_bytes + pl.codes_bytes + TT * pl.trow);
   auto issue = [&](int it) {
@@ -300,70 +262,81 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
     for (int it = 0; it < S - 1 && it < ntiles; ++it) issue(it);
   }
 
-  // ================================================================== consumers
-  // prologue: q rows -> f32 row sums (min term) + f16 copy (staged in sbuf)
+  // ---------------------------------------------------------------- prologue: q -> f16 fragments
   {
-    __half* q16 = reinterpret_cast<__half*>(sbuf);
-    for (int g = warp; g < MT * 16; g += NCW) {
+    __half* q16 = reinterpret_cast<__half*>(smean);  // staging [MROWS][D]
+    for (int g = warp; g < MROWS; g += NW) {
       float v[4] = {0.f, 0.f, 0.f, 0.f};
       if (g < HQ) {
         if (a.q_dtype == TADA_F32) load4(reinterpret_cast<const float*>(a.q) + (int64_t(b) * HQ + g) * D + 4 * lane, v);
         else load4(reinterpret_cast<const __nv_bfloat16*>(a.q) + (int64_t(b) * HQ + g) * D + 4 * lane, v);
       }
-      const float ssum = warp_sum(v[0] + v[1] + v[2] + v[3]);
+      const uint32_t lo = pack_h2(v[0], v[1]), hi = pack_h2(v[2], v[3]);
+      *reinterpret_cast<uint2*>(q16 + g * D + 4 * lane) = make_uint2(lo, hi);
+      // Σq of the f16-rounded q, so that every term of the factored form uses the same q
+      const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&lo));
+      const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&hi));
+      const float ssum = warp_sum((f0.x + f0.y) + (f1.x + f1.y));
       if (lane == 0 && g < HQ) qsum[g] = ssum;
-      *reinterpret_cast<uint2*>(q16 + g * D + 4 * lane) = make_uint2(pack_h2(v[0], v[1]), pack_h2(v[2], v[3]));
     }
   }
-  consumer_sync();
-  const int kh = warp & 1, tq = 8 * (warp >> 1) + r;  // QK: k-half and this thread's B column (token)
-  const int tc0 = 8 * (warp >> 1) + 2 * qi;           // QK accumulator columns (tokens) tc0, tc0+1
-  uint32_t qa[MT][4][4];
+  __syncthreads();
+  // QK code B operand (Q_h^T, d permuted to the code slots), column n = r <-> q head h*G + r
+  uint32_t qb[8][2];
   {
-    const __half* q16 = reinterpret_cast<const __half*>(sbuf);
+    const __half* q16 = reinterpret_cast<const __half*>(smean);
+    const int g = h * G + r;
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-      for (int k4 = 0; k4 < 4; ++k4) {
-        const int s = 4 * kh + k4, dq = 32 * qi;
-        const int g0 = 16 * mt + r, g1 = g0 + 8;
-        auto q2 = [&](int g, int w0, int w1) -> uint32_t {
-          const __half2 h = __halves2half2(q16[g * D + dq + slot_d<BITS>(s, w0)], q16[g * D + dq + slot_d<BITS>(s, w1)]);
-          return *reinterpret_cast<const uint32_t*>(&h);
-        };
-        qa[mt][k4][0] = q2(g0, 0, 1);
-        qa[mt][k4][1] = q2(g1, 0, 1);
-        qa[mt][k4][2] = q2(g0, 2, 3);
-        qa[mt][k4][3] = q2(g1, 2, 3);
+    for (int s = 0; s < 8; ++s) {
+      if (r < G) {
+        const __half* qr = q16 + g * D;
+        qb[s][0] = pack_h2(__half2float(qr[dq<BITS>(s, c, 0)]), __half2float(qr[dq<BITS>(s, c, 1)]));
+        qb[s][1] = pack_h2(__half2float(qr[dq<BITS>(s, c, 2)]), __half2float(qr[dq<BITS>(s, c, 3)]));
+      } else {
+        qb[s][0] = qb[s][1] = 0u;
       }
-  }
-  // kv head of this thread's accumulator rows (16mt + r, 16mt + r + 8); -1 = padding row
-  int kvr[MT][2];
-  float qsr[MT][2];
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int g = 16 * mt + r + 8 * e;
-      kvr[mt][e] = g < HQ ? g / G : -1;
-      qsr[mt][e] = g < HQ ? qsum[g] : 0.f;
     }
-  // QK code addresses: (row tq, byte h*GB + off) with off = (32qi + 16kh)*BITS/8 < 128
-  constexpr int CW = BITS == 8 ? 4 : (BITS == 4 ? 2 : 1);  // code words per (token, head) per thread
-  const int qk_c0 = swz(tq, ((32 * qi + 16 * kh) * BITS) / 8);
-  // PV: warp = (d slice dq of 32, token half kk); B column r <-> d = 32dq + 4r + n (n-tile n = 0..3)
-  const int dq = warp & 3, kk = warp >> 2;
-  float oacc[MT][4][4];
+  }
+  // QK mean A operand per piece (q tile mt, d half kh): slots (2c,2c+1 | 2c+8,2c+9) <-> d = 16s+4c+(0,1 | 2,3)
+  uint32_t qa[NPW][4][4];
 #pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
+  for (int pi = 0; pi < NPW; ++pi) {
+    const int p = warp + NW * pi;
+    const int mt = p >> 3, kh = p & 1;
+    const __half* q16 = reinterpret_cast<const __half*>(smean);
 #pragma unroll
-    for (int n = 0; n < 4; ++n)
+    for (int k4 = 0; k4 < 4; ++k4) {
+      const int s = 4 * kh + k4;
+      if (p < NPIECE) {
+        const __half* r0 = q16 + (16 * mt + r) * D + 16 * s + 4 * c;
+        const __half* r1 = r0 + 8 * D;
+        qa[pi][k4][0] = *reinterpret_cast<const uint32_t*>(r0);
+        qa[pi][k4][1] = *reinterpret_cast<const uint32_t*>(r1);
+        qa[pi][k4][2] = *reinterpret_cast<const uint32_t*>(r0 + 2);
+        qa[pi][k4][3] = *reinterpret_cast<const uint32_t*>(r1 + 2);
+      } else {
+        qa[pi][k4][0] = qa[pi][k4][1] = qa[pi][k4][2] = qa[pi][k4][3] = 0u;
+      }
+    }
+  }
+  float qs[2];  // Σq of this thread's two code columns n = 2c, 2c+1
 #pragma unroll
-      for (int e = 0; e < 4; ++e) oacc[mt][n][e] = 0.f;
-  const int sg = tid / TPH, spart = tid % TPH, sh = sg / G;  // softmax ownership
-  float m_run = -__int_as_float(0x7f800000), l_part = 0.f, bp_part = 0.f;
+  for (int e = 0; e < 2; ++e) qs[e] = (2 * c + e < G) ? qsum[h * G + 2 * c + e] : 0.f;
+  __syncthreads();  // the q staging area becomes S_mean
+
+  // accumulators
+  float oc[8][4];        // PV code term, O_h^T: m-tile of 16 d (rows) x 8 n (cols)
+  float om[NPW][4][4];   // PV mean-term piece: q tile rows x 4 n-tiles of d
+#pragma unroll
+  for (int i = 0; i < 8; ++i) oc[i][0] = oc[i][1] = oc[i][2] = oc[i][3] = 0.f;
+#pragma unroll
+  for (int pi = 0; pi < NPW; ++pi)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) om[pi][j][0] = om[pi][j][1] = om[pi][j][2] = om[pi][j][3] = 0.f;
+  float m_run[2] = {-__int_as_float(0x7f800000), -__int_as_float(0x7f800000)};
+  float l_part[2] = {0.f, 0.f}, bp_part[2] = {0.f, 0.f};
   const float scale_log2 = a.scale * 1.4426950408889634f;
-  consumer_sync();  // q16 staging area is dead from here on
+  const float NEG_INF = -__int_as_float(0x7f800000);
 
   for (int it = 0; it < ntiles; ++it) {
     const int stg = it % S;
@@ -373,219 +346,255 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
     const uint8_t* base = smem + stg * pl.stage_bytes;
     const uint8_t* kmean = base;
     const uint8_t* kcodes = base + pl.mean_bytes;
-    const uint8_t* kmeta = base + 2 * pl.side_bytes;
     const uint8_t* vmean = base + pl.side_bytes;
     const uint8_t* vcodes = vmean + pl.mean_bytes;
+    const uint8_t* kmeta = base + 2 * pl.side_bytes;
     const uint8_t* vmeta = kmeta + pl.meta_bytes;
+    if (nv < TT) {  // tail tile: rows past the sequence may hold anything; P·vmean needs them finite
+      uint8_t* vm = const_cast<uint8_t*>(vmean);
+      for (int i = tid; i < (TT - nv) * 32; i += NTHR) {
+        const int t = nv + (i >> 5), j = i & 31;
+        *reinterpret_cast<uint4*>(vm + (j >> 3) * BAND + t * 128 + (j & 7) * 16) = make_uint4(0u, 0u, 0u, 0u);
+      }
+      fence_proxy_async();  // generic writes before the next async (TMA) refill of this stage
+    }
 
-    // ---------------------------------------------------------------- QK (warp = token octet x k-half)
-    {
-      float acc[MT][4];
+    // ------------------------------------------------------------ QK mean pieces -> S_mean
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
-      // mean term: d = 32qi + 16kh + [0,16) of token tq = band qi, bytes 64kh + [0,64)
-      float x[16];
+    for (int pi = 0; pi < NPW; ++pi) {
+      const int p = warp + NW * pi;
+      if (p < NPIECE) {
+        const int mt = p >> 3, nt = (p >> 1) & 3, kh = p & 1;
+        const int tok = 8 * nt + r;
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float4 v = *reinterpret_cast<const float4*>(kmean + qi * BAND + swz(tq, 64 * kh + 16 * u));
-        x[4 * u] = v.x; x[4 * u + 1] = v.y; x[4 * u + 2] = v.z; x[4 * u + 3] = v.w;
-      }
-#pragma unroll
-      for (int k4 = 0; k4 < 4; ++k4) {
-        const int rb = slot_base<BITS>(k4), o1 = slot_off1<BITS>();  // == slot_base(4kh+k4) - 16kh
-        uint32_t h0, l0, h1, l1;
-        split_h2(x[rb], x[rb + o1], h0, l0);
-        split_h2(x[rb + 1], x[rb + o1 + 1], h1, l1);
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          mma(acc[mt], qa[mt][k4], h0, h1);
-          mma(acc[mt], qa[mt][k4], l0, l1);
+        for (int k4 = 0; k4 < 4; ++k4) {
+          const int s = 4 * kh + k4;
+          const float4 x = *reinterpret_cast<const float4*>(kmean + (s >> 1) * BAND + swz(tok, 64 * (s & 1) + 16 * c));
+          uint32_t h0, l0, h1, l1;
+          split_h2(x.x, x.y, h0, l0);
+          split_h2(x.z, x.w, h1, l1);
+          mma(acc, qa[pi][k4], h0, h1);
+          mma(acc, qa[pi][k4], l0, l1);
         }
-      }
-      // code term: per m-tile, its HPM kv heads as independent accumulation chains
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        uint32_t w[HPM][CW];
-        float cacc[HPM][4];
-#pragma unroll
-        for (int j = 0; j < HPM; ++j) {
-          const int h = mt * HPM + j;
-          const int hb = h * GB;
-          const uint8_t* cp = kcodes + (hb >> 7) * BAND + (qk_c0 ^ (hb & 127));
-          if (CW == 4) {
-            const uint4 v = *reinterpret_cast<const uint4*>(cp);
-            w[j][0] = v.x; w[j][1 % CW] = v.y; w[j][2 % CW] = v.z; w[j][3 % CW] = v.w;
-          } else if (CW == 2) {
-            const uint2 v = *reinterpret_cast<const uint2*>(cp);
-            w[j][0] = v.x; w[j][1 % CW] = v.y;
-          } else {
-            w[j][0] = *reinterpret_cast<const uint32_t*>(cp);
-          }
-          cacc[j][0] = cacc[j][1] = cacc[j][2] = cacc[j][3] = 0.f;
-        }
-#pragma unroll
-        for (int k4 = 0; k4 < 4; ++k4)
-#pragma unroll
-          for (int j = 0; j < HPM; ++j) {
-            uint32_t b0, b1;
-            qk_code_pair<BITS>(w[j], k4, b0, b1);
-            mma(cacc[j], qa[mt][k4], b0, b1);
-          }
-#pragma unroll
-        for (int j = 0; j < HPM; ++j) {
-          const int h = mt * HPM + j;
-          const float2 ma = *reinterpret_cast<const float2*>(kmeta + tc0 * pl.trow + h * 8);
-          const float2 mb = *reinterpret_cast<const float2*>(kmeta + (tc0 + 1) * pl.trow + h * 8);
-          const float mna = kh == 0 ? ma.y : 0.f, mnb = kh == 0 ? mb.y : 0.f;
-          if (kvr[mt][0] == h) {
-            acc[mt][0] = fmaf(-ma.x, cacc[j][0], fmaf(-mna, qsr[mt][0], acc[mt][0]));
-            acc[mt][1] = fmaf(-mb.x, cacc[j][1], fmaf(-mnb, qsr[mt][0], acc[mt][1]));
-          }
-          if (kvr[mt][1] == h) {
-            acc[mt][2] = fmaf(-ma.x, cacc[j][2], fmaf(-mna, qsr[mt][1], acc[mt][2]));
-            acc[mt][3] = fmaf(-mb.x, cacc[j][3], fmaf(-mnb, qsr[mt][1], acc[mt][3]));
-          }
-        }
-      }
-      float* sb = sbuf + kh * HQ * SROW;
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        const int g0 = 16 * mt + r, g1 = g0 + 8;
-        if (g0 < HQ) *reinterpret_cast<float2*>(sb + g0 * SROW + tc0) = make_float2(acc[mt][0], acc[mt][1]);
-        if (g1 < HQ) *reinterpret_cast<float2*>(sb + g1 * SROW + tc0) = make_float2(acc[mt][2], acc[mt][3]);
+        float* sm = smean + (kh * MROWS + 16 * mt + r) * SROW + 8 * nt + 2 * c;
+        *reinterpret_cast<float2*>(sm) = make_float2(acc[0], acc[1]);
+        *reinterpret_cast<float2*>(sm + 8 * SROW) = make_float2(acc[2], acc[3]);
       }
     }
-    consumer_sync();
-
-    // every warp has finished tile it-1 (its PV) -> refill that stage with tile it+S-1
+    // ------------------------------------------------------------ QK code term (head h, token half)
+    const int ta = HT * half + r, tb = ta + 8;  // this thread's accumulator rows (tokens)
+    float cs[4] = {0.f, 0.f, 0.f, 0.f};
+    {
+      constexpr int NWD = BITS == 8 ? 8 : (BITS == 4 ? 4 : 2);  // code words per row segment
+      uint32_t wa[NWD], wb[NWD];
+      const int hb = h * GB + c * (GB / 4);
+      const uint8_t* cb = kcodes + (hb >> 7) * BAND;
+      const int o = hb & 127;
+      if (BITS == 4) {
+        const uint4 x = *reinterpret_cast<const uint4*>(cb + swz(ta, o));
+        const uint4 y = *reinterpret_cast<const uint4*>(cb + swz(tb, o));
+        wa[0] = x.x; wa[1 % NWD] = x.y; wa[2 % NWD] = x.z; wa[3 % NWD] = x.w;
+        wb[0] = y.x; wb[1 % NWD] = y.y; wb[2 % NWD] = y.z; wb[3 % NWD] = y.w;
+      } else if (BITS == 2) {
+        const uint2 x = *reinterpret_cast<const uint2*>(cb + swz(ta, o));
+        const uint2 y = *reinterpret_cast<const uint2*>(cb + swz(tb, o));
+        wa[0] = x.x; wa[1] = x.y;
+        wb[0] = y.x; wb[1] = y.y;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint4 x = *reinterpret_cast<const uint4*>(cb + swz(ta, o + 16 * u));
+          const uint4 y = *reinterpret_cast<const uint4*>(cb + swz(tb, o + 16 * u));
+          wa[(4 * u) % NWD] = x.x; wa[(4 * u + 1) % NWD] = x.y; wa[(4 * u + 2) % NWD] = x.z; wa[(4 * u + 3) % NWD] = x.w;
+          wb[(4 * u) % NWD] = y.x; wb[(4 * u + 1) % NWD] = y.y; wb[(4 * u + 2) % NWD] = y.z; wb[(4 * u + 3) % NWD] = y.w;
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        uint32_t af[4];
+        af[0] = qk_pair<BITS>(wa, s, 0);
+        af[1] = qk_pair<BITS>(wb, s, 0);
+        af[2] = qk_pair<BITS>(wa, s, 1);
+        af[3] = qk_pair<BITS>(wb, s, 1);
+        mma(cs, af, qb[s][0], qb[s][1]);
+      }
+    }
+    __syncthreads();  // ---- BARRIER A: S_mean complete; every warp is done with the previous tile
     if (tid == 0 && it + S - 1 < ntiles) issue(it + S - 1);
-    // ---------------------------------------------------------------- online softmax
-    {
-      float x[TPT];
-      float tmax = -__int_as_float(0x7f800000);
-#pragma unroll
-      for (int u = 0; u < TPT; ++u) {
-        const int t = spart + TPH * u;
-        x[u] = t < nv ? (sbuf[sg * SROW + t] + sbuf[(HQ + sg) * SROW + t]) * scale_log2 : -__int_as_float(0x7f800000);
-        tmax = fmaxf(tmax, x[u]);
-      }
-#pragma unroll
-      for (int o = TPH / 2; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
-      const float m_new = fmaxf(m_run, tmax);  // in log2 units
-      const float corr = exp2f(m_run - m_new);
-      m_run = m_new;
-      float lsum = 0.f, bsum = 0.f;
-      __half* p2row = p2m + (sh * 16 + (sg & 15)) * PROW;
-#pragma unroll
-      for (int u = 0; u < TPT; ++u) {
-        const int t = spart + TPH * u;
-        const float p = exp2f(x[u] - m_new);
-        const float2 vm = t < nv ? *reinterpret_cast<const float2*>(vmeta + t * pl.trow + sh * 8) : make_float2(0.f, 0.f);
-        lsum += p;
-        bsum = fmaf(p, vm.y, bsum);
-        pbuf[sg * PROW + t] = __float2half_rn(p);
-        p2row[t] = __float2half_rn(-p * vm.x);
-      }
-      l_part = l_part * corr + lsum;
-      bp_part = bp_part * corr + bsum;
-      if (spart == 0) corr_s[sg] = corr;
-    }
-    consumer_sync();
 
-    // ---------------------------------------------------------------- PV (warp = 32-wide d slice x 16 tokens)
+    // ------------------------------------------------------------ online softmax (own head, own half)
+    float corr[2];
     {
+      const float2 ka = *reinterpret_cast<const float2*>(kmeta + ta * pl.trow + 8 * h);
+      const float2 kb = *reinterpret_cast<const float2*>(kmeta + tb * pl.trow + 8 * h);
+      const float2 va = *reinterpret_cast<const float2*>(vmeta + ta * pl.trow + 8 * h);
+      const float2 vb = *reinterpret_cast<const float2*>(vmeta + tb * pl.trow + 8 * h);
+      const bool oka = ta < nv, okb = tb < nv;
+      float x[4];
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        const float c0 = kvr[mt][0] >= 0 ? corr_s[16 * mt + r] : 0.f;
-        const float c1 = kvr[mt][1] >= 0 ? corr_s[16 * mt + r + 8] : 0.f;
-#pragma unroll
-        for (int n = 0; n < 4; ++n) {
-          oacc[mt][n][0] *= c0;
-          oacc[mt][n][1] *= c0;
-          oacc[mt][n][2] *= c1;
-          oacc[mt][n][3] *= c1;
+      for (int e = 0; e < 2; ++e) {
+        const int n = 2 * c + e;
+        const int g = h * G + n;
+        if (n < G) {
+          const float* s0 = smean + g * SROW;
+          const float* s1 = smean + (MROWS + g) * SROW;
+          x[e] = oka ? ((s0[ta] + s1[ta]) - fmaf(ka.x, cs[e], ka.y * qs[e])) * scale_log2 : NEG_INF;
+          x[2 + e] = okb ? ((s0[tb] + s1[tb]) - fmaf(kb.x, cs[2 + e], kb.y * qs[e])) * scale_log2 : NEG_INF;
+        } else {
+          x[e] = x[2 + e] = NEG_INF;
         }
       }
-      const int ta = 16 * kk + 2 * qi;  // this thread's B rows: tokens ta, ta+1, ta+8, ta+9
-      // mean term: float4 of d = 32dq + 4r .. +3 for each of the 4 tokens
-      uint32_t bh[4][2], bl[4][2];
-      {
-        const uint8_t* vb = vmean + dq * BAND;
-        const float4 xa = *reinterpret_cast<const float4*>(vb + swz(ta, 16 * r));
-        const float4 xb = *reinterpret_cast<const float4*>(vb + swz(ta + 1, 16 * r));
-        const float4 xc = *reinterpret_cast<const float4*>(vb + swz(ta + 8, 16 * r));
-        const float4 xd = *reinterpret_cast<const float4*>(vb + swz(ta + 9, 16 * r));
-        split_h2(xa.x, xb.x, bh[0][0], bl[0][0]);
-        split_h2(xc.x, xd.x, bh[0][1], bl[0][1]);
-        split_h2(xa.y, xb.y, bh[1][0], bl[1][0]);
-        split_h2(xc.y, xd.y, bh[1][1], bl[1][1]);
-        split_h2(xa.z, xb.z, bh[2][0], bl[2][0]);
-        split_h2(xc.z, xd.z, bh[2][1], bl[2][1]);
-        split_h2(xa.w, xb.w, bh[3][0], bl[3][0]);
-        split_h2(xc.w, xd.w, bh[3][1], bl[3][1]);
-      }
-      const int mrow = (lane & 7) + 8 * ((lane >> 3) & 1), tcol = 16 * kk + 8 * (lane >> 4);
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
+      for (int e = 0; e < 2; ++e) {
+        float tmax = fmaxf(x[e], x[2 + e]);
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
+        const float m_new = fmaxf(m_run[e], tmax);
+        corr[e] = m_new == NEG_INF ? 1.f : exp2f(m_run[e] - m_new);
+        m_run[e] = m_new;
+        const float pa = x[e] == NEG_INF ? 0.f : exp2f(x[e] - m_new);
+        const float pb = x[2 + e] == NEG_INF ? 0.f : exp2f(x[2 + e] - m_new);
+        l_part[e] = fmaf(l_part[e], corr[e], pa + pb);
+        bp_part[e] = fmaf(bp_part[e], corr[e], fmaf(pa, oka ? va.y : 0.f, pb * (okb ? vb.y : 0.f)));
+        const int n = 2 * c + e;
+        p2[n * PROW + r] = __float2half_rn(oka ? -pa * va.x : 0.f);
+        p2[n * PROW + r + 8] = __float2half_rn(okb ? -pb * vb.x : 0.f);
+        if (n < G) {
+          const int g = h * G + n;
+          __half* prow = pbuf + (half * MROWS + g) * PROW;
+          prow[r] = __float2half_rn(pa);
+          prow[r + 8] = __float2half_rn(pb);
+          if (r == 0) corrb[half * MROWS + g] = corr[e];
+        }
+      }
+    }
+    __syncwarp();
+    // ------------------------------------------------------------ PV code term (head h, token half), d-on-M
+    {
+      if (__any_sync(0xffffffffu, corr[0] != 1.f || corr[1] != 1.f)) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          oc[i][0] *= corr[0];
+          oc[i][1] *= corr[1];
+          oc[i][2] *= corr[0];
+          oc[i][3] *= corr[1];
+        }
+      }
+      const uint32_t b0 = *reinterpret_cast<const uint32_t*>(p2 + r * PROW + 2 * c);
+      const uint32_t b1 = *reinterpret_cast<const uint32_t*>(p2 + r * PROW + 2 * c + 8);
+      // rows: m-tile mt, row r <-> d = 16r + 2mt, row r+8 <-> d = 16r + 2mt + 1
+      const int hb = h * GB + 2 * r * BITS;  // byte of d = 16r within head h's group
+      const uint8_t* cb = vcodes + (hb >> 7) * BAND;
+      const int o = hb & 127;
+      const int t0a = HT * half + 2 * c;  // tokens t0a, t0a+1 (k slots 2c, 2c+1) and t0a+8, t0a+9
+      if (BITS == 4) {
+        uint2 w[4];
+        w[0] = *reinterpret_cast<const uint2*>(cb + swz(t0a, o));
+        w[1] = *reinterpret_cast<const uint2*>(cb + swz(t0a + 1, o));
+        w[2] = *reinterpret_cast<const uint2*>(cb + swz(t0a + 8, o));
+        w[3] = *reinterpret_cast<const uint2*>(cb + swz(t0a + 9, o));
+#pragma unroll
+        for (int wi = 0; wi < 2; ++wi) {
+          const uint32_t xa = wi ? w[0].y : w[0].x, xb = wi ? w[1].y : w[1].x;
+          const uint32_t xc = wi ? w[2].y : w[2].x, xd = wi ? w[3].y : w[3].x;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {  // d + 8wi + 4hh + (0..3)
+            const uint32_t sel = hh ? 0x7632u : 0x5410u;
+            const uint32_t u = prmt(xa, xb, sel), v = prmt(xc, xd, sel);
+#pragma unroll
+            for (int sh = 0; sh < 2; ++sh) {  // d + 8wi + 4hh + 2sh + (0, 1)
+              const uint32_t uu = sh ? (u >> 8) : u, vv = sh ? (v >> 8) : v;
+              uint32_t af[4];
+              af[0] = field_h2<0>(uu, 0x000F000Fu);
+              af[1] = field_h2<4>(uu, 0x000F000Fu);
+              af[2] = field_h2<0>(vv, 0x000F000Fu);
+              af[3] = field_h2<4>(vv, 0x000F000Fu);
+              mma(oc[4 * wi + 2 * hh + sh], af, b0, b1);
+            }
+          }
+        }
+      } else if (BITS == 2) {
+        const uint32_t xa = *reinterpret_cast<const uint32_t*>(cb + swz(t0a, o));
+        const uint32_t xb = *reinterpret_cast<const uint32_t*>(cb + swz(t0a + 1, o));
+        const uint32_t xc = *reinterpret_cast<const uint32_t*>(cb + swz(t0a + 8, o));
+        const uint32_t xd = *reinterpret_cast<const uint32_t*>(cb + swz(t0a + 9, o));
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {  // codes 8hh .. 8hh+7 of the thread's 16
+          const uint32_t sel = hh ? 0x7632u : 0x5410u;
+          const uint32_t u = prmt(xa, xb, sel), v = prmt(xc, xd, sel);
+#pragma unroll
+          for (int sh = 0; sh < 2; ++sh) {
+            const uint32_t uu = sh ? (u >> 8) : u, vv = sh ? (v >> 8) : v;
+            uint32_t af[4];
+            af[0] = field_h2<0>(uu, 0x00030003u);
+            af[1] = field_h2<2>(uu, 0x00030003u);
+            af[2] = field_h2<0>(vv, 0x00030003u);
+            af[3] = field_h2<2>(vv, 0x00030003u);
+            mma(oc[4 * hh + 2 * sh], af, b0, b1);
+            af[0] = field_h2<4>(uu, 0x00030003u);
+            af[1] = field_h2<6>(uu, 0x00030003u);
+            af[2] = field_h2<4>(vv, 0x00030003u);
+            af[3] = field_h2<6>(vv, 0x00030003u);
+            mma(oc[4 * hh + 2 * sh + 1], af, b0, b1);
+          }
+        }
+      } else {
+        const uint4 xa = *reinterpret_cast<const uint4*>(cb + swz(t0a, o));
+        const uint4 xb = *reinterpret_cast<const uint4*>(cb + swz(t0a + 1, o));
+        const uint4 xc = *reinterpret_cast<const uint4*>(cb + swz(t0a + 8, o));
+        const uint4 xd = *reinterpret_cast<const uint4*>(cb + swz(t0a + 9, o));
+        const uint32_t A[4] = {xa.x, xa.y, xa.z, xa.w}, B[4] = {xb.x, xb.y, xb.z, xb.w};
+        const uint32_t Cc[4] = {xc.x, xc.y, xc.z, xc.w}, Dd[4] = {xd.x, xd.y, xd.z, xd.w};
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {  // d = 16r + 2mt (+1): bytes 2(mt&1) (+1) of word mt/2
+          const uint32_t sel = (mt & 1) ? 0x7632u : 0x5410u;  // [x.b(j), x.b(j+1), y.b(j), y.b(j+1)], j = 2(mt&1)
+          const uint32_t u = prmt(A[mt >> 1], B[mt >> 1], sel), v = prmt(Cc[mt >> 1], Dd[mt >> 1], sel);
+          uint32_t af[4];
+          af[0] = hsub2(lop_and_or(u, 0x00FF00FFu, 0x64006400u), 0x64006400u);
+          af[1] = hsub2(lop_and_or(u >> 8, 0x00FF00FFu, 0x64006400u), 0x64006400u);
+          af[2] = hsub2(lop_and_or(v, 0x00FF00FFu, 0x64006400u), 0x64006400u);
+          af[3] = hsub2(lop_and_or(v >> 8, 0x00FF00FFu, 0x64006400u), 0x64006400u);
+          mma(oc[mt], af, b0, b1);
+        }
+      }
+    }
+    __syncthreads();  // ---- BARRIER B: P, corr of every head visible
+    // ------------------------------------------------------------ PV mean pieces
+#pragma unroll
+    for (int pi = 0; pi < NPW; ++pi) {
+      const int p = warp + NW * pi;
+      if (p < NPIECE) {
+        const int mt = p >> 3, hf = (p >> 2) & 1, db = p & 3;
+        const float c0 = corrb[hf * MROWS + 16 * mt + r], c1 = corrb[hf * MROWS + 16 * mt + r + 8];
+        if (c0 != 1.f || c1 != 1.f) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            om[pi][j][0] *= c0;
+            om[pi][j][1] *= c0;
+            om[pi][j][2] *= c1;
+            om[pi][j][3] *= c1;
+          }
+        }
         uint32_t pa[4];
-        ldsm_x4(pa, su32(pbuf + (16 * mt + mrow) * PROW + tcol));
+        const int mrow = (lane & 7) + 8 * ((lane >> 3) & 1), tcol = 8 * (lane >> 4);
+        ldsm_x4(pa, su32(pbuf + (hf * MROWS + 16 * mt + mrow) * PROW + tcol));
+        const uint8_t* vb = vmean + db * BAND;
+        const int t = HT * hf + 2 * c;
+        const float4 x0 = *reinterpret_cast<const float4*>(vb + swz(t, 16 * r));
+        const float4 x1 = *reinterpret_cast<const float4*>(vb + swz(t + 1, 16 * r));
+        const float4 x2 = *reinterpret_cast<const float4*>(vb + swz(t + 8, 16 * r));
+        const float4 x3 = *reinterpret_cast<const float4*>(vb + swz(t + 9, 16 * r));
+        const float e0[4] = {x0.x, x0.y, x0.z, x0.w}, e1[4] = {x1.x, x1.y, x1.z, x1.w};
+        const float e2[4] = {x2.x, x2.y, x2.z, x2.w}, e3[4] = {x3.x, x3.y, x3.z, x3.w};
 #pragma unroll
-        for (int n = 0; n < 4; ++n) {
-          mma(oacc[mt][n], pa, bh[n][0], bh[n][1]);
-          mma(oacc[mt][n], pa, bl[n][0], bl[n][1]);
-        }
-      }
-      // code term: per kv head, A = P'_h (pre-masked rows), B = its codes of d = 32dq + 4r .. +3
-      constexpr int CB = BITS * 4 / 8;  // code bytes per token for the thread's 4 d
-      const int pv_c = (32 * dq + 4 * r) * BITS / 8;
-#pragma unroll
-      for (int h = 0; h < H; ++h) {
-        const int hb = h * GB + pv_c;
-        const uint8_t* cband = vcodes + (hb >> 7) * BAND;
-        const int co = hb & 127;
-        uint32_t xa, xb, xc, xd;
-        if (CB == 4) {
-          xa = *reinterpret_cast<const uint32_t*>(cband + swz(ta, co));
-          xb = *reinterpret_cast<const uint32_t*>(cband + swz(ta + 1, co));
-          xc = *reinterpret_cast<const uint32_t*>(cband + swz(ta + 8, co));
-          xd = *reinterpret_cast<const uint32_t*>(cband + swz(ta + 9, co));
-        } else if (CB == 2) {
-          xa = *reinterpret_cast<const uint16_t*>(cband + swz(ta, co));
-          xb = *reinterpret_cast<const uint16_t*>(cband + swz(ta + 1, co));
-          xc = *reinterpret_cast<const uint16_t*>(cband + swz(ta + 8, co));
-          xd = *reinterpret_cast<const uint16_t*>(cband + swz(ta + 9, co));
-        } else {
-          xa = cband[swz(ta, co)];
-          xb = cband[swz(ta + 1, co)];
-          xc = cband[swz(ta + 8, co)];
-          xd = cband[swz(ta + 9, co)];
-        }
-        uint32_t bc[4][2];
-        if (BITS == 8) {
-#pragma unroll
-          for (int n = 0; n < 4; ++n) {
-            const uint32_t sel = n | (n << 4) | ((4 + n) << 8) | ((4 + n) << 12);
-            bc[n][0] = ints_to_h2(prmt(xa, xb, sel) & 0x00FF00FFu);
-            bc[n][1] = ints_to_h2(prmt(xc, xd, sel) & 0x00FF00FFu);
-          }
-        } else {
-          constexpr uint32_t M = BITS == 4 ? 0x000F000Fu : 0x00030003u;
-          const uint32_t u = xa | (xb << 16), v = xc | (xd << 16);
-#pragma unroll
-          for (int n = 0; n < 4; ++n) {
-            bc[n][0] = ints_to_h2((u >> (BITS * n)) & M);
-            bc[n][1] = ints_to_h2((v >> (BITS * n)) & M);
-          }
-        }
-        constexpr int mth_div = 16 / G;
-        const int mth = h / (mth_div < 1 ? 1 : mth_div);
-        uint32_t am[4];
-        ldsm_x4(am, su32(p2m + (h * 16 + mrow) * PROW + tcol));
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          if (mt != mth) continue;
-#pragma unroll
-          for (int n = 0; n < 4; ++n) mma(oacc[mt][n], am, bc[n][0], bc[n][1]);
+        for (int j = 0; j < 4; ++j) {  // n-tile j: column r <-> d = 32db + 4r + j
+          uint32_t bh0, bl0, bh1, bl1;
+          split_h2(e0[j], e1[j], bh0, bl0);
+          split_h2(e2[j], e3[j], bh1, bl1);
+          mma(om[pi][j], pa, bh0, bh1);
+          mma(om[pi][j], pa, bl0, bl1);
         }
       }
     }
@@ -593,57 +602,81 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
 
   // ------------------------------------------------------------------ epilogue
 #pragma unroll
-  for (int o = TPH / 2; o > 0; o >>= 1) {
-    l_part += __shfl_xor_sync(0xffffffffu, l_part, o);
-    bp_part += __shfl_xor_sync(0xffffffffu, bp_part, o);
-  }
-  if (spart == 0) {
-    stats[4 * sg + 0] = m_run;
-    stats[4 * sg + 1] = l_part;
-    stats[4 * sg + 2] = bp_part;
-  }
-  // the two token halves (kk) hold partial O: kk = 1 parks its half in smem, kk = 0 adds it
-  float* park = reinterpret_cast<float*>(smem);  // stages are idle now: [MT*16][D] floats
-  consumer_sync();
-  // thread rows g = 16mt + r (+8); cols: n-tile n, col 2qi / 2qi+1 <-> d = 32dq + 8qi + n / + 4 + n
-  if (kk == 1) {
+  for (int e = 0; e < 2; ++e) {
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
+    for (int o = 4; o < 32; o <<= 1) {
+      l_part[e] += __shfl_xor_sync(0xffffffffu, l_part[e], o);
+      bp_part[e] += __shfl_xor_sync(0xffffffffu, bp_part[e], o);
+    }
+  }
+  if (r == 0) {
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        float* row = park + (16 * mt + r + 8 * e) * D + 32 * dq + 8 * qi;
-        *reinterpret_cast<float4*>(row) =
-            make_float4(oacc[mt][0][2 * e], oacc[mt][1][2 * e], oacc[mt][2][2 * e], oacc[mt][3][2 * e]);
-        *reinterpret_cast<float4*>(row + 4) =
-            make_float4(oacc[mt][0][2 * e + 1], oacc[mt][1][2 * e + 1], oacc[mt][2][2 * e + 1], oacc[mt][3][2 * e + 1]);
+    for (int e = 0; e < 2; ++e) {
+      const int n = 2 * c + e;
+      if (n < G) {
+        float* st = stats + (half * HQ + h * G + n) * 4;
+        st[0] = m_run[e];
+        st[1] = l_part[e];
+        st[2] = bp_part[e];
       }
+    }
   }
-  consumer_sync();
-  if (kk == 0) {
-    const float LN2 = 0.6931471805599453f;
+  float* park = reinterpret_cast<float*>(smem);  // [2 halves][HQ][D]: the stages are idle now
+  __syncthreads();
+  // 1) mean-term pieces (plain stores; the pieces tile (half, q, d) exactly)
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
+  for (int pi = 0; pi < NPW; ++pi) {
+    const int p = warp + NW * pi;
+    if (p < NPIECE) {
+      const int mt = p >> 3, hf = (p >> 2) & 1, db = p & 3;
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int g = 16 * mt + r + 8 * e;
-        if (g >= HQ) continue;
-        const float m = stats[4 * g], l = stats[4 * g + 1], bp = stats[4 * g + 2];
-        const float* row = park + g * D + 32 * dq + 8 * qi;
-        const float4 p0 = *reinterpret_cast<const float4*>(row);
-        const float4 p1 = *reinterpret_cast<const float4*>(row + 4);
-        float* pa = a.part_acc + ((int64_t(b) * HQ + g) * a.slots + split) * D + 32 * dq + 8 * qi;
-        *reinterpret_cast<float4*>(pa) =
-            make_float4(oacc[mt][0][2 * e] + p0.x - bp, oacc[mt][1][2 * e] + p0.y - bp, oacc[mt][2][2 * e] + p0.z - bp,
-                        oacc[mt][3][2 * e] + p0.w - bp);
-        *reinterpret_cast<float4*>(pa + 4) =
-            make_float4(oacc[mt][0][2 * e + 1] + p1.x - bp, oacc[mt][1][2 * e + 1] + p1.y - bp,
-                        oacc[mt][2][2 * e + 1] + p1.z - bp, oacc[mt][3][2 * e + 1] + p1.w - bp);
-        if (dq == 0 && qi == 0) {
-          float* ml = a.part_ml + ((int64_t(b) * HQ + g) * a.slots + split) * 2;
-          ml[0] = l > 0.f ? m * LN2 : -__int_as_float(0x7f800000);  // back to natural-log units for K3
-          ml[1] = l;
+        if (g < HQ) {
+          float* row = park + (hf * HQ + g) * D + 32 * db;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            row[8 * c + j] = om[pi][j][2 * e];
+            row[8 * c + 4 + j] = om[pi][j][2 * e + 1];
+          }
         }
       }
+    }
+  }
+  __syncthreads();
+  // 2) code-term accumulators of (head h, half): rows d = 16r + 2mt (+1), cols n = 2c (+1)
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int n = 2 * c + e;
+    if (n < G) {
+      float* row = park + (half * HQ + h * G + n) * D + 16 * r;
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        row[2 * mt] += oc[mt][e];
+        row[2 * mt + 1] += oc[mt][2 + e];
+      }
+    }
+  }
+  __syncthreads();
+  // 3) merge the two token halves -> split slot (natural-log LSE units for K3)
+  const float LN2 = 0.6931471805599453f;
+  for (int i = tid; i < HQ * D; i += NTHR) {
+    const int g = i / D, d = i - g * D;
+    const float* s0 = stats + g * 4;
+    const float* s1 = stats + (HQ + g) * 4;
+    const float M = fmaxf(s0[0], s1[0]);
+    const float w0 = s0[1] > 0.f ? exp2f(s0[0] - M) : 0.f;
+    const float w1 = s1[1] > 0.f ? exp2f(s1[0] - M) : 0.f;
+    float acc = 0.f;
+    if (w0 > 0.f) acc = fmaf(w0, park[g * D + d] - s0[2], acc);
+    if (w1 > 0.f) acc = fmaf(w1, park[(HQ + g) * D + d] - s1[2], acc);
+    const int64_t slot = (int64_t(b) * HQ + g) * a.slots + split;
+    a.part_acc[slot * D + d] = acc;
+    if (d == 0) {
+      const float l = w0 * s0[1] + w1 * s1[1];
+      a.part_ml[slot * 2] = l > 0.f ? M * LN2 : NEG_INF;
+      a.part_ml[slot * 2 + 1] = l;
+    }
   }
 }
 
@@ -803,7 +836,7 @@ static int get_maps(const AttnArgs& a, TmaMaps* out) {
 template <int BITS, int HQ>
 static int launch_fast_t(const AttnArgs& a, int batch, cudaStream_t st) {
   const fast::Plan pl = fast::make_plan(a.L.heads, a.L.group_bytes, HQ);
-  auto kern = fast::attn_fast_kernel<BITS, HQ, 8>;
+  auto kern = fast::attn_fast_kernel<BITS, HQ>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
