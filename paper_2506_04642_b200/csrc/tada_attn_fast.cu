@@ -149,13 +149,15 @@ __device__ __forceinline__ uint32_t qk_pair(const uint32_t* w, int s, int which)
 struct Plan {
   int mean_bytes, codes_bytes, meta_bytes, side_bytes, stage_bytes, stages;
   int trow;
-  int off_smean, off_pbuf, off_p2, off_corr, off_stats, off_qsum, off_bar, total;
+  int off_smean, off_scode, off_pbuf, off_p2, off_corr, off_red, off_qsum, off_bar, total;
 };
 
-__host__ __device__ inline int up128(int x) { return (x + 127) / 128 * 128; }
-__host__ __device__ inline int up1k(int x) { return (x + 1023) / 1024 * 1024; }
+__host__ __device__ constexpr int up128(int x) { return (x + 127) / 128 * 128; }
+__host__ __device__ constexpr int up1k(int x) { return (x + 1023) / 1024 * 1024; }
+constexpr int PROW2 = TT + 8;  // P / P' row stride (halves): 80-byte rows, conflict-free ldmatrix / B loads
+constexpr int NKQ = 4;         // QK mean-term partial sums (d quarters)
 
-__host__ __device__ inline Plan make_plan(int H, int gb, int HQ) {
+__host__ __device__ constexpr Plan make_plan(int H, int gb, int HQ) {
   Plan p{};
   const int mrows = HQ >= 16 ? HQ : 16;
   p.trow = H * 8 + 16;  // meta box row: the 16 B past the row are TMA zero fill (shifts banks by 4 per row)
@@ -165,24 +167,28 @@ __host__ __device__ inline Plan make_plan(int H, int gb, int HQ) {
   p.meta_bytes = up128(TT * p.trow);
   p.side_bytes = p.mean_bytes + p.codes_bytes;
   p.stage_bytes = up1k(2 * p.side_bytes + 2 * p.meta_bytes);
-  const int smean = up128(2 * mrows * SROW * 4);  // also the f16 q staging area of the prologue
-  const int tail = smean + up128(2 * mrows * PROW * 2) + up128(NW * 8 * PROW * 2) + up128(2 * mrows * 4) +
-                   up128(2 * HQ * 16) + up128(HQ * 4) + 128 + 1024;
+  const int smean = up128(NKQ * mrows * SROW * 4);  // also the f16 q staging area of the prologue
+  const int scode = up128(mrows * SROW * 4);
+  const int pb = up128(mrows * PROW2 * 2);
+  const int p2 = up128(H * 8 * PROW2 * 2);
+  const int tail = smean + scode + pb + p2 + up128(mrows * 4) + up128(3 * NTHR * 4) + up128(HQ * 4) + 128 + 1024;
   const int budget = 227 * 1024;
   p.stages = (3 * p.stage_bytes + tail <= budget) ? 3 : ((2 * p.stage_bytes + tail <= budget) ? 2 : 1);
   int off = p.stages * p.stage_bytes;
-  // the epilogue parks both halves' partial outputs [2][HQ][D] f32 in the (idle) stages
-  if (off < 2 * HQ * D * 4) p.stages = 0;
+  // the epilogue parks the partial output [HQ][D] f32 in the (idle) stages
+  if (off < HQ * D * 4) p.stages = 0;
   p.off_smean = off;
   off += smean;
+  p.off_scode = off;
+  off += scode;
   p.off_pbuf = off;
-  off += up128(2 * mrows * PROW * 2);
+  off += pb;
   p.off_p2 = off;
-  off += up128(NW * 8 * PROW * 2);
+  off += p2;
   p.off_corr = off;
-  off += up128(2 * mrows * 4);
-  p.off_stats = off;
-  off += up128(2 * HQ * 16);
+  off += up128(mrows * 4);
+  p.off_red = off;
+  off += up128(3 * NTHR * 4);
   p.off_qsum = off;
   off += up128(HQ * 4);
   p.off_bar = off;
@@ -192,6 +198,12 @@ __host__ __device__ inline Plan make_plan(int H, int gb, int HQ) {
 }
 
 // ------------------------------------------------------------------ the kernel
+// Per 32-token tile (phases separated by the two CTA barriers):
+//  A  QK mean piece  (warp w: token octet w&3, d quarter w>>2, all q tiles) -> S_mean partial [w>>2]
+//     QK code term   (warp (h, half))                                        -> S_code [q][tok]
+//  B  softmax, dense: thread = (q head, TT/TPQ tokens); P [q][tok], P'_h^T [n][tok], corr [q]
+//  C  PV code term   (warp (h, half): its 16 tokens, all d)       -> O_h^T in registers
+//     PV mean piece  (warp w: d octet w, all q tiles, all tokens) -> O_mean in registers
 template <int BITS, int HQ>
 __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __grid_constant__ TmaMaps maps) {
   extern __shared__ uint8_t smem_raw[];
@@ -203,20 +215,22 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
   constexpr int MT = HQ >= 16 ? HQ / 16 : 1;    // 16-row q tiles
   constexpr int MROWS = MT * 16;
   constexpr int GB = BITS * D / 8;              // code bytes per (token, head)
-  constexpr int NPIECE = 8 * MT;                // mean-term pieces per tile (each of QK and PV)
-  constexpr int NPW = (NPIECE + NW - 1) / NW;   // pieces per warp
+  constexpr Plan pl = make_plan(H, GB, HQ);
+  constexpr int S = pl.stages;
+  constexpr int TPQ = (NTHR / HQ) < 32 ? (NTHR / HQ) : 32;  // softmax threads per q head
+  constexpr int TPT = TT / TPQ;                             // tokens per softmax thread
+  constexpr int NSM = HQ * TPQ;                             // active softmax threads
   const int P = a.L.page_tokens;
-  const Plan pl = make_plan(H, GB, HQ);
-  const int S = pl.stages;
   const int b = blockIdx.y, split = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r = lane >> 2, c = lane & 3;
   const int h = warp & 7, half = warp >> 3;
 
-  float* smean = reinterpret_cast<float*>(smem + pl.off_smean);  // [2 d-halves][MROWS][SROW]
-  __half* pbuf = reinterpret_cast<__half*>(smem + pl.off_pbuf);  // [2 token halves][MROWS][PROW]
-  __half* p2 = reinterpret_cast<__half*>(smem + pl.off_p2) + warp * 8 * PROW;  // this warp's P'^T [8 n][PROW]
-  float* corrb = reinterpret_cast<float*>(smem + pl.off_corr);   // [2][MROWS]
-  float* stats = reinterpret_cast<float*>(smem + pl.off_stats);  // [2][HQ][4] = (m, l, bp, -)
+  float* smean = reinterpret_cast<float*>(smem + pl.off_smean);  // [NKQ][MROWS][SROW]
+  float* scode = reinterpret_cast<float*>(smem + pl.off_scode);  // [MROWS][SROW]
+  __half* pbuf = reinterpret_cast<__half*>(smem + pl.off_pbuf);  // [MROWS][PROW2]
+  __half* p2all = reinterpret_cast<__half*>(smem + pl.off_p2);   // [H][8 n][PROW2]: P'_h^T
+  float* corrb = reinterpret_cast<float*>(smem + pl.off_corr);   // [MROWS]
+  float* red = reinterpret_cast<float*>(smem + pl.off_red);      // [3][NTHR] epilogue reductions
   float* qsum = reinterpret_cast<float*>(smem + pl.off_qsum);    // [HQ]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + pl.off_bar);
 
@@ -229,14 +243,16 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
     for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // padded P rows (q >= HQ) must read as zero forever
-  for (int i = tid; i < (2 * MROWS * PROW) / 2; i += NTHR) reinterpret_cast<uint32_t*>(pbuf)[i] = 0u;
+  // P rows of padding q heads and P' rows of unused columns n >= G stay zero forever
+  for (int i = tid; i < (MROWS * PROW2) / 2; i += NTHR) reinterpret_cast<uint32_t*>(pbuf)[i] = 0u;
+  for (int i = tid; i < (H * 8 * PROW2) / 2; i += NTHR) reinterpret_cast<uint32_t*>(p2all)[i] = 0u;
+  for (int i = tid; i < MROWS; i += NTHR) corrb[i] = 1.f;
   __syncthreads();
 
   // TMA producer (thread 0): tile `it` -> stage it % S.  A stage is refilled only after the CTA
   // barrier that every warp reaches once it has finished the stage's previous tile.
   const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
-  const uint32_t tx = 2u * uint32_t(pl.mean_bytes + pl.codes_bytes + TT * pl.trow);
+  constexpr uint32_t tx = 2u * uint32_t(pl.mean_bytes + pl.codes_bytes + TT * pl.trow);
   auto issue = [&](int it) {
     const int stg = it % S;
     const int t0 = t_begin + it * TT;
@@ -297,27 +313,22 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
       }
     }
   }
-  // QK mean A operand per piece (q tile mt, d half kh): slots (2c,2c+1 | 2c+8,2c+9) <-> d = 16s+4c+(0,1 | 2,3)
-  uint32_t qa[NPW][4][4];
-#pragma unroll
-  for (int pi = 0; pi < NPW; ++pi) {
-    const int p = warp + NW * pi;
-    const int mt = p >> 3, kh = p & 1;
+  // QK mean A operand: q tile mt, k-step s = 2*kq + ks; slots (2c,2c+1 | 2c+8,2c+9) <-> d = 16s+4c+(0,1 | 2,3)
+  const int nt = warp & 3, kq = warp >> 2;
+  uint32_t qa[MT][2][4];
+  {
     const __half* q16 = reinterpret_cast<const __half*>(smean);
 #pragma unroll
-    for (int k4 = 0; k4 < 4; ++k4) {
-      const int s = 4 * kh + k4;
-      if (p < NPIECE) {
-        const __half* r0 = q16 + (16 * mt + r) * D + 16 * s + 4 * c;
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const __half* r0 = q16 + (16 * mt + r) * D + 16 * (2 * kq + ks) + 4 * c;
         const __half* r1 = r0 + 8 * D;
-        qa[pi][k4][0] = *reinterpret_cast<const uint32_t*>(r0);
-        qa[pi][k4][1] = *reinterpret_cast<const uint32_t*>(r1);
-        qa[pi][k4][2] = *reinterpret_cast<const uint32_t*>(r0 + 2);
-        qa[pi][k4][3] = *reinterpret_cast<const uint32_t*>(r1 + 2);
-      } else {
-        qa[pi][k4][0] = qa[pi][k4][1] = qa[pi][k4][2] = qa[pi][k4][3] = 0u;
+        qa[mt][ks][0] = *reinterpret_cast<const uint32_t*>(r0);
+        qa[mt][ks][1] = *reinterpret_cast<const uint32_t*>(r1);
+        qa[mt][ks][2] = *reinterpret_cast<const uint32_t*>(r0 + 2);
+        qa[mt][ks][3] = *reinterpret_cast<const uint32_t*>(r1 + 2);
       }
-    }
   }
   float qs[2];  // Σq of this thread's two code columns n = 2c, 2c+1
 #pragma unroll
@@ -325,18 +336,19 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
   __syncthreads();  // the q staging area becomes S_mean
 
   // accumulators
-  float oc[8][4];        // PV code term, O_h^T: m-tile of 16 d (rows) x 8 n (cols)
-  float om[NPW][4][4];   // PV mean-term piece: q tile rows x 4 n-tiles of d
+  float oc[8][4];    // PV code term, O_h^T: m-tile of 16 d (rows) x 8 n (cols), this warp's tokens
+  float om[MT][4];   // PV mean term: q tile rows x this warp's 8 d
 #pragma unroll
   for (int i = 0; i < 8; ++i) oc[i][0] = oc[i][1] = oc[i][2] = oc[i][3] = 0.f;
 #pragma unroll
-  for (int pi = 0; pi < NPW; ++pi)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) om[pi][j][0] = om[pi][j][1] = om[pi][j][2] = om[pi][j][3] = 0.f;
-  float m_run[2] = {-__int_as_float(0x7f800000), -__int_as_float(0x7f800000)};
-  float l_part[2] = {0.f, 0.f}, bp_part[2] = {0.f, 0.f};
+  for (int mt = 0; mt < MT; ++mt) om[mt][0] = om[mt][1] = om[mt][2] = om[mt][3] = 0.f;
+  // softmax ownership: q head sg, tokens sj + TPQ*u
+  const int sg = tid / TPQ, sj = tid % TPQ, sh = sg / G;
+  const bool s_active = tid < NSM;
+  float m_run = -__int_as_float(0x7f800000), l_part = 0.f, bp_part = 0.f;
   const float scale_log2 = a.scale * 1.4426950408889634f;
   const float NEG_INF = -__int_as_float(0x7f800000);
+  __half* p2 = p2all + h * 8 * PROW2;
 
   for (int it = 0; it < ntiles; ++it) {
     const int stg = it % S;
@@ -359,36 +371,40 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
       fence_proxy_async();  // generic writes before the next async (TMA) refill of this stage
     }
 
-    // ------------------------------------------------------------ QK mean pieces -> S_mean
+    // ------------------------------------------------------------ A1: QK mean piece -> S_mean[kq]
+    {
+      const int tok = 8 * nt + r;
+      float acc[MT][4];
 #pragma unroll
-    for (int pi = 0; pi < NPW; ++pi) {
-      const int p = warp + NW * pi;
-      if (p < NPIECE) {
-        const int mt = p >> 3, nt = (p >> 1) & 3, kh = p & 1;
-        const int tok = 8 * nt + r;
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
 #pragma unroll
-        for (int k4 = 0; k4 < 4; ++k4) {
-          const int s = 4 * kh + k4;
-          const float4 x = *reinterpret_cast<const float4*>(kmean + (s >> 1) * BAND + swz(tok, 64 * (s & 1) + 16 * c));
-          uint32_t h0, l0, h1, l1;
-          split_h2(x.x, x.y, h0, l0);
-          split_h2(x.z, x.w, h1, l1);
-          mma(acc, qa[pi][k4], h0, h1);
-          mma(acc, qa[pi][k4], l0, l1);
+      for (int ks = 0; ks < 2; ++ks) {
+        const int s = 2 * kq + ks;
+        const float4 x = *reinterpret_cast<const float4*>(kmean + (s >> 1) * BAND + swz(tok, 64 * (s & 1) + 16 * c));
+        uint32_t h0, l0, h1, l1;
+        split_h2(x.x, x.y, h0, l0);
+        split_h2(x.z, x.w, h1, l1);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          mma(acc[mt], qa[mt][ks], h0, h1);
+          mma(acc[mt], qa[mt][ks], l0, l1);
         }
-        float* sm = smean + (kh * MROWS + 16 * mt + r) * SROW + 8 * nt + 2 * c;
-        *reinterpret_cast<float2*>(sm) = make_float2(acc[0], acc[1]);
-        *reinterpret_cast<float2*>(sm + 8 * SROW) = make_float2(acc[2], acc[3]);
+      }
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        float* sm = smean + (kq * MROWS + 16 * mt + r) * SROW + 8 * nt + 2 * c;
+        *reinterpret_cast<float2*>(sm) = make_float2(acc[mt][0], acc[mt][1]);
+        *reinterpret_cast<float2*>(sm + 8 * SROW) = make_float2(acc[mt][2], acc[mt][3]);
       }
     }
-    // ------------------------------------------------------------ QK code term (head h, token half)
-    const int ta = HT * half + r, tb = ta + 8;  // this thread's accumulator rows (tokens)
-    float cs[4] = {0.f, 0.f, 0.f, 0.f};
+    // ------------------------------------------------------------ A2: QK code term (head h, token half) -> S_code
     {
+      const int ta = HT * half + r, tb = ta + 8;  // accumulator rows (tokens)
+      float cs[4] = {0.f, 0.f, 0.f, 0.f};
       constexpr int NWD = BITS == 8 ? 8 : (BITS == 4 ? 4 : 2);  // code words per row segment
       uint32_t wa[NWD], wb[NWD];
-      const int hb = h * GB + c * (GB / 4);
+      constexpr int SEG = GB / 4;
+      const int hb = h * GB + c * SEG;
       const uint8_t* cb = kcodes + (hb >> 7) * BAND;
       const int o = hb & 127;
       if (BITS == 4) {
@@ -419,71 +435,75 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
         af[3] = qk_pair<BITS>(wb, s, 1);
         mma(cs, af, qb[s][0], qb[s][1]);
       }
+      // − scale·(q·code) − min·Σq, for the G real columns
+      if (2 * c < G) {
+        const float2 ka = *reinterpret_cast<const float2*>(kmeta + ta * pl.trow + 8 * h);
+        const float2 kb = *reinterpret_cast<const float2*>(kmeta + tb * pl.trow + 8 * h);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (2 * c + e < G) {
+            float* row = scode + (h * G + 2 * c + e) * SROW;
+            row[ta] = -fmaf(ka.x, cs[e], ka.y * qs[e]);
+            row[tb] = -fmaf(kb.x, cs[2 + e], kb.y * qs[e]);
+          }
+        }
+      }
     }
-    __syncthreads();  // ---- BARRIER A: S_mean complete; every warp is done with the previous tile
+    __syncthreads();  // ---- BARRIER A: S complete; every warp is done with the previous tile
     if (tid == 0 && it + S - 1 < ntiles) issue(it + S - 1);
 
-    // ------------------------------------------------------------ online softmax (own head, own half)
-    float corr[2];
-    {
-      const float2 ka = *reinterpret_cast<const float2*>(kmeta + ta * pl.trow + 8 * h);
-      const float2 kb = *reinterpret_cast<const float2*>(kmeta + tb * pl.trow + 8 * h);
-      const float2 va = *reinterpret_cast<const float2*>(vmeta + ta * pl.trow + 8 * h);
-      const float2 vb = *reinterpret_cast<const float2*>(vmeta + tb * pl.trow + 8 * h);
-      const bool oka = ta < nv, okb = tb < nv;
-      float x[4];
+    // ------------------------------------------------------------ B: online softmax, dense over (q, token)
+    if (s_active) {
+      float x[TPT];
+      float tmax = NEG_INF;
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int n = 2 * c + e;
-        const int g = h * G + n;
-        if (n < G) {
-          const float* s0 = smean + g * SROW;
-          const float* s1 = smean + (MROWS + g) * SROW;
-          x[e] = oka ? ((s0[ta] + s1[ta]) - fmaf(ka.x, cs[e], ka.y * qs[e])) * scale_log2 : NEG_INF;
-          x[2 + e] = okb ? ((s0[tb] + s1[tb]) - fmaf(kb.x, cs[2 + e], kb.y * qs[e])) * scale_log2 : NEG_INF;
-        } else {
-          x[e] = x[2 + e] = NEG_INF;
-        }
+      for (int u = 0; u < TPT; ++u) {
+        const int t = sj + TPQ * u;
+        float sv = scode[sg * SROW + t];
+#pragma unroll
+        for (int k = 0; k < NKQ; ++k) sv += smean[(k * MROWS + sg) * SROW + t];
+        x[u] = t < nv ? sv * scale_log2 : NEG_INF;
+        tmax = fmaxf(tmax, x[u]);
       }
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        float tmax = fmaxf(x[e], x[2 + e]);
-        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
-        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
-        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
-        const float m_new = fmaxf(m_run[e], tmax);
-        corr[e] = m_new == NEG_INF ? 1.f : exp2f(m_run[e] - m_new);
-        m_run[e] = m_new;
-        const float pa = x[e] == NEG_INF ? 0.f : exp2f(x[e] - m_new);
-        const float pb = x[2 + e] == NEG_INF ? 0.f : exp2f(x[2 + e] - m_new);
-        l_part[e] = fmaf(l_part[e], corr[e], pa + pb);
-        bp_part[e] = fmaf(bp_part[e], corr[e], fmaf(pa, oka ? va.y : 0.f, pb * (okb ? vb.y : 0.f)));
-        const int n = 2 * c + e;
-        p2[n * PROW + r] = __float2half_rn(oka ? -pa * va.x : 0.f);
-        p2[n * PROW + r + 8] = __float2half_rn(okb ? -pb * vb.x : 0.f);
-        if (n < G) {
-          const int g = h * G + n;
-          __half* prow = pbuf + (half * MROWS + g) * PROW;
-          prow[r] = __float2half_rn(pa);
-          prow[r + 8] = __float2half_rn(pb);
-          if (r == 0) corrb[half * MROWS + g] = corr[e];
-        }
+      for (int o = TPQ / 2; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+      const float m_new = fmaxf(m_run, tmax);  // finite: every tile has >= 1 valid token
+      const float corr = exp2f(m_run - m_new);
+      m_run = m_new;
+      float lsum = 0.f, bsum = 0.f;
+      __half* prow = pbuf + sg * PROW2;
+      __half* p2r = p2all + (sh * 8 + (sg - sh * G)) * PROW2;
+#pragma unroll
+      for (int u = 0; u < TPT; ++u) {
+        const int t = sj + TPQ * u;
+        const float p = exp2f(x[u] - m_new);
+        const float2 vm = *reinterpret_cast<const float2*>(vmeta + t * pl.trow + 8 * sh);
+        const bool ok = t < nv;
+        lsum += p;
+        bsum = fmaf(p, ok ? vm.y : 0.f, bsum);
+        prow[t] = __float2half_rn(p);
+        p2r[t] = __float2half_rn(ok ? -p * vm.x : 0.f);
       }
+      l_part = fmaf(l_part, corr, lsum);
+      bp_part = fmaf(bp_part, corr, bsum);
+      if (sj == 0) corrb[sg] = corr;
     }
-    __syncwarp();
-    // ------------------------------------------------------------ PV code term (head h, token half), d-on-M
+    __syncthreads();  // ---- BARRIER B: P, P', corr visible
+    // ------------------------------------------------------------ C1: PV code term (head h, token half), d-on-M
     {
-      if (__any_sync(0xffffffffu, corr[0] != 1.f || corr[1] != 1.f)) {
+      const float c0 = (2 * c < G) ? corrb[h * G + 2 * c] : 1.f;
+      const float c1 = (2 * c + 1 < G) ? corrb[h * G + 2 * c + 1] : 1.f;
+      if (__any_sync(0xffffffffu, c0 != 1.f || c1 != 1.f)) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          oc[i][0] *= corr[0];
-          oc[i][1] *= corr[1];
-          oc[i][2] *= corr[0];
-          oc[i][3] *= corr[1];
+          oc[i][0] *= c0;
+          oc[i][1] *= c1;
+          oc[i][2] *= c0;
+          oc[i][3] *= c1;
         }
       }
-      const uint32_t b0 = *reinterpret_cast<const uint32_t*>(p2 + r * PROW + 2 * c);
-      const uint32_t b1 = *reinterpret_cast<const uint32_t*>(p2 + r * PROW + 2 * c + 8);
+      const uint32_t b0 = *reinterpret_cast<const uint32_t*>(p2 + r * PROW2 + HT * half + 2 * c);
+      const uint32_t b1 = *reinterpret_cast<const uint32_t*>(p2 + r * PROW2 + HT * half + 2 * c + 8);
       // rows: m-tile mt, row r <-> d = 16r + 2mt, row r+8 <-> d = 16r + 2mt + 1
       const int hb = h * GB + 2 * r * BITS;  // byte of d = 16r within head h's group
       const uint8_t* cb = vcodes + (hb >> 7) * BAND;
@@ -504,14 +524,14 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
             const uint32_t sel = hh ? 0x7632u : 0x5410u;
             const uint32_t u = prmt(xa, xb, sel), v = prmt(xc, xd, sel);
 #pragma unroll
-            for (int sh = 0; sh < 2; ++sh) {  // d + 8wi + 4hh + 2sh + (0, 1)
-              const uint32_t uu = sh ? (u >> 8) : u, vv = sh ? (v >> 8) : v;
+            for (int sh2 = 0; sh2 < 2; ++sh2) {  // d + 8wi + 4hh + 2sh2 + (0, 1)
+              const uint32_t uu = sh2 ? (u >> 8) : u, vv = sh2 ? (v >> 8) : v;
               uint32_t af[4];
               af[0] = field_h2<0>(uu, 0x000F000Fu);
               af[1] = field_h2<4>(uu, 0x000F000Fu);
               af[2] = field_h2<0>(vv, 0x000F000Fu);
               af[3] = field_h2<4>(vv, 0x000F000Fu);
-              mma(oc[4 * wi + 2 * hh + sh], af, b0, b1);
+              mma(oc[4 * wi + 2 * hh + sh2], af, b0, b1);
             }
           }
         }
@@ -525,19 +545,19 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
           const uint32_t sel = hh ? 0x7632u : 0x5410u;
           const uint32_t u = prmt(xa, xb, sel), v = prmt(xc, xd, sel);
 #pragma unroll
-          for (int sh = 0; sh < 2; ++sh) {
-            const uint32_t uu = sh ? (u >> 8) : u, vv = sh ? (v >> 8) : v;
+          for (int sh2 = 0; sh2 < 2; ++sh2) {
+            const uint32_t uu = sh2 ? (u >> 8) : u, vv = sh2 ? (v >> 8) : v;
             uint32_t af[4];
             af[0] = field_h2<0>(uu, 0x00030003u);
             af[1] = field_h2<2>(uu, 0x00030003u);
             af[2] = field_h2<0>(vv, 0x00030003u);
             af[3] = field_h2<2>(vv, 0x00030003u);
-            mma(oc[4 * hh + 2 * sh], af, b0, b1);
+            mma(oc[4 * hh + 2 * sh2], af, b0, b1);
             af[0] = field_h2<4>(uu, 0x00030003u);
             af[1] = field_h2<6>(uu, 0x00030003u);
             af[2] = field_h2<4>(vv, 0x00030003u);
             af[3] = field_h2<6>(vv, 0x00030003u);
-            mma(oc[4 * hh + 2 * sh + 1], af, b0, b1);
+            mma(oc[4 * hh + 2 * sh2 + 1], af, b0, b1);
           }
         }
       } else {
@@ -548,8 +568,8 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
         const uint32_t A[4] = {xa.x, xa.y, xa.z, xa.w}, B[4] = {xb.x, xb.y, xb.z, xb.w};
         const uint32_t Cc[4] = {xc.x, xc.y, xc.z, xc.w}, Dd[4] = {xd.x, xd.y, xd.z, xd.w};
 #pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {  // d = 16r + 2mt (+1): bytes 2(mt&1) (+1) of word mt/2
-          const uint32_t sel = (mt & 1) ? 0x7632u : 0x5410u;  // [x.b(j), x.b(j+1), y.b(j), y.b(j+1)], j = 2(mt&1)
+        for (int mt = 0; mt < 8; ++mt) {  // d = 16r + 2mt (+1): bytes j, j+1 (j = 2(mt&1)) of word mt/2
+          const uint32_t sel = (mt & 1) ? 0x7632u : 0x5410u;  // [x.b(j), x.b(j+1), y.b(j), y.b(j+1)]
           const uint32_t u = prmt(A[mt >> 1], B[mt >> 1], sel), v = prmt(Cc[mt >> 1], Dd[mt >> 1], sel);
           uint32_t af[4];
           af[0] = hsub2(lop_and_or(u, 0x00FF00FFu, 0x64006400u), 0x64006400u);
@@ -560,121 +580,101 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
         }
       }
     }
-    __syncthreads();  // ---- BARRIER B: P, corr of every head visible
-    // ------------------------------------------------------------ PV mean pieces
+    // ------------------------------------------------------------ C2: PV mean piece (d octet = warp)
+    {
+      float cr[MT][2];
 #pragma unroll
-    for (int pi = 0; pi < NPW; ++pi) {
-      const int p = warp + NW * pi;
-      if (p < NPIECE) {
-        const int mt = p >> 3, hf = (p >> 2) & 1, db = p & 3;
-        const float c0 = corrb[hf * MROWS + 16 * mt + r], c1 = corrb[hf * MROWS + 16 * mt + r + 8];
-        if (c0 != 1.f || c1 != 1.f) {
+      for (int mt = 0; mt < MT; ++mt) {
+        cr[mt][0] = corrb[16 * mt + r];
+        cr[mt][1] = corrb[16 * mt + r + 8];
+      }
+      bool any = false;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            om[pi][j][0] *= c0;
-            om[pi][j][1] *= c0;
-            om[pi][j][2] *= c1;
-            om[pi][j][3] *= c1;
-          }
+      for (int mt = 0; mt < MT; ++mt) any |= (cr[mt][0] != 1.f) || (cr[mt][1] != 1.f);
+      if (any) {
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          om[mt][0] *= cr[mt][0];
+          om[mt][1] *= cr[mt][0];
+          om[mt][2] *= cr[mt][1];
+          om[mt][3] *= cr[mt][1];
         }
-        uint32_t pa[4];
-        const int mrow = (lane & 7) + 8 * ((lane >> 3) & 1), tcol = 8 * (lane >> 4);
-        ldsm_x4(pa, su32(pbuf + (hf * MROWS + 16 * mt + mrow) * PROW + tcol));
-        const uint8_t* vb = vmean + db * BAND;
-        const int t = HT * hf + 2 * c;
-        const float4 x0 = *reinterpret_cast<const float4*>(vb + swz(t, 16 * r));
-        const float4 x1 = *reinterpret_cast<const float4*>(vb + swz(t + 1, 16 * r));
-        const float4 x2 = *reinterpret_cast<const float4*>(vb + swz(t + 8, 16 * r));
-        const float4 x3 = *reinterpret_cast<const float4*>(vb + swz(t + 9, 16 * r));
-        const float e0[4] = {x0.x, x0.y, x0.z, x0.w}, e1[4] = {x1.x, x1.y, x1.z, x1.w};
-        const float e2[4] = {x2.x, x2.y, x2.z, x2.w}, e3[4] = {x3.x, x3.y, x3.z, x3.w};
+      }
+      const int d = 8 * warp + r;  // this thread's B column
+      const uint8_t* vb = vmean + (d >> 5) * BAND;
+      const int ob = 4 * (d & 31);
+      const int mrow = (lane & 7) + 8 * ((lane >> 3) & 1), tcol = 8 * (lane >> 4);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {  // n-tile j: column r <-> d = 32db + 4r + j
-          uint32_t bh0, bl0, bh1, bl1;
-          split_h2(e0[j], e1[j], bh0, bl0);
-          split_h2(e2[j], e3[j], bh1, bl1);
-          mma(om[pi][j], pa, bh0, bh1);
-          mma(om[pi][j], pa, bl0, bl1);
+      for (int ks = 0; ks < 2; ++ks) {
+        const int t = 16 * ks + 2 * c;
+        const float e0 = *reinterpret_cast<const float*>(vb + swz(t, ob));
+        const float e1 = *reinterpret_cast<const float*>(vb + swz(t + 1, ob));
+        const float e2 = *reinterpret_cast<const float*>(vb + swz(t + 8, ob));
+        const float e3 = *reinterpret_cast<const float*>(vb + swz(t + 9, ob));
+        uint32_t bh0, bl0, bh1, bl1;
+        split_h2(e0, e1, bh0, bl0);
+        split_h2(e2, e3, bh1, bl1);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          uint32_t pa[4];
+          ldsm_x4(pa, su32(pbuf + (16 * mt + mrow) * PROW2 + 16 * ks + tcol));
+          mma(om[mt], pa, bh0, bh1);
+          mma(om[mt], pa, bl0, bl1);
         }
       }
     }
   }
 
   // ------------------------------------------------------------------ epilogue
+  // per-thread partial l and Σp·vmin -> per q head
+  red[tid] = s_active ? l_part : 0.f;
+  red[NTHR + tid] = s_active ? bp_part : 0.f;
+  red[2 * NTHR + tid] = m_run;
+  float* park = reinterpret_cast<float*>(smem);  // [HQ][D]: the stages are idle now
+  __syncthreads();
+  // 1) mean term: rows q = 16mt + r (+8), cols d = 8*warp + 2c (+1)
 #pragma unroll
-  for (int e = 0; e < 2; ++e) {
-#pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-      l_part[e] += __shfl_xor_sync(0xffffffffu, l_part[e], o);
-      bp_part[e] += __shfl_xor_sync(0xffffffffu, bp_part[e], o);
-    }
-  }
-  if (r == 0) {
+  for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      const int n = 2 * c + e;
-      if (n < G) {
-        float* st = stats + (half * HQ + h * G + n) * 4;
-        st[0] = m_run[e];
-        st[1] = l_part[e];
-        st[2] = bp_part[e];
-      }
+      const int g = 16 * mt + r + 8 * e;
+      if (g < HQ) *reinterpret_cast<float2*>(park + g * D + 8 * warp + 2 * c) = make_float2(om[mt][2 * e], om[mt][2 * e + 1]);
     }
-  }
-  float* park = reinterpret_cast<float*>(smem);  // [2 halves][HQ][D]: the stages are idle now
   __syncthreads();
-  // 1) mean-term pieces (plain stores; the pieces tile (half, q, d) exactly)
+  // 2) code term, half 0 then half 1 (same softmax reference): rows d = 16r + 2mt (+1), cols n = 2c (+1)
 #pragma unroll
-  for (int pi = 0; pi < NPW; ++pi) {
-    const int p = warp + NW * pi;
-    if (p < NPIECE) {
-      const int mt = p >> 3, hf = (p >> 2) & 1, db = p & 3;
+  for (int hp = 0; hp < 2; ++hp) {
+    if (half == hp) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int g = 16 * mt + r + 8 * e;
-        if (g < HQ) {
-          float* row = park + (hf * HQ + g) * D + 32 * db;
+        const int n = 2 * c + e;
+        if (n < G) {
+          float* row = park + (h * G + n) * D + 16 * r;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            row[8 * c + j] = om[pi][j][2 * e];
-            row[8 * c + 4 + j] = om[pi][j][2 * e + 1];
+          for (int mt = 0; mt < 8; ++mt) {
+            row[2 * mt] += oc[mt][e];
+            row[2 * mt + 1] += oc[mt][2 + e];
           }
         }
       }
     }
+    __syncthreads();
   }
-  __syncthreads();
-  // 2) code-term accumulators of (head h, half): rows d = 16r + 2mt (+1), cols n = 2c (+1)
-#pragma unroll
-  for (int e = 0; e < 2; ++e) {
-    const int n = 2 * c + e;
-    if (n < G) {
-      float* row = park + (half * HQ + h * G + n) * D + 16 * r;
-#pragma unroll
-      for (int mt = 0; mt < 8; ++mt) {
-        row[2 * mt] += oc[mt][e];
-        row[2 * mt + 1] += oc[mt][2 + e];
-      }
-    }
-  }
-  __syncthreads();
-  // 3) merge the two token halves -> split slot (natural-log LSE units for K3)
+  // 3) write the split slot (natural-log LSE units for K3)
   const float LN2 = 0.6931471805599453f;
   for (int i = tid; i < HQ * D; i += NTHR) {
     const int g = i / D, d = i - g * D;
-    const float* s0 = stats + g * 4;
-    const float* s1 = stats + (HQ + g) * 4;
-    const float M = fmaxf(s0[0], s1[0]);
-    const float w0 = s0[1] > 0.f ? exp2f(s0[0] - M) : 0.f;
-    const float w1 = s1[1] > 0.f ? exp2f(s1[0] - M) : 0.f;
-    float acc = 0.f;
-    if (w0 > 0.f) acc = fmaf(w0, park[g * D + d] - s0[2], acc);
-    if (w1 > 0.f) acc = fmaf(w1, park[(HQ + g) * D + d] - s1[2], acc);
+    float l = 0.f, bp = 0.f;
+#pragma unroll 4
+    for (int k = 0; k < TPQ; ++k) {
+      l += red[g * TPQ + k];
+      bp += red[NTHR + g * TPQ + k];
+    }
+    const float m = red[2 * NTHR + g * TPQ];
     const int64_t slot = (int64_t(b) * HQ + g) * a.slots + split;
-    a.part_acc[slot * D + d] = acc;
+    a.part_acc[slot * D + d] = l > 0.f ? park[g * D + d] - bp : 0.f;
     if (d == 0) {
-      const float l = w0 * s0[1] + w1 * s1[1];
-      a.part_ml[slot * 2] = l > 0.f ? M * LN2 : NEG_INF;
+      a.part_ml[slot * 2] = l > 0.f ? m * LN2 : NEG_INF;
       a.part_ml[slot * 2 + 1] = l;
     }
   }
@@ -835,7 +835,7 @@ static int get_maps(const AttnArgs& a, TmaMaps* out) {
 
 template <int BITS, int HQ>
 static int launch_fast_t(const AttnArgs& a, int batch, cudaStream_t st) {
-  const fast::Plan pl = fast::make_plan(a.L.heads, a.L.group_bytes, HQ);
+  constexpr fast::Plan pl = fast::make_plan(8, BITS * 128 / 8, HQ);
   auto kern = fast::attn_fast_kernel<BITS, HQ>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {

@@ -47,6 +47,11 @@ def main():
         top = sorted(stalls.items(), key=lambda kv: -kv[1])[:3]
         print(f"{100*s/tot:5.1f}% {f.split('/')[-1]}:{d['Line No']:>4} {d['Source'].strip()[:70]:70s} "
               + " ".join(f"{k}={v:.0f}" for k, v in top))
+    itot = sum(num(d, "Instructions Executed") for _, d in rows) or 1
+    print(f"--- top lines by warp instructions executed (total {itot:.0f})")
+    for f, d in sorted(rows, key=lambda x: -num(x[1], "Instructions Executed"))[:n]:
+        print(f"{100*num(d, 'Instructions Executed')/itot:5.1f}% {f.split('/')[-1]}:{d['Line No']:>4} "
+              f"{d['Source'].strip()[:90]}")
     print("--- top lines by excessive shared wavefronts")
     for f, d in sorted(rows, key=lambda x: -num(x[1], "L1 Wavefronts Shared Excessive"))[:12]:
         print(f"{num(d, 'L1 Wavefronts Shared Excessive'):12.0f} / {num(d, 'L1 Wavefronts Shared'):12.0f} "
