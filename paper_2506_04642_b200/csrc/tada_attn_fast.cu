@@ -110,6 +110,14 @@ __device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
   const __half2 h = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<const uint32_t*>(&h);
 }
+__device__ __forceinline__ void red_add(float* p, float v) {
+  asm volatile("red.shared.add.f32 [%0], %1;" ::"r"(su32(p)), "f"(v) : "memory");
+}
+__device__ __forceinline__ float ex2(float x) {  // 2^x; ex2(-inf) = 0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 // f32 pair -> f16 hi pair + f16 residual pair (≈ 22 significant bits together)
 __device__ __forceinline__ void split_h2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
   const __half2 h = __floats2half2_rn(x0, x1);
@@ -149,13 +157,12 @@ __device__ __forceinline__ uint32_t qk_pair(const uint32_t* w, int s, int which)
 struct Plan {
   int mean_bytes, codes_bytes, meta_bytes, side_bytes, stage_bytes, stages;
   int trow;
-  int off_smean, off_scode, off_pbuf, off_p2, off_corr, off_red, off_qsum, off_bar, total;
+  int off_sbuf, off_q16, off_pbuf, off_p2, off_corr, off_red, off_qsum, off_bar, total;
 };
 
 __host__ __device__ constexpr int up128(int x) { return (x + 127) / 128 * 128; }
 __host__ __device__ constexpr int up1k(int x) { return (x + 1023) / 1024 * 1024; }
 constexpr int PROW2 = TT + 8;  // P / P' row stride (halves): 80-byte rows, conflict-free ldmatrix / B loads
-constexpr int NKQ = 4;         // QK mean-term partial sums (d quarters)
 
 __host__ __device__ constexpr Plan make_plan(int H, int gb, int HQ) {
   Plan p{};
@@ -167,20 +174,20 @@ __host__ __device__ constexpr Plan make_plan(int H, int gb, int HQ) {
   p.meta_bytes = up128(TT * p.trow);
   p.side_bytes = p.mean_bytes + p.codes_bytes;
   p.stage_bytes = up1k(2 * p.side_bytes + 2 * p.meta_bytes);
-  const int smean = up128(NKQ * mrows * SROW * 4);  // also the f16 q staging area of the prologue
-  const int scode = up128(mrows * SROW * 4);
+  const int sb = up128(mrows * SROW * 4);
+  const int q16 = up128(mrows * D * 2);
   const int pb = up128(mrows * PROW2 * 2);
   const int p2 = up128(H * 8 * PROW2 * 2);
-  const int tail = smean + scode + pb + p2 + up128(mrows * 4) + up128(3 * NTHR * 4) + up128(HQ * 4) + 128 + 1024;
+  const int tail = sb + q16 + pb + p2 + up128(mrows * 4) + up128(3 * HQ * 4) + up128(HQ * 4) + 128 + 1024;
   const int budget = 227 * 1024;
   p.stages = (3 * p.stage_bytes + tail <= budget) ? 3 : ((2 * p.stage_bytes + tail <= budget) ? 2 : 1);
   int off = p.stages * p.stage_bytes;
   // the epilogue parks the partial output [HQ][D] f32 in the (idle) stages
   if (off < HQ * D * 4) p.stages = 0;
-  p.off_smean = off;
-  off += smean;
-  p.off_scode = off;
-  off += scode;
+  p.off_sbuf = off;
+  off += sb;
+  p.off_q16 = off;
+  off += q16;
   p.off_pbuf = off;
   off += pb;
   p.off_p2 = off;
@@ -188,7 +195,7 @@ __host__ __device__ constexpr Plan make_plan(int H, int gb, int HQ) {
   p.off_corr = off;
   off += up128(mrows * 4);
   p.off_red = off;
-  off += up128(3 * NTHR * 4);
+  off += up128(3 * HQ * 4);
   p.off_qsum = off;
   off += up128(HQ * 4);
   p.off_bar = off;
@@ -199,8 +206,8 @@ __host__ __device__ constexpr Plan make_plan(int H, int gb, int HQ) {
 
 // ------------------------------------------------------------------ the kernel
 // Per 32-token tile (phases separated by the two CTA barriers):
-//  A  QK mean piece  (warp w: token octet w&3, d quarter w>>2, all q tiles) -> S_mean partial [w>>2]
-//     QK code term   (warp (h, half))                                        -> S_code [q][tok]
+//  A  QK mean piece  (warp w: token octet w&3, d quarter w>>2, all q tiles) -> S [q][tok] (red.shared.add)
+//     QK code term   (warp (h, half))                                        -> S [q][tok] (red.shared.add)
 //  B  softmax, dense: thread = (q head, TT/TPQ tokens); P [q][tok], P'_h^T [n][tok], corr [q]
 //  C  PV code term   (warp (h, half): its 16 tokens, all d)       -> O_h^T in registers
 //     PV mean piece  (warp w: d octet w, all q tiles, all tokens) -> O_mean in registers
@@ -225,12 +232,12 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r = lane >> 2, c = lane & 3;
   const int h = warp & 7, half = warp >> 3;
 
-  float* smean = reinterpret_cast<float*>(smem + pl.off_smean);  // [NKQ][MROWS][SROW]
-  float* scode = reinterpret_cast<float*>(smem + pl.off_scode);  // [MROWS][SROW]
+  float* sbuf = reinterpret_cast<float*>(smem + pl.off_sbuf);    // [MROWS][SROW]: logits, zeroed by their reader
+  __half* q16s = reinterpret_cast<__half*>(smem + pl.off_q16);   // [MROWS][D] f16 q
   __half* pbuf = reinterpret_cast<__half*>(smem + pl.off_pbuf);  // [MROWS][PROW2]
   __half* p2all = reinterpret_cast<__half*>(smem + pl.off_p2);   // [H][8 n][PROW2]: P'_h^T
   float* corrb = reinterpret_cast<float*>(smem + pl.off_corr);   // [MROWS]
-  float* red = reinterpret_cast<float*>(smem + pl.off_red);      // [3][NTHR] epilogue reductions
+  float* red = reinterpret_cast<float*>(smem + pl.off_red);      // [3][HQ] epilogue (l, Σp·vmin, m)
   float* qsum = reinterpret_cast<float*>(smem + pl.off_qsum);    // [HQ]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + pl.off_bar);
 
@@ -247,40 +254,41 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
   for (int i = tid; i < (MROWS * PROW2) / 2; i += NTHR) reinterpret_cast<uint32_t*>(pbuf)[i] = 0u;
   for (int i = tid; i < (H * 8 * PROW2) / 2; i += NTHR) reinterpret_cast<uint32_t*>(p2all)[i] = 0u;
   for (int i = tid; i < MROWS; i += NTHR) corrb[i] = 1.f;
+  for (int i = tid; i < MROWS * SROW; i += NTHR) sbuf[i] = 0.f;
   __syncthreads();
 
   // TMA producer (thread 0): tile `it` -> stage it % S.  A stage is refilled only after the CTA
   // barrier that every warp reaches once it has finished the stage's previous tile.
   const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
   constexpr uint32_t tx = 2u * uint32_t(pl.mean_bytes + pl.codes_bytes + TT * pl.trow);
+  // warp-collective: lane 0 arms the barrier, then lane j issues copy j (all copies of a tile at once)
+  constexpr int NB = (H * GB) / 128;  // code bands per side
+  constexpr int NCOPY = 2 * (4 + NB + 1);
+  static_assert(NCOPY <= 32, "one TMA copy per lane");
   auto issue = [&](int it) {
     const int stg = it % S;
     const int t0 = t_begin + it * TT;
     const int page = pt[t0 / P];
     const int row0 = t0 % P;
     uint8_t* dst = smem + stg * pl.stage_bytes;
-    mbar_expect_tx(&full[stg], tx);
-#pragma unroll
-    for (int side = 0; side < 2; ++side) {
+    if (lane == 0) mbar_expect_tx(&full[stg], tx);
+    __syncwarp();
+    if (lane < NCOPY) {
+      const int side = lane / (5 + NB), j = lane % (5 + NB);
       uint8_t* d0 = dst + side * pl.side_bytes;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) tma_3d(d0 + j * BAND, &maps.m[side][0], 128 * j, row0, page, &full[stg]);
-#pragma unroll
-      for (int j = 0; j < (H * GB) / 128; ++j)
-        tma_3d(d0 + pl.mean_bytes + j * BAND, &maps.m[side][1], 128 * j, row0, page, &full[stg]);
-      tma_3d(dst + 2 * pl.side_bytes + side * pl.meta_bytes, &maps.m[side][2], 0, row0, page, &full[stg]);
+      if (j < 4) tma_3d(d0 + j * BAND, &maps.m[side][0], 128 * j, row0, page, &full[stg]);
+      else if (j < 4 + NB) tma_3d(d0 + pl.mean_bytes + (j - 4) * BAND, &maps.m[side][1], 128 * (j - 4), row0, page, &full[stg]);
+      else tma_3d(dst + 2 * pl.side_bytes + side * pl.meta_bytes, &maps.m[side][2], 0, row0, page, &full[stg]);
     }
   };
-  if (tid == 0) {
-    for (int s2 = 0; s2 < 2; ++s2)
-      for (int k = 0; k < 3; ++k)
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[s2][k])) : "memory");
+  if (warp == 0) {
+    if (lane < 6) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[lane / 3][lane % 3])) : "memory");
     for (int it = 0; it < S - 1 && it < ntiles; ++it) issue(it);
   }
 
   // ---------------------------------------------------------------- prologue: q -> f16 fragments
   {
-    __half* q16 = reinterpret_cast<__half*>(smean);  // staging [MROWS][D]
+    __half* q16 = q16s;
     for (int g = warp; g < MROWS; g += NW) {
       float v[4] = {0.f, 0.f, 0.f, 0.f};
       if (g < HQ) {
@@ -300,7 +308,7 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
   // QK code B operand (Q_h^T, d permuted to the code slots), column n = r <-> q head h*G + r
   uint32_t qb[8][2];
   {
-    const __half* q16 = reinterpret_cast<const __half*>(smean);
+    const __half* q16 = q16s;
     const int g = h * G + r;
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
@@ -317,7 +325,7 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
   const int nt = warp & 3, kq = warp >> 2;
   uint32_t qa[MT][2][4];
   {
-    const __half* q16 = reinterpret_cast<const __half*>(smean);
+    const __half* q16 = q16s;
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -333,7 +341,6 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
   float qs[2];  // Σq of this thread's two code columns n = 2c, 2c+1
 #pragma unroll
   for (int e = 0; e < 2; ++e) qs[e] = (2 * c + e < G) ? qsum[h * G + 2 * c + e] : 0.f;
-  __syncthreads();  // the q staging area becomes S_mean
 
   // accumulators
   float oc[8][4];    // PV code term, O_h^T: m-tile of 16 d (rows) x 8 n (cols), this warp's tokens
@@ -392,9 +399,11 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
       }
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
-        float* sm = smean + (kq * MROWS + 16 * mt + r) * SROW + 8 * nt + 2 * c;
-        *reinterpret_cast<float2*>(sm) = make_float2(acc[mt][0], acc[mt][1]);
-        *reinterpret_cast<float2*>(sm + 8 * SROW) = make_float2(acc[mt][2], acc[mt][3]);
+        float* sm = sbuf + (16 * mt + r) * SROW + 8 * nt + 2 * c;
+        red_add(sm, acc[mt][0]);
+        red_add(sm + 1, acc[mt][1]);
+        red_add(sm + 8 * SROW, acc[mt][2]);
+        red_add(sm + 8 * SROW + 1, acc[mt][3]);
       }
     }
     // ------------------------------------------------------------ A2: QK code term (head h, token half) -> S_code
@@ -442,47 +451,67 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           if (2 * c + e < G) {
-            float* row = scode + (h * G + 2 * c + e) * SROW;
-            row[ta] = -fmaf(ka.x, cs[e], ka.y * qs[e]);
-            row[tb] = -fmaf(kb.x, cs[2 + e], kb.y * qs[e]);
+            float* row = sbuf + (h * G + 2 * c + e) * SROW;
+            red_add(row + ta, -fmaf(ka.x, cs[e], ka.y * qs[e]));
+            red_add(row + tb, -fmaf(kb.x, cs[2 + e], kb.y * qs[e]));
           }
         }
       }
     }
     __syncthreads();  // ---- BARRIER A: S complete; every warp is done with the previous tile
-    if (tid == 0 && it + S - 1 < ntiles) issue(it + S - 1);
+    if (warp == 0 && it + S - 1 < ntiles) issue(it + S - 1);
 
     // ------------------------------------------------------------ B: online softmax, dense over (q, token)
-    if (s_active) {
+    if (s_active) {  // thread = (q head sg, tokens TPT*sj .. +TPT-1)
       float x[TPT];
+      float* srow = sbuf + sg * SROW + TPT * sj;
+      if (TPT == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(srow);
+        x[0] = v.x; x[TPT > 1 ? 1 : 0] = v.y; x[TPT > 2 ? 2 : 0] = v.z; x[TPT > 3 ? 3 : 0] = v.w;
+        *reinterpret_cast<float4*>(srow) = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else if (TPT == 2) {
+        const float2 v = *reinterpret_cast<const float2*>(srow);
+        x[0] = v.x; x[TPT > 1 ? 1 : 0] = v.y;
+        *reinterpret_cast<float2*>(srow) = make_float2(0.f, 0.f);
+      } else {
+        x[0] = srow[0];
+        srow[0] = 0.f;
+      }
       float tmax = NEG_INF;
 #pragma unroll
       for (int u = 0; u < TPT; ++u) {
-        const int t = sj + TPQ * u;
-        float sv = scode[sg * SROW + t];
-#pragma unroll
-        for (int k = 0; k < NKQ; ++k) sv += smean[(k * MROWS + sg) * SROW + t];
-        x[u] = t < nv ? sv * scale_log2 : NEG_INF;
+        x[u] = (TPT * sj + u < nv) ? x[u] * scale_log2 : NEG_INF;
         tmax = fmaxf(tmax, x[u]);
       }
 #pragma unroll
       for (int o = TPQ / 2; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
       const float m_new = fmaxf(m_run, tmax);  // finite: every tile has >= 1 valid token
-      const float corr = exp2f(m_run - m_new);
+      const float corr = ex2(m_run - m_new);
       m_run = m_new;
       float lsum = 0.f, bsum = 0.f;
-      __half* prow = pbuf + sg * PROW2;
-      __half* p2r = p2all + (sh * 8 + (sg - sh * G)) * PROW2;
+      __half pv[TPT], p2v[TPT];
 #pragma unroll
       for (int u = 0; u < TPT; ++u) {
-        const int t = sj + TPQ * u;
-        const float p = exp2f(x[u] - m_new);
+        const int t = TPT * sj + u;
+        const float p = ex2(x[u] - m_new);
         const float2 vm = *reinterpret_cast<const float2*>(vmeta + t * pl.trow + 8 * sh);
         const bool ok = t < nv;
         lsum += p;
         bsum = fmaf(p, ok ? vm.y : 0.f, bsum);
-        prow[t] = __float2half_rn(p);
-        p2r[t] = __float2half_rn(ok ? -p * vm.x : 0.f);
+        pv[u] = __float2half_rn(p);
+        p2v[u] = __float2half_rn(ok ? -p * vm.x : 0.f);
+      }
+      __half* prow = pbuf + sg * PROW2 + TPT * sj;
+      __half* p2r = p2all + (sh * 8 + (sg - sh * G)) * PROW2 + TPT * sj;
+      if (TPT == 4) {
+        *reinterpret_cast<uint2*>(prow) = *reinterpret_cast<const uint2*>(pv);
+        *reinterpret_cast<uint2*>(p2r) = *reinterpret_cast<const uint2*>(p2v);
+      } else if (TPT == 2) {
+        *reinterpret_cast<uint32_t*>(prow) = *reinterpret_cast<const uint32_t*>(pv);
+        *reinterpret_cast<uint32_t*>(p2r) = *reinterpret_cast<const uint32_t*>(p2v);
+      } else {
+        prow[0] = pv[0];
+        p2r[0] = p2v[0];
       }
       l_part = fmaf(l_part, corr, lsum);
       bp_part = fmaf(bp_part, corr, bsum);
@@ -627,9 +656,18 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
 
   // ------------------------------------------------------------------ epilogue
   // per-thread partial l and Σp·vmin -> per q head
-  red[tid] = s_active ? l_part : 0.f;
-  red[NTHR + tid] = s_active ? bp_part : 0.f;
-  red[2 * NTHR + tid] = m_run;
+  if (s_active) {
+#pragma unroll
+    for (int o = TPQ / 2; o > 0; o >>= 1) {
+      l_part += __shfl_xor_sync(0xffffffffu, l_part, o);
+      bp_part += __shfl_xor_sync(0xffffffffu, bp_part, o);
+    }
+    if (sj == 0) {
+      red[sg] = l_part;
+      red[HQ + sg] = bp_part;
+      red[2 * HQ + sg] = m_run;
+    }
+  }
   float* park = reinterpret_cast<float*>(smem);  // [HQ][D]: the stages are idle now
   __syncthreads();
   // 1) mean term: rows q = 16mt + r (+8), cols d = 8*warp + 2c (+1)
@@ -664,13 +702,7 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
   const float LN2 = 0.6931471805599453f;
   for (int i = tid; i < HQ * D; i += NTHR) {
     const int g = i / D, d = i - g * D;
-    float l = 0.f, bp = 0.f;
-#pragma unroll 4
-    for (int k = 0; k < TPQ; ++k) {
-      l += red[g * TPQ + k];
-      bp += red[NTHR + g * TPQ + k];
-    }
-    const float m = red[2 * NTHR + g * TPQ];
+    const float l = red[g], bp = red[HQ + g], m = red[2 * HQ + g];
     const int64_t slot = (int64_t(b) * HQ + g) * a.slots + split;
     a.part_acc[slot * D + d] = l > 0.f ? park[g * D + d] - bp : 0.f;
     if (d == 0) {
