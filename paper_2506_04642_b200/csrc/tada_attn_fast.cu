@@ -163,6 +163,7 @@ struct Plan {
 __host__ __device__ constexpr int up128(int x) { return (x + 127) / 128 * 128; }
 __host__ __device__ constexpr int up1k(int x) { return (x + 1023) / 1024 * 1024; }
 constexpr int PROW2 = TT + 8;  // P / P' row stride (halves): 80-byte rows, conflict-free ldmatrix / B loads
+constexpr int NSP = 5;         // logit partial planes: 4 QK mean-term d quarters + the code term
 
 __host__ __device__ constexpr Plan make_plan(int H, int gb, int HQ) {
   Plan p{};
@@ -174,7 +175,7 @@ __host__ __device__ constexpr Plan make_plan(int H, int gb, int HQ) {
   p.meta_bytes = up128(TT * p.trow);
   p.side_bytes = p.mean_bytes + p.codes_bytes;
   p.stage_bytes = up1k(2 * p.side_bytes + 2 * p.meta_bytes);
-  const int sb = up128(mrows * SROW * 4);
+  const int sb = up128(NSP * mrows * SROW * 4);
   const int q16 = up128(mrows * D * 2);
   const int pb = up128(mrows * PROW2 * 2);
   const int p2 = up128(H * 8 * PROW2 * 2);
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r = lane >> 2, c = lane & 3;
   const int h = warp & 7, half = warp >> 3;
 
-  float* sbuf = reinterpret_cast<float*>(smem + pl.off_sbuf);    // [MROWS][SROW]: logits, zeroed by their reader
+  float* sbuf = reinterpret_cast<float*>(smem + pl.off_sbuf);    // [NSP][MROWS][SROW]: logit partials
   __half* q16s = reinterpret_cast<__half*>(smem + pl.off_q16);   // [MROWS][D] f16 q
   __half* pbuf = reinterpret_cast<__half*>(smem + pl.off_pbuf);  // [MROWS][PROW2]
   __half* p2all = reinterpret_cast<__half*>(smem + pl.off_p2);   // [H][8 n][PROW2]: P'_h^T
@@ -254,7 +255,6 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
   for (int i = tid; i < (MROWS * PROW2) / 2; i += NTHR) reinterpret_cast<uint32_t*>(pbuf)[i] = 0u;
   for (int i = tid; i < (H * 8 * PROW2) / 2; i += NTHR) reinterpret_cast<uint32_t*>(p2all)[i] = 0u;
   for (int i = tid; i < MROWS; i += NTHR) corrb[i] = 1.f;
-  for (int i = tid; i < MROWS * SROW; i += NTHR) sbuf[i] = 0.f;
   __syncthreads();
 
   // TMA producer (thread 0): tile `it` -> stage it % S.  A stage is refilled only after the CTA
@@ -399,11 +399,9 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
       }
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
-        float* sm = sbuf + (16 * mt + r) * SROW + 8 * nt + 2 * c;
-        red_add(sm, acc[mt][0]);
-        red_add(sm + 1, acc[mt][1]);
-        red_add(sm + 8 * SROW, acc[mt][2]);
-        red_add(sm + 8 * SROW + 1, acc[mt][3]);
+        float* sm = sbuf + (kq * MROWS + 16 * mt + r) * SROW + 8 * nt + 2 * c;
+        *reinterpret_cast<float2*>(sm) = make_float2(acc[mt][0], acc[mt][1]);
+        *reinterpret_cast<float2*>(sm + 8 * SROW) = make_float2(acc[mt][2], acc[mt][3]);
       }
     }
     // ------------------------------------------------------------ A2: QK code term (head h, token half) -> S_code
@@ -451,9 +449,9 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           if (2 * c + e < G) {
-            float* row = sbuf + (h * G + 2 * c + e) * SROW;
-            red_add(row + ta, -fmaf(ka.x, cs[e], ka.y * qs[e]));
-            red_add(row + tb, -fmaf(kb.x, cs[2 + e], kb.y * qs[e]));
+            float* row = sbuf + (4 * MROWS + h * G + 2 * c + e) * SROW;
+            row[ta] = -fmaf(ka.x, cs[e], ka.y * qs[e]);
+            row[tb] = -fmaf(kb.x, cs[2 + e], kb.y * qs[e]);
           }
         }
       }
@@ -464,18 +462,20 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
     // ------------------------------------------------------------ B: online softmax, dense over (q, token)
     if (s_active) {  // thread = (q head sg, tokens TPT*sj .. +TPT-1)
       float x[TPT];
-      float* srow = sbuf + sg * SROW + TPT * sj;
-      if (TPT == 4) {
-        const float4 v = *reinterpret_cast<const float4*>(srow);
-        x[0] = v.x; x[TPT > 1 ? 1 : 0] = v.y; x[TPT > 2 ? 2 : 0] = v.z; x[TPT > 3 ? 3 : 0] = v.w;
-        *reinterpret_cast<float4*>(srow) = make_float4(0.f, 0.f, 0.f, 0.f);
-      } else if (TPT == 2) {
-        const float2 v = *reinterpret_cast<const float2*>(srow);
-        x[0] = v.x; x[TPT > 1 ? 1 : 0] = v.y;
-        *reinterpret_cast<float2*>(srow) = make_float2(0.f, 0.f);
-      } else {
-        x[0] = srow[0];
-        srow[0] = 0.f;
+#pragma unroll
+      for (int u = 0; u < TPT; ++u) x[u] = 0.f;
+#pragma unroll
+      for (int k = 0; k < NSP; ++k) {
+        const float* srow = sbuf + (k * MROWS + sg) * SROW + TPT * sj;
+        if (TPT == 4) {
+          const float4 v = *reinterpret_cast<const float4*>(srow);
+          x[0] += v.x; x[TPT > 1 ? 1 : 0] += v.y; x[TPT > 2 ? 2 : 0] += v.z; x[TPT > 3 ? 3 : 0] += v.w;
+        } else if (TPT == 2) {
+          const float2 v = *reinterpret_cast<const float2*>(srow);
+          x[0] += v.x; x[TPT > 1 ? 1 : 0] += v.y;
+        } else {
+          x[0] += srow[0];
+        }
       }
       float tmax = NEG_INF;
 #pragma unroll
