@@ -72,6 +72,20 @@ __device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, int c0
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_5d(void* dst, const CUtensorMap* map, int c1, int c4, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %2, %2, %4}], [%5];" ::
+          "r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(c1), "r"(c4), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* map, int c1, int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %2, %4}], [%5];" ::
+          "r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(c1), "r"(c3), "r"(su32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -171,8 +185,8 @@ __host__ __device__ constexpr Plan make_plan(int H, int gb, int HQ) {
   p.trow = H * 8 + 16;  // meta box row: the 16 B past the row are TMA zero fill (shifts banks by 4 per row)
   p.mean_bytes = (D * 4 / 128) * BAND;
   p.codes_bytes = (H * gb / 128) * BAND;
-  // stage = [K mean][K codes][V mean][V codes][K meta][V meta]: swizzled regions stay 1 KB aligned
-  p.meta_bytes = up128(TT * p.trow);
+  // stage = [means K, V][codes K, V][metas K, V] (one TMA copy each); swizzled regions 1 KB aligned
+  p.meta_bytes = TT * p.trow;
   p.side_bytes = p.mean_bytes + p.codes_bytes;
   p.stage_bytes = up1k(2 * p.side_bytes + 2 * p.meta_bytes);
   const int sb = up128(NSP * mrows * SROW * 4);
@@ -261,29 +275,20 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
   // barrier that every warp reaches once it has finished the stage's previous tile.
   const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
   constexpr uint32_t tx = 2u * uint32_t(pl.mean_bytes + pl.codes_bytes + TT * pl.trow);
-  // warp-collective: lane 0 arms the barrier, then lane j issues copy j (all copies of a tile at once)
-  constexpr int NB = (H * GB) / 128;  // code bands per side
-  constexpr int NCOPY = 2 * (4 + NB + 1);
-  static_assert(NCOPY <= 32, "one TMA copy per lane");
-  auto issue = [&](int it) {
+  auto page_of = [&](int it) { return it < ntiles ? pt[(t_begin + it * TT) / P] : 0; };
+  auto issue = [&](int it, int page) {  // one thread: three copies per tile
     const int stg = it % S;
-    const int t0 = t_begin + it * TT;
-    const int page = pt[t0 / P];
-    const int row0 = t0 % P;
+    const int row0 = (t_begin + it * TT) % P;
     uint8_t* dst = smem + stg * pl.stage_bytes;
-    if (lane == 0) mbar_expect_tx(&full[stg], tx);
-    __syncwarp();
-    if (lane < NCOPY) {
-      const int side = lane / (5 + NB), j = lane % (5 + NB);
-      uint8_t* d0 = dst + side * pl.side_bytes;
-      if (j < 4) tma_3d(d0 + j * BAND, &maps.m[side][0], 128 * j, row0, page, &full[stg]);
-      else if (j < 4 + NB) tma_3d(d0 + pl.mean_bytes + (j - 4) * BAND, &maps.m[side][1], 128 * (j - 4), row0, page, &full[stg]);
-      else tma_3d(dst + 2 * pl.side_bytes + side * pl.meta_bytes, &maps.m[side][2], 0, row0, page, &full[stg]);
-    }
+    mbar_expect_tx(&full[stg], tx);
+    tma_5d(dst, &maps.m[0][0], row0, page, &full[stg]);
+    tma_5d(dst + 2 * pl.mean_bytes, &maps.m[0][1], row0, page, &full[stg]);
+    tma_4d(dst + 2 * pl.side_bytes, &maps.m[0][2], row0, page, &full[stg]);
   };
-  if (warp == 0) {
-    if (lane < 6) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[lane / 3][lane % 3])) : "memory");
-    for (int it = 0; it < S - 1 && it < ntiles; ++it) issue(it);
+  if (tid == 0) {
+    for (int k = 0; k < 3; ++k)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[0][k])) : "memory");
+    for (int it = 0; it < S - 1 && it < ntiles; ++it) issue(it, page_of(it));
   }
 
   // ---------------------------------------------------------------- prologue: q -> f16 fragments
@@ -357,6 +362,9 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
   const float NEG_INF = -__int_as_float(0x7f800000);
   __half* p2 = p2all + h * 8 * PROW2;
 
+  // warp 0 issues the refills right after barrier A; a late page-table load there would hold up
+  // barrier B for every warp, so the page of the next refill is fetched one tile ahead
+  int next_page = tid == 0 ? page_of(S - 1) : 0;
   for (int it = 0; it < ntiles; ++it) {
     const int stg = it % S;
     const int t0 = t_begin + it * TT;
@@ -364,9 +372,9 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
     mbar_wait(&full[stg], (it / S) & 1);
     const uint8_t* base = smem + stg * pl.stage_bytes;
     const uint8_t* kmean = base;
-    const uint8_t* kcodes = base + pl.mean_bytes;
-    const uint8_t* vmean = base + pl.side_bytes;
-    const uint8_t* vcodes = vmean + pl.mean_bytes;
+    const uint8_t* vmean = base + pl.mean_bytes;
+    const uint8_t* kcodes = base + 2 * pl.mean_bytes;
+    const uint8_t* vcodes = kcodes + pl.codes_bytes;
     const uint8_t* kmeta = base + 2 * pl.side_bytes;
     const uint8_t* vmeta = kmeta + pl.meta_bytes;
     if (nv < TT) {  // tail tile: rows past the sequence may hold anything; P·vmean needs them finite
@@ -433,6 +441,7 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
           wb[(4 * u) % NWD] = y.x; wb[(4 * u + 1) % NWD] = y.y; wb[(4 * u + 2) % NWD] = y.z; wb[(4 * u + 3) % NWD] = y.w;
         }
       }
+      float cs2[4] = {0.f, 0.f, 0.f, 0.f};  // second accumulator: two independent MMA chains of 4
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
         uint32_t af[4];
@@ -440,8 +449,11 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
         af[1] = qk_pair<BITS>(wb, s, 0);
         af[2] = qk_pair<BITS>(wa, s, 1);
         af[3] = qk_pair<BITS>(wb, s, 1);
-        mma(cs, af, qb[s][0], qb[s][1]);
+        if (s & 1) mma(cs2, af, qb[s][0], qb[s][1]);
+        else mma(cs, af, qb[s][0], qb[s][1]);
       }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) cs[e] += cs2[e];
       // − scale·(q·code) − min·Σq, for the G real columns
       if (2 * c < G) {
         const float2 ka = *reinterpret_cast<const float2*>(kmeta + ta * pl.trow + 8 * h);
@@ -457,7 +469,10 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
       }
     }
     __syncthreads();  // ---- BARRIER A: S complete; every warp is done with the previous tile
-    if (warp == 0 && it + S - 1 < ntiles) issue(it + S - 1);
+    if (tid == 0 && it + S - 1 < ntiles) {
+      issue(it + S - 1, next_page);
+      next_page = page_of(it + S);
+    }
 
     // ------------------------------------------------------------ B: online softmax, dense over (q, token)
     if (s_active) {  // thread = (q head sg, tokens TPT*sj .. +TPT-1)
@@ -483,11 +498,19 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
         x[u] = (TPT * sj + u < nv) ? x[u] * scale_log2 : NEG_INF;
         tmax = fmaxf(tmax, x[u]);
       }
+      // Lazy rescaling: the reference max only moves when a logit exceeds it by more than
+      // 2^LAZY (p <= 256 stays exact enough in f16/f32), so most tiles skip the row reduction
+      // and the O rescale.  A q row's TPQ threads are lanes of one warp, so the vote is uniform.
+      constexpr float LAZY = 8.f;
+      float corr = 1.f;
+      if (__any_sync(0xffffffffu, tmax > m_run + LAZY)) {
 #pragma unroll
-      for (int o = TPQ / 2; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
-      const float m_new = fmaxf(m_run, tmax);  // finite: every tile has >= 1 valid token
-      const float corr = ex2(m_run - m_new);
-      m_run = m_new;
+        for (int o = TPQ / 2; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+        const float m_new = fmaxf(m_run, tmax);  // finite: every tile has >= 1 valid token
+        corr = ex2(m_run - m_new);
+        m_run = m_new;
+      }
+      const float m_new = m_run;
       float lsum = 0.f, bsum = 0.f;
       __half pv[TPT], p2v[TPT];
 #pragma unroll
@@ -809,18 +832,37 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// 3-D byte tensor over the pool: (byte in row, row in page, page); box = [box0 B, 32 rows, 1 page].
-static bool encode_region(CUtensorMap* m, const uint8_t* base, uint64_t row_bytes, uint64_t rows, uint64_t page_bytes,
-                          uint32_t box0, bool swizzle) {
+// One tensor map per region (means, codes, metas) covering BOTH sides, so a 32-token tile is three
+// TMA copies.  Byte tensor dims (innermost first): byte within a 128-byte band, row (token) in the
+// page, band, side, page.  The box [128 | 32 | bands | 2 | 1] lands in shared memory as
+// [side][band][row][128 B]: every 128-byte line is one (band, row), so the 128B swizzle XORs the
+// 16-byte chunk index with (row & 7) exactly like swz().
+static bool encode_region5(CUtensorMap* m, const uint8_t* base, uint64_t row_bytes, uint64_t rows, uint64_t side_stride,
+                           uint64_t page_bytes) {
   auto enc = get_encode();
   if (!enc) return false;
-  const cuuint64_t dims[3] = {row_bytes, rows, uint64_t(1) << 20};
-  const cuuint64_t strides[2] = {row_bytes, page_bytes};
-  const cuuint32_t box[3] = {box0, uint32_t(fast::TT), 1};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  const uint64_t nband = row_bytes / 128;
+  const cuuint64_t dims[5] = {128, rows, nband, 2, uint64_t(1) << 20};
+  const cuuint64_t strides[4] = {row_bytes, 128, side_stride, page_bytes};
+  const cuuint32_t box[5] = {128, uint32_t(fast::TT), uint32_t(nband), 2, 1};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<uint8_t*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// metas: (byte in row, row, side, page); the box is 16 bytes wider than a row (zero fill) so that
+// smem rows are trow = H*8 + 16 bytes apart (bank spread for the per-token loads)
+static bool encode_meta(CUtensorMap* m, const uint8_t* base, uint64_t row_bytes, uint64_t rows, uint64_t side_stride,
+                        uint64_t page_bytes, uint32_t box0) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  const cuuint64_t dims[4] = {row_bytes, rows, 2, uint64_t(1) << 20};
+  const cuuint64_t strides[3] = {row_bytes, side_stride, page_bytes};
+  const cuuint32_t box[4] = {box0, uint32_t(fast::TT), 2, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 static int get_maps(const AttnArgs& a, TmaMaps* out) {
@@ -849,16 +891,16 @@ static int get_maps(const AttnArgs& a, TmaMaps* out) {
   }
   TmaMaps m{};
   const tada_page_layout& L = a.L;
-  const uint32_t trow = uint32_t(L.heads * 8 + 16);
-  for (int side = 0; side < 2; ++side) {
-    if (!encode_region(&m.m[side][0], a.pool + L.off_mean[side], uint64_t(L.head_dim) * 4, L.page_tokens, L.page_bytes,
-                       128, true) ||
-        !encode_region(&m.m[side][1], a.pool + L.off_codes[side], uint64_t(L.heads) * L.group_bytes, L.page_tokens,
-                       L.page_bytes, 128, true) ||
-        !encode_region(&m.m[side][2], a.pool + L.off_meta[side], uint64_t(L.heads) * 8, L.page_tokens, L.page_bytes,
-                       trow, false))
-      return fail(TADA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the decode-attention pool");
-  }
+  const uint64_t side_stride = uint64_t(L.off_mean[1] - L.off_mean[0]);
+  if (uint64_t(L.off_codes[1] - L.off_codes[0]) != side_stride || uint64_t(L.off_meta[1] - L.off_meta[0]) != side_stride)
+    return fail(TADA_ERR_CONFIG, "page layout sides are not uniformly strided");
+  if (!encode_region5(&m.m[0][0], a.pool + L.off_mean[0], uint64_t(L.head_dim) * 4, L.page_tokens, side_stride,
+                      L.page_bytes) ||
+      !encode_region5(&m.m[0][1], a.pool + L.off_codes[0], uint64_t(L.heads) * L.group_bytes, L.page_tokens,
+                      side_stride, L.page_bytes) ||
+      !encode_meta(&m.m[0][2], a.pool + L.off_meta[0], uint64_t(L.heads) * 8, L.page_tokens, side_stride, L.page_bytes,
+                   uint32_t(L.heads * 8 + 16)))
+    return fail(TADA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the decode-attention pool");
   if (cache.size() > 256) cache.clear();
   cache.emplace(key, m);
   *out = m;
