@@ -177,10 +177,13 @@ struct Plan {
 __host__ __device__ constexpr int up128(int x) { return (x + 127) / 128 * 128; }
 __host__ __device__ constexpr int up1k(int x) { return (x + 1023) / 1024 * 1024; }
 constexpr int PROW2 = TT + 8;  // P / P' row stride (halves): 80-byte rows, conflict-free ldmatrix / B loads
-constexpr int NSP = 5;         // logit partial planes: 4 QK mean-term d quarters + the code term
+// QK mean-term partial planes (d splits): 4 (16 warps x 2 k-steps), or 2 (8 warps x 4 k-steps) where
+// shared memory is tight (8-bit); plus one plane for the code term
+__host__ __device__ constexpr int nkq_for(int gb) { return gb >= 128 ? 2 : 4; }
 
 __host__ __device__ constexpr Plan make_plan(int H, int gb, int HQ) {
   Plan p{};
+  const int NSP = nkq_for(gb) + 1;
   const int mrows = HQ >= 16 ? HQ : 16;
   p.trow = H * 8 + 16;  // meta box row: the 16 B past the row are TMA zero fill (shifts banks by 4 per row)
   p.mean_bytes = (D * 4 / 128) * BAND;
@@ -190,10 +193,9 @@ __host__ __device__ constexpr Plan make_plan(int H, int gb, int HQ) {
   p.side_bytes = p.mean_bytes + p.codes_bytes;
   p.stage_bytes = up1k(2 * p.side_bytes + 2 * p.meta_bytes);
   const int sb = up128(NSP * mrows * SROW * 4);
-  const int q16 = up128(mrows * D * 2);
   const int pb = up128(mrows * PROW2 * 2);
   const int p2 = up128(H * 8 * PROW2 * 2);
-  const int tail = sb + q16 + pb + p2 + up128(mrows * 4) + up128(3 * HQ * 4) + up128(HQ * 4) + 128 + 1024;
+  const int tail = sb + pb + p2 + up128(mrows * 4) + up128(3 * HQ * 4) + up128(HQ * 4) + 128 + 1024;
   const int budget = 227 * 1024;
   p.stages = (3 * p.stage_bytes + tail <= budget) ? 3 : ((2 * p.stage_bytes + tail <= budget) ? 2 : 1);
   int off = p.stages * p.stage_bytes;
@@ -201,8 +203,7 @@ __host__ __device__ constexpr Plan make_plan(int H, int gb, int HQ) {
   if (off < HQ * D * 4) p.stages = 0;
   p.off_sbuf = off;
   off += sb;
-  p.off_q16 = off;
-  off += q16;
+  p.off_q16 = (p.stages - 1) * p.stage_bytes;  // prologue-only q staging: the last stage is loaded after it
   p.off_pbuf = off;
   off += pb;
   p.off_p2 = off;
@@ -238,7 +239,8 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
   constexpr int MROWS = MT * 16;
   constexpr int GB = BITS * D / 8;              // code bytes per (token, head)
   constexpr Plan pl = make_plan(H, GB, HQ);
-  constexpr int S = pl.stages;
+  constexpr int S = pl.stages < 2 ? 2 : pl.stages;  // geometries with < 2 stages are never launched
+  constexpr int NKQ = nkq_for(GB), NSP = NKQ + 1, KS = 8 / NKQ;  // mean-term d splits, planes, k-steps each
   constexpr int TPQ = (NTHR / HQ) < 32 ? (NTHR / HQ) : 32;  // softmax threads per q head
   constexpr int TPT = TT / TPQ;                             // tokens per softmax thread
   constexpr int NSM = HQ * TPQ;                             // active softmax threads
@@ -327,15 +329,15 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
     }
   }
   // QK mean A operand: q tile mt, k-step s = 2*kq + ks; slots (2c,2c+1 | 2c+8,2c+9) <-> d = 16s+4c+(0,1 | 2,3)
-  const int nt = warp & 3, kq = warp >> 2;
-  uint32_t qa[MT][2][4];
+  const int nt = warp & 3, kq = warp >> 2;  // piece of warps with kq < NKQ
+  uint32_t qa[MT][KS][4];
   {
     const __half* q16 = q16s;
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        const __half* r0 = q16 + (16 * mt + r) * D + 16 * (2 * kq + ks) + 4 * c;
+      for (int ks = 0; ks < KS; ++ks) {
+        const __half* r0 = q16 + (16 * mt + r) * D + 16 * ((KS * kq + ks) & 7) + 4 * c;
         const __half* r1 = r0 + 8 * D;
         qa[mt][ks][0] = *reinterpret_cast<const uint32_t*>(r0);
         qa[mt][ks][1] = *reinterpret_cast<const uint32_t*>(r1);
@@ -343,6 +345,7 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
         qa[mt][ks][3] = *reinterpret_cast<const uint32_t*>(r1 + 2);
       }
   }
+  fence_proxy_async();  // q staging lives in the last stage, which TMA fills after the next barrier
   float qs[2];  // Σq of this thread's two code columns n = 2c, 2c+1
 #pragma unroll
   for (int e = 0; e < 2; ++e) qs[e] = (2 * c + e < G) ? qsum[h * G + 2 * c + e] : 0.f;
@@ -387,14 +390,14 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
     }
 
     // ------------------------------------------------------------ A1: QK mean piece -> S_mean[kq]
-    {
+    if (kq < NKQ) {
       const int tok = 8 * nt + r;
       float acc[MT][4];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
 #pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        const int s = 2 * kq + ks;
+      for (int ks = 0; ks < KS; ++ks) {
+        const int s = KS * kq + ks;
         const float4 x = *reinterpret_cast<const float4*>(kmean + (s >> 1) * BAND + swz(tok, 64 * (s & 1) + 16 * c));
         uint32_t h0, l0, h1, l1;
         split_h2(x.x, x.y, h0, l0);
