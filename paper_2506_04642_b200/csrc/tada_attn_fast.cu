@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           if (2 * c + e < G) {
-            float* row = sbuf + (4 * MROWS + h * G + 2 * c + e) * SROW;
+            float* row = sbuf + (NKQ * MROWS + h * G + 2 * c + e) * SROW;
             row[ta] = -fmaf(ka.x, cs[e], ka.y * qs[e]);
             row[tb] = -fmaf(kb.x, cs[2 + e], kb.y * qs[e]);
           }
