@@ -131,6 +131,13 @@ int tada_residual_write(float* res_k, float* res_v, int64_t res_seq_stride, int3
                         int32_t batch, int64_t n_tok, int64_t src_seq_stride, const int32_t* pos,
                         int32_t pos_offset, void* stream);
 
+/* tada_residual_write at pos[b] (pos_offset 0) followed by pos[b] += n_tok, in one launch:
+ * the no-flush branch of append_tokens (cache.py:174-175) for a decode step. */
+int tada_residual_append(float* res_k, float* res_v, int64_t res_seq_stride, int32_t heads,
+                         int32_t head_dim, const void* src_k, const void* src_v, int32_t dtype,
+                         int32_t batch, int64_t n_tok, int64_t src_seq_stride, int32_t* pos,
+                         void* stream);
+
 /* arr[b] += delta for b < batch (device-side length bookkeeping, graph-capturable). */
 int tada_lengths_add(int32_t* arr, int32_t batch, int32_t delta, void* stream);
 

@@ -174,6 +174,122 @@ __global__ void combine_lse_kernel(const float* __restrict__ o, const float* __r
   }
 }
 
+// ------------------------------------------------------------------ K3 for the tensor-core path:
+// residual rows + split merge, one CTA per (KV head, sequence).
+// The raw f32 residual tokens (cache.py:174-180) are attended exactly like the reference's
+// residual tiles (attention.py:94-100: f32 dot, scale after the dot) and merged with the
+// compressed-token splits by the log-sum-exp rule:
+//   out = (Σ_s e^{m_s-M} acc_s + e^{m_r-M} Σ_t p_t v_t) / (Σ_s e^{m_s-M} l_s + e^{m_r-M} l_r)
+__device__ __forceinline__ float block_max128(float v, float* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  const float r = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+  __syncthreads();
+  return r;
+}
+__device__ __forceinline__ float block_sum128(float v, float* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  const float r = (red[0] + red[1]) + (red[2] + red[3]);
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(128) combine_residual_kernel(AttnArgs a) {
+  extern __shared__ __align__(16) float sm[];
+  const int H = a.L.heads, D = a.L.head_dim, Hq = a.Hq, G = Hq / H, S = a.splits;
+  const int h = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  const int R = a.res_len[b];
+  const int rcap = int(a.res_seq_stride);
+  float* qs = sm;                  // [G][D]
+  float* pr = qs + G * D;          // [G][rcap]  residual logits -> probabilities
+  float* ws = pr + G * rcap;       // [G][S]     split weights
+  float* st = ws + G * S;          // [G][4]     (M, w_res, L, -)
+  float* red = st + 4 * G;         // [4]
+  for (int i = tid; i < G * D; i += blockDim.x) {
+    const int64_t qi = (int64_t(b) * Hq + h * G) * D + i;
+    qs[i] = a.q_dtype == TADA_F32 ? reinterpret_cast<const float*>(a.q)[qi]
+                                  : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(a.q)[qi]);
+  }
+  __syncthreads();
+  const int64_t rbase = int64_t(b) * a.res_seq_stride;
+  for (int t = tid; t < R; t += blockDim.x) {
+    const float* kr = a.res_k + ((rbase + t) * H + h) * D;
+    float dot[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int d = 0; d < D; d += 4) {  // the fast path has D % 4 == 0 (D = 128)
+      const float4 k4 = *reinterpret_cast<const float4*>(kr + d);
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        if (g < G) {
+          const float4 q4 = *reinterpret_cast<const float4*>(qs + g * D + d);
+          dot[g] = __fmaf_rn(q4.w, k4.w, __fmaf_rn(q4.z, k4.z, __fmaf_rn(q4.y, k4.y, __fmaf_rn(q4.x, k4.x, dot[g]))));
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+      if (g < G) pr[g * rcap + t] = __fmul_rn(dot[g], a.scale);
+  }
+  __syncthreads();
+  for (int g = 0; g < G; ++g) {
+    const int gq = h * G + g;
+    const float* ml = a.part_ml + (int64_t(b) * Hq + gq) * a.slots * 2;
+    float mx = -__int_as_float(0x7f800000);
+    for (int t = tid; t < R; t += blockDim.x) mx = fmaxf(mx, pr[g * rcap + t]);
+    for (int s2 = tid; s2 < S; s2 += blockDim.x)
+      if (ml[2 * s2 + 1] > 0.f) mx = fmaxf(mx, ml[2 * s2]);
+    const float M = block_max128(mx, red);
+    float lr = 0.f;
+    for (int t = tid; t < R; t += blockDim.x) {
+      const float p = expf(pr[g * rcap + t] - M);
+      pr[g * rcap + t] = p;
+      lr += p;
+    }
+    float lsum = lr;
+    for (int s2 = tid; s2 < S; s2 += blockDim.x) {
+      const float w = ml[2 * s2 + 1] > 0.f ? expf(ml[2 * s2] - M) : 0.f;
+      ws[g * S + s2] = w;
+      lsum += w * ml[2 * s2 + 1];
+    }
+    const float L = block_sum128(lsum, red);
+    if (tid == 0) {
+      st[4 * g] = M;
+      st[4 * g + 2] = L;
+    }
+  }
+  __syncthreads();
+  for (int d = tid; d < D; d += blockDim.x) {
+    for (int g = 0; g < G; ++g) {
+      const int gq = h * G + g;
+      const float* pa = a.part_acc + (int64_t(b) * Hq + gq) * a.slots * D + d;
+      float acc = 0.f;
+      for (int s2 = 0; s2 < S; ++s2) {
+        const float w = ws[g * S + s2];
+        if (w != 0.f) acc = fmaf(w, pa[int64_t(s2) * D], acc);
+      }
+      const float* vr = a.res_v + (rbase * H + h) * D + d;
+      for (int t = 0; t < R; ++t) acc = fmaf(pr[g * rcap + t], vr[int64_t(t) * H * D], acc);
+      const float L = st[4 * g + 2];
+      store_any(a.out, a.out_dtype, (int64_t(b) * Hq + gq) * D + d, acc / L);
+      if (d == 0 && a.lse_out) a.lse_out[int64_t(b) * Hq + gq] = st[4 * g] + logf(L);
+    }
+  }
+}
+
+static int launch_combine_residual(const AttnArgs& a, int batch, cudaStream_t st) {
+  const int G = a.Hq / a.L.heads;
+  const size_t smem = (size_t(G) * a.L.head_dim + size_t(G) * a.res_seq_stride + size_t(G) * a.splits + 4 * G + 4) * 4;
+  if (smem > 220 * 1024) return fail(TADA_ERR_CONFIG, "residual_length x group size too large for the combine kernel");
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(combine_residual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string("combine smem: ") + cudaGetErrorString(e));
+  }
+  combine_residual_kernel<<<dim3(a.L.heads, batch), 128, smem, st>>>(a);
+  return check_launch("decode_attn_combine_residual");
+}
+
 template <typename QT>
 static int launch_generic(const AttnArgs& a, int batch, cudaStream_t st) {
   const int Hq = a.Hq, D = a.L.head_dim;
@@ -258,7 +374,7 @@ static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool,
   a.res_seq_stride = res_seq_stride;
   a.scale = scale;
   a.splits = num_splits;
-  a.slots = fast ? num_splits + 1 : num_splits;
+  a.slots = num_splits;
   a.part_acc = reinterpret_cast<float*>(workspace);
   a.part_ml = a.part_acc + int64_t(batch) * num_q_heads * a.slots * layout->head_dim;
   a.out = out;
@@ -269,7 +385,8 @@ static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool,
   int rc;
   if (fast) {
     rc = launch_fast(a, batch, st);
-    if (rc == TADA_OK) rc = launch_residual(a, batch, st);
+    if (rc == TADA_OK) rc = launch_combine_residual(a, batch, st);
+    return rc;
   } else {
     rc = q_dtype == TADA_F32 ? launch_generic<float>(a, batch, st) : launch_generic<__nv_bfloat16>(a, batch, st);
     if (rc != TADA_OK || num_splits == 1) return rc;

@@ -52,6 +52,5 @@ struct alignas(64) TmaMaps {
 // geometry is unsupported so the caller can fall back to the generic kernel.
 bool fast_supported(const tada_page_layout& L, int Hq);
 int launch_fast(const AttnArgs& a, int batch, cudaStream_t st);
-int launch_residual(const AttnArgs& a, int batch, cudaStream_t st);
 
 }  // namespace tada

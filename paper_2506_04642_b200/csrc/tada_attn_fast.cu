@@ -740,78 +740,6 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
 
 }  // namespace fast
 
-// ------------------------------------------------------------------ residual rows -> extra split slot
-// The raw f32 residual tokens (cache.py:174-180) of each sequence, attended exactly like
-// the reference's residual tiles (attention.py:94-100); result goes to slot `splits`.
-__global__ void __launch_bounds__(256) attn_residual_kernel(AttnArgs a) {
-  extern __shared__ __align__(16) float sm[];
-  const int H = a.L.heads, D = a.L.head_dim, Hq = a.Hq, G = Hq / H;
-  const int b = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
-  const int R = a.res_len[b];
-  constexpr int TILE = 32;
-  float* qs = sm;                 // [Hq][D]
-  float* acc = qs + Hq * D;       // [Hq][D]
-  float* lg = acc + Hq * D;       // [Hq][TILE]
-  float* mrow = lg + Hq * TILE;
-  float* lrow = mrow + Hq;
-  float* crow = lrow + Hq;
-  for (int i = tid; i < Hq * D; i += bd) {
-    qs[i] = a.q_dtype == TADA_F32 ? reinterpret_cast<const float*>(a.q)[int64_t(b) * Hq * D + i]
-                                  : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(a.q)[int64_t(b) * Hq * D + i]);
-    acc[i] = 0.f;
-  }
-  for (int g = tid; g < Hq; g += bd) {
-    mrow[g] = -__int_as_float(0x7f800000);
-    lrow[g] = 0.f;
-  }
-  __syncthreads();
-  const int64_t base = int64_t(b) * a.res_seq_stride;
-  for (int t0 = 0; t0 < R; t0 += TILE) {
-    const int nt = min(TILE, R - t0);
-    for (int pair = tid; pair < Hq * nt; pair += bd) {
-      const int g = pair / nt, j = pair - g * nt, h = g / G;
-      const float* kr = a.res_k + ((base + t0 + j) * H + h) * D;
-      const float* qg = qs + g * D;
-      float dot = 0.f;
-      for (int d = 0; d < D; ++d) dot = __fmaf_rn(qg[d], kr[d], dot);
-      lg[g * TILE + j] = __fmul_rn(dot, a.scale);
-    }
-    __syncthreads();
-    for (int g = tid; g < Hq; g += bd) {
-      float tmax = lg[g * TILE];
-      for (int j = 1; j < nt; ++j) tmax = fmaxf(tmax, lg[g * TILE + j]);
-      const float m_new = fmaxf(mrow[g], tmax);
-      const float corr = expf(mrow[g] - m_new);
-      float sum = 0.f;
-      for (int j = 0; j < nt; ++j) {
-        const float p = expf(lg[g * TILE + j] - m_new);
-        lg[g * TILE + j] = p;
-        sum += p;
-      }
-      lrow[g] = lrow[g] * corr + sum;
-      mrow[g] = m_new;
-      crow[g] = corr;
-    }
-    __syncthreads();
-    for (int pair = tid; pair < Hq * D; pair += bd) {
-      const int g = pair / D, d = pair - g * D, h = g / G;
-      float av = acc[pair] * crow[g];
-      for (int j = 0; j < nt; ++j) av = __fmaf_rn(lg[g * TILE + j], a.res_v[((base + t0 + j) * H + h) * D + d], av);
-      acc[pair] = av;
-    }
-    __syncthreads();
-  }
-  for (int pair = tid; pair < Hq * D; pair += bd) {
-    const int g = pair / D, d = pair - g * D;
-    a.part_acc[((int64_t(b) * Hq + g) * a.slots + a.splits) * D + d] = acc[pair];
-  }
-  for (int g = tid; g < Hq; g += bd) {
-    float* ml = a.part_ml + ((int64_t(b) * Hq + g) * a.slots + a.splits) * 2;
-    ml[0] = mrow[g];
-    ml[1] = lrow[g];
-  }
-}
-
 bool fast_supported(const tada_page_layout& L, int Hq) {
   // compiled geometries: 8 KV heads (the Llama-3 family) with 8/16/32/64 q heads
   if (L.head_dim != 128 || !(L.bits == 2 || L.bits == 4 || L.bits == 8) || L.heads != 8) return false;
@@ -943,16 +871,6 @@ int launch_fast(const AttnArgs& a, int batch, cudaStream_t st) {
     case 4: return launch_fast_b<4>(a, batch, st);
     default: return launch_fast_b<8>(a, batch, st);
   }
-}
-
-int launch_residual(const AttnArgs& a, int batch, cudaStream_t st) {
-  const size_t smem = (size_t(2) * a.Hq * a.L.head_dim + size_t(a.Hq) * 32 + 3 * a.Hq) * 4;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(attn_residual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string("attn_residual smem: ") + cudaGetErrorString(e));
-  }
-  attn_residual_kernel<<<batch, 256, smem, st>>>(a);
-  return check_launch("decode_attn_residual");
 }
 
 }  // namespace tada

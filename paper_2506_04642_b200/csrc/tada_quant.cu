@@ -351,6 +351,29 @@ __global__ void residual_write_kernel(float* __restrict__ rk, float* __restrict_
   }
 }
 
+// Residual append for the no-flush case (cache.py:174-175): one CTA per sequence copies its n_tok
+// rows to res[pos[b] ..] and then advances pos[b] by n_tok (the length update rides along, so a
+// decode step's append is one launch).
+template <typename T>
+__global__ void __launch_bounds__(256) residual_append_kernel(float* __restrict__ rk, float* __restrict__ rv,
+                                                              int64_t res_seq_stride, int row,
+                                                              const T* __restrict__ sk, const T* __restrict__ sv,
+                                                              int64_t n_tok, int64_t src_seq_stride, int32_t* pos) {
+  const int b = blockIdx.x;
+  const int64_t p0 = pos[b];
+  const int64_t n = n_tok * row;
+  const T* s0 = sk + int64_t(b) * src_seq_stride * row;
+  const T* s1 = sv + int64_t(b) * src_seq_stride * row;
+  float* d0 = rk + (int64_t(b) * res_seq_stride + p0) * row;
+  float* d1 = rv + (int64_t(b) * res_seq_stride + p0) * row;
+  for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+    d0[e] = to_f32(s0[e]);
+    d1[e] = to_f32(s1[e]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) pos[b] = int32_t(p0 + n_tok);
+}
+
 __global__ void lengths_add_kernel(int32_t* arr, int batch, int32_t delta) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < batch) arr[i] += delta;
@@ -588,6 +611,25 @@ int tada_residual_write(float* res_k, float* res_v, int64_t res_seq_stride, int3
         res_k, res_v, res_seq_stride, row, reinterpret_cast<const __nv_bfloat16*>(src_k),
         reinterpret_cast<const __nv_bfloat16*>(src_v), n_tok, src_seq_stride, pos, pos_offset, batch);
   return check_launch("residual_write");
+}
+
+int tada_residual_append(float* res_k, float* res_v, int64_t res_seq_stride, int32_t heads, int32_t head_dim,
+                         const void* src_k, const void* src_v, int32_t dtype, int32_t batch, int64_t n_tok,
+                         int64_t src_seq_stride, int32_t* pos, void* stream) {
+  if (!valid_dtype(dtype)) return fail(TADA_ERR_CONFIG, "dtype must be f32 or bf16");
+  if (batch < 0 || n_tok < 0) return fail(TADA_ERR_SHAPE, "bad batch/token geometry");
+  if (batch == 0 || n_tok == 0) return TADA_OK;
+  const int row = heads * head_dim;
+  if (dtype == TADA_F32)
+    residual_append_kernel<float><<<batch, 256, 0, S(stream)>>>(res_k, res_v, res_seq_stride, row,
+                                                                 reinterpret_cast<const float*>(src_k),
+                                                                 reinterpret_cast<const float*>(src_v), n_tok,
+                                                                 src_seq_stride, pos);
+  else
+    residual_append_kernel<__nv_bfloat16><<<batch, 256, 0, S(stream)>>>(
+        res_k, res_v, res_seq_stride, row, reinterpret_cast<const __nv_bfloat16*>(src_k),
+        reinterpret_cast<const __nv_bfloat16*>(src_v), n_tok, src_seq_stride, pos);
+  return check_launch("residual_append");
 }
 
 int tada_lengths_add(int32_t* arr, int32_t batch, int32_t delta, void* stream) {

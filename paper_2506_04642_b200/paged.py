@@ -180,9 +180,11 @@ class PagedKVCache:
             return
         total = r + n
         ncomp = (total // R) * R
-        if ncomp == 0:
-            self._residual_write(layer, k, v, 0, n, 0)
-            self._add(self.res_len, self.res_host, layer, n)
+        if ncomp == 0:  # no flush: one launch writes the rows and advances res_len
+            call("tada_residual_append", self.res_k[layer].data_ptr(), self.res_v[layer].data_ptr(),
+                 self.res_k[layer].shape[1], self.H, self.D, k.data_ptr(), v.data_ptr(), dt, self.B, n, n,
+                 self.res_len[layer].data_ptr(), _dev.stream())
+            self.res_host[layer] += n
             return
         self._ensure_pages(C + ncomp)
         if r:  # the buffered residual rows are the oldest tokens of the flushed blocks
