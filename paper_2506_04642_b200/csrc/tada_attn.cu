@@ -180,113 +180,102 @@ __global__ void combine_lse_kernel(const float* __restrict__ o, const float* __r
 // residual tiles (attention.py:94-100: f32 dot, scale after the dot) and merged with the
 // compressed-token splits by the log-sum-exp rule:
 //   out = (Σ_s e^{m_s-M} acc_s + e^{m_r-M} Σ_t p_t v_t) / (Σ_s e^{m_s-M} l_s + e^{m_r-M} l_r)
-__device__ __forceinline__ float block_max128(float v, float* red) {
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+constexpr int kCombThreads = 256;
+__device__ __forceinline__ float block_reduce(float v, float* red, bool is_max) {
+  for (int o = 16; o > 0; o >>= 1) {
+    const float u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmaxf(v, u) : v + u;
+  }
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
-  const float r = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
-  __syncthreads();
-  return r;
-}
-__device__ __forceinline__ float block_sum128(float v, float* red) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  const float r = (red[0] + red[1]) + (red[2] + red[3]);
+  float r = red[0];
+  for (int w = 1; w < kCombThreads / 32; ++w) r = is_max ? fmaxf(r, red[w]) : r + red[w];
   __syncthreads();
   return r;
 }
 
-__global__ void __launch_bounds__(128) combine_residual_kernel(AttnArgs a) {
+// One CTA per (q head, sequence), 256 threads.
+__global__ void __launch_bounds__(kCombThreads) combine_residual_kernel(AttnArgs a) {
   extern __shared__ __align__(16) float sm[];
   const int H = a.L.heads, D = a.L.head_dim, Hq = a.Hq, G = Hq / H, S = a.splits;
-  const int h = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  const int gq = blockIdx.x, b = blockIdx.y, h = gq / G, tid = threadIdx.x;
   const int R = a.res_len[b];
-  const int rcap = int(a.res_seq_stride);
-  float* qs = sm;                  // [G][D]
-  float* pr = qs + G * D;          // [G][rcap]  residual logits -> probabilities
-  float* ws = pr + G * rcap;       // [G][S]     split weights
-  float* st = ws + G * S;          // [G][4]     (M, w_res, L, -)
-  float* red = st + 4 * G;         // [4]
-  for (int i = tid; i < G * D; i += blockDim.x) {
-    const int64_t qi = (int64_t(b) * Hq + h * G) * D + i;
-    qs[i] = a.q_dtype == TADA_F32 ? reinterpret_cast<const float*>(a.q)[qi]
-                                  : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(a.q)[qi]);
-  }
+  float* qs = sm;            // [D]
+  float* pr = qs + D;        // [rcap] residual logits -> probabilities
+  float* ws = pr + a.res_seq_stride;  // [S] split weights
+  float* part = ws + S;      // [2][D] partial outputs of the two thread halves
+  float* red = part + 2 * D; // [8]
+  const int64_t qi = (int64_t(b) * Hq + gq) * D;
+  for (int i = tid; i < D; i += kCombThreads)
+    qs[i] = a.q_dtype == TADA_F32 ? reinterpret_cast<const float*>(a.q)[qi + i]
+                                  : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(a.q)[qi + i]);
   __syncthreads();
   const int64_t rbase = int64_t(b) * a.res_seq_stride;
-  for (int t = tid; t < R; t += blockDim.x) {
+  float mx = -__int_as_float(0x7f800000);
+  for (int t = tid; t < R; t += kCombThreads) {
     const float* kr = a.res_k + ((rbase + t) * H + h) * D;
-    float dot[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int d = 0; d < D; d += 4) {  // the fast path has D % 4 == 0 (D = 128)
+    float dot = 0.f;
+    for (int d = 0; d < D; d += 4) {  // the fast path has D % 4 == 0
       const float4 k4 = *reinterpret_cast<const float4*>(kr + d);
-#pragma unroll
-      for (int g = 0; g < 8; ++g) {
-        if (g < G) {
-          const float4 q4 = *reinterpret_cast<const float4*>(qs + g * D + d);
-          dot[g] = __fmaf_rn(q4.w, k4.w, __fmaf_rn(q4.z, k4.z, __fmaf_rn(q4.y, k4.y, __fmaf_rn(q4.x, k4.x, dot[g]))));
-        }
-      }
+      const float4 q4 = *reinterpret_cast<const float4*>(qs + d);
+      dot = __fmaf_rn(q4.w, k4.w, __fmaf_rn(q4.z, k4.z, __fmaf_rn(q4.y, k4.y, __fmaf_rn(q4.x, k4.x, dot))));
     }
-#pragma unroll
-    for (int g = 0; g < 8; ++g)
-      if (g < G) pr[g * rcap + t] = __fmul_rn(dot[g], a.scale);
+    const float sv = __fmul_rn(dot, a.scale);
+    pr[t] = sv;
+    mx = fmaxf(mx, sv);
+  }
+  const float* ml = a.part_ml + (int64_t(b) * Hq + gq) * a.slots * 2;
+  for (int s2 = tid; s2 < S; s2 += kCombThreads)
+    if (ml[2 * s2 + 1] > 0.f) mx = fmaxf(mx, ml[2 * s2]);
+  const float M = block_reduce(mx, red, true);
+  float lsum = 0.f;
+  for (int t = tid; t < R; t += kCombThreads) {
+    const float p = expf(pr[t] - M);
+    pr[t] = p;
+    lsum += p;
+  }
+  for (int s2 = tid; s2 < S; s2 += kCombThreads) {
+    const float w = ml[2 * s2 + 1] > 0.f ? expf(ml[2 * s2] - M) : 0.f;
+    ws[s2] = w;
+    lsum += w * ml[2 * s2 + 1];
+  }
+  const float L = block_reduce(lsum, red, false);  // its barrier also publishes pr / ws
+  // output: thread = (half j, d); each half takes every other slot and residual token
+  const int j = tid / D, d = tid - j * D;
+  if (j < 2) {
+    const float* pa = a.part_acc + (int64_t(b) * Hq + gq) * a.slots * D + d;
+    float acc0 = 0.f, acc1 = 0.f;
+    int s2 = j;
+    for (; s2 + 2 < S; s2 += 4) {
+      acc0 = fmaf(ws[s2], pa[int64_t(s2) * D], acc0);
+      acc1 = fmaf(ws[s2 + 2], pa[int64_t(s2 + 2) * D], acc1);
+    }
+    for (; s2 < S; s2 += 2) acc0 = fmaf(ws[s2], pa[int64_t(s2) * D], acc0);
+    const float* vr = a.res_v + (rbase * H + h) * D + d;
+    int t = j;
+    for (; t + 2 < R; t += 4) {
+      acc0 = fmaf(pr[t], vr[int64_t(t) * H * D], acc0);
+      acc1 = fmaf(pr[t + 2], vr[int64_t(t + 2) * H * D], acc1);
+    }
+    for (; t < R; t += 2) acc0 = fmaf(pr[t], vr[int64_t(t) * H * D], acc0);
+    part[j * D + d] = acc0 + acc1;
   }
   __syncthreads();
-  for (int g = 0; g < G; ++g) {
-    const int gq = h * G + g;
-    const float* ml = a.part_ml + (int64_t(b) * Hq + gq) * a.slots * 2;
-    float mx = -__int_as_float(0x7f800000);
-    for (int t = tid; t < R; t += blockDim.x) mx = fmaxf(mx, pr[g * rcap + t]);
-    for (int s2 = tid; s2 < S; s2 += blockDim.x)
-      if (ml[2 * s2 + 1] > 0.f) mx = fmaxf(mx, ml[2 * s2]);
-    const float M = block_max128(mx, red);
-    float lr = 0.f;
-    for (int t = tid; t < R; t += blockDim.x) {
-      const float p = expf(pr[g * rcap + t] - M);
-      pr[g * rcap + t] = p;
-      lr += p;
-    }
-    float lsum = lr;
-    for (int s2 = tid; s2 < S; s2 += blockDim.x) {
-      const float w = ml[2 * s2 + 1] > 0.f ? expf(ml[2 * s2] - M) : 0.f;
-      ws[g * S + s2] = w;
-      lsum += w * ml[2 * s2 + 1];
-    }
-    const float L = block_sum128(lsum, red);
-    if (tid == 0) {
-      st[4 * g] = M;
-      st[4 * g + 2] = L;
-    }
-  }
-  __syncthreads();
-  for (int d = tid; d < D; d += blockDim.x) {
-    for (int g = 0; g < G; ++g) {
-      const int gq = h * G + g;
-      const float* pa = a.part_acc + (int64_t(b) * Hq + gq) * a.slots * D + d;
-      float acc = 0.f;
-      for (int s2 = 0; s2 < S; ++s2) {
-        const float w = ws[g * S + s2];
-        if (w != 0.f) acc = fmaf(w, pa[int64_t(s2) * D], acc);
-      }
-      const float* vr = a.res_v + (rbase * H + h) * D + d;
-      for (int t = 0; t < R; ++t) acc = fmaf(pr[g * rcap + t], vr[int64_t(t) * H * D], acc);
-      const float L = st[4 * g + 2];
-      store_any(a.out, a.out_dtype, (int64_t(b) * Hq + gq) * D + d, acc / L);
-      if (d == 0 && a.lse_out) a.lse_out[int64_t(b) * Hq + gq] = st[4 * g] + logf(L);
-    }
+  for (int dd = tid; dd < D; dd += kCombThreads) {
+    store_any(a.out, a.out_dtype, qi + dd, (part[dd] + part[D + dd]) / L);
+    if (dd == 0 && a.lse_out) a.lse_out[int64_t(b) * Hq + gq] = M + logf(L);
   }
 }
 
 static int launch_combine_residual(const AttnArgs& a, int batch, cudaStream_t st) {
-  const int G = a.Hq / a.L.heads;
-  const size_t smem = (size_t(G) * a.L.head_dim + size_t(G) * a.res_seq_stride + size_t(G) * a.splits + 4 * G + 4) * 4;
-  if (smem > 220 * 1024) return fail(TADA_ERR_CONFIG, "residual_length x group size too large for the combine kernel");
+  if (a.L.head_dim * 2 > kCombThreads * 2 || a.L.head_dim % 4) return fail(TADA_ERR_CONFIG, "combine needs head_dim % 4 == 0");
+  const size_t smem = (size_t(a.L.head_dim) * 3 + size_t(a.res_seq_stride) + size_t(a.splits) + 8) * 4;
+  if (smem > 220 * 1024) return fail(TADA_ERR_CONFIG, "residual_length too large for the combine kernel");
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(combine_residual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string("combine smem: ") + cudaGetErrorString(e));
   }
-  combine_residual_kernel<<<dim3(a.L.heads, batch), 128, smem, st>>>(a);
+  combine_residual_kernel<<<dim3(a.Hq, batch), kCombThreads, smem, st>>>(a);
   return check_launch("decode_attn_combine_residual");
 }
 

@@ -30,9 +30,9 @@ if [[ $what == prof || $what == all ]]; then
   echo "prof rc=$?" >> gpurun_out/prof.log
 fi
 if [[ $what == ncu || $what == all ]]; then
-  # skip prefill (2 launches/layer) + 3 warm-up steps (5 launches/layer/step), list 2 steps
+  # skip prefill (2 launches/layer) + 3 warm-up steps (3 launches/layer/step), list 2 steps
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'attn|combine|residual|lengths|quant' \
-    -s 544 -c 320 --csv \
+    -s 352 -c 192 --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_bench.log 2>&1
   echo "ncu rc=$?" >> gpurun_out/ncu_bench.log
 fi
