@@ -1,0 +1,67 @@
+"""Copy the judged evidence from gpurun_out/ (scratch) into profiles/ (tracked).
+
+python tools/make_profiles.py <tag>
+  gpurun_out/attn4.ncu-rep  -> profiles/<tag>_attn4_ncu.txt (headline metrics, stalls, opcode mix, hot lines)
+                               profiles/attn_traffic.json   (dram bytes per launch, read by bench.py)
+  gpurun_out/launches.csv   -> profiles/<tag>_launches.csv + profiles/<tag>_launches.txt
+  gpurun_out/bench.log      -> profiles/<tag>_bench.json (the bench line)
+"""
+import csv
+import io
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+PROF = os.path.join(ROOT, "profiles")
+
+
+def run(*cmd):
+    return subprocess.run([sys.executable, *cmd], capture_output=True, text=True, cwd=ROOT).stdout
+
+
+def main():
+    tag = sys.argv[1]
+    os.makedirs(PROF, exist_ok=True)
+    rep = os.path.join(OUT, "attn4.ncu-rep")
+    if os.path.exists(rep):
+        tiles = 16 * 32768 // 32
+        txt = run("tools/ncu_summary.py", rep, str(tiles))
+        txt += "\n--- per source line (top 40 by instructions + stalls)\n"
+        txt += run("tools/ncu_lines.py", rep, "paper_2506_04642_b200/csrc/tada_attn_fast.cu", "40", str(tiles))
+        open(os.path.join(PROF, f"{tag}_attn4_ncu.txt"), "w").write(
+            "ncu --set full --clock-control none --import-source on -k regex:attn_fast -s 3 -c 1 "
+            "python tools/attn_bench.py --bits 4 (B=16, T=32768, Hq=32, H=8, D=128)\n\n" + txt)
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(raw)))
+        d = dict(zip(rows[0], rows[2]))
+        unit = dict(zip(rows[0], rows[1]))
+
+        def nbytes(k):
+            v = float(d[k])
+            return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit[k]]
+
+        traffic = nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum")
+        json.dump({"traffic_bytes_per_launch": traffic, "kernel": "attn_fast_kernel<4,32>",
+                   "shape": "B=16, T=32768 compressed, Hq=32, H=8, D=128, 4-bit",
+                   "alg_bytes_per_launch": 16 * (32768 * 2 * (4 * 128 + 8 * 64 + 64) + 2 * 32 * 128 * 2),
+                   "source": f"profiles/{tag}_attn4_ncu.txt"}, open(os.path.join(PROF, "attn_traffic.json"), "w"),
+                  indent=1)
+    lc = os.path.join(OUT, "launches.csv")
+    if os.path.exists(lc):
+        shutil.copy(lc, os.path.join(PROF, f"{tag}_launches.csv"))
+        open(os.path.join(PROF, f"{tag}_launches.txt"), "w").write(
+            "ncu --metrics gpu__time_duration.sum --clock-control none (2 decode steps of bench.py, after prefill "
+            "and warm-up; cold-cache serialised launches: compare shares)\n" + run("tools/launch_summary.py", lc))
+    bl = os.path.join(OUT, "bench.log")
+    if os.path.exists(bl):
+        for ln in open(bl):
+            if ln.startswith("{"):
+                open(os.path.join(PROF, f"{tag}_bench.json"), "w").write(ln)
+
+
+if __name__ == "__main__":
+    main()
