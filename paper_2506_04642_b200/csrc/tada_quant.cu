@@ -431,6 +431,116 @@ static int launch_quantize(const void* rows, int64_t n, int D, int bits, uint8_t
   return check_launch("quantize_groups");
 }
 
+// ------------------------------------------------------------------ K1 fast path (head_dim 128, 8 heads)
+//
+// One warp per (token, side).  Lane l owns columns d = 4l .. 4l+3 of all 8 heads, so
+//  * the cross-head mean of its 4 columns is a register-only f64 sequential sum (cache.py:109);
+//  * each (token, head) group's min / max is one CREDUX.MIN/MAX.F32 across the warp;
+//  * lane h computes group h's fp64 scale + refinement (quant.py:153-167) and broadcasts it;
+//  * codes use an f32 round-to-nearest estimate q = (d - min) / s through the 2^23 magic add;
+//    when |q - RN(q)| is within 2^-12 of a half-integer the lane's group falls back to the
+//    exact fp64 half-up sequence (quant_code), which decides every tie like the reference.
+// Loads are 8-byte (bf16) / 16-byte (f32) per lane and head, stores 16-bit (4-bit) codes per
+// lane and head, a float4 of the mean per lane, and (scale, min) by lanes 0..7.
+__device__ __forceinline__ float redux_min(float v) {
+  float r;
+  asm volatile("redux.sync.min.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ float redux_max(float v) {
+  float r;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+
+template <typename T, int BITS>
+__global__ void __launch_bounds__(256) quant_append_fast_kernel(AppendArgs a, int batch) {
+  constexpr int H = 8, D = 128, GB = D * BITS / 8, CMAX = (1 << BITS) - 1;
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (wid >= int64_t(batch) * a.n_tok * 2) return;
+  const int side = int(wid & 1);
+  const int64_t ti = wid >> 1;
+  const int b = int(ti / a.n_tok);
+  const int64_t i = ti - int64_t(b) * a.n_tok;
+  const T* src = reinterpret_cast<const T*>(a.src[side]) + (int64_t(b) * a.src_seq_stride + i) * (H * D) + 4 * lane;
+  float x[H][4];
+#pragma unroll
+  for (int h = 0; h < H; ++h) load4(src + h * D, x[h]);
+  // mean: f64 sequential head sum from +0.0, /H, RN to f32
+  float mean[4];
+  bool bad = false;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    double acc = 0.0;
+#pragma unroll
+    for (int h = 0; h < H; ++h) acc = __dadd_rn(acc, double(x[h][k]));
+    mean[k] = __double2float_rn(__dmul_rn(acc, 0.125));  // /8 is exact
+    bad |= !finite(mean[k]);  // any non-finite input makes its column's sum non-finite
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0 && a.err) atomicOr(a.err, 1);
+  // deviations, group extrema
+  float mnh[H], mxh[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[h][k] = __fsub_rn(mean[k], x[h][k]);
+    mnh[h] = redux_min(fminf(fminf(x[h][0], x[h][1]), fminf(x[h][2], x[h][3])));
+    mxh[h] = redux_max(fmaxf(fmaxf(x[h][0], x[h][1]), fmaxf(x[h][2], x[h][3])));
+  }
+  // lane h < H: scale of group h
+  float my_mn = 0.f, my_mx = 0.f;
+#pragma unroll
+  for (int h = 0; h < H; ++h)
+    if (lane == h) {
+      my_mn = mnh[h];
+      my_mx = mxh[h];
+    }
+  float my_s = 0.f, my_inv = 0.f;
+  if (lane < H) {
+    my_s = group_scale(my_mn, my_mx, BITS);
+    my_inv = (my_s >= 0x1p-100f && my_s <= 0x1p100f) ? __frcp_rn(my_s) : 0.f;
+  }
+  const int64_t c = a.dst_start[b] + a.dst_offset + i;
+  const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
+  uint8_t* page = a.pool + int64_t(pt[c / a.L.page_tokens]) * a.L.page_bytes;
+  const int64_t row = c % a.L.page_tokens;
+  *reinterpret_cast<float4*>(reinterpret_cast<float*>(page + a.L.off_mean[side]) + row * D + 4 * lane) =
+      make_float4(mean[0], mean[1], mean[2], mean[3]);
+  if (lane < H)
+    *reinterpret_cast<float2*>(page + a.L.off_meta[side] + (row * H + lane) * 8) = make_float2(my_s, my_mn);
+  uint8_t* codes = page + a.L.off_codes[side] + row * (H * GB) + lane * (BITS / 2);
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    const float s = __shfl_sync(0xffffffffu, my_s, h);
+    const float inv = __shfl_sync(0xffffffffu, my_inv, h);
+    const float mn = mnh[h];
+    uint32_t word = 0;
+    if (s != 0.f) {
+      uint32_t cd[4];
+      bool unsafe = inv == 0.f;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float q = __fmul_rn(__fsub_rn(x[h][k], mn), inv);
+        const float t = __fadd_rn(q, 8388608.f);  // 2^23: RN(q) lands in the low mantissa bits
+        const float e = __fsub_rn(q, __fsub_rn(t, 8388608.f));
+        unsafe |= fabsf(e) > 0.5f - 0x1p-12f;
+        const uint32_t ci = __float_as_uint(t) & 0x7FFFFFu;
+        cd[k] = ci > uint32_t(CMAX) ? uint32_t(CMAX) : ci;
+      }
+      if (__any_sync(0xffffffffu, unsafe)) {  // rare: exact fp64 half-up for this group
+#pragma unroll
+        for (int k = 0; k < 4; ++k) cd[k] = quant_code(x[h][k], mn, s, 0.f, false, CMAX);
+      }
+      word = cd[0] | (cd[1] << BITS) | (cd[2] << (2 * BITS)) | (cd[3] << (3 * BITS));
+    }
+    uint8_t* dst = codes + h * GB;
+    if (BITS == 8) *reinterpret_cast<uint32_t*>(dst) = word;
+    else if (BITS == 4) *reinterpret_cast<uint16_t*>(dst) = uint16_t(word);
+    else *dst = uint8_t(word);
+  }
+}
+
 template <typename T, int NCH>
 static int launch_append_n(const AppendArgs& a, int batch, size_t smem, cudaStream_t st) {
   auto kern = quant_append_kernel<T, NCH>;
@@ -446,6 +556,14 @@ static int launch_append_n(const AppendArgs& a, int batch, size_t smem, cudaStre
 template <typename T>
 static int launch_append(const AppendArgs& a, int batch, size_t smem, cudaStream_t st) {
   const int D = a.L.head_dim;
+  if (D == 128 && a.L.heads == 8 && a.vec_ok && (a.L.bits == 2 || a.L.bits == 4 || a.L.bits == 8)) {
+    const int64_t warps = int64_t(batch) * a.n_tok * 2;
+    const unsigned grid = unsigned((warps + 7) / 8);
+    if (a.L.bits == 2) quant_append_fast_kernel<T, 2><<<grid, 256, 0, st>>>(a, batch);
+    else if (a.L.bits == 4) quant_append_fast_kernel<T, 4><<<grid, 256, 0, st>>>(a, batch);
+    else quant_append_fast_kernel<T, 8><<<grid, 256, 0, st>>>(a, batch);
+    return check_launch("quant_append_fast");
+  }
   if (D <= 128) return launch_append_n<T, 1>(a, batch, smem, st);
   if (D <= 256) return launch_append_n<T, 2>(a, batch, smem, st);
   if (D <= 512) return launch_append_n<T, 4>(a, batch, smem, st);

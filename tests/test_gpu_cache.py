@@ -158,3 +158,43 @@ def test_paged_multilayer_batched_vs_oracle(plan):
             assert np.array_equal(ex["k_mean"].cpu().numpy(), ref.kmean)
             assert ex["v_dev"].to_host().codes == ref.vdev.payload
             assert np.array_equal(ex["residual_v"].cpu().numpy(), ref.rv)
+
+
+def _k1_inputs(kind, B, T, H, D, rng):
+    if kind == "normal":
+        return orc.bf16_round(rng.normal(size=(B, T, H, D)).astype(np.float32))
+    if kind == "ties":  # small integers: means on a 1/8 grid, many (x - min)/s exactly on .5
+        return rng.integers(-8, 9, size=(B, T, H, D)).astype(np.float32)
+    if kind == "outlier":  # shared outlier channels (analysis.py:37-57 regime)
+        x = rng.normal(size=(B, T, H, D)).astype(np.float32) * 0.1
+        x[..., :2] += 8.0 * rng.normal(size=(B, T, 1, 2)).astype(np.float32)
+        return orc.bf16_round(x)
+    if kind == "constant":  # zero-range groups -> scale 0, codes 0
+        return np.repeat(rng.normal(size=(B, T, H, 1)).astype(np.float32), D, axis=3)
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("bits", [2, 4, 8])
+@pytest.mark.parametrize("kind", ["normal", "ties", "outlier", "constant"])
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_k1_fast_path_bit_exact(bits, kind, dtype):
+    """K1 for head_dim 128 x 8 heads (the warp-per-token kernel): codes, scales, mins, means bit-exact."""
+    m = tk()
+    B, T, H, D = 2, 257, 8, 128
+    rng = np.random.default_rng(hash((bits, kind)) % 2**32)
+    k = _k1_inputs(kind, B, T, H, D, rng)
+    v = _k1_inputs(kind, B, T, H, D, rng)
+    store = m.PagedKVCache(1, H, D, (bits,), 0, batch=B, page_tokens=64, max_tokens=T, shuffle_pages=True)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    store.append(0, torch.from_numpy(k).cuda().to(tdt), torch.from_numpy(v).cuda().to(tdt))
+    store.check_errors()
+    for b in range(B):
+        ref = orc.LayerState(H, D, bits, 0)
+        orc.append(ref, k[b], v[b])
+        ex = store.export(0, b)
+        for side, rec, mean in (("k", ref.kdev, ref.kmean), ("v", ref.vdev, ref.vmean)):
+            got = ex[f"{side}_dev"].to_host()
+            assert got.codes == rec.payload
+            assert np.array_equal(np.asarray(got.scales).view(np.uint32), rec.scales.view(np.uint32))
+            assert np.array_equal(np.asarray(got.mins), rec.mins)
+            assert np.array_equal(ex[f"{side}_mean"].cpu().numpy().view(np.uint32), mean.view(np.uint32))
