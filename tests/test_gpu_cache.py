@@ -170,7 +170,7 @@ def _k1_inputs(kind, B, T, H, D, rng):
         x[..., :2] += 8.0 * rng.normal(size=(B, T, 1, 2)).astype(np.float32)
         return orc.bf16_round(x)
     if kind == "constant":  # zero-range groups -> scale 0, codes 0
-        return np.repeat(rng.normal(size=(B, T, H, 1)).astype(np.float32), D, axis=3)
+        return orc.bf16_round(np.repeat(rng.normal(size=(B, T, H, 1)).astype(np.float32), D, axis=3))
     raise ValueError(kind)
 
 

@@ -36,3 +36,8 @@ if [[ $what == ncu || $what == all ]]; then
     --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_bench.log 2>&1
   echo "ncu rc=$?" >> gpurun_out/ncu_bench.log
 fi
+if [[ $what == profk1 || $what == all ]]; then
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:quant_append -s 2 -c 1 \
+    -o gpurun_out/k1 -f python tools/k1_bench.py --bits 4 > gpurun_out/profk1.log 2>&1
+  echo "profk1 rc=$?" >> gpurun_out/profk1.log
+fi
