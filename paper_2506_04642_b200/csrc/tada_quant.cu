@@ -442,6 +442,11 @@ static int launch_quantize(const void* rows, int64_t n, int D, int bits, uint8_t
 //    exact fp64 half-up sequence (quant_code), which decides every tie like the reference.
 // Loads are 8-byte (bf16) / 16-byte (f32) per lane and head, stores 16-bit (4-bit) codes per
 // lane and head, a float4 of the mean per lane, and (scale, min) by lanes 0..7.
+__device__ __forceinline__ uint32_t prmt(uint32_t x, uint32_t y, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(x), "r"(y), "r"(sel));
+  return r;
+}
 __device__ __forceinline__ float redux_min(float v) {
   float r;
   asm volatile("redux.sync.min.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
@@ -454,90 +459,100 @@ __device__ __forceinline__ float redux_max(float v) {
 }
 
 template <typename T, int BITS>
-__global__ void __launch_bounds__(256) quant_append_fast_kernel(AppendArgs a, int batch) {
-  constexpr int H = 8, D = 128, GB = D * BITS / 8, CMAX = (1 << BITS) - 1;
+__global__ void __launch_bounds__(256) quant_append_fast_kernel(AppendArgs a, int tpw, int page_shift) {
+  constexpr int H = 8, D = 128, GB = D * BITS / 8;
   const int lane = threadIdx.x & 31;
-  const int64_t wid = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
-  if (wid >= int64_t(batch) * a.n_tok * 2) return;
-  const int side = int(wid & 1);
-  const int64_t ti = wid >> 1;
-  const int b = int(ti / a.n_tok);
-  const int64_t i = ti - int64_t(b) * a.n_tok;
-  const T* src = reinterpret_cast<const T*>(a.src[side]) + (int64_t(b) * a.src_seq_stride + i) * (H * D) + 4 * lane;
-  float x[H][4];
-#pragma unroll
-  for (int h = 0; h < H; ++h) load4(src + h * D, x[h]);
-  // mean: f64 sequential head sum from +0.0, /H, RN to f32
-  float mean[4];
-  bool bad = false;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    double acc = 0.0;
-#pragma unroll
-    for (int h = 0; h < H; ++h) acc = __dadd_rn(acc, double(x[h][k]));
-    mean[k] = __double2float_rn(__dmul_rn(acc, 0.125));  // /8 is exact
-    bad |= !finite(mean[k]);  // any non-finite input makes its column's sum non-finite
-  }
-  if (__any_sync(0xffffffffu, bad) && lane == 0 && a.err) atomicOr(a.err, 1);
-  // deviations, group extrema
-  float mnh[H], mxh[H];
-#pragma unroll
-  for (int h = 0; h < H; ++h) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) x[h][k] = __fsub_rn(mean[k], x[h][k]);
-    mnh[h] = redux_min(fminf(fminf(x[h][0], x[h][1]), fminf(x[h][2], x[h][3])));
-    mxh[h] = redux_max(fmaxf(fmaxf(x[h][0], x[h][1]), fmaxf(x[h][2], x[h][3])));
-  }
-  // lane h < H: scale of group h
-  float my_mn = 0.f, my_mx = 0.f;
-#pragma unroll
-  for (int h = 0; h < H; ++h)
-    if (lane == h) {
-      my_mn = mnh[h];
-      my_mx = mxh[h];
-    }
-  float my_s = 0.f, my_inv = 0.f;
-  if (lane < H) {
-    my_s = group_scale(my_mn, my_mx, BITS);
-    my_inv = (my_s >= 0x1p-100f && my_s <= 0x1p100f) ? __frcp_rn(my_s) : 0.f;
-  }
-  const int64_t c = a.dst_start[b] + a.dst_offset + i;
+  const int side = blockIdx.y & 1, b = blockIdx.y >> 1;
+  const int64_t i_begin = (int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5)) * tpw;
+  const int64_t i_end = min(a.n_tok, i_begin + tpw);
   const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
-  uint8_t* page = a.pool + int64_t(pt[c / a.L.page_tokens]) * a.L.page_bytes;
-  const int64_t row = c % a.L.page_tokens;
-  *reinterpret_cast<float4*>(reinterpret_cast<float*>(page + a.L.off_mean[side]) + row * D + 4 * lane) =
-      make_float4(mean[0], mean[1], mean[2], mean[3]);
-  if (lane < H)
-    *reinterpret_cast<float2*>(page + a.L.off_meta[side] + (row * H + lane) * 8) = make_float2(my_s, my_mn);
-  uint8_t* codes = page + a.L.off_codes[side] + row * (H * GB) + lane * (BITS / 2);
+  const int64_t c0 = a.dst_start[b] + a.dst_offset;
+  const T* src_seq = reinterpret_cast<const T*>(a.src[side]) + int64_t(b) * a.src_seq_stride * (H * D) + 4 * lane;
+  const int P = a.L.page_tokens;
+  for (int64_t i = i_begin; i < i_end; ++i) {
+    const T* src = src_seq + i * (H * D);
+    float x[H][4];
 #pragma unroll
-  for (int h = 0; h < H; ++h) {
-    const float s = __shfl_sync(0xffffffffu, my_s, h);
-    const float inv = __shfl_sync(0xffffffffu, my_inv, h);
-    const float mn = mnh[h];
-    uint32_t word = 0;
-    if (s != 0.f) {
-      uint32_t cd[4];
-      bool unsafe = inv == 0.f;
+    for (int h = 0; h < H; ++h) load4(src + h * D, x[h]);
+    // mean: f64 sequential head sum from +0.0, /H (exact for H = 8), RN to f32
+    float mean[4];
+    bool bad = false;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float q = __fmul_rn(__fsub_rn(x[h][k], mn), inv);
-        const float t = __fadd_rn(q, 8388608.f);  // 2^23: RN(q) lands in the low mantissa bits
-        const float e = __fsub_rn(q, __fsub_rn(t, 8388608.f));
-        unsafe |= fabsf(e) > 0.5f - 0x1p-12f;
-        const uint32_t ci = __float_as_uint(t) & 0x7FFFFFu;
-        cd[k] = ci > uint32_t(CMAX) ? uint32_t(CMAX) : ci;
-      }
-      if (__any_sync(0xffffffffu, unsafe)) {  // rare: exact fp64 half-up for this group
+    for (int k = 0; k < 4; ++k) {
+      double acc = 0.0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) cd[k] = quant_code(x[h][k], mn, s, 0.f, false, CMAX);
-      }
-      word = cd[0] | (cd[1] << BITS) | (cd[2] << (2 * BITS)) | (cd[3] << (3 * BITS));
+      for (int h = 0; h < H; ++h) acc = __dadd_rn(acc, double(x[h][k]));
+      mean[k] = __double2float_rn(__dmul_rn(acc, 0.125));
+      bad |= !finite(mean[k]);  // any non-finite input makes its column's sum non-finite
     }
-    uint8_t* dst = codes + h * GB;
-    if (BITS == 8) *reinterpret_cast<uint32_t*>(dst) = word;
-    else if (BITS == 4) *reinterpret_cast<uint16_t*>(dst) = uint16_t(word);
-    else *dst = uint8_t(word);
+    if (__any_sync(0xffffffffu, bad) && lane == 0 && a.err) atomicOr(a.err, 1);
+    float mnh[H], mxh[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) x[h][k] = __fsub_rn(mean[k], x[h][k]);
+      mnh[h] = redux_min(fminf(fminf(x[h][0], x[h][1]), fminf(x[h][2], x[h][3])));
+      mxh[h] = redux_max(fmaxf(fmaxf(x[h][0], x[h][1]), fmaxf(x[h][2], x[h][3])));
+    }
+    float my_mn = 0.f, my_mx = 0.f;
+#pragma unroll
+    for (int h = 0; h < H; ++h)
+      if (lane == h) {
+        my_mn = mnh[h];
+        my_mx = mxh[h];
+      }
+    float my_s = 0.f, my_inv = 0.f;
+    if (lane < H) {
+      my_s = group_scale(my_mn, my_mx, BITS);
+      my_inv = (my_s >= 0x1p-100f && my_s <= 0x1p100f) ? __frcp_rn(my_s) : 0.f;
+    }
+    const int64_t c = c0 + i;
+    const int64_t pg = page_shift >= 0 ? (c >> page_shift) : c / P;
+    const int64_t row = page_shift >= 0 ? (c & (P - 1)) : c - pg * P;
+    uint8_t* page = a.pool + int64_t(pt[pg]) * a.L.page_bytes;
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(page + a.L.off_mean[side]) + row * D + 4 * lane) =
+        make_float4(mean[0], mean[1], mean[2], mean[3]);
+    if (lane < H)
+      *reinterpret_cast<float2*>(page + a.L.off_meta[side] + (row * H + lane) * 8) = make_float2(my_s, my_mn);
+    uint8_t* codes = page + a.L.off_codes[side] + row * (H * GB) + lane * (BITS / 2);
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const float s = __shfl_sync(0xffffffffu, my_s, h);
+      const float inv = __shfl_sync(0xffffffffu, my_inv, h);
+      const float mn = mnh[h];
+      uint32_t word = 0;
+      if (s != 0.f) {
+        // RN(q) via the 2^23 magic add; q <= cmax (+ulps) so no clamp is needed on this path
+        float r[4], emax = 0.f;
+        uint32_t tb[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float q = __fmul_rn(__fsub_rn(x[h][k], mn), inv);
+          const float t = __fadd_rn(q, 8388608.f);
+          r[k] = __fsub_rn(t, 8388608.f);
+          emax = fmaxf(emax, fabsf(__fsub_rn(q, r[k])));
+          tb[k] = __float_as_uint(t);
+        }
+        if (__any_sync(0xffffffffu, emax > 0.5f - 0x1p-12f || inv == 0.f)) {
+          // within 2^-12 of a rounding boundary somewhere in the group: exact fp64 half-up
+          constexpr int CMAX = (1 << BITS) - 1;
+          uint32_t cd[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) cd[k] = quant_code(x[h][k], mn, s, 0.f, false, CMAX);
+          word = cd[0] | (cd[1] << BITS) | (cd[2] << (2 * BITS)) | (cd[3] << (3 * BITS));
+        } else if (BITS == 8) {
+          word = prmt(prmt(tb[0], tb[1], 0x0040u), prmt(tb[2], tb[3], 0x0040u), 0x5410u);
+        } else {  // exact small-integer arithmetic in f32, read back through the magic add
+          constexpr float M1 = float(1 << BITS), M2 = M1 * M1, M3 = M2 * M1;
+          const float v = fmaf(r[3], M3, fmaf(r[2], M2, fmaf(r[1], M1, r[0])));
+          word = __float_as_uint(__fadd_rn(v, 8388608.f));
+        }
+      }
+      uint8_t* dst = codes + h * GB;
+      if (BITS == 8) *reinterpret_cast<uint32_t*>(dst) = word;
+      else if (BITS == 4) *reinterpret_cast<uint16_t*>(dst) = uint16_t(word);
+      else *dst = uint8_t(word);
+    }
   }
 }
 
@@ -557,11 +572,13 @@ template <typename T>
 static int launch_append(const AppendArgs& a, int batch, size_t smem, cudaStream_t st) {
   const int D = a.L.head_dim;
   if (D == 128 && a.L.heads == 8 && a.vec_ok && (a.L.bits == 2 || a.L.bits == 4 || a.L.bits == 8)) {
-    const int64_t warps = int64_t(batch) * a.n_tok * 2;
-    const unsigned grid = unsigned((warps + 7) / 8);
-    if (a.L.bits == 2) quant_append_fast_kernel<T, 2><<<grid, 256, 0, st>>>(a, batch);
-    else if (a.L.bits == 4) quant_append_fast_kernel<T, 4><<<grid, 256, 0, st>>>(a, batch);
-    else quant_append_fast_kernel<T, 8><<<grid, 256, 0, st>>>(a, batch);
+    const int tpw = a.n_tok >= 4096 ? 4 : 1;  // tokens per warp: amortise the per-warp setup on bulk appends
+    const dim3 grid(unsigned((a.n_tok + 8 * tpw - 1) / (8 * tpw)), unsigned(2 * batch));
+    const int P = a.L.page_tokens;
+    const int shift = (P & (P - 1)) == 0 ? __builtin_ctz(unsigned(P)) : -1;
+    if (a.L.bits == 2) quant_append_fast_kernel<T, 2><<<grid, 256, 0, st>>>(a, tpw, shift);
+    else if (a.L.bits == 4) quant_append_fast_kernel<T, 4><<<grid, 256, 0, st>>>(a, tpw, shift);
+    else quant_append_fast_kernel<T, 8><<<grid, 256, 0, st>>>(a, tpw, shift);
     return check_launch("quant_append_fast");
   }
   if (D <= 128) return launch_append_n<T, 1>(a, batch, smem, st);
