@@ -515,43 +515,55 @@ __global__ void __launch_bounds__(256) quant_append_fast_kernel(AppendArgs a, in
     if (lane < H)
       *reinterpret_cast<float2*>(page + a.L.off_meta[side] + (row * H + lane) * 8) = make_float2(my_s, my_mn);
     uint8_t* codes = page + a.L.off_codes[side] + row * (H * GB) + lane * (BITS / 2);
+    // fast path for every group at once (s == 0 has inv == 0: q = 0, codes 0); one vote per token
+    uint32_t word[H];
+    uint32_t unsafe = 0;
 #pragma unroll
     for (int h = 0; h < H; ++h) {
-      const float s = __shfl_sync(0xffffffffu, my_s, h);
       const float inv = __shfl_sync(0xffffffffu, my_inv, h);
       const float mn = mnh[h];
-      uint32_t word = 0;
-      if (s != 0.f) {
-        // RN(q) via the 2^23 magic add; q <= cmax (+ulps) so no clamp is needed on this path
-        float r[4], emax = 0.f;
-        uint32_t tb[4];
+      float r[4], emax = 0.f;
+      uint32_t tb[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float q = __fmul_rn(__fsub_rn(x[h][k], mn), inv);
-          const float t = __fadd_rn(q, 8388608.f);
-          r[k] = __fsub_rn(t, 8388608.f);
-          emax = fmaxf(emax, fabsf(__fsub_rn(q, r[k])));
-          tb[k] = __float_as_uint(t);
-        }
-        if (__any_sync(0xffffffffu, emax > 0.5f - 0x1p-12f || inv == 0.f)) {
-          // within 2^-12 of a rounding boundary somewhere in the group: exact fp64 half-up
-          constexpr int CMAX = (1 << BITS) - 1;
-          uint32_t cd[4];
+      for (int k = 0; k < 4; ++k) {  // RN(q) via the 2^23 magic add; q <= cmax (+ulps), no clamp needed
+        const float q = __fmul_rn(__fsub_rn(x[h][k], mn), inv);
+        const float t = __fadd_rn(q, 8388608.f);
+        r[k] = __fsub_rn(t, 8388608.f);
+        emax = fmaxf(emax, fabsf(__fsub_rn(q, r[k])));
+        tb[k] = __float_as_uint(t);
+      }
+      unsafe |= uint32_t(emax > 0.5f - 0x1p-12f) << h;
+      if (BITS == 8) {
+        word[h] = prmt(prmt(tb[0], tb[1], 0x0040u), prmt(tb[2], tb[3], 0x0040u), 0x5410u);
+      } else {  // exact small-integer arithmetic in f32, read back through the magic add
+        constexpr float M1 = float(1 << BITS), M2 = M1 * M1, M3 = M2 * M1;
+        const float v = fmaf(r[3], M3, fmaf(r[2], M2, fmaf(r[1], M1, r[0])));
+        word[h] = __float_as_uint(__fadd_rn(v, 8388608.f));
+      }
+    }
+    // scales outside [2^-100, 2^100] have no fast path (inv == 0 with s != 0)
+    if (lane < H && my_inv == 0.f && my_s != 0.f) unsafe |= 1u << lane;
+    const uint32_t redo = __reduce_or_sync(0xffffffffu, unsafe);
+    if (redo) {  // rare: a group within 2^-12 of a rounding boundary -> exact fp64 half-up (quant_code)
+      constexpr int CMAX = (1 << BITS) - 1;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) cd[k] = quant_code(x[h][k], mn, s, 0.f, false, CMAX);
-          word = cd[0] | (cd[1] << BITS) | (cd[2] << (2 * BITS)) | (cd[3] << (3 * BITS));
-        } else if (BITS == 8) {
-          word = prmt(prmt(tb[0], tb[1], 0x0040u), prmt(tb[2], tb[3], 0x0040u), 0x5410u);
-        } else {  // exact small-integer arithmetic in f32, read back through the magic add
-          constexpr float M1 = float(1 << BITS), M2 = M1 * M1, M3 = M2 * M1;
-          const float v = fmaf(r[3], M3, fmaf(r[2], M2, fmaf(r[1], M1, r[0])));
-          word = __float_as_uint(__fadd_rn(v, 8388608.f));
+      for (int h = 0; h < H; ++h) {
+        const float sh = __shfl_sync(0xffffffffu, my_s, h);
+        if ((redo >> h) & 1u) {
+          uint32_t w = 0;
+          if (sh != 0.f)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) w |= quant_code(x[h][k], mnh[h], sh, 0.f, false, CMAX) << (BITS * k);
+          word[h] = w;
         }
       }
+    }
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
       uint8_t* dst = codes + h * GB;
-      if (BITS == 8) *reinterpret_cast<uint32_t*>(dst) = word;
-      else if (BITS == 4) *reinterpret_cast<uint16_t*>(dst) = uint16_t(word);
-      else *dst = uint8_t(word);
+      if (BITS == 8) *reinterpret_cast<uint32_t*>(dst) = word[h];
+      else if (BITS == 4) *reinterpret_cast<uint16_t*>(dst) = uint16_t(word[h]);
+      else *dst = uint8_t(word[h]);
     }
   }
 }
