@@ -458,19 +458,52 @@ __device__ __forceinline__ float redux_max(float v) {
   return r;
 }
 
+// Each warp streams its tokens' rows (H*D contiguous elements) into a private 3-deep shared
+// ring with cp.async.bulk + an mbarrier per slot, so the next rows are in flight while the
+// current one is quantized (the kernel is otherwise latency-bound on its global loads).
+constexpr int K1_RING = 3;
+__device__ __forceinline__ uint32_t k1_su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
 template <typename T, int BITS>
 __global__ void __launch_bounds__(256) quant_append_fast_kernel(AppendArgs a, int tpw, int page_shift) {
   constexpr int H = 8, D = 128, GB = D * BITS / 8;
-  const int lane = threadIdx.x & 31;
+  constexpr uint32_t ROWB = H * D * sizeof(T);  // bytes of one token's rows
+  extern __shared__ __align__(128) uint8_t k1_smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T* ring = reinterpret_cast<T*>(k1_smem + warp * K1_RING * ROWB);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(k1_smem + 8 * K1_RING * ROWB) + warp * K1_RING;
   const int side = blockIdx.y & 1, b = blockIdx.y >> 1;
-  const int64_t i_begin = (int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5)) * tpw;
+  const int64_t i_begin = (int64_t(blockIdx.x) * 8 + warp) * tpw;
   const int64_t i_end = min(a.n_tok, i_begin + tpw);
   const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
   const int64_t c0 = a.dst_start[b] + a.dst_offset;
-  const T* src_seq = reinterpret_cast<const T*>(a.src[side]) + int64_t(b) * a.src_seq_stride * (H * D) + 4 * lane;
+  const T* src_seq = reinterpret_cast<const T*>(a.src[side]) + int64_t(b) * a.src_seq_stride * (H * D);
   const int P = a.L.page_tokens;
+  auto fetch = [&](int64_t i) {  // lane 0
+    const int slot = int((i - i_begin) % K1_RING);
+    const uint32_t bar = k1_su32(&bars[slot]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(ROWB) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     k1_su32(ring + slot * (H * D))),
+                 "l"(src_seq + i * (H * D)), "r"(ROWB), "r"(bar)
+                 : "memory");
+  };
+  if (lane == 0) {
+    for (int k = 0; k < K1_RING; ++k)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(k1_su32(&bars[k])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int64_t i = i_begin; i < i_end && i < i_begin + K1_RING - 1; ++i) fetch(i);
+  }
+  __syncwarp();
   for (int64_t i = i_begin; i < i_end; ++i) {
-    const T* src = src_seq + i * (H * D);
+    const int slot = int((i - i_begin) % K1_RING);
+    const uint32_t parity = uint32_t(((i - i_begin) / K1_RING) & 1);
+    asm volatile(
+        "{\n.reg .pred p;\nK1_WAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra K1_WAIT_%=;\n}\n" ::"r"(
+            k1_su32(&bars[slot])),
+        "r"(parity)
+        : "memory");
+    const T* src = ring + slot * (H * D) + 4 * lane;
     float x[H][4];
 #pragma unroll
     for (int h = 0; h < H; ++h) load4(src + h * D, x[h]);
@@ -484,6 +517,12 @@ __global__ void __launch_bounds__(256) quant_append_fast_kernel(AppendArgs a, in
       for (int h = 0; h < H; ++h) acc = __dadd_rn(acc, double(x[h][k]));
       mean[k] = __double2float_rn(__dmul_rn(acc, 0.125));
       bad |= !finite(mean[k]);  // any non-finite input makes its column's sum non-finite
+    }
+    // every lane has its rows in registers (the mean consumed them): refill the slot freed last
+    __syncwarp();
+    if (lane == 0 && i + K1_RING - 1 < i_end) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      fetch(i + K1_RING - 1);
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0 && a.err) atomicOr(a.err, 1);
     float mnh[H], mxh[H];
@@ -584,13 +623,18 @@ template <typename T>
 static int launch_append(const AppendArgs& a, int batch, size_t smem, cudaStream_t st) {
   const int D = a.L.head_dim;
   if (D == 128 && a.L.heads == 8 && a.vec_ok && (a.L.bits == 2 || a.L.bits == 4 || a.L.bits == 8)) {
-    const int tpw = a.n_tok >= 4096 ? 4 : 1;  // tokens per warp: amortise the per-warp setup on bulk appends
+    const int tpw = a.n_tok >= 16384 ? 8 : (a.n_tok >= 2048 ? 4 : 1);  // tokens per warp (streamed through the ring)
     const dim3 grid(unsigned((a.n_tok + 8 * tpw - 1) / (8 * tpw)), unsigned(2 * batch));
     const int P = a.L.page_tokens;
     const int shift = (P & (P - 1)) == 0 ? __builtin_ctz(unsigned(P)) : -1;
-    if (a.L.bits == 2) quant_append_fast_kernel<T, 2><<<grid, 256, 0, st>>>(a, tpw, shift);
-    else if (a.L.bits == 4) quant_append_fast_kernel<T, 4><<<grid, 256, 0, st>>>(a, tpw, shift);
-    else quant_append_fast_kernel<T, 8><<<grid, 256, 0, st>>>(a, tpw, shift);
+    const size_t smem = size_t(8) * K1_RING * 8 * 128 * sizeof(T) + 8 * K1_RING * 8;
+    auto k = a.L.bits == 2 ? quant_append_fast_kernel<T, 2>
+                           : (a.L.bits == 4 ? quant_append_fast_kernel<T, 4> : quant_append_fast_kernel<T, 8>);
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string("quant_append smem: ") + cudaGetErrorString(e));
+    }
+    k<<<grid, 256, smem, st>>>(a, tpw, shift);
     return check_launch("quant_append_fast");
   }
   if (D <= 128) return launch_append_n<T, 1>(a, batch, smem, st);
