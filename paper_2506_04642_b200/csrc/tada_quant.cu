@@ -465,7 +465,7 @@ constexpr int K1_RING = 3;
 __device__ __forceinline__ uint32_t k1_su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
 template <typename T, int BITS>
-__global__ void __launch_bounds__(256) quant_append_fast_kernel(AppendArgs a, int tpw, int page_shift) {
+__global__ void __launch_bounds__(256, 3) quant_append_fast_kernel(AppendArgs a, int tpw, int page_shift) {
   constexpr int H = 8, D = 128, GB = D * BITS / 8;
   constexpr uint32_t ROWB = H * D * sizeof(T);  // bytes of one token's rows
   extern __shared__ __align__(128) uint8_t k1_smem[];
