@@ -38,13 +38,13 @@ namespace tada {
 namespace fast {
 
 constexpr int D = 128;
-constexpr int TT = 32;              // tokens per tile
-constexpr int HT = TT / 2;          // tokens per warp half
-constexpr int NW = 16;              // warps
-constexpr int NTHR = NW * 32;
-constexpr int SROW = TT + 4;        // S_mean row stride (floats)
-constexpr int PROW = HT + 8;        // P / P' row stride (halves): 48-byte rows, conflict-free ldmatrix
-constexpr int BAND = TT * 128;      // bytes of one 128-byte-wide swizzled band of a tile
+constexpr int HT = 16;  // tokens per warp (one m16 tile of the token-on-M QK code term)
+// Tile geometry: TT tokens per tile, TT/2 warps (warp = KV head x 16-token half), so TT = 32 runs
+// one 512-thread CTA per SM and TT = 16 runs two 256-thread CTAs per SM (their barriers interleave).
+__host__ __device__ constexpr int nw_of(int tt) { return tt / 2; }
+__host__ __device__ constexpr int sr_of(int tt) { return tt + 4; }   // S row stride (floats)
+__host__ __device__ constexpr int pr_of(int tt) { return tt + 8; }   // P / P' row stride (halves): conflict-free
+__host__ __device__ constexpr int band_of(int tt) { return tt * 128; }  // bytes of one 128-B-wide swizzled band
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -176,14 +176,14 @@ struct Plan {
 
 __host__ __device__ constexpr int up128(int x) { return (x + 127) / 128 * 128; }
 __host__ __device__ constexpr int up1k(int x) { return (x + 1023) / 1024 * 1024; }
-constexpr int PROW2 = TT + 8;  // P / P' row stride (halves): 80-byte rows, conflict-free ldmatrix / B loads
 // QK mean-term partial planes (d splits): 4 (16 warps x 2 k-steps), or 2 (8 warps x 4 k-steps) where
 // shared memory is tight (8-bit); plus one plane for the code term
 __host__ __device__ constexpr int nkq_for(int gb) { return gb >= 128 ? 2 : 4; }
 
-__host__ __device__ constexpr Plan make_plan(int H, int gb, int HQ) {
+__host__ __device__ constexpr Plan make_plan(int H, int gb, int HQ, int TT) {
   Plan p{};
   const int NSP = nkq_for(gb) + 1;
+  const int BAND = band_of(TT), SROW = sr_of(TT), PROW2 = pr_of(TT);
   const int mrows = HQ >= 16 ? HQ : 16;
   p.trow = H * 8 + 16;  // meta box row: the 16 B past the row are TMA zero fill (shifts banks by 4 per row)
   p.mean_bytes = (D * 4 / 128) * BAND;
@@ -196,7 +196,7 @@ __host__ __device__ constexpr Plan make_plan(int H, int gb, int HQ) {
   const int pb = up128(mrows * PROW2 * 2);
   const int p2 = up128(H * 8 * PROW2 * 2);
   const int tail = sb + pb + p2 + up128(mrows * 4) + up128(3 * HQ * 4) + up128(HQ * 4) + 128 + 1024;
-  const int budget = 227 * 1024;
+  const int budget = TT == 16 ? 113 * 1024 : 227 * 1024;  // TT = 16: two CTAs per SM
   p.stages = (3 * p.stage_bytes + tail <= budget) ? 3 : ((2 * p.stage_bytes + tail <= budget) ? 2 : 1);
   int off = p.stages * p.stage_bytes;
   // the epilogue parks the partial output [HQ][D] f32 in the (idle) stages
@@ -227,8 +227,10 @@ __host__ __device__ constexpr Plan make_plan(int H, int gb, int HQ) {
 //  B  softmax, dense: thread = (q head, TT/TPQ tokens); P [q][tok], P'_h^T [n][tok], corr [q]
 //  C  PV code term   (warp (h, half): its 16 tokens, all d)       -> O_h^T in registers
 //     PV mean piece  (warp w: d octet w, all q tiles, all tokens) -> O_mean in registers
-template <int BITS, int HQ>
-__global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __grid_constant__ TmaMaps maps) {
+template <int BITS, int HQ, int TT>
+__global__ void __launch_bounds__(TT * 16, TT == 16 ? 2 : 1) attn_fast_kernel(AttnArgs a,
+                                                                              const __grid_constant__ TmaMaps maps) {
+  constexpr int NW = nw_of(TT), NTHR = NW * 32, SROW = sr_of(TT), PROW2 = pr_of(TT), BAND = band_of(TT);
   extern __shared__ uint8_t smem_raw[];
   // 1 KB alignment (128B-swizzle atoms) by pointer arithmetic on the __shared__ array, so the
   // compiler keeps the shared state space (LDS, 32-bit addressing) for every access below
@@ -238,10 +240,11 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
   constexpr int MT = HQ >= 16 ? HQ / 16 : 1;    // 16-row q tiles
   constexpr int MROWS = MT * 16;
   constexpr int GB = BITS * D / 8;              // code bytes per (token, head)
-  constexpr Plan pl = make_plan(H, GB, HQ);
+  constexpr Plan pl = make_plan(H, GB, HQ, TT);
   constexpr int S = pl.stages < 2 ? 2 : pl.stages;  // geometries with < 2 stages are never launched
   constexpr int NKQ = nkq_for(GB), NSP = NKQ + 1, KS = 8 / NKQ;  // mean-term d splits, planes, k-steps each
-  constexpr int TPQ = (NTHR / HQ) < 32 ? (NTHR / HQ) : 32;  // softmax threads per q head
+  constexpr int TPQ0 = (NTHR / HQ) < 32 ? (NTHR / HQ) : 32;
+  constexpr int TPQ = TPQ0 < TT ? TPQ0 : TT;                // softmax threads per q head
   constexpr int TPT = TT / TPQ;                             // tokens per softmax thread
   constexpr int NSM = HQ * TPQ;                             // active softmax threads
   const int P = a.L.page_tokens;
@@ -329,7 +332,8 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
     }
   }
   // QK mean A operand: q tile mt, k-step s = 2*kq + ks; slots (2c,2c+1 | 2c+8,2c+9) <-> d = 16s+4c+(0,1 | 2,3)
-  const int nt = warp & 3, kq = warp >> 2;  // piece of warps with kq < NKQ
+  constexpr int NT8 = TT / 8;  // token octets per tile
+  const int nt = warp % NT8, kq = warp / NT8;  // QK mean piece of warps with kq < NKQ
   uint32_t qa[MT][KS][4];
   {
     const __half* q16 = q16s;
@@ -352,11 +356,14 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
 
   // accumulators
   float oc[8][4];    // PV code term, O_h^T: m-tile of 16 d (rows) x 8 n (cols), this warp's tokens
-  float om[MT][4];   // PV mean term: q tile rows x this warp's 8 d
+  constexpr int NDT = 16 / NW;  // d octets per warp in the PV mean term
+  float om[NDT][MT][4];  // PV mean term: q tile rows x this warp's d octets
 #pragma unroll
   for (int i = 0; i < 8; ++i) oc[i][0] = oc[i][1] = oc[i][2] = oc[i][3] = 0.f;
 #pragma unroll
-  for (int mt = 0; mt < MT; ++mt) om[mt][0] = om[mt][1] = om[mt][2] = om[mt][3] = 0.f;
+  for (int j = 0; j < NDT; ++j)
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) om[j][mt][0] = om[j][mt][1] = om[j][mt][2] = om[j][mt][3] = 0.f;
   // softmax ownership: q head sg, tokens sj + TPQ*u
   const int sg = tid / TPQ, sj = tid % TPQ, sh = sg / G;
   const bool s_active = tid < NSM;
@@ -648,33 +655,39 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
       for (int mt = 0; mt < MT; ++mt) any |= (cr[mt][0] != 1.f) || (cr[mt][1] != 1.f);
       if (any) {
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          om[mt][0] *= cr[mt][0];
-          om[mt][1] *= cr[mt][0];
-          om[mt][2] *= cr[mt][1];
-          om[mt][3] *= cr[mt][1];
-        }
+        for (int j = 0; j < NDT; ++j)
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            om[j][mt][0] *= cr[mt][0];
+            om[j][mt][1] *= cr[mt][0];
+            om[j][mt][2] *= cr[mt][1];
+            om[j][mt][3] *= cr[mt][1];
+          }
       }
-      const int d = 8 * warp + r;  // this thread's B column
-      const uint8_t* vb = vmean + (d >> 5) * BAND;
-      const int ob = 4 * (d & 31);
       const int mrow = (lane & 7) + 8 * ((lane >> 3) & 1), tcol = 8 * (lane >> 4);
 #pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        const int t = 16 * ks + 2 * c;
-        const float e0 = *reinterpret_cast<const float*>(vb + swz(t, ob));
-        const float e1 = *reinterpret_cast<const float*>(vb + swz(t + 1, ob));
-        const float e2 = *reinterpret_cast<const float*>(vb + swz(t + 8, ob));
-        const float e3 = *reinterpret_cast<const float*>(vb + swz(t + 9, ob));
-        uint32_t bh0, bl0, bh1, bl1;
-        split_h2(e0, e1, bh0, bl0);
-        split_h2(e2, e3, bh1, bl1);
+      for (int ks = 0; ks < TT / 16; ++ks) {
+        uint32_t pa[MT][4];
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          uint32_t pa[4];
-          ldsm_x4(pa, su32(pbuf + (16 * mt + mrow) * PROW2 + 16 * ks + tcol));
-          mma(om[mt], pa, bh0, bh1);
-          mma(om[mt], pa, bl0, bl1);
+        for (int mt = 0; mt < MT; ++mt) ldsm_x4(pa[mt], su32(pbuf + (16 * mt + mrow) * PROW2 + 16 * ks + tcol));
+        const int t = 16 * ks + 2 * c;
+#pragma unroll
+        for (int j = 0; j < NDT; ++j) {
+          const int d = 8 * (warp + NW * j) + r;  // this thread's B column
+          const uint8_t* vb = vmean + (d >> 5) * BAND;
+          const int ob = 4 * (d & 31);
+          const float e0 = *reinterpret_cast<const float*>(vb + swz(t, ob));
+          const float e1 = *reinterpret_cast<const float*>(vb + swz(t + 1, ob));
+          const float e2 = *reinterpret_cast<const float*>(vb + swz(t + 8, ob));
+          const float e3 = *reinterpret_cast<const float*>(vb + swz(t + 9, ob));
+          uint32_t bh0, bl0, bh1, bl1;
+          split_h2(e0, e1, bh0, bl0);
+          split_h2(e2, e3, bh1, bl1);
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            mma(om[j][mt], pa[mt], bh0, bh1);
+            mma(om[j][mt], pa[mt], bl0, bl1);
+          }
         }
       }
     }
@@ -702,7 +715,11 @@ __global__ void __launch_bounds__(NTHR, 1) attn_fast_kernel(AttnArgs a, const __
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int g = 16 * mt + r + 8 * e;
-      if (g < HQ) *reinterpret_cast<float2*>(park + g * D + 8 * warp + 2 * c) = make_float2(om[mt][2 * e], om[mt][2 * e + 1]);
+      if (g < HQ)
+#pragma unroll
+        for (int j = 0; j < NDT; ++j)
+          *reinterpret_cast<float2*>(park + g * D + 8 * (warp + NW * j) + 2 * c) =
+              make_float2(om[j][mt][2 * e], om[j][mt][2 * e + 1]);
     }
   __syncthreads();
   // 2) code term, half 0 then half 1 (same softmax reference): rows d = 16r + 2mt (+1), cols n = 2c (+1)
@@ -744,9 +761,10 @@ bool fast_supported(const tada_page_layout& L, int Hq) {
   // compiled geometries: 8 KV heads (the Llama-3 family) with 8/16/32/64 q heads
   if (L.head_dim != 128 || !(L.bits == 2 || L.bits == 4 || L.bits == 8) || L.heads != 8) return false;
   if (!(Hq == 8 || Hq == 16 || Hq == 32 || Hq == 64)) return false;
-  if (L.page_tokens % fast::TT) return false;
-  const fast::Plan pl = fast::make_plan(L.heads, L.group_bytes, Hq);
-  return pl.stages >= 2 && pl.total <= 227 * 1024;  // one stage cannot overlap load and compute
+  const int tt = fast::make_plan(8, L.group_bytes, Hq, 16).stages >= 2
+                     ? 16
+                     : (fast::make_plan(8, L.group_bytes, Hq, 32).stages >= 2 ? 32 : 0);
+  return tt != 0 && L.page_tokens % tt == 0;  // one stage cannot overlap load and compute
 }
 
 // ---------------------------------------------------------------- TMA descriptors
@@ -769,13 +787,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 // [side][band][row][128 B]: every 128-byte line is one (band, row), so the 128B swizzle XORs the
 // 16-byte chunk index with (row & 7) exactly like swz().
 static bool encode_region5(CUtensorMap* m, const uint8_t* base, uint64_t row_bytes, uint64_t rows, uint64_t side_stride,
-                           uint64_t page_bytes) {
+                           uint64_t page_bytes, uint32_t tt) {
   auto enc = get_encode();
   if (!enc) return false;
   const uint64_t nband = row_bytes / 128;
   const cuuint64_t dims[5] = {128, rows, nband, 2, uint64_t(1) << 20};
   const cuuint64_t strides[4] = {row_bytes, 128, side_stride, page_bytes};
-  const cuuint32_t box[5] = {128, uint32_t(fast::TT), uint32_t(nband), 2, 1};
+  const cuuint32_t box[5] = {128, tt, uint32_t(nband), 2, 1};
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<uint8_t*>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -784,26 +802,26 @@ static bool encode_region5(CUtensorMap* m, const uint8_t* base, uint64_t row_byt
 // metas: (byte in row, row, side, page); the box is 16 bytes wider than a row (zero fill) so that
 // smem rows are trow = H*8 + 16 bytes apart (bank spread for the per-token loads)
 static bool encode_meta(CUtensorMap* m, const uint8_t* base, uint64_t row_bytes, uint64_t rows, uint64_t side_stride,
-                        uint64_t page_bytes, uint32_t box0) {
+                        uint64_t page_bytes, uint32_t box0, uint32_t tt) {
   auto enc = get_encode();
   if (!enc) return false;
   const cuuint64_t dims[4] = {row_bytes, rows, 2, uint64_t(1) << 20};
   const cuuint64_t strides[3] = {row_bytes, side_stride, page_bytes};
-  const cuuint32_t box[4] = {box0, uint32_t(fast::TT), 2, 1};
+  const cuuint32_t box[4] = {box0, tt, 2, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static int get_maps(const AttnArgs& a, TmaMaps* out) {
+static int get_maps(const AttnArgs& a, TmaMaps* out, int tt) {
   struct Key {
     const uint8_t* pool;
     int64_t page_bytes;
-    int bits, heads, page_tokens;
+    int bits, heads, page_tokens, tt;
     bool operator==(const Key& o) const {
       return pool == o.pool && page_bytes == o.page_bytes && bits == o.bits && heads == o.heads &&
-             page_tokens == o.page_tokens;
+             page_tokens == o.page_tokens && tt == o.tt;
     }
   };
   struct Hash {
@@ -813,7 +831,7 @@ static int get_maps(const AttnArgs& a, TmaMaps* out) {
   };
   static std::mutex mu;
   static std::unordered_map<Key, TmaMaps, Hash> cache;
-  const Key key{a.pool, a.L.page_bytes, a.L.bits, a.L.heads, a.L.page_tokens};
+  const Key key{a.pool, a.L.page_bytes, a.L.bits, a.L.heads, a.L.page_tokens, tt};
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) {
@@ -826,11 +844,11 @@ static int get_maps(const AttnArgs& a, TmaMaps* out) {
   if (uint64_t(L.off_codes[1] - L.off_codes[0]) != side_stride || uint64_t(L.off_meta[1] - L.off_meta[0]) != side_stride)
     return fail(TADA_ERR_CONFIG, "page layout sides are not uniformly strided");
   if (!encode_region5(&m.m[0][0], a.pool + L.off_mean[0], uint64_t(L.head_dim) * 4, L.page_tokens, side_stride,
-                      L.page_bytes) ||
+                      L.page_bytes, uint32_t(tt)) ||
       !encode_region5(&m.m[0][1], a.pool + L.off_codes[0], uint64_t(L.heads) * L.group_bytes, L.page_tokens,
-                      side_stride, L.page_bytes) ||
+                      side_stride, L.page_bytes, uint32_t(tt)) ||
       !encode_meta(&m.m[0][2], a.pool + L.off_meta[0], uint64_t(L.heads) * 8, L.page_tokens, side_stride, L.page_bytes,
-                   uint32_t(L.heads * 8 + 16)))
+                   uint32_t(L.heads * 8 + 16), uint32_t(tt)))
     return fail(TADA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the decode-attention pool");
   if (cache.size() > 256) cache.clear();
   cache.emplace(key, m);
@@ -838,21 +856,36 @@ static int get_maps(const AttnArgs& a, TmaMaps* out) {
   return TADA_OK;
 }
 
-template <int BITS, int HQ>
-static int launch_fast_t(const AttnArgs& a, int batch, cudaStream_t st) {
-  constexpr fast::Plan pl = fast::make_plan(8, BITS * 128 / 8, HQ);
-  auto kern = fast::attn_fast_kernel<BITS, HQ>;
+// Tile size per geometry: 16-token tiles (two CTAs per SM) where two stages fit in half the
+// shared memory, else 32-token tiles (one CTA per SM).
+static int tile_tokens(int bits, int hq) {
+  const int gb = bits * 128 / 8;
+  if (fast::make_plan(8, gb, hq, 16).stages >= 2) return 16;
+  if (fast::make_plan(8, gb, hq, 32).stages >= 2) return 32;
+  return 0;
+}
+
+template <int BITS, int HQ, int TT>
+static int launch_fast_tt(const AttnArgs& a, int batch, cudaStream_t st) {
+  constexpr fast::Plan pl = fast::make_plan(8, BITS * 128 / 8, HQ, TT);
+  auto kern = fast::attn_fast_kernel<BITS, HQ, TT>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.total);
     if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string("attn_fast smem: ") + cudaGetErrorString(e));
     attr_set = true;
   }
   TmaMaps maps;
-  const int rc = get_maps(a, &maps);
+  const int rc = get_maps(a, &maps, TT);
   if (rc != TADA_OK) return rc;
-  kern<<<dim3(a.splits, batch), fast::NTHR, pl.total, st>>>(a, maps);
+  kern<<<dim3(a.splits, batch), TT * 16, pl.total, st>>>(a, maps);
   return check_launch("decode_attn_fast");
+}
+
+template <int BITS, int HQ>
+static int launch_fast_t(const AttnArgs& a, int batch, cudaStream_t st) {
+  return tile_tokens(BITS, HQ) == 16 ? launch_fast_tt<BITS, HQ, 16>(a, batch, st)
+                                     : launch_fast_tt<BITS, HQ, 32>(a, batch, st);
 }
 
 template <int BITS>
@@ -872,5 +905,7 @@ int launch_fast(const AttnArgs& a, int batch, cudaStream_t st) {
     default: return launch_fast_b<8>(a, batch, st);
   }
 }
+
+int fast_tile_tokens(const tada_page_layout& L, int Hq) { return tile_tokens(L.bits, Hq); }
 
 }  // namespace tada
