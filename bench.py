@@ -241,7 +241,7 @@ def run_ours(args):
     vs = [torch.randn((L, B, 1, H, D), generator=gen, device=dev).to(torch.bfloat16) for _ in range(nsets)]
     outs = torch.empty((L, B, HQ, D), dtype=torch.bfloat16, device=dev)
     gathered = torch.empty((world, L, B, HQ, D), dtype=torch.bfloat16, device=dev) if world > 1 else None
-    splits = store.suggest_splits(0)
+    splits = {bits: store.suggest_splits(PLAN.index(bits), HQ) for bits in sorted(set(PLAN))}
     attn_events = []
 
     def step(i, q_in=None, k_in=None, v_in=None, record=False):
@@ -254,7 +254,7 @@ def run_ours(args):
             if record:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e0.record()
-            store.attend(layer, q_all[layer], out=outs[layer], num_splits=splits, mode=args.mode)
+            store.attend(layer, q_all[layer], out=outs[layer], num_splits=splits[PLAN[layer]], mode=args.mode)
             if record:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record()
@@ -357,7 +357,7 @@ def run_ours(args):
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u8 codes / f32 means+scales, bf16 q/out", "data": "synthetic (torch.randn bf16, seeded)",
             "config": {"workload": WORKLOAD, "global_batch": B * world, "seq_len": T, "layers": L,
-                       "parallelism": f"seq-shard x{world}", "num_splits": splits, "page_tokens": 64,
+                       "parallelism": f"seq-shard x{world}", "num_splits": {str(k): v for k, v in splits.items()}, "page_tokens": 64,
                        "kernel_mode": args.mode, "l2": "cache 35 GB/GPU >> 126 MB L2 (no flush needed)"},
             "hbm_gbs": step_bytes / (ms_per_step / 1e3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

@@ -191,7 +191,13 @@ int tada_decode_attn_lse(const tada_page_layout* layout, const uint8_t* pool, co
 int tada_combine_lse(const float* o_parts, const float* lse_parts, int32_t n_parts, int64_t rows,
                      int32_t head_dim, void* out, int32_t out_dtype, float* lse_out, void* stream);
 
-/* Suggested split count for a batch/context on this device (fills ~4 waves of SMs). */
+/* Split count for this layer's kernel on the current device: the fewest whole waves of resident
+ * CTAs (SM count x CTAs per SM of the instantiation that will run) whose last wave is >= 90% full,
+ * with >= 256 tokens per split. */
+int32_t tada_decode_attn_plan_splits(const tada_page_layout* layout, int32_t num_q_heads, int32_t batch,
+                                     int64_t max_tokens);
+
+/* Suggested split count assuming one CTA per SM on a 148-SM B200 (geometry-agnostic). */
 int32_t tada_decode_attn_suggest_splits(int32_t batch, int64_t max_tokens, int32_t page_tokens);
 
 #ifdef __cplusplus

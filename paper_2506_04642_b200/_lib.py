@@ -71,6 +71,7 @@ SIGNATURES = {
                                    P, I32, I32, P, P]),
     "tada_combine_lse": (I32, [P, P, I32, I64, I32, P, I32, P, P]),
     "tada_decode_attn_suggest_splits": (I32, [I32, I64, I32]),
+    "tada_decode_attn_plan_splits": (I32, [C.POINTER(PageLayout), I32, I32, I64]),
 }
 
 _lib = None

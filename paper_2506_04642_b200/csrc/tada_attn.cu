@@ -310,24 +310,37 @@ int64_t tada_decode_attn_workspace_bytes(int32_t batch, int32_t num_q_heads, int
   return int64_t(batch) * num_q_heads * (num_splits + 1) * (int64_t(head_dim) + 2) * 4;
 }
 
-int32_t tada_decode_attn_suggest_splits(int32_t batch, int64_t max_tokens, int32_t page_tokens) {
+// Split count for `slots` concurrently resident CTAs: the fewest whole waves whose last wave is
+// >= 90% full, keeping >= 256 tokens per split (fewer, longer splits amortise the per-CTA q setup).
+static int32_t plan_splits(int64_t slots, int32_t batch, int64_t max_tokens) {
   if (batch <= 0 || max_tokens <= 0) return 1;
-  // One CTA per SM (the tensor-core kernel uses ~150-220 KB of smem): pick the smallest
-  // number of whole waves (<= 4) that keeps >= 256 tokens per split.
-  const int64_t sms = 148;
   const int64_t max_s = (max_tokens + 255) / 256;
   int64_t best = 1;
-  for (int64_t waves = 4; waves >= 1; --waves) {
-    const int64_t s = (sms * waves + batch - 1) / batch;
-    if (s <= max_s) {
-      best = s;
-      break;
-    }
+  for (int64_t waves = 1; waves <= 8; ++waves) {
+    const int64_t s = waves * slots / batch;
+    if (s < 1) continue;
+    const int64_t ctas = s * batch;
+    const int64_t used = (ctas + slots - 1) / slots * slots;
+    best = s;
+    if (ctas * 10 >= used * 9) break;
   }
   if (best > max_s) best = max_s;
-  if (best < 1) best = 1;
+  return int32_t(best < 1 ? 1 : best);
+}
+
+int32_t tada_decode_attn_suggest_splits(int32_t batch, int64_t max_tokens, int32_t page_tokens) {
   (void)page_tokens;
-  return int32_t(best);
+  return plan_splits(148, batch, max_tokens);
+}
+
+int32_t tada_decode_attn_plan_splits(const tada_page_layout* layout, int32_t num_q_heads, int32_t batch,
+                                     int64_t max_tokens) {
+  if (!layout || num_q_heads <= 0) return 1;
+  int per_sm = 1;
+  if (fast_supported(*layout, num_q_heads)) per_sm = fast_tile_tokens(*layout, num_q_heads) == 16 ? 2 : 1;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return plan_splits(int64_t(sms) * per_sm, batch, max_tokens);
 }
 
 static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool, const void* q, int32_t q_dtype,

@@ -52,5 +52,6 @@ struct alignas(64) TmaMaps {
 // geometry is unsupported so the caller can fall back to the generic kernel.
 bool fast_supported(const tada_page_layout& L, int Hq);
 int launch_fast(const AttnArgs& a, int batch, cudaStream_t st);
+int fast_tile_tokens(const tada_page_layout& L, int Hq);  // 16 or 32 (0: unsupported)
 
 }  // namespace tada

@@ -213,11 +213,14 @@ class PagedKVCache:
             self._ws = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
         return self._ws
 
-    def suggest_splits(self, layer: int) -> int:
+    def suggest_splits(self, layer: int, num_q_heads: int | None = None) -> int:
+        """Split-K factor for this layer's kernel (whole waves of resident CTAs on this device)."""
         from ._lib import load
 
         tokens = int((self.comp_host[layer] + self.res_host[layer]).max())
-        return int(load().tada_decode_attn_suggest_splits(self.B, tokens, self.P))
+        if num_q_heads is None:
+            return int(load().tada_decode_attn_suggest_splits(self.B, tokens, self.P))
+        return int(load().tada_decode_attn_plan_splits(self._layout_ptr(layer), num_q_heads, self.B, tokens))
 
     def attend(self, layer: int, q: torch.Tensor, out: torch.Tensor | None = None, out_dtype=torch.float32,
                num_splits: int | None = None, mode: int = 0, scale: float | None = None) -> torch.Tensor:
@@ -235,7 +238,7 @@ class PagedKVCache:
         if q.dtype not in (torch.float32, torch.bfloat16):
             q = q.float()
         q = q.contiguous()
-        splits = num_splits or self.suggest_splits(layer)
+        splits = num_splits or self.suggest_splits(layer, hq)
         ws = self.workspace(hq, splits)
         if out is None:
             out = torch.empty((self.B, hq, self.D), dtype=out_dtype, device=self.dev)
@@ -262,7 +265,7 @@ class PagedKVCache:
         if q.dtype not in (torch.float32, torch.bfloat16):
             q = q.float()
         q = q.contiguous()
-        splits = num_splits or self.suggest_splits(layer)
+        splits = num_splits or self.suggest_splits(layer, hq)
         ws = self.workspace(hq, splits)
         out = torch.empty((self.B, hq, self.D), dtype=torch.float32, device=self.dev)
         lse = torch.empty((self.B, hq), dtype=torch.float32, device=self.dev)

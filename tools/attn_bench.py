@@ -39,7 +39,7 @@ def main():
             store.append(layer, k, v)
     q = torch.randn((B, args.hq, D), generator=g, device="cuda").bfloat16()
     out = torch.empty((B, args.hq, D), dtype=torch.bfloat16, device="cuda")
-    splits = args.splits or store.suggest_splits(0)
+    splits = args.splits or store.suggest_splits(0, args.hq)
     for i in range(3):
         store.attend(i % args.layers, q, out=out, num_splits=splits, mode=args.mode)
     torch.cuda.synchronize()
