@@ -171,7 +171,7 @@ __device__ __forceinline__ uint32_t qk_pair(const uint32_t* w, int s, int which)
 struct Plan {
   int mean_bytes, codes_bytes, meta_bytes, side_bytes, stage_bytes, stages;
   int trow;
-  int off_sbuf, off_q16, off_pbuf, off_p2, off_corr, off_red, off_qsum, off_bar, total;
+  int off_sbuf, off_q16, off_qa, qa_bytes, off_pbuf, off_p2, off_corr, off_red, off_qsum, off_bar, total;
 };
 
 __host__ __device__ constexpr int up128(int x) { return (x + 127) / 128 * 128; }
@@ -195,7 +195,9 @@ __host__ __device__ constexpr Plan make_plan(int H, int gb, int HQ, int TT) {
   const int sb = up128(NSP * mrows * SROW * 4);
   const int pb = up128(mrows * PROW2 * 2);
   const int p2 = up128(H * 8 * PROW2 * 2);
-  const int tail = sb + pb + p2 + up128(mrows * 4) + up128(3 * HQ * 4) + up128(HQ * 4) + 128 + 1024;
+  // TT = 16 keeps the QK mean-term Q fragments in shared memory (registers are the limit at 128)
+  p.qa_bytes = TT == 16 ? up128(mrows * D * 2) : 0;
+  const int tail = sb + p.qa_bytes + pb + p2 + up128(mrows * 4) + up128(3 * HQ * 4) + up128(HQ * 4) + 128 + 1024;
   const int budget = TT == 16 ? 113 * 1024 : 227 * 1024;  // TT = 16: two CTAs per SM
   p.stages = (3 * p.stage_bytes + tail <= budget) ? 3 : ((2 * p.stage_bytes + tail <= budget) ? 2 : 1);
   int off = p.stages * p.stage_bytes;
@@ -204,6 +206,8 @@ __host__ __device__ constexpr Plan make_plan(int H, int gb, int HQ, int TT) {
   p.off_sbuf = off;
   off += sb;
   p.off_q16 = (p.stages - 1) * p.stage_bytes;  // prologue-only q staging: the last stage is loaded after it
+  p.off_qa = off;
+  off += p.qa_bytes;
   p.off_pbuf = off;
   off += pb;
   p.off_p2 = off;
@@ -334,20 +338,33 @@ __global__ void __launch_bounds__(TT * 16, TT == 16 ? 2 : 1) attn_fast_kernel(At
   // QK mean A operand: q tile mt, k-step s = 2*kq + ks; slots (2c,2c+1 | 2c+8,2c+9) <-> d = 16s+4c+(0,1 | 2,3)
   constexpr int NT8 = TT / 8;  // token octets per tile
   const int nt = warp % NT8, kq = warp / NT8;  // QK mean piece of warps with kq < NKQ
-  uint32_t qa[MT][KS][4];
+  constexpr bool QA_SMEM = pl.qa_bytes > 0;
+  uint32_t qa[QA_SMEM ? 1 : MT][QA_SMEM ? 1 : KS][4];
+  uint4* qa_s = reinterpret_cast<uint4*>(smem + pl.off_qa);  // [kq][mt][ks][lane] fragments
   {
     const __half* q16 = q16s;
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        const __half* r0 = q16 + (16 * mt + r) * D + 16 * ((KS * kq + ks) & 7) + 4 * c;
+    if (QA_SMEM) {  // pack every piece's fragments once: (kq, mt, ks) by the warps, lane-major
+      for (int f = warp; f < NKQ * MT * KS; f += NW) {
+        const int kq2 = f / (MT * KS), mt = (f / KS) % MT, ks = f % KS;
+        const __half* r0 = q16 + (16 * mt + r) * D + 16 * (KS * kq2 + ks) + 4 * c;
         const __half* r1 = r0 + 8 * D;
-        qa[mt][ks][0] = *reinterpret_cast<const uint32_t*>(r0);
-        qa[mt][ks][1] = *reinterpret_cast<const uint32_t*>(r1);
-        qa[mt][ks][2] = *reinterpret_cast<const uint32_t*>(r0 + 2);
-        qa[mt][ks][3] = *reinterpret_cast<const uint32_t*>(r1 + 2);
+        qa_s[f * 32 + lane] = make_uint4(*reinterpret_cast<const uint32_t*>(r0), *reinterpret_cast<const uint32_t*>(r1),
+                                         *reinterpret_cast<const uint32_t*>(r0 + 2),
+                                         *reinterpret_cast<const uint32_t*>(r1 + 2));
       }
+    } else {
+#pragma unroll
+      for (int mt = 0; mt < (QA_SMEM ? 1 : MT); ++mt)
+#pragma unroll
+        for (int ks = 0; ks < (QA_SMEM ? 1 : KS); ++ks) {
+          const __half* r0 = q16 + (16 * mt + r) * D + 16 * ((KS * kq + ks) & 7) + 4 * c;
+          const __half* r1 = r0 + 8 * D;
+          qa[mt][ks][0] = *reinterpret_cast<const uint32_t*>(r0);
+          qa[mt][ks][1] = *reinterpret_cast<const uint32_t*>(r1);
+          qa[mt][ks][2] = *reinterpret_cast<const uint32_t*>(r0 + 2);
+          qa[mt][ks][3] = *reinterpret_cast<const uint32_t*>(r1 + 2);
+        }
+    }
   }
   fence_proxy_async();  // q staging lives in the last stage, which TMA fills after the next barrier
   float qs[2];  // Σq of this thread's two code columns n = 2c, 2c+1
@@ -411,8 +428,19 @@ __global__ void __launch_bounds__(TT * 16, TT == 16 ? 2 : 1) attn_fast_kernel(At
         split_h2(x.z, x.w, h1, l1);
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
-          mma(acc[mt], qa[mt][ks], h0, h1);
-          mma(acc[mt], qa[mt][ks], l0, l1);
+          uint32_t af[4];
+          if (QA_SMEM) {
+            const uint4 f = qa_s[((kq * MT + mt) * KS + ks) * 32 + lane];
+            af[0] = f.x;
+            af[1] = f.y;
+            af[2] = f.z;
+            af[3] = f.w;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) af[e] = qa[QA_SMEM ? 0 : mt][QA_SMEM ? 0 : ks][e];
+          }
+          mma(acc[mt], af, h0, h1);
+          mma(acc[mt], af, l0, l1);
         }
       }
 #pragma unroll

@@ -28,7 +28,7 @@ def main():
     os.makedirs(PROF, exist_ok=True)
     rep = os.path.join(OUT, "attn4.ncu-rep")
     if os.path.exists(rep):
-        tiles = 16 * 32768 // 32
+        tiles = 16 * 32768 // 16  # 16-token tiles (attn_fast_kernel<4,32,16>)
         txt = run("tools/ncu_summary.py", rep, str(tiles))
         txt += "\n--- per source line (top 40 by instructions + stalls)\n"
         txt += run("tools/ncu_lines.py", rep, "paper_2506_04642_b200/csrc/tada_attn_fast.cu", "40", str(tiles))
@@ -45,11 +45,16 @@ def main():
             return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit[k]]
 
         traffic = nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum")
-        json.dump({"traffic_bytes_per_launch": traffic, "kernel": "attn_fast_kernel<4,32>",
+        json.dump({"traffic_bytes_per_launch": traffic, "kernel": "attn_fast_kernel<4,32,16>",
                    "shape": "B=16, T=32768 compressed, Hq=32, H=8, D=128, 4-bit",
                    "alg_bytes_per_launch": 16 * (32768 * 2 * (4 * 128 + 8 * 64 + 64) + 2 * 32 * 128 * 2),
                    "source": f"profiles/{tag}_attn4_ncu.txt"}, open(os.path.join(PROF, "attn_traffic.json"), "w"),
                   indent=1)
+    k1 = os.path.join(OUT, "k1.ncu-rep")
+    if os.path.exists(k1):
+        open(os.path.join(PROF, f"{tag}_k1_ncu.txt"), "w").write(
+            "ncu --set full -k regex:quant_append -s 2 -c 1 python tools/k1_bench.py --bits 4 (B=8, T=32768, H=8, D=128)"
+            "\n('tile' = one token, both sides)\n\n" + run("tools/ncu_summary.py", k1, str(8 * 32768)))
     lc = os.path.join(OUT, "launches.csv")
     if os.path.exists(lc):
         shutil.copy(lc, os.path.join(PROF, f"{tag}_launches.csv"))
