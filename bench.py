@@ -39,9 +39,31 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "decode attn tokens/s + HBM GB/s vs roofline (Llama-3-8B, 32k ctx); quant-append GB/s"
-PLAN = [8] * 2 + [4] * 22 + [2] * 8
-L, HQ, H, D, T, B_PER_GPU, R = 32, 32, 8, 128, 32768, 16, 128
-WORKLOAD = "llama3-8b decode, 32 layers, 32q/8kv heads, head_dim 128, 32k ctx, batch 16/GPU, plan [8]*2+[4]*22+[2]*8"
+# BASELINE.json configs that fit one GPU (per-GPU share for the weak-scaled ones).  2 is the headline.
+CONFIGS = {
+    2: dict(L=32, HQ=32, T=32768, B=16, plan=[8] * 2 + [4] * 22 + [2] * 8,
+            workload="llama3-8b decode, 32 layers, 32q/8kv heads, head_dim 128, 32k ctx, batch 16/GPU, "
+                     "plan [8]*2+[4]*22+[2]*8"),
+    4: dict(L=32, HQ=32, T=131072, B=4, plan=[2] * 32,
+            workload="llama3-8b long-context decode, 32 layers, 32q/8kv heads, head_dim 128, 128k ctx, batch 4/GPU, "
+                     "uniform 2-bit"),
+    5: dict(L=80, HQ=64, T=32768, B=16, plan=[4] * 80,
+            workload="llama3-70b decode, 80 layers, 64q/8kv heads, head_dim 128, 32k ctx, batch 16/GPU "
+                     "(128 at 8 GPUs), uniform 4-bit"),
+}
+H, D, R = 8, 128, 128
+L = HQ = T = B_PER_GPU = 0
+PLAN: list = []
+WORKLOAD = ""
+
+
+def use_config(n: int) -> None:
+    global L, HQ, T, B_PER_GPU, PLAN, WORKLOAD
+    c = CONFIGS[n]
+    L, HQ, T, B_PER_GPU, PLAN, WORKLOAD = c["L"], c["HQ"], c["T"], c["B"], list(c["plan"]), c["workload"]
+
+
+use_config(2)
 
 
 def tok_bytes(bits: int) -> int:
@@ -125,46 +147,53 @@ class ClockSampler:
 
 # ------------------------------------------------------------------------------------------ CPU oracle leg
 def _cpu_worker(args):
-    """One host core: build oracle caches at T=32768 for widths 8/4/2, then time attend on each `reps` times."""
-    seed, tokens, reps = args
+    """One host core: build oracle caches at T tokens for the plan's widths, then time attend on each `reps` times."""
+    seed, tokens, reps, hq, widths = args
     os.environ["OMP_NUM_THREADS"] = os.environ["OPENBLAS_NUM_THREADS"] = "1"
     from oracle import tada_oracle as orc
 
     rng = np.random.default_rng(seed)
     times = {}
-    for bits in (8, 4, 2):
+    for bits in widths:
         st = orc.LayerState(H, D, bits, R)
         k = orc.bf16_round(rng.normal(size=(tokens, H, D)).astype(np.float32))
         v = orc.bf16_round(rng.normal(size=(tokens, H, D)).astype(np.float32))
         orc.append(st, k, v)
         del k, v
-        q = orc.bf16_round(rng.normal(size=(HQ, D)).astype(np.float32))
+        q = orc.bf16_round(rng.normal(size=(hq, D)).astype(np.float32))
         ts = []
         for _ in range(reps):
             t0 = time.perf_counter()
-            orc.attend(q, st, HQ, block=64)
+            orc.attend(q, st, hq, block=64)
             ts.append(time.perf_counter() - t0)
         times[bits] = ts
     return times
 
 
-def cpu_oracle_leg(reps: int, tokens: int = T, workers: int | None = None):
-    """Per-unit (1 sequence x 1 layer) attend times on `workers` cores in parallel -> C2 decode tokens/s."""
+def cpu_oracle_leg(reps: int, workers: int | None = None):
+    """Per-unit (1 sequence x 1 layer) attend times on `workers` cores in parallel -> decode tokens/s of the config.
+
+    The unit is timed at min(T, 32768) context and scaled linearly to T (attend is linear in T), so
+    the leg stays bounded for the 128k config.
+    """
     cores = os.cpu_count() or 1
     workers = workers or min(cores, 32)
+    tokens = min(T, 32768)
+    widths = sorted(set(PLAN), reverse=True)
     ctx = mp.get_context("spawn")
     with ctx.Pool(workers) as pool:
-        res = pool.map(_cpu_worker, [(1000 + i, tokens, reps) for i in range(workers)])
-    per = {b: [t for r in res for t in r[b]] for b in (8, 4, 2)}
-    med = {b: statistics.median(per[b]) for b in per}
-    unit_mix = sum(med[b] for b in PLAN)  # one sequence through all 32 layers, one core
-    step_s = unit_mix * B_PER_GPU / workers  # 16 sequences spread over `workers` cores
-    alg = sum(attn_alg_bytes(b, 1, tokens, 0) for b in PLAN) * B_PER_GPU
+        res = pool.map(_cpu_worker, [(1000 + i, tokens, reps, HQ, widths) for i in range(workers)])
+    per = {b: [t for r in res for t in r[b]] for b in widths}
+    med = {b: statistics.median(per[b]) * (T / tokens) for b in widths}
+    unit_mix = sum(med[b] for b in PLAN)  # one sequence through all layers, one core
+    step_s = unit_mix * B_PER_GPU / workers  # the batch spread over `workers` cores
+    alg = sum(attn_alg_bytes(b, 1, T, 0) for b in PLAN) * B_PER_GPU
     return {
         "tokens_per_s": B_PER_GPU / step_s, "step_s": step_s, "alg_gbs": alg / step_s / 1e9, "workers": workers,
-        "unit_s": {str(b): med[b] for b in med}, "per_step_samples": workers * 3,
-        "sample": f"{workers} workers x 1 (seq, layer) unit per width {{8,4,2}} at T={tokens} x {reps} reps; "
-                  f"step = 16 seqs x 32 layers extrapolated linearly from the per-width medians",
+        "unit_s": {str(b): med[b] for b in med}, "per_step_samples": workers * len(widths),
+        "sample": f"{workers} workers x 1 (seq, layer) unit per width {widths} at T={tokens} x {reps} reps"
+                  + (f", scaled x{T // tokens} to T={T}" if T != tokens else "")
+                  + f"; step = {B_PER_GPU} seqs x {L} layers extrapolated linearly from the per-width medians",
     }
 
 
@@ -389,7 +418,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", type=int, default=0, help="attention kernel: 0 auto, 1 exact generic, 2 tensor-core")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle leg")
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS),
+                    help="BASELINE.json config (2 = headline; 4 = 128k 2-bit; 5 = 70B shape)")
     args = ap.parse_args()
+    use_config(args.config)
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
