@@ -197,7 +197,7 @@ __host__ __device__ constexpr Plan make_plan(int H, int gb, int HQ, int TT) {
   const int p2 = up128(H * 8 * PROW2 * 2);
   // TT = 16 keeps the QK mean-term Q fragments in shared memory (registers are the limit at 128)
   p.qa_bytes = TT == 16 ? up128(mrows * D * 2) : 0;
-  const int tail = sb + p.qa_bytes + pb + p2 + up128(mrows * 4) + up128(3 * HQ * 4) + up128(HQ * 4) + 128 + 1024;
+  const int tail = sb + p.qa_bytes + pb + p2 + up128(mrows * 4) + up128(3 * HQ * 4) + up128(HQ * 4) + 128;
   const int budget = TT == 16 ? 113 * 1024 : 227 * 1024;  // TT = 16: two CTAs per SM
   p.stages = (3 * p.stage_bytes + tail <= budget) ? 3 : ((2 * p.stage_bytes + tail <= budget) ? 2 : 1);
   int off = p.stages * p.stage_bytes;
@@ -220,7 +220,7 @@ __host__ __device__ constexpr Plan make_plan(int H, int gb, int HQ, int TT) {
   off += up128(HQ * 4);
   p.off_bar = off;
   off += 128;
-  p.total = off + 1024;
+  p.total = off;
   return p;
 }
 
@@ -235,10 +235,11 @@ template <int BITS, int HQ, int TT>
 __global__ void __launch_bounds__(TT * 16, TT == 16 ? 2 : 1) attn_fast_kernel(AttnArgs a,
                                                                               const __grid_constant__ TmaMaps maps) {
   constexpr int NW = nw_of(TT), NTHR = NW * 32, SROW = sr_of(TT), PROW2 = pr_of(TT), BAND = band_of(TT);
-  extern __shared__ uint8_t smem_raw[];
-  // 1 KB alignment (128B-swizzle atoms) by pointer arithmetic on the __shared__ array, so the
-  // compiler keeps the shared state space (LDS, 32-bit addressing) for every access below
-  uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+  // The dynamic shared window of a CTA without static shared memory starts 1 KB aligned (the TMA
+  // 128B-swizzle atom); with the base a link-time constant every shared address below is an
+  // immediate offset.  Checked once, loudly.
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if (threadIdx.x == 0 && (su32(smem) & 1023u) != 0) __trap();
   constexpr int H = 8;
   constexpr int G = HQ / H;                     // q heads per KV head (N columns used)
   constexpr int MT = HQ >= 16 ? HQ / 16 : 1;    // 16-row q tiles
