@@ -97,6 +97,13 @@ __device__ __forceinline__ void mma(float (&c)[4], const uint32_t (&a)[4], uint3
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+// Exact integer QK code term: u8 codes x s8 q pieces -> s32 (IMMA.16832.U8.S8)
+__device__ __forceinline__ void imma(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t r;
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
@@ -142,29 +149,22 @@ __device__ __forceinline__ void split_h2(float x0, float x1, uint32_t& hi, uint3
 // byte offset of (row t, byte o) inside a 128B-swizzled [TT x 128 B] band
 __device__ __forceinline__ int swz(int t, int o) { return t * 128 + ((((o >> 4) ^ t) & 7) << 4) + (o & 15); }
 
-// ------------------------------------------------------------------ QK code operand (token-on-M)
-// Thread quad-index c owns d in [32c, 32c+32) of every token row; k-step s takes 4 of them
-// (slots 2c, 2c+1 | 2c+8, 2c+9).  dq() is the d of each slot, used to lay out Q to match.
+// ------------------------------------------------------------------ QK code operand (token-on-M, IMMA)
+// m16n8k32 u8 A fragment: a0/a1 = rows (r, r+8), k = 4c+i; a2/a3 = the same rows, k = 16+4c+i.  Thread
+// quad-index c owns d in [32c, 32c+32) of every token row; k-step s takes 8 of them as two byte quads
+// (which = 0 -> a0/a1, which = 1 -> a2/a3).  dk() is the d of byte i, used to lay out q to match.
 template <int BITS>
-__host__ __device__ __forceinline__ int dq(int s, int c, int slot) {
-  const int lo = slot & 1, hi = slot >> 1;  // slot: 0 = (2c), 1 = (2c+1), 2 = (2c+8), 3 = (2c+9)
-  if (BITS == 4) return 32 * c + 8 * (s >> 1) + 2 * (s & 1) + hi + 4 * lo;
-  if (BITS == 2) return 32 * c + 16 * (s >> 2) + 2 * (s & 3) + hi + 8 * lo;
-  return 32 * c + 4 * s + hi + 2 * lo;
+__host__ __device__ __forceinline__ int dk(int c, int s, int which, int i) {
+  if (BITS == 4) return 32 * c + 8 * s + 2 * i + which;                       // lo / hi nibbles of word s
+  if (BITS == 2) return 32 * c + 16 * (s >> 1) + 4 * i + 2 * (s & 1) + which;  // crumb 2(s&1)+which of word s/2
+  return 32 * c + 8 * s + 4 * which + i;                                       // words 2s, 2s+1
 }
-// f16x2 of (slot 2c, 2c+1) [which = 0] or (2c+8, 2c+9) [which = 1] of k-step s from the row's words
+// the u8x4 code quad of k-step s from a row's words
 template <int BITS>
-__device__ __forceinline__ uint32_t qk_pair(const uint32_t* w, int s, int which) {
-  if (BITS == 4) {
-    const uint32_t x = (s & 1) ? (w[s >> 1] >> 8) : w[s >> 1];
-    return which ? field_h2<4>(x, 0x000F000Fu) : field_h2<0>(x, 0x000F000Fu);
-  } else if (BITS == 2) {
-    const uint32_t x = (s & 2) ? (w[s >> 2] >> 8) : w[s >> 2];
-    if (s & 1) return which ? field_h2<6>(x, 0x00030003u) : field_h2<4>(x, 0x00030003u);
-    return which ? field_h2<2>(x, 0x00030003u) : field_h2<0>(x, 0x00030003u);
-  } else {
-    return hsub2(prmt(w[s], 0x64646464u, which ? 0x4341u : 0x4240u), 0x64006400u);
-  }
+__device__ __forceinline__ uint32_t qk_quad(const uint32_t* w, int s, int which) {
+  if (BITS == 4) return (which ? (w[s] >> 4) : w[s]) & 0x0F0F0F0Fu;
+  if (BITS == 2) return (w[s >> 1] >> (4 * (s & 1) + 2 * which)) & 0x03030303u;
+  return w[2 * s + which];
 }
 
 // ------------------------------------------------------------------ shared memory plan
@@ -312,28 +312,53 @@ __global__ void __launch_bounds__(TT * 16, TT == 16 ? 2 : 1) attn_fast_kernel(At
       }
       const uint32_t lo = pack_h2(v[0], v[1]), hi = pack_h2(v[2], v[3]);
       *reinterpret_cast<uint2*>(q16 + g * D + 4 * lane) = make_uint2(lo, hi);
-      // Σq of the f16-rounded q, so that every term of the factored form uses the same q
+      // max |q| of the f16-rounded row: the fixed-point scale of the integer code term
       const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&lo));
       const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&hi));
-      const float ssum = warp_sum((f0.x + f0.y) + (f1.x + f1.y));
-      if (lane == 0 && g < HQ) qsum[g] = ssum;
+      float amax = fmaxf(fmaxf(fabsf(f0.x), fabsf(f0.y)), fmaxf(fabsf(f1.x), fabsf(f1.y)));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      if (lane == 0 && g < HQ) qsum[g] = amax;
     }
   }
   __syncthreads();
-  // QK code B operand (Q_h^T, d permuted to the code slots), column n = r <-> q head h*G + r
-  uint32_t qb[8][2];
+  // QK code B operand: Q_h^T as 16-bit fixed point (scale sq per KV head) split into two s8 pieces
+  // (q = sq * (256 * hi + lo)), k laid out by dk(); column n = r <-> q head h*G + r.  The integer
+  // products and sums are exact, so the code term is q_fx . code with no rounding at all.
+  uint32_t qbh[4][2], qbl[4][2];
+  float sq, qs[2];  // qs: Σ q_fx of this thread's two code columns n = 2c, 2c+1
   {
     const __half* q16 = q16s;
-    const int g = h * G + r;
+    float mx = 0.f;
+    for (int e = 0; e < G; ++e) mx = fmaxf(mx, qsum[h * G + e]);
+    constexpr float QMAX = 32639.f;  // 127 * 256 + 127: both pieces stay in s8
+    sq = mx > 0.f ? mx / QMAX : 1.f;
+    const float inv = mx > 0.f ? QMAX / mx : 0.f;
+    const __half* qr = q16 + (h * G + (r < G ? r : 0)) * D;
+    int isum = 0;
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      if (r < G) {
-        const __half* qr = q16 + g * D;
-        qb[s][0] = pack_h2(__half2float(qr[dq<BITS>(s, c, 0)]), __half2float(qr[dq<BITS>(s, c, 1)]));
-        qb[s][1] = pack_h2(__half2float(qr[dq<BITS>(s, c, 2)]), __half2float(qr[dq<BITS>(s, c, 3)]));
-      } else {
-        qb[s][0] = qb[s][1] = 0u;
+    for (int s = 0; s < 4; ++s)
+#pragma unroll
+      for (int which = 0; which < 2; ++which) {
+        uint32_t ph = 0u, pl8 = 0u;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          int qi = __float2int_rn(__half2float(qr[dk<BITS>(c, s, which, i)]) * inv);
+          qi = r < G ? max(-32639, min(32639, qi)) : 0;
+          isum += qi;
+          const int qh = (qi + 128) >> 8, ql = qi - qh * 256;
+          ph |= uint32_t(qh & 0xFF) << (8 * i);
+          pl8 |= uint32_t(ql & 0xFF) << (8 * i);
+        }
+        qbh[s][which] = ph;
+        qbl[s][which] = pl8;
       }
+    isum += __shfl_xor_sync(0xffffffffu, isum, 1);
+    isum += __shfl_xor_sync(0xffffffffu, isum, 2);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int v = __shfl_sync(0xffffffffu, isum, ((2 * c + e) & 7) * 4);
+      qs[e] = (2 * c + e < G) ? sq * float(v) : 0.f;
     }
   }
   // QK mean A operand: q tile mt, k-step s = 2*kq + ks; slots (2c,2c+1 | 2c+8,2c+9) <-> d = 16s+4c+(0,1 | 2,3)
@@ -368,9 +393,6 @@ __global__ void __launch_bounds__(TT * 16, TT == 16 ? 2 : 1) attn_fast_kernel(At
     }
   }
   fence_proxy_async();  // q staging lives in the last stage, which TMA fills after the next barrier
-  float qs[2];  // Σq of this thread's two code columns n = 2c, 2c+1
-#pragma unroll
-  for (int e = 0; e < 2; ++e) qs[e] = (2 * c + e < G) ? qsum[h * G + 2 * c + e] : 0.f;
 
   // accumulators
   float oc[8][4];    // PV code term, O_h^T: m-tile of 16 d (rows) x 8 n (cols), this warp's tokens
@@ -454,7 +476,6 @@ __global__ void __launch_bounds__(TT * 16, TT == 16 ? 2 : 1) attn_fast_kernel(At
     // ------------------------------------------------------------ A2: QK code term (head h, token half) -> S_code
     {
       const int ta = HT * half + r, tb = ta + 8;  // accumulator rows (tokens)
-      float cs[4] = {0.f, 0.f, 0.f, 0.f};
       constexpr int NWD = BITS == 8 ? 8 : (BITS == 4 ? 4 : 2);  // code words per row segment
       uint32_t wa[NWD], wb[NWD];
       constexpr int SEG = GB / 4;
@@ -480,19 +501,20 @@ __global__ void __launch_bounds__(TT * 16, TT == 16 ? 2 : 1) attn_fast_kernel(At
           wb[(4 * u) % NWD] = y.x; wb[(4 * u + 1) % NWD] = y.y; wb[(4 * u + 2) % NWD] = y.z; wb[(4 * u + 3) % NWD] = y.w;
         }
       }
-      float cs2[4] = {0.f, 0.f, 0.f, 0.f};  // second accumulator: two independent MMA chains of 4
+      int ch[4] = {0, 0, 0, 0}, cl[4] = {0, 0, 0, 0};  // hi / lo q-piece accumulators
 #pragma unroll
-      for (int s = 0; s < 8; ++s) {
+      for (int s = 0; s < 4; ++s) {
         uint32_t af[4];
-        af[0] = qk_pair<BITS>(wa, s, 0);
-        af[1] = qk_pair<BITS>(wb, s, 0);
-        af[2] = qk_pair<BITS>(wa, s, 1);
-        af[3] = qk_pair<BITS>(wb, s, 1);
-        if (s & 1) mma(cs2, af, qb[s][0], qb[s][1]);
-        else mma(cs, af, qb[s][0], qb[s][1]);
+        af[0] = qk_quad<BITS>(wa, s, 0);
+        af[1] = qk_quad<BITS>(wb, s, 0);
+        af[2] = qk_quad<BITS>(wa, s, 1);
+        af[3] = qk_quad<BITS>(wb, s, 1);
+        imma(ch, af, qbh[s][0], qbh[s][1]);
+        imma(cl, af, qbl[s][0], qbl[s][1]);
       }
+      float cs[4];  // q_fx . code / sq  (|.| <= 2^30: exact in int32)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) cs[e] += cs2[e];
+      for (int e = 0; e < 4; ++e) cs[e] = float(ch[e] * 256 + cl[e]);
       // − scale·(q·code) − min·Σq, for the G real columns
       if (2 * c < G) {
         const float2 ka = *reinterpret_cast<const float2*>(kmeta + ta * pl.trow + 8 * h);
@@ -501,8 +523,8 @@ __global__ void __launch_bounds__(TT * 16, TT == 16 ? 2 : 1) attn_fast_kernel(At
         for (int e = 0; e < 2; ++e) {
           if (2 * c + e < G) {
             float* row = sbuf + (NKQ * MROWS + h * G + 2 * c + e) * SROW;
-            row[ta] = -fmaf(ka.x, cs[e], ka.y * qs[e]);
-            row[tb] = -fmaf(kb.x, cs[2 + e], kb.y * qs[e]);
+            row[ta] = -fmaf(ka.x * sq, cs[e], ka.y * qs[e]);
+            row[tb] = -fmaf(kb.x * sq, cs[2 + e], kb.y * qs[e]);
           }
         }
       }
