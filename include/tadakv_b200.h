@@ -162,7 +162,8 @@ int tada_scatter_compressed(const tada_page_layout* layout, uint8_t* pool, const
  * workspace must hold tada_decode_attn_workspace_bytes(...) bytes.
  * out: [batch][num_q_heads][head_dim] in out_dtype.
  * mode: 0 = auto, 1 = exact generic kernel (f32 reconstruct-then-dot, any geometry),
- *       2 = fast tensor-core kernel (head_dim 128, bits 2/4/8). */
+ *       2 = fast tensor-core kernel (head_dim 128, bits 2/4/8),
+ *       3 = fast tensor-core kernel, previous two-barrier-per-tile variant (A/B comparisons). */
 int64_t tada_decode_attn_workspace_bytes(int32_t batch, int32_t num_q_heads, int32_t head_dim,
                                          int32_t num_splits);
 int tada_decode_attn(const tada_page_layout* layout, const uint8_t* pool, const void* q,

@@ -356,9 +356,10 @@ static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool,
   if (num_splits < 1 || num_splits > 4096) return fail(TADA_ERR_CONFIG, "num_splits out of range");
   if (batch == 0) return TADA_OK;
   if (!q || !out || !comp_len || !res_len) return fail(TADA_ERR_SHAPE, "null buffer");
-  if (mode < 0 || mode > 2) return fail(TADA_ERR_CONFIG, "mode must be 0 (auto), 1 (exact) or 2 (fast)");
-  const bool fast = mode == 2 || (mode == 0 && fast_supported(*layout, num_q_heads));
-  if (mode == 2 && !fast_supported(*layout, num_q_heads))
+  if (mode < 0 || mode > 3)
+    return fail(TADA_ERR_CONFIG, "mode must be 0 (auto), 1 (exact), 2 (fast) or 3 (fast, two-barrier kernel)");
+  const bool fast = mode >= 2 || (mode == 0 && fast_supported(*layout, num_q_heads));
+  if (mode >= 2 && !fast_supported(*layout, num_q_heads))
     return fail(TADA_ERR_CONFIG, "fast decode attention needs head_dim 128, bits 2/4/8, num_q_heads in {8,16,32,64}, "
                                  "group size in {1,2,4,8} and page_tokens % 32 == 0");
   if ((num_splits > 1 || fast) && !workspace) return fail(TADA_ERR_SHAPE, "workspace required");
@@ -386,7 +387,7 @@ static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool,
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int rc;
   if (fast) {
-    rc = launch_fast(a, batch, st);
+    rc = (mode != 3 && v8_supported(*layout, num_q_heads)) ? launch_v8(a, batch, st) : launch_fast(a, batch, st);
     if (rc == TADA_OK) rc = launch_combine_residual(a, batch, st);
     return rc;
   } else {

@@ -53,5 +53,10 @@ struct alignas(64) TmaMaps {
 bool fast_supported(const tada_page_layout& L, int Hq);
 int launch_fast(const AttnArgs& a, int batch, cudaStream_t st);
 int fast_tile_tokens(const tada_page_layout& L, int Hq);  // 16 or 32 (0: unsupported)
+// One-barrier-per-tile kernel (tada_attn_v8.cu): 2/4-bit (8-bit where two stages fit), Hq in {8, 16, 32}.
+bool v8_supported(const tada_page_layout& L, int Hq);
+int launch_v8(const AttnArgs& a, int batch, cudaStream_t st);
+// Cached TMA descriptors of a layer pool for TT-token tiles (tada_attn_fast.cu).
+int get_tma_maps(const AttnArgs& a, TmaMaps* out, int tt);
 
 }  // namespace tada

@@ -33,9 +33,11 @@
 #include <unordered_map>
 
 #include "tada_attn.cuh"
+#include "tada_mma.cuh"
 
 namespace tada {
 namespace fast {
+using namespace mmaops;
 
 constexpr int D = 128;
 constexpr int HT = 16;  // tokens per warp (one m16 tile of the token-on-M QK code term)
@@ -45,127 +47,6 @@ __host__ __device__ constexpr int nw_of(int tt) { return tt / 2; }
 __host__ __device__ constexpr int sr_of(int tt) { return tt + 4; }   // S row stride (floats)
 __host__ __device__ constexpr int pr_of(int tt) { return tt + 8; }   // P / P' row stride (halves): conflict-free
 __host__ __device__ constexpr int band_of(int tt) { return tt * 128; }  // bytes of one 128-B-wide swizzled band
-
-// ------------------------------------------------------------------ PTX wrappers
-__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n.reg .pred p;\n"
-      "TADA_WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra TADA_WAIT_%=;\n}\n" ::"r"(su32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
-          "r"(su32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tma_5d(void* dst, const CUtensorMap* map, int c1, int c4, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %2, %2, %4}], [%5];" ::
-          "r"(su32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(c1), "r"(c4), "r"(su32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* map, int c1, int c3, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %2, %4}], [%5];" ::
-          "r"(su32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(c1), "r"(c3), "r"(su32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(addr));
-}
-__device__ __forceinline__ void mma(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-// Exact integer QK code term: u8 codes x s8 q pieces -> s32 (IMMA.16832.U8.S8)
-__device__ __forceinline__ void imma(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
-  uint32_t r;
-  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
-  return r;
-}
-__device__ __forceinline__ uint32_t lop_and_or(uint32_t x, uint32_t m, uint32_t o) {  // (x & m) | o, one LOP3
-  uint32_t r;
-  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(x), "r"(m), "r"(o));
-  return r;
-}
-__device__ __forceinline__ uint32_t hsub2(uint32_t a, uint32_t b) {
-  uint32_t r;
-  asm("sub.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
-  return r;
-}
-// Integer code field (value v at bit position pos of each 16-bit half) -> exact f16x2 (v, v):
-// OR-ing the f16 exponent of 2^(10-pos) makes the half read 2^(10-pos) + v; subtracting the
-// bias is exact.  pos in {0, 2, 4, 6} (bits 0-7 of a half are mantissa bits).
-template <int POS>
-__device__ __forceinline__ uint32_t field_h2(uint32_t x, uint32_t mask_at_0) {
-  constexpr uint32_t bias = POS == 0 ? 0x64006400u : (POS == 2 ? 0x5C005C00u : (POS == 4 ? 0x54005400u : 0x4C004C00u));
-  return hsub2(lop_and_or(x, mask_at_0 << POS, bias), bias);
-}
-__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
-  const __half2 h = __floats2half2_rn(lo, hi);
-  return *reinterpret_cast<const uint32_t*>(&h);
-}
-__device__ __forceinline__ void red_add(float* p, float v) {
-  asm volatile("red.shared.add.f32 [%0], %1;" ::"r"(su32(p)), "f"(v) : "memory");
-}
-__device__ __forceinline__ float ex2(float x) {  // 2^x; ex2(-inf) = 0
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-// f32 pair -> f16 hi pair + f16 residual pair (≈ 22 significant bits together)
-__device__ __forceinline__ void split_h2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
-  const __half2 h = __floats2half2_rn(x0, x1);
-  const float2 back = __half22float2(h);
-  hi = *reinterpret_cast<const uint32_t*>(&h);
-  lo = pack_h2(x0 - back.x, x1 - back.y);
-}
-// byte offset of (row t, byte o) inside a 128B-swizzled [TT x 128 B] band
-__device__ __forceinline__ int swz(int t, int o) { return t * 128 + ((((o >> 4) ^ t) & 7) << 4) + (o & 15); }
-
-// ------------------------------------------------------------------ QK code operand (token-on-M, IMMA)
-// m16n8k32 u8 A fragment: a0/a1 = rows (r, r+8), k = 4c+i; a2/a3 = the same rows, k = 16+4c+i.  Thread
-// quad-index c owns d in [32c, 32c+32) of every token row; k-step s takes 8 of them as two byte quads
-// (which = 0 -> a0/a1, which = 1 -> a2/a3).  dk() is the d of byte i, used to lay out q to match.
-template <int BITS>
-__host__ __device__ __forceinline__ int dk(int c, int s, int which, int i) {
-  if (BITS == 4) return 32 * c + 8 * s + 2 * i + which;                       // lo / hi nibbles of word s
-  if (BITS == 2) return 32 * c + 16 * (s >> 1) + 4 * i + 2 * (s & 1) + which;  // crumb 2(s&1)+which of word s/2
-  return 32 * c + 8 * s + 4 * which + i;                                       // words 2s, 2s+1
-}
-// the u8x4 code quad of k-step s from a row's words
-template <int BITS>
-__device__ __forceinline__ uint32_t qk_quad(const uint32_t* w, int s, int which) {
-  if (BITS == 4) return (which ? (w[s] >> 4) : w[s]) & 0x0F0F0F0Fu;
-  if (BITS == 2) return (w[s >> 1] >> (4 * (s & 1) + 2 * which)) & 0x03030303u;
-  return w[2 * s + which];
-}
 
 // ------------------------------------------------------------------ shared memory plan
 struct Plan {
@@ -865,7 +746,7 @@ static bool encode_meta(CUtensorMap* m, const uint8_t* base, uint64_t row_bytes,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static int get_maps(const AttnArgs& a, TmaMaps* out, int tt) {
+int get_tma_maps(const AttnArgs& a, TmaMaps* out, int tt) {
   struct Key {
     const uint8_t* pool;
     int64_t page_bytes;
@@ -927,7 +808,7 @@ static int launch_fast_tt(const AttnArgs& a, int batch, cudaStream_t st) {
     attr_set = true;
   }
   TmaMaps maps;
-  const int rc = get_maps(a, &maps, TT);
+  const int rc = get_tma_maps(a, &maps, TT);
   if (rc != TADA_OK) return rc;
   kern<<<dim3(a.splits, batch), TT * 16, pl.total, st>>>(a, maps);
   return check_launch("decode_attn_fast");

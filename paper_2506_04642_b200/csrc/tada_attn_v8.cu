@@ -1,0 +1,599 @@
+// K2-v8: split-K flash decoding over the compressed paged cache, sm_100a, ONE CTA barrier per tile.
+//
+// Reference semantics: attend_streaming (pkg/src/tadakv/attention.py:103-151) with
+// K̂ = mean - (min + scale*code) (cache.py:193-200, quant.py:177-180), evaluated in the factored form
+//   q·k̂   = q·mean − min·Σq − scale·(q·code)
+//   Σ p·v̂ = p·vmean − Σ(p·vmin) + p'·vcode,      p' = −p·vscale
+// (SURVEY §7 hard part 2).  CTA = (split, sequence): 8 warps, warp h = KV head h, 16-token tiles, two
+// CTAs per SM, a two-stage TMA ring.  Per tile:
+//   X   (before the barrier, cooperative, every warp an equal share)
+//       - QK mean piece: S_mean[q][tok] for all q heads, one token octet x one d quarter per warp, from
+//         the f32 means as f16 hi + lo (mma.sync, f32 accumulate) -> 4 partial planes;
+//       - vmean split: f32 -> f16 hi / lo words of token pairs, [pair][d] (the PV mean A operand).
+//   --- barrier (the only one): S_mean / split vmean of this tile complete; every warp is done with
+//       the previous tile, whose stage is refilled by TMA right here.
+//   c   QK code term with q on M: IMMA m16n8k32, A = q_h as two s8 pieces of a 16-bit fixed point,
+//       B = the packed codes expanded to u8 in registers (exact integer products and sums).
+//   d   online softmax in registers (thread = q head r of the group x 4 tokens); P and P' = −p·vscale
+//       stay in registers as B operands.
+//   e   PV with d on M, ONE accumulator per warp: vmean hi·P + vmean lo·P + (bias + vcode)·P', the codes
+//       entering as exact f16 bias + code (no subtraction; bias·Σp' is removed once at the end).
+// Shared offsets are per-thread registers computed once; the loop is unrolled by two so the stage and
+// the double-buffer slot are compile-time immediates.
+#include <cuda_runtime.h>
+
+#include <string>
+#include <type_traits>
+
+#include "tada_attn.cuh"
+#include "tada_mma.cuh"
+
+namespace tada {
+namespace v8 {
+using namespace mmaops;
+
+constexpr int D = 128, H = 8, TT = 16, NW = 8, NTHR = 256;
+constexpr int BAND = TT * 128;   // bytes of one 128-B-wide swizzled band of a tile region
+// Split vmean, one part (hi or lo): 16-B chunk (c, r, mt) = the PV mean A fragment of lane (r, c), m-tile mt:
+// words (pair c, d), (pair c, d+1), (pair c+4, d), (pair c+4, d+1) with d = 16r + 2mt, a word holding the
+// f16 of tokens (2p, 2p+1).  Chunk index 74c + 9r + mt: the padding makes every quarter-warp access
+// conflict-free ((2c + r + mt) mod 8 distinct).
+constexpr int VMP = 4 * 74 * 16;    // one part (hi or lo) of the split vmean
+constexpr int kBudget = 113 * 1024; // two CTAs per SM
+
+__host__ __device__ constexpr int up128(int x) { return (x + 127) / 128 * 128; }
+__host__ __device__ constexpr int up1k(int x) { return (x + 1023) / 1024 * 1024; }
+
+struct Plan {
+  int mean_bytes, codes_bytes, meta_bytes, side_bytes, stage_bytes, trow, sm_slot;
+  int off_vm, off_sm, off_qa, off_bar, total;
+  bool ok;
+};
+
+// [stage 0][stage 1] | VM [2 slots][hi, lo][VMP] | SM [2 slots][4 planes][MROWS][16] f32 |
+// QA [4 quarters][MT][2 k-steps][32 lanes] uint4 | mbarriers.  Prologue-only q staging and row maxima
+// live in stage 1; the epilogue's (l, Σp·vmin, m) table lives in the then idle VM region.
+__host__ __device__ constexpr Plan make_plan(int gb, int HQ) {
+  Plan p{};
+  const int mrows = HQ >= 16 ? HQ : 16, mt = mrows / 16;
+  p.trow = H * 8 + 16;  // meta box row: 16 B of TMA zero fill per row spread the banks
+  p.mean_bytes = 4 * BAND;
+  p.codes_bytes = (H * gb / 128) * BAND;
+  p.meta_bytes = TT * p.trow;
+  p.side_bytes = p.mean_bytes + p.codes_bytes;
+  p.stage_bytes = up1k(2 * p.side_bytes + 2 * p.meta_bytes);
+  p.sm_slot = 4 * mrows * TT * 4;
+  int off = 2 * p.stage_bytes;
+  p.off_vm = off;
+  off += 2 * 2 * VMP;  // [slot][hi, lo]
+  p.off_sm = off;
+  off += 2 * p.sm_slot;
+  p.off_qa = off;
+  off += 4 * mt * 2 * 512;
+  p.off_bar = off;
+  off += 128;
+  p.total = off;
+  // the prologue stages q [MROWS][D] f16 in stage 1; the epilogue parks [HQ][D + 4] f32 over the stages
+  p.ok = off <= kBudget && p.stage_bytes >= mrows * (D * 2 + 4) && 2 * p.stage_bytes >= HQ * (D + 4) * 4 &&
+         2 * 2 * VMP >= 3 * HQ * 4;
+  return p;
+}
+
+// PV code A operand (d on M).  Thread (r, c) owns d in [16r, 16r+16) of head h; m-tile mt holds
+// d = 16r + 2mt in rows r and d = 16r + 2mt + 1 in rows r + 8.  Each code enters the MMA as the exact
+// f16 value bias + code (the code field ORed under a fixed exponent, no subtraction); bias(mt, half)
+// is removed once at the end as bias * Σp'.  Fields sit at mantissa bit 4 or above (bias <= 64) for
+// 2/4-bit codes, so the biased f32 accumulation loses at most ~2^-17 of the code term (8-bit: bias
+// 1024 against codes up to 255).
+template <int BITS>
+__host__ __device__ constexpr float pv_bias(int mt, int half) {
+  if (BITS == 8) return 1024.f;
+  if (BITS == 4) return 64.f;
+  // 2-bit: k = mt & 3 -> (rows r, rows r + 8) fields at POS (4, 6), (4, 6), (8, 4), (6, 8)
+  const int k = mt & 3;
+  const int pos = k < 2 ? (half ? 6 : 4) : (k == 2 ? (half ? 4 : 8) : (half ? 8 : 6));
+  return pos == 4 ? 64.f : (pos == 6 ? 16.f : 4.f);
+}
+template <int POS>
+__device__ __forceinline__ uint32_t crumb(uint32_t x) {  // 2-bit field at POS -> f16 pair 2^(10-POS) + v
+  constexpr uint32_t e = POS == 4 ? 0x54005400u : (POS == 6 ? 0x4C004C00u : 0x44004400u);
+  return lop_and_or(x, 0x00030003u << POS, e);
+}
+__device__ __forceinline__ uint32_t nib4(uint32_t x) { return lop_and_or(x, 0x00F000F0u, 0x54005400u); }  // 64 + v
+
+template <typename T>
+__device__ __forceinline__ T& sh(uint8_t* base, int off) {
+  return *reinterpret_cast<T*>(base + off);
+}
+
+// ------------------------------------------------------------------ the kernel
+template <int BITS, int HQ>
+__global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __grid_constant__ TmaMaps maps) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if (threadIdx.x == 0 && (su32(smem) & 1023u) != 0) __trap();
+  constexpr int G = HQ / H;                   // q heads per KV head
+  constexpr int MT = HQ >= 16 ? HQ / 16 : 1;  // 16-row q tiles of the QK mean piece
+  constexpr int MROWS = MT * 16;
+  constexpr int GB = BITS * D / 8;            // code bytes per (token, head)
+  constexpr Plan pl = make_plan(GB, HQ);
+  constexpr int SB = pl.stage_bytes;
+  constexpr int PLANE = MROWS * TT * 4;
+  const int P = a.L.page_tokens;
+  const int b = blockIdx.y, split = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r = lane >> 2, c = lane & 3;
+  const int h = warp;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + pl.off_bar);
+  float* qmax = reinterpret_cast<float*>(smem + SB + MROWS * D * 2);  // [MROWS], prologue only
+  float* red = reinterpret_cast<float*>(smem + pl.off_vm);           // [3][HQ] epilogue (l, Σp·vmin, m)
+
+  const int C = a.comp_len[b];
+  int t_begin, t_end;
+  split_range(C, a.splits, split, TT, t_begin, t_end);
+  const int ntiles = t_end > t_begin ? (t_end - t_begin + TT - 1) / TT : 0;
+
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // TMA producer (thread 0): tile `it` -> stage it & 1, three copies (means, codes, metas; both sides).
+  // The (page, row) cursor advances by TT rows per tile (P is a multiple of TT): no divisions in the loop.
+  const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
+  constexpr uint32_t tx = 2u * uint32_t(pl.mean_bytes + pl.codes_bytes + TT * pl.trow);
+  int cur_pg = t_begin / P, cur_row = t_begin - (t_begin / P) * P, cur_page = 0;  // next tile to issue
+  auto issue = [&](int stg) {
+    uint8_t* dst = smem + stg * SB;
+    mbar_expect_tx(&full[stg], tx);
+    tma_5d(dst, &maps.m[0][0], cur_row, cur_page, &full[stg]);
+    tma_5d(dst + 2 * pl.mean_bytes, &maps.m[0][1], cur_row, cur_page, &full[stg]);
+    tma_4d(dst + 2 * pl.side_bytes, &maps.m[0][2], cur_row, cur_page, &full[stg]);
+    cur_row += TT;
+    if (cur_row == P) {
+      cur_row = 0;
+      ++cur_pg;
+    }
+  };
+  if (tid == 0) {
+    for (int k = 0; k < 3; ++k)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[0][k])) : "memory");
+    if (ntiles > 0) {
+      cur_page = pt[cur_pg];
+      issue(0);
+      if (ntiles > 1) cur_page = pt[cur_pg];  // the page of tile 1, loaded a tile ahead
+    }
+  }
+
+  // ---------------------------------------------------------------- prologue: q -> f16, staged in stage 1
+  __half* q16 = reinterpret_cast<__half*>(smem + SB);  // [MROWS][D]
+  for (int g = warp; g < MROWS; g += NW) {
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (g < HQ) {
+      if (a.q_dtype == TADA_F32) load4(reinterpret_cast<const float*>(a.q) + (int64_t(b) * HQ + g) * D + 4 * lane, v);
+      else load4(reinterpret_cast<const __nv_bfloat16*>(a.q) + (int64_t(b) * HQ + g) * D + 4 * lane, v);
+    }
+    const uint32_t lo = pack_h2(v[0], v[1]), hi = pack_h2(v[2], v[3]);
+    *reinterpret_cast<uint2*>(q16 + g * D + 4 * lane) = make_uint2(lo, hi);
+    const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&lo));
+    const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&hi));
+    float amax = fmaxf(fmaxf(fabsf(f0.x), fabsf(f0.y)), fmaxf(fabsf(f1.x), fabsf(f1.y)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if (lane == 0) qmax[g] = amax;
+  }
+  __syncthreads();
+  // IMMA A operand: q head h*G + r (r < G) as 16-bit fixed point (scale sq) split into two s8 pieces,
+  // q = sq * (256 hi + lo): hi in row r, lo in row r + 8, so one IMMA yields both partial sums; k laid
+  // out by dk() to match the code bytes.  Stored in fragment order {a0, a1, a2, a3}.
+  uint32_t qA[4][4];
+  float sq, qs;  // qs = Σ_d q_fx of q head h*G + r (the min term)
+  {
+    float mx = 0.f;
+#pragma unroll
+    for (int e = 0; e < G; ++e) mx = fmaxf(mx, qmax[h * G + e]);
+    constexpr float QMAX = 32639.f;  // 127 * 256 + 127: both pieces stay in s8
+    sq = mx > 0.f ? mx / QMAX : 1.f;
+    const float inv = mx > 0.f ? QMAX / mx : 0.f;
+    const __half* qr = q16 + (h * G + (r < G ? r : 0)) * D;
+    int isum = 0;
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+#pragma unroll
+      for (int which = 0; which < 2; ++which) {
+        uint32_t ph = 0u, pl8 = 0u;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          int qi = __float2int_rn(__half2float(qr[dk<BITS>(c, s, which, i)]) * inv);
+          qi = r < G ? max(-32639, min(32639, qi)) : 0;
+          isum += qi;
+          const int qh = (qi + 128) >> 8, ql = qi - qh * 256;
+          ph |= uint32_t(qh & 0xFF) << (8 * i);
+          pl8 |= uint32_t(ql & 0xFF) << (8 * i);
+        }
+        qA[s][2 * which] = ph;
+        qA[s][2 * which + 1] = pl8;
+      }
+    isum += __shfl_xor_sync(0xffffffffu, isum, 1);
+    isum += __shfl_xor_sync(0xffffffffu, isum, 2);
+    qs = sq * float(isum);
+  }
+  // QK mean A fragments of every piece, lane-major: [quarter qd][mt][ks][lane]; q rows 16mt + r (+8),
+  // k-step ks slots (2c, 2c+1 | 2c+8, 2c+9) <-> d = 32qd + 16ks + 4c + (0, 1 | 2, 3)
+  for (int f = warp; f < 4 * MT * 2; f += NW) {
+    const int qd2 = f / (MT * 2), mt = (f >> 1) % MT, ks = f & 1;
+    const __half* r0 = q16 + (16 * mt + r) * D + 32 * qd2 + 16 * ks + 4 * c;
+    const __half* r1 = r0 + 8 * D;
+    sh<uint4>(smem, pl.off_qa + f * 512 + lane * 16) =
+        make_uint4(*reinterpret_cast<const uint32_t*>(r0), *reinterpret_cast<const uint32_t*>(r1),
+                   *reinterpret_cast<const uint32_t*>(r0 + 2), *reinterpret_cast<const uint32_t*>(r1 + 2));
+  }
+  fence_proxy_async();  // the q staging lives in stage 1, which TMA refills after the first barrier
+  __syncthreads();
+
+  // ---------------------------------------------------------------- per-thread shared offsets
+  const int qd = warp & 3, oct = warp >> 2;
+  const int oX0 = qd * BAND + swz(8 * oct + r, 16 * c);  // kmean, stage-relative
+  const int oX1 = qd * BAND + swz(8 * oct + r, 64 + 16 * c);
+  const int oQA = pl.off_qa + qd * (MT * 2 * 512) + lane * 16;
+  const int oSW = pl.off_sm + qd * PLANE + (r * TT + ((8 * oct + 2 * c) ^ (8 * ((r >> 1) & 1)))) * 4;
+  const int vc = tid >> 6, vdp = tid & 63;  // vmean split: pairs vc, vc + 4; d = 2vdp, 2vdp + 1
+  const int oV0 = pl.mean_bytes + (vdp >> 4) * BAND + swz(2 * vc, (vdp & 15) * 8);  // token 2vc; +8 at +1024
+  const int oV1 = pl.mean_bytes + (vdp >> 4) * BAND + swz(2 * vc + 1, (vdp & 15) * 8);
+  const int oVW = pl.off_vm + (74 * vc + 9 * (vdp >> 3) + (vdp & 7)) * 16;
+  const int hbK = h * GB + c * (GB / 4);
+  const int oK = 2 * pl.mean_bytes + (hbK >> 7) * BAND + swz(r, hbK & 127);  // row r; row r + 8 at +1024
+  const int oK2 = 2 * pl.mean_bytes + (hbK >> 7) * BAND + swz(r, (hbK & 127) + 16);  // 8-bit second half
+  const bool live = r < G;
+  const int qrow = h * G + (live ? r : 0);
+  const int qx = 8 * ((qrow >> 1) & 1);
+  const int oS0 = pl.off_sm + (qrow * TT + ((2 * c) ^ qx)) * 4, oS1 = pl.off_sm + (qrow * TT + ((8 + 2 * c) ^ qx)) * 4;
+  const int oM = 2 * pl.side_bytes + 2 * c * pl.trow + 8 * h;  // kmeta of token 2c; vmeta at + meta_bytes
+  const int oVR = pl.off_vm + (74 * c + 9 * r) * 16;           // split vmean chunk (c, r, 0)
+  const int hbV = h * GB + 2 * r * BITS;
+  const int oC0 = 2 * pl.mean_bytes + pl.codes_bytes + (hbV >> 7) * BAND + swz(2 * c, hbV & 127);  // token 2c
+  const int oC1 = 2 * pl.mean_bytes + pl.codes_bytes + (hbV >> 7) * BAND + swz(2 * c + 1, hbV & 127);
+
+  float oc[8][4];  // O_h^T: rows d (16r + 2mt, +1), cols n = 2c, 2c+1 (q heads h*G + n)
+#pragma unroll
+  for (int i = 0; i < 8; ++i) oc[i][0] = oc[i][1] = oc[i][2] = oc[i][3] = 0.f;
+  const float NEG_INF = -__int_as_float(0x7f800000);
+  // rows r >= G carry the mean-term logits of q head h*G (finite); their columns are never stored
+  float m_run = NEG_INF, l_run = 0.f, bp_run = 0.f, sp_run = 0.f;
+  const float sl2 = a.scale * 1.4426950408889634f;
+
+  auto body = [&](auto slot_c, int it) {
+    constexpr int SL = decltype(slot_c)::value;
+    constexpr int ST = SL * SB;  // this tile's stage
+    const int t0 = t_begin + it * TT;
+    const int nv = min(TT, t_end - t0);
+    const bool tail = nv < TT;
+    mbar_wait(&full[SL], (it >> 1) & 1);
+
+    // ------------------------------------------------------------ X1: QK mean piece -> S_mean plane qd
+    {
+      float acc[MT][4];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const float4 x = sh<float4>(smem, ST + (ks ? oX1 : oX0));
+        uint32_t h0, l0, h1, l1;
+        split_h2(x.x, x.y, h0, l0);
+        split_h2(x.z, x.w, h1, l1);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const uint4 f = sh<uint4>(smem, oQA + (mt * 2 + ks) * 512);
+          const uint32_t af[4] = {f.x, f.y, f.z, f.w};
+          mma(acc[mt], af, h0, h1);
+          mma(acc[mt], af, l0, l1);
+        }
+      }
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          sh<float2>(smem, oSW + SL * pl.sm_slot + (16 * mt + 8 * e) * TT * 4) = make_float2(acc[mt][2 * e], acc[mt][2 * e + 1]);
+    }
+    // ------------------------------------------------------------ X2: vmean -> f16 hi / lo fragment chunks
+    {  // words (pair vc | vc + 4, d = 2vdp | 2vdp + 1); a word holds tokens (2p, 2p + 1)
+      const float2 x0 = sh<float2>(smem, ST + oV0), x1 = sh<float2>(smem, ST + oV1);
+      const float2 x8 = sh<float2>(smem, ST + oV0 + 1024), x9 = sh<float2>(smem, ST + oV1 + 1024);
+      uint4 hi, lo;
+      split_h2(x0.x, x1.x, hi.x, lo.x);
+      split_h2(x0.y, x1.y, hi.y, lo.y);
+      split_h2(x8.x, x9.x, hi.z, lo.z);
+      split_h2(x8.y, x9.y, hi.w, lo.w);
+      if (tail) {  // rows past the sequence may hold anything: zero their halves
+        const uint32_t k0 = (2 * vc < nv ? 0x0000FFFFu : 0u) | (2 * vc + 1 < nv ? 0xFFFF0000u : 0u);
+        const uint32_t k8 = (2 * vc + 8 < nv ? 0x0000FFFFu : 0u) | (2 * vc + 9 < nv ? 0xFFFF0000u : 0u);
+        hi.x &= k0; hi.y &= k0; hi.z &= k8; hi.w &= k8;
+        lo.x &= k0; lo.y &= k0; lo.z &= k8; lo.w &= k8;
+      }
+      sh<uint4>(smem, oVW + SL * 2 * VMP) = hi;
+      sh<uint4>(smem, oVW + SL * 2 * VMP + VMP) = lo;
+    }
+    __syncthreads();  // ---- the barrier: S_mean / split vmean complete; tile it-1 fully consumed
+    if (tid == 0 && it + 1 < ntiles) {
+      issue(1 - SL);
+      if (it + 2 < ntiles) cur_page = pt[cur_pg];  // a late page-table load here would stall the next barrier
+    }
+
+    // ------------------------------------------------------------ c: QK code term (q on M) + logits
+    float x[2][2];  // logits (log2 units) of q head h*G + r for tokens 8nt + 2c + e
+    {
+      constexpr int NWD = BITS == 8 ? 8 : (BITS == 4 ? 4 : 2);  // code words per row segment
+      uint32_t wa[NWD], wb[NWD];
+      if (BITS == 4) {
+        const uint4 p0 = sh<uint4>(smem, ST + oK), p1 = sh<uint4>(smem, ST + oK + 1024);
+        wa[0] = p0.x; wa[1 % NWD] = p0.y; wa[2 % NWD] = p0.z; wa[3 % NWD] = p0.w;
+        wb[0] = p1.x; wb[1 % NWD] = p1.y; wb[2 % NWD] = p1.z; wb[3 % NWD] = p1.w;
+      } else if (BITS == 2) {
+        const uint2 p0 = sh<uint2>(smem, ST + oK), p1 = sh<uint2>(smem, ST + oK + 1024);
+        wa[0] = p0.x; wa[1] = p0.y;
+        wb[0] = p1.x; wb[1] = p1.y;
+      } else {
+        const uint4 p0 = sh<uint4>(smem, ST + oK), p1 = sh<uint4>(smem, ST + oK + 1024);
+        const uint4 p2 = sh<uint4>(smem, ST + oK2), p3 = sh<uint4>(smem, ST + oK2 + 1024);
+        wa[0] = p0.x; wa[1 % NWD] = p0.y; wa[2 % NWD] = p0.z; wa[3 % NWD] = p0.w;
+        wa[4 % NWD] = p2.x; wa[5 % NWD] = p2.y; wa[6 % NWD] = p2.z; wa[7 % NWD] = p2.w;
+        wb[0] = p1.x; wb[1 % NWD] = p1.y; wb[2 % NWD] = p1.z; wb[3 % NWD] = p1.w;
+        wb[4 % NWD] = p3.x; wb[5 % NWD] = p3.y; wb[6 % NWD] = p3.z; wb[7 % NWD] = p3.w;
+      }
+      // rows r: hi . code, rows r + 8: lo . code; q_fx . code / sq = 256 hi + lo (exact, |.| < 2^31)
+      int acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        imma_su(acc[0], qA[s], qk_quad<BITS>(wa, s, 0), qk_quad<BITS>(wa, s, 1));
+        imma_su(acc[1], qA[s], qk_quad<BITS>(wb, s, 0), qk_quad<BITS>(wb, s, 1));
+      }
+      // S_mean of (q row, tokens 2c, 2c+1 | 8+2c, 9+2c): the 4 d-quarter planes
+      float sm[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 v0 = sh<float2>(smem, oS0 + SL * pl.sm_slot + k * PLANE);
+        const float2 v1 = sh<float2>(smem, oS1 + SL * pl.sm_slot + k * PLANE);
+        sm[0][0] += v0.x;
+        sm[0][1] += v0.y;
+        sm[1][0] += v1.x;
+        sm[1][1] += v1.y;
+      }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const float2 km = sh<float2>(smem, ST + oM + (8 * nt + e) * pl.trow);  // (scale, min)
+          const float cs = float(acc[nt][e] * 256 + acc[nt][2 + e]);
+          x[nt][e] = (sm[nt][e] - fmaf(km.x * sq, cs, km.y * qs)) * sl2;
+        }
+    }
+    // ------------------------------------------------------------ d: online softmax (registers)
+    uint32_t bp0, bp1, bq0, bq1;  // B fragments (k = tokens 2c, 2c+1 | 8+2c, 9+2c; n = q head r): P, P'
+    {
+      if (tail) {
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            if (8 * nt + 2 * c + e >= nv) x[nt][e] = NEG_INF;
+      }
+      float tmax = fmaxf(fmaxf(x[0][0], x[0][1]), fmaxf(x[1][0], x[1][1]));
+      // Lazy rescaling: the reference max only moves when a logit exceeds it by more than 2^LAZY
+      // (p <= 256 stays exact enough in f16/f32), so most tiles skip the reduction and the O rescale.
+      constexpr float LAZY = 8.f;
+      float corr = 1.f;
+      const bool resc = __any_sync(0xffffffffu, tmax > m_run + LAZY);
+      if (resc) {
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+        const float m_new = fmaxf(m_run, tmax);  // finite: every tile has a valid token
+        corr = ex2(m_run - m_new);
+        m_run = m_new;
+      }
+      float p[2][2], pp[2][2], lsum = 0.f, bsum = 0.f;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const float2 vm = sh<float2>(smem, ST + oM + pl.meta_bytes + (8 * nt + e) * pl.trow);  // (scale, min)
+          const float pe = ex2(x[nt][e] - m_run);
+          p[nt][e] = pe;
+          lsum += pe;
+          if (tail && 8 * nt + 2 * c + e >= nv) {  // rows past the sequence may hold anything
+            pp[nt][e] = 0.f;
+          } else {
+            pp[nt][e] = -pe * vm.x;
+            bsum = fmaf(pe, vm.y, bsum);
+          }
+        }
+      bp0 = pack_h2(p[0][0], p[0][1]);
+      bp1 = pack_h2(p[1][0], p[1][1]);
+      bq0 = pack_h2(pp[0][0], pp[0][1]);
+      bq1 = pack_h2(pp[1][0], pp[1][1]);
+      float ssum;
+      {  // Σp' of exactly the f16 values the PV code MMA sees (the bias correction)
+        const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&bq0));
+        const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&bq1));
+        ssum = (f0.x + f0.y) + (f1.x + f1.y);
+      }
+      l_run = fmaf(l_run, corr, lsum);
+      bp_run = fmaf(bp_run, corr, bsum);
+      sp_run = fmaf(sp_run, corr, ssum);
+      if (resc) {  // columns n = 2c, 2c+1 of oc belong to the softmax rows of lanes 4n
+        const float c0 = __shfl_sync(0xffffffffu, corr, 8 * c), c1 = __shfl_sync(0xffffffffu, corr, 8 * c + 4);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          oc[i][0] *= c0;
+          oc[i][1] *= c1;
+          oc[i][2] *= c0;
+          oc[i][3] *= c1;
+        }
+      }
+    }
+    // ------------------------------------------------------------ e: PV (d on M): vmean hi, lo (P) + codes (P')
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        const uint4 w = sh<uint4>(smem, oVR + SL * 2 * VMP + part * VMP + 16 * mt);
+        const uint32_t af[4] = {w.x, w.y, w.z, w.w};
+        mma(oc[mt], af, bp0, bp1);
+      }
+    if (BITS == 4) {
+      const uint2 w0 = sh<uint2>(smem, ST + oC0), w1 = sh<uint2>(smem, ST + oC1);
+      const uint2 w2 = sh<uint2>(smem, ST + oC0 + 1024), w3 = sh<uint2>(smem, ST + oC1 + 1024);
+#pragma unroll
+      for (int wi = 0; wi < 2; ++wi) {
+        const uint32_t xa = wi ? w0.y : w0.x, xb = wi ? w1.y : w1.x;
+        const uint32_t xc = wi ? w2.y : w2.x, xd = wi ? w3.y : w3.x;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {  // bytes 2hh, 2hh+1 of the word: d = 16r + 8wi + 4hh + (0..3)
+          const uint32_t sel = hh ? 0x7632u : 0x5410u;
+          const uint32_t u = prmt(xa, xb, sel), v = prmt(xc, xd, sel);
+          uint32_t af[4];
+          af[0] = nib4(u << 4);
+          af[1] = nib4(u);
+          af[2] = nib4(v << 4);
+          af[3] = nib4(v);
+          mma(oc[4 * wi + 2 * hh], af, bq0, bq1);
+          af[0] = nib4(u >> 4);
+          af[1] = nib4(u >> 8);
+          af[2] = nib4(v >> 4);
+          af[3] = nib4(v >> 8);
+          mma(oc[4 * wi + 2 * hh + 1], af, bq0, bq1);
+        }
+      }
+    } else if (BITS == 2) {
+      const uint32_t xa = sh<uint32_t>(smem, ST + oC0), xb = sh<uint32_t>(smem, ST + oC1);
+      const uint32_t xc = sh<uint32_t>(smem, ST + oC0 + 1024), xd = sh<uint32_t>(smem, ST + oC1 + 1024);
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {  // bytes 2hh, 2hh+1: d = 16r + 8hh + (0..7), crumb k at bit 2k
+        const uint32_t sel = hh ? 0x7632u : 0x5410u;
+        const uint32_t u = prmt(xa, xb, sel), v = prmt(xc, xd, sel);
+        const uint32_t ul = u << 4, vl = v << 4, uh = u >> 6, vh = v >> 6;
+        uint32_t af[4];
+        af[0] = crumb<4>(ul); af[1] = crumb<6>(ul); af[2] = crumb<4>(vl); af[3] = crumb<6>(vl);  // +0, +1
+        mma(oc[4 * hh + 0], af, bq0, bq1);
+        af[0] = crumb<4>(u); af[1] = crumb<6>(u); af[2] = crumb<4>(v); af[3] = crumb<6>(v);      // +2, +3
+        mma(oc[4 * hh + 1], af, bq0, bq1);
+        af[0] = crumb<8>(u); af[1] = crumb<4>(uh); af[2] = crumb<8>(v); af[3] = crumb<4>(vh);    // +4, +5
+        mma(oc[4 * hh + 2], af, bq0, bq1);
+        af[0] = crumb<6>(uh); af[1] = crumb<8>(uh); af[2] = crumb<6>(vh); af[3] = crumb<8>(vh);  // +6, +7
+        mma(oc[4 * hh + 3], af, bq0, bq1);
+      }
+    } else {
+      const uint4 xa = sh<uint4>(smem, ST + oC0), xb = sh<uint4>(smem, ST + oC1);
+      const uint4 xc = sh<uint4>(smem, ST + oC0 + 1024), xd = sh<uint4>(smem, ST + oC1 + 1024);
+      const uint32_t A[4] = {xa.x, xa.y, xa.z, xa.w}, B[4] = {xb.x, xb.y, xb.z, xb.w};
+      const uint32_t Cc[4] = {xc.x, xc.y, xc.z, xc.w}, Dd[4] = {xd.x, xd.y, xd.z, xd.w};
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {  // d = 16r + 2mt (+1): bytes j, j+1 (j = 2(mt&1)) of word mt/2
+        const uint32_t sel = (mt & 1) ? 0x7632u : 0x5410u;
+        const uint32_t u = prmt(A[mt >> 1], B[mt >> 1], sel), v = prmt(Cc[mt >> 1], Dd[mt >> 1], sel);
+        uint32_t af[4];
+        af[0] = lop_and_or(u, 0x00FF00FFu, 0x64006400u);  // 1024 + code
+        af[1] = lop_and_or(u >> 8, 0x00FF00FFu, 0x64006400u);
+        af[2] = lop_and_or(v, 0x00FF00FFu, 0x64006400u);
+        af[3] = lop_and_or(v >> 8, 0x00FF00FFu, 0x64006400u);
+        mma(oc[mt], af, bq0, bq1);
+      }
+    }
+  };
+  for (int it = 0; it < ntiles; it += 2) {
+    body(std::integral_constant<int, 0>{}, it);
+    if (it + 1 < ntiles) body(std::integral_constant<int, 1>{}, it + 1);
+  }
+
+  // ------------------------------------------------------------------ epilogue
+  // per q head: l, Σp·vmin and Σp' over the row's four c lanes
+#pragma unroll
+  for (int o = 1; o <= 2; o <<= 1) {
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, o);
+    bp_run += __shfl_xor_sync(0xffffffffu, bp_run, o);
+    sp_run += __shfl_xor_sync(0xffffffffu, sp_run, o);
+  }
+  const float sp0 = __shfl_sync(0xffffffffu, sp_run, 8 * c), sp1 = __shfl_sync(0xffffffffu, sp_run, 8 * c + 4);
+  __syncthreads();  // every tile consumed: the stages and the split vmean are idle
+  if (live && c == 0) {
+    red[qrow] = l_run;
+    red[HQ + qrow] = bp_run;
+    red[2 * HQ + qrow] = m_run;
+  }
+  constexpr int PR = D + 4;  // park row (padded)
+  float* park = reinterpret_cast<float*>(smem);  // [HQ][PR]
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int n = 2 * c + e;
+    if (n < G) {
+      const float sp = e ? sp1 : sp0;
+      float* row = park + (h * G + n) * PR + 16 * r;
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        row[2 * mt] = oc[mt][e] - pv_bias<BITS>(mt, 0) * sp;
+        row[2 * mt + 1] = oc[mt][2 + e] - pv_bias<BITS>(mt, 1) * sp;
+      }
+    }
+  }
+  __syncthreads();
+  // write the split slot (natural-log LSE units for K3)
+  const float LN2 = 0.6931471805599453f;
+  for (int i = tid; i < HQ * D; i += NTHR) {
+    const int g = i / D, d = i - g * D;
+    const float l = red[g], bp = red[HQ + g], m = red[2 * HQ + g];
+    const int64_t slot = (int64_t(b) * HQ + g) * a.slots + split;
+    a.part_acc[slot * D + d] = l > 0.f ? park[g * PR + d] - bp : 0.f;
+    if (d == 0) {
+      a.part_ml[slot * 2] = l > 0.f ? m * LN2 : NEG_INF;
+      a.part_ml[slot * 2 + 1] = l;
+    }
+  }
+}
+
+}  // namespace v8
+
+bool v8_supported(const tada_page_layout& L, int Hq) {
+  if (L.head_dim != 128 || L.heads != 8 || !(L.bits == 2 || L.bits == 4 || L.bits == 8)) return false;
+  if (!(Hq == 8 || Hq == 16 || Hq == 32)) return false;
+  if (L.page_tokens % v8::TT != 0) return false;
+  return v8::make_plan(L.group_bytes, Hq).ok;
+}
+
+template <int BITS, int HQ>
+static int launch_v8_t(const AttnArgs& a, int batch, cudaStream_t st) {
+  constexpr v8::Plan pl = v8::make_plan(BITS * 128 / 8, HQ);
+  if constexpr (!pl.ok) {
+    return fail(TADA_ERR_CONFIG, "decode_attn_v8: geometry does not fit two stages");
+  } else {
+    auto kern = v8::attn_v8_kernel<BITS, HQ>;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.total);
+      if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string("attn_v8 smem: ") + cudaGetErrorString(e));
+      attr_set = true;
+    }
+    TmaMaps maps;
+    const int rc = get_tma_maps(a, &maps, v8::TT);
+    if (rc != TADA_OK) return rc;
+    kern<<<dim3(a.splits, batch), v8::NTHR, pl.total, st>>>(a, maps);
+    return check_launch("decode_attn_v8");
+  }
+}
+
+template <int BITS>
+static int launch_v8_b(const AttnArgs& a, int batch, cudaStream_t st) {
+  switch (a.Hq) {
+    case 8: return launch_v8_t<BITS, 8>(a, batch, st);
+    case 16: return launch_v8_t<BITS, 16>(a, batch, st);
+    default: return launch_v8_t<BITS, 32>(a, batch, st);
+  }
+}
+
+int launch_v8(const AttnArgs& a, int batch, cudaStream_t st) {
+  switch (a.L.bits) {
+    case 2: return launch_v8_b<2>(a, batch, st);
+    case 4: return launch_v8_b<4>(a, batch, st);
+    default: return launch_v8_b<8>(a, batch, st);
+  }
+}
+
+}  // namespace tada
