@@ -77,6 +77,13 @@ def attn_alg_bytes(bits: int, batch: int, ctx_c: int, ctx_r: int) -> int:
     return batch * (2 * ctx_c * tok_bytes(bits) + 2 * ctx_r * H * D * 2 + 2 * HQ * D * 2)
 
 
+def attn_kernel_name(bits: int, hq: int) -> str:
+    """The tensor-core decode kernel tada_decode_attn dispatches for this geometry (tada_attn.cu)."""
+    if bits in (2, 4) and hq in (8, 16, 32):
+        return f"attn_v8_kernel<{bits},{hq}>"
+    return f"attn_fast_kernel<{bits},{hq},{16 if bits != 8 else 32}>"
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -391,7 +398,7 @@ def run_ours(args):
             "hbm_gbs": step_bytes / (ms_per_step / 1e3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic,
-                         "kernel": f"decode attention K2+K3 (tada_decode_attn), {dom}-bit layers: attn_fast_kernel<{dom},32>"
+                         "kernel": f"decode attention K2+K3 (tada_decode_attn), {dom}-bit layers: {attn_kernel_name(dom, HQ)}"
                                    f" + combine_residual_kernel",
                          "alg_bytes_per_launch": attn_alg_bytes(dom, B, T, 1), "peak_source": peak_kind,
                          "frac_of_8tbs_spec": achieved / 8000.0, "per_width": per_width,

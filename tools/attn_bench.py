@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--splits", type=int, default=0)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--layers", type=int, default=4, help="distinct layer pools cycled (defeats L2)")
+    ap.add_argument("--reps", type=int, default=5, help="timed repetitions; the median is reported")
     args = ap.parse_args()
     B, T, H, D = args.batch, args.tokens, args.heads, 128
     store = tk.PagedKVCache(args.layers, H, D, [args.bits] * args.layers, 128, batch=B, page_tokens=64,
@@ -43,18 +44,22 @@ def main():
     for i in range(3):
         store.attend(i % args.layers, q, out=out, num_splits=splits, mode=args.mode)
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for i in range(args.iters):
-        store.attend(i % args.layers, q, out=out, num_splits=splits, mode=args.mode)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.iters
+    times = []
+    for _ in range(args.reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(args.iters):
+            store.attend(i % args.layers, q, out=out, num_splits=splits, mode=args.mode)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / args.iters)
+    times.sort()
+    ms = times[len(times) // 2]
     c, r = store.lengths(0)
     tokb = 4 * D + H * (D * args.bits // 8) + 8 * H
     alg = B * (2 * c * tokb + 2 * r * H * D * 2 + 2 * args.hq * D * 2)
     print(json.dumps({"bits": args.bits, "batch": B, "tokens": c + r, "hq": args.hq, "mode": args.mode,
-                      "splits": splits, "ms": ms, "alg_GBps": alg / ms / 1e6}))
+                      "splits": splits, "ms": ms, "ms_min": times[0], "alg_GBps": alg / ms / 1e6}))
 
 
 if __name__ == "__main__":

@@ -25,7 +25,7 @@ if [[ $what == bench || $what == all ]]; then
   timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 fi
 if [[ $what == prof || $what == all ]]; then
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_fast -s 3 -c 1 \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:${PROF_KERNEL:-attn_v8} -s 3 -c 1 \
     -o gpurun_out/attn4 -f python tools/attn_bench.py --bits ${PROF_BITS:-4} --iters 2 > gpurun_out/prof.log 2>&1
   echo "prof rc=$?" >> gpurun_out/prof.log
 fi

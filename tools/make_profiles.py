@@ -28,12 +28,12 @@ def main():
     os.makedirs(PROF, exist_ok=True)
     rep = os.path.join(OUT, "attn4.ncu-rep")
     if os.path.exists(rep):
-        tiles = 16 * 32768 // 16  # 16-token tiles (attn_fast_kernel<4,32,16>)
+        tiles = 16 * 32768 // 16  # 16-token tiles of attn_v8_kernel<4,32>
         txt = run("tools/ncu_summary.py", rep, str(tiles))
         txt += "\n--- per source line (top 40 by instructions + stalls)\n"
-        txt += run("tools/ncu_lines.py", rep, "paper_2506_04642_b200/csrc/tada_attn_fast.cu", "40", str(tiles))
+        txt += run("tools/ncu_lines.py", rep, "paper_2506_04642_b200/csrc/tada_attn_v8.cu", "40", str(tiles))
         open(os.path.join(PROF, f"{tag}_attn4_ncu.txt"), "w").write(
-            "ncu --set full --clock-control none --import-source on -k regex:attn_fast -s 3 -c 1 "
+            "ncu --set full --clock-control none --import-source on -k regex:attn_v8 -s 3 -c 1 "
             "python tools/attn_bench.py --bits 4 (B=16, T=32768, Hq=32, H=8, D=128)\n\n" + txt)
         raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
         rows = list(csv.reader(io.StringIO(raw)))
@@ -45,7 +45,7 @@ def main():
             return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit[k]]
 
         traffic = nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum")
-        json.dump({"traffic_bytes_per_launch": traffic, "kernel": "attn_fast_kernel<4,32,16>",
+        json.dump({"traffic_bytes_per_launch": traffic, "kernel": "attn_v8_kernel<4,32>",
                    "shape": "B=16, T=32768 compressed, Hq=32, H=8, D=128, 4-bit",
                    "alg_bytes_per_launch": 16 * (32768 * 2 * (4 * 128 + 8 * 64 + 64) + 2 * 32 * 128 * 2),
                    "source": f"profiles/{tag}_attn4_ncu.txt"}, open(os.path.join(PROF, "attn_traffic.json"), "w"),
