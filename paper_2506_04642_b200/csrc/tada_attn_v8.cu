@@ -275,20 +275,25 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
       float acc[MT][4];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
+      uint32_t hb[2][2], lb[2][2];  // B fragments (hi, lo) of both k-steps
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks) {
         const float4 x = sh<float4>(smem, ST + (ks ? oX1 : oX0));
-        uint32_t h0, l0, h1, l1;
-        split_h2(x.x, x.y, h0, l0);
-        split_h2(x.z, x.w, h1, l1);
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          const uint4 f = sh<uint4>(smem, oQA + (mt * 2 + ks) * 512);
-          const uint32_t af[4] = {f.x, f.y, f.z, f.w};
-          mma(acc[mt], af, h0, h1);
-          mma(acc[mt], af, l0, l1);
-        }
+        split_h2(x.x, x.y, hb[ks][0], lb[ks][0]);
+        split_h2(x.z, x.w, hb[ks][1], lb[ks][1]);
       }
+      // 4 MT independent accumulation chains, interleaved so no MMA waits on the previous one
+#pragma unroll
+      for (int pass = 0; pass < 2; ++pass)
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            const uint4 f = sh<uint4>(smem, oQA + (mt * 2 + ks) * 512);
+            const uint32_t af[4] = {f.x, f.y, f.z, f.w};
+            if (pass == 0) mma(acc[mt], af, hb[ks][0], hb[ks][1]);
+            else mma(acc[mt], af, lb[ks][0], lb[ks][1]);
+          }
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -432,9 +437,9 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
     }
     // ------------------------------------------------------------ e: PV (d on M): vmean hi, lo (P) + codes (P')
 #pragma unroll
-    for (int mt = 0; mt < 8; ++mt)
+    for (int part = 0; part < 2; ++part)
 #pragma unroll
-      for (int part = 0; part < 2; ++part) {
+      for (int mt = 0; mt < 8; ++mt) {
         const uint4 w = sh<uint4>(smem, oVR + SL * 2 * VMP + part * VMP + 16 * mt);
         const uint32_t af[4] = {w.x, w.y, w.z, w.w};
         mma(oc[mt], af, bp0, bp1);
