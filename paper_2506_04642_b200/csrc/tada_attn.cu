@@ -212,16 +212,20 @@ __global__ void __launch_bounds__(kCombThreads) combine_residual_kernel(AttnArgs
   __syncthreads();
   const int64_t rbase = int64_t(b) * a.res_seq_stride;
   float mx = -__int_as_float(0x7f800000);
-  for (int t = tid; t < R; t += kCombThreads) {
+  // residual logits: one warp per token, lanes split d (4 each) and reduce by shuffles
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int t = warp; t < R; t += kCombThreads / 32) {
     const float* kr = a.res_k + ((rbase + t) * H + h) * D;
     float dot = 0.f;
-    for (int d = 0; d < D; d += 4) {  // the fast path has D % 4 == 0
+    for (int d = 4 * lane; d < D; d += 128) {  // the fast path has D % 4 == 0
       const float4 k4 = *reinterpret_cast<const float4*>(kr + d);
       const float4 q4 = *reinterpret_cast<const float4*>(qs + d);
       dot = __fmaf_rn(q4.w, k4.w, __fmaf_rn(q4.z, k4.z, __fmaf_rn(q4.y, k4.y, __fmaf_rn(q4.x, k4.x, dot))));
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
     const float sv = __fmul_rn(dot, a.scale);
-    pr[t] = sv;
+    if (lane == 0) pr[t] = sv;
     mx = fmaxf(mx, sv);
   }
   const float* ml = a.part_ml + (int64_t(b) * Hq + gq) * a.slots * 2;
@@ -243,21 +247,31 @@ __global__ void __launch_bounds__(kCombThreads) combine_residual_kernel(AttnArgs
   // output: thread = (half j, d); each half takes every other slot and residual token
   const int j = tid / D, d = tid - j * D;
   if (j < 2) {
+    // the partial slots live in L2 (written by K2 just before): issue a batch of loads, then the FMAs
+    constexpr int U = 8;
     const float* pa = a.part_acc + (int64_t(b) * Hq + gq) * a.slots * D + d;
     float acc0 = 0.f, acc1 = 0.f;
-    int s2 = j;
-    for (; s2 + 2 < S; s2 += 4) {
-      acc0 = fmaf(ws[s2], pa[int64_t(s2) * D], acc0);
-      acc1 = fmaf(ws[s2 + 2], pa[int64_t(s2 + 2) * D], acc1);
+    for (int s0 = j; s0 < S; s0 += 2 * U) {
+      float v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = s0 + 2 * u < S ? pa[int64_t(s0 + 2 * u) * D] : 0.f;
+#pragma unroll
+      for (int u = 0; u < U; u += 2) {
+        acc0 = fmaf(s0 + 2 * u < S ? ws[s0 + 2 * u] : 0.f, v[u], acc0);
+        acc1 = fmaf(s0 + 2 * u + 2 < S ? ws[s0 + 2 * u + 2] : 0.f, v[u + 1], acc1);
+      }
     }
-    for (; s2 < S; s2 += 2) acc0 = fmaf(ws[s2], pa[int64_t(s2) * D], acc0);
     const float* vr = a.res_v + (rbase * H + h) * D + d;
-    int t = j;
-    for (; t + 2 < R; t += 4) {
-      acc0 = fmaf(pr[t], vr[int64_t(t) * H * D], acc0);
-      acc1 = fmaf(pr[t + 2], vr[int64_t(t + 2) * H * D], acc1);
+    for (int t0 = j; t0 < R; t0 += 2 * U) {
+      float v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = t0 + 2 * u < R ? vr[int64_t(t0 + 2 * u) * H * D] : 0.f;
+#pragma unroll
+      for (int u = 0; u < U; u += 2) {
+        acc0 = fmaf(t0 + 2 * u < R ? pr[t0 + 2 * u] : 0.f, v[u], acc0);
+        acc1 = fmaf(t0 + 2 * u + 2 < R ? pr[t0 + 2 * u + 2] : 0.f, v[u + 1], acc1);
+      }
     }
-    for (; t < R; t += 2) acc0 = fmaf(pr[t], vr[int64_t(t) * H * D], acc0);
     part[j * D + d] = acc0 + acc1;
   }
   __syncthreads();
