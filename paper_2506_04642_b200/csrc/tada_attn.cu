@@ -7,6 +7,7 @@
 // reference's f32(f64 min + code * f64 scale) (SURVEY §8a "Dequant").
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <string>
 
 #include "tada_attn.cuh"
@@ -351,7 +352,8 @@ int32_t tada_decode_attn_plan_splits(const tada_page_layout* layout, int32_t num
                                      int64_t max_tokens) {
   if (!layout || num_q_heads <= 0) return 1;
   int per_sm = 1;
-  if (fast_supported(*layout, num_q_heads)) per_sm = fast_tile_tokens(*layout, num_q_heads) == 16 ? 2 : 1;
+  if (v8_supported(*layout, num_q_heads)) per_sm = 2;  // attn_v8_kernel: two CTAs per SM
+  else if (fast_supported(*layout, num_q_heads)) per_sm = fast_tile_tokens(*layout, num_q_heads) == 16 ? 2 : 1;
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   return plan_splits(int64_t(sms) * per_sm, batch, max_tokens);
@@ -398,6 +400,10 @@ static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool,
   a.out_dtype = out_dtype;
   a.q_dtype = q_dtype;
   a.lse_out = lse_out;
+  {
+    static const int diag = getenv("TADA_ATTN_DIAG") ? atoi(getenv("TADA_ATTN_DIAG")) : 0;
+    a.diag = diag;
+  }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int rc;
   if (fast) {

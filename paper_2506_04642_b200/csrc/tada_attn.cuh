@@ -27,6 +27,7 @@ struct AttnArgs {
   void* out;
   int out_dtype;
   int q_dtype;
+  int diag;  // diagnostics only (env TADA_ATTN_DIAG): 1 = TMA ring without compute, 2 = compute on one L2-resident page
   float* lse_out;  // optional [B][Hq]: natural-log sum-exp of the scaled logits (cross-rank merge)
 };
 

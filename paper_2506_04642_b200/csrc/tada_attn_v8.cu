@@ -1,25 +1,28 @@
-// K2-v8: split-K flash decoding over the compressed paged cache, sm_100a, ONE CTA barrier per tile.
+// K2-v8: split-K flash decoding over the compressed paged cache, sm_100a.
 //
 // Reference semantics: attend_streaming (pkg/src/tadakv/attention.py:103-151) with
 // K̂ = mean - (min + scale*code) (cache.py:193-200, quant.py:177-180), evaluated in the factored form
 //   q·k̂   = q·mean − min·Σq − scale·(q·code)
 //   Σ p·v̂ = p·vmean − Σ(p·vmin) + p'·vcode,      p' = −p·vscale
 // (SURVEY §7 hard part 2).  CTA = (split, sequence): 8 warps, warp h = KV head h, 16-token tiles, two
-// CTAs per SM, a two-stage TMA ring.  Per tile:
-//   X   (before the barrier, cooperative, every warp an equal share)
-//       - QK mean piece: S_mean[q][tok] for all q heads, one token octet x one d quarter per warp, from
-//         the f32 means as f16 hi + lo (mma.sync, f32 accumulate) -> 4 partial planes;
-//       - vmean split: f32 -> f16 hi / lo words of token pairs, [pair][d] (the PV mean A operand).
-//   --- barrier (the only one): S_mean / split vmean of this tile complete; every warp is done with
-//       the previous tile, whose stage is refilled by TMA right here.
-//   c   QK code term with q on M: IMMA m16n8k32, A = q_h as two s8 pieces of a 16-bit fixed point,
-//       B = the packed codes expanded to u8 in registers (exact integer products and sums).
-//   d   online softmax in registers (thread = q head r of the group x 4 tokens); P and P' = −p·vscale
-//       stay in registers as B operands.
-//   e   PV with d on M, ONE accumulator per warp: vmean hi·P + vmean lo·P + (bias + vcode)·P', the codes
-//       entering as exact f16 bias + code (no subtraction; bias·Σp' is removed once at the end).
-// Shared offsets are per-thread registers computed once; the loop is unrolled by two so the stage and
-// the double-buffer slot are compile-time immediates.
+// CTAs per SM, a 2-stage (4-bit) or 3-stage (2-bit) TMA ring.  Per tile, two CTA barriers:
+//   A   QK mean piece, cooperative: S_mean[q][tok] for all q heads, one token octet x one d quarter
+//       per warp, from the f32 means as f16 hi + lo (mma.sync, f32 accumulate) -> 4 partial planes.
+//   --- barrier 1: S_mean complete; the previous tile's P / split vmean are consumed.
+//   B   per warp (its KV head):
+//       - QK code term with q on M: IMMA m16n8k32, A = q_h as two s8 pieces of a 16-bit fixed point
+//         (hi in rows r, lo in rows r + 8), B = the packed codes expanded to u8 (exact integers);
+//       - online softmax in registers (thread = q head r x 4 tokens); P -> shared (f16) for C,
+//         P' = −p·vscale stays in registers;
+//       - PV code term with d on M: A = vcodes as exact f16 bias + code (bias·Σp' removed at the end);
+//       - its share of the vmean split: f32 -> f16 hi / lo rows (the B operand of C).
+//   --- barrier 2: P, corr and the split vmean complete; this tile's stage is free -> TMA refill
+//       (S tiles ahead).
+//   C   PV mean piece, cooperative: O_mean[q][16w..16w+15] = O_mean·corr + P · vmean (hi + lo).
+// Every shared access of the hot loop reads each byte once per CTA except the q-independent metas;
+// the shared-memory data pipe, not HBM, was the limit of the one-barrier variant (replicated vmean
+// reads).  Per-thread shared offsets are computed once; the loop is unrolled by S so the stage is an
+// immediate.
 #include <cuda_runtime.h>
 
 #include <string>
@@ -33,26 +36,23 @@ namespace v8 {
 using namespace mmaops;
 
 constexpr int D = 128, H = 8, TT = 16, NW = 8, NTHR = 256;
-constexpr int BAND = TT * 128;   // bytes of one 128-B-wide swizzled band of a tile region
-// Split vmean, one part (hi or lo): 16-B chunk (c, r, mt) = the PV mean A fragment of lane (r, c), m-tile mt:
-// words (pair c, d), (pair c, d+1), (pair c+4, d), (pair c+4, d+1) with d = 16r + 2mt, a word holding the
-// f16 of tokens (2p, 2p+1).  Chunk index 74c + 9r + mt: the padding makes every quarter-warp access
-// conflict-free ((2c + r + mt) mod 8 distinct).
-constexpr int VMP = 4 * 74 * 16;    // one part (hi or lo) of the split vmean
-constexpr int kBudget = 113 * 1024; // two CTAs per SM
+constexpr int BAND = TT * 128;       // bytes of one 128-B-wide swizzled band of a tile region
+constexpr int VMPART = TT * D * 2;   // one f16 part (hi or lo) of the split vmean: [16 tok][256 B]
+constexpr int kBudget = 113 * 1024;  // two CTAs per SM
 
 __host__ __device__ constexpr int up128(int x) { return (x + 127) / 128 * 128; }
 __host__ __device__ constexpr int up1k(int x) { return (x + 1023) / 1024 * 1024; }
 
 struct Plan {
-  int mean_bytes, codes_bytes, meta_bytes, side_bytes, stage_bytes, trow, sm_slot;
-  int off_vm, off_sm, off_qa, off_bar, total;
+  int mean_bytes, codes_bytes, meta_bytes, side_bytes, stage_bytes, stages, trow;
+  int off_vm, off_sm, off_p, off_corr, off_qa, off_bar, total;
   bool ok;
 };
 
-// [stage 0][stage 1] | VM [2 slots][hi, lo][VMP] | SM [2 slots][4 planes][MROWS][16] f32 |
-// QA [4 quarters][MT][2 k-steps][32 lanes] uint4 | mbarriers.  Prologue-only q staging and row maxima
-// live in stage 1; the epilogue's (l, Σp·vmin, m) table lives in the then idle VM region.
+// [stage 0 .. S-1] | VM [hi, lo][16 tok][256 B] | SM [4 planes][MROWS][16] f32 | P [MROWS][16] f16 |
+// corr [MROWS] | QA [4 quarters][MT][2 k-steps][32 lanes] uint4 | mbarriers.  The prologue's q staging
+// and row maxima live in the last stage; the epilogue parks [HQ][D + 4] f32 over the stages and keeps
+// its (l, Σp·vmin, m) table in the then idle VM region.
 __host__ __device__ constexpr Plan make_plan(int gb, int HQ) {
   Plan p{};
   const int mrows = HQ >= 16 ? HQ : 16, mt = mrows / 16;
@@ -62,21 +62,31 @@ __host__ __device__ constexpr Plan make_plan(int gb, int HQ) {
   p.meta_bytes = TT * p.trow;
   p.side_bytes = p.mean_bytes + p.codes_bytes;
   p.stage_bytes = up1k(2 * p.side_bytes + 2 * p.meta_bytes);
-  p.sm_slot = 4 * mrows * TT * 4;
-  int off = 2 * p.stage_bytes;
+  const int tail = 2 * VMPART + 4 * mrows * TT * 4 + mrows * TT * 2 + up128(mrows * 4) + 4 * mt * 2 * 512 + 128;
+  p.stages = (3 * p.stage_bytes + tail <= kBudget) ? 3 : ((2 * p.stage_bytes + tail <= kBudget) ? 2 : 0);
+  int off = p.stages * p.stage_bytes;
   p.off_vm = off;
-  off += 2 * 2 * VMP;  // [slot][hi, lo]
+  off += 2 * VMPART;
   p.off_sm = off;
-  off += 2 * p.sm_slot;
+  off += 4 * mrows * TT * 4;
+  p.off_p = off;
+  off += mrows * TT * 2;
+  p.off_corr = off;
+  off += up128(mrows * 4);
   p.off_qa = off;
   off += 4 * mt * 2 * 512;
   p.off_bar = off;
   off += 128;
   p.total = off;
-  // the prologue stages q [MROWS][D] f16 in stage 1; the epilogue parks [HQ][D + 4] f32 over the stages
-  p.ok = off <= kBudget && p.stage_bytes >= mrows * (D * 2 + 4) && 2 * p.stage_bytes >= HQ * (D + 4) * 4 &&
-         2 * 2 * VMP >= 3 * HQ * 4;
+  p.ok = p.stages >= 2 && p.stage_bytes >= mrows * (D * 2 + 4) && p.stages * p.stage_bytes >= HQ * (D + 4) * 4 &&
+         2 * VMPART >= 3 * HQ * 4;
   return p;
+}
+
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
 }
 
 // PV code A operand (d on M).  Thread (r, c) owns d in [16r, 16r+16) of head h; m-tile mt holds
@@ -112,10 +122,11 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   extern __shared__ __align__(1024) uint8_t smem[];
   if (threadIdx.x == 0 && (su32(smem) & 1023u) != 0) __trap();
   constexpr int G = HQ / H;                   // q heads per KV head
-  constexpr int MT = HQ >= 16 ? HQ / 16 : 1;  // 16-row q tiles of the QK mean piece
+  constexpr int MT = HQ >= 16 ? HQ / 16 : 1;  // 16-row q tiles of the shared mean terms
   constexpr int MROWS = MT * 16;
   constexpr int GB = BITS * D / 8;            // code bytes per (token, head)
   constexpr Plan pl = make_plan(GB, HQ);
+  constexpr int S = pl.stages < 2 ? 2 : pl.stages;  // geometries with < 2 stages are never launched
   constexpr int SB = pl.stage_bytes;
   constexpr int PLANE = MROWS * TT * 4;
   const int P = a.L.page_tokens;
@@ -123,8 +134,8 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r = lane >> 2, c = lane & 3;
   const int h = warp;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + pl.off_bar);
-  float* qmax = reinterpret_cast<float*>(smem + SB + MROWS * D * 2);  // [MROWS], prologue only
-  float* red = reinterpret_cast<float*>(smem + pl.off_vm);           // [3][HQ] epilogue (l, Σp·vmin, m)
+  float* qmax = reinterpret_cast<float*>(smem + (S - 1) * SB + MROWS * D * 2);  // [MROWS], prologue only
+  float* red = reinterpret_cast<float*>(smem + pl.off_vm);                     // [3][HQ] epilogue (l, Σp·vmin, m)
 
   const int C = a.comp_len[b];
   int t_begin, t_end;
@@ -132,13 +143,15 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   const int ntiles = t_end > t_begin ? (t_end - t_begin + TT - 1) / TT : 0;
 
   if (tid == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // P rows of padding q heads stay zero; corr starts at 1
+  for (int i = tid; i < MROWS * TT / 2; i += NTHR) sh<uint32_t>(smem, pl.off_p + 4 * i) = 0u;
+  for (int i = tid; i < MROWS; i += NTHR) sh<float>(smem, pl.off_corr + 4 * i) = 1.f;
   __syncthreads();
 
-  // TMA producer (thread 0): tile `it` -> stage it & 1, three copies (means, codes, metas; both sides).
+  // TMA producer (thread 0): tile `it` -> stage it % S, three copies (means, codes, metas; both sides).
   // The (page, row) cursor advances by TT rows per tile (P is a multiple of TT): no divisions in the loop.
   const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
   constexpr uint32_t tx = 2u * uint32_t(pl.mean_bytes + pl.codes_bytes + TT * pl.trow);
@@ -158,15 +171,14 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   if (tid == 0) {
     for (int k = 0; k < 3; ++k)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[0][k])) : "memory");
-    if (ntiles > 0) {
+    for (int k = 0; k < S - 1 && k < ntiles; ++k) {
       cur_page = pt[cur_pg];
-      issue(0);
-      if (ntiles > 1) cur_page = pt[cur_pg];  // the page of tile 1, loaded a tile ahead
+      issue(k);
     }
   }
 
-  // ---------------------------------------------------------------- prologue: q -> f16, staged in stage 1
-  __half* q16 = reinterpret_cast<__half*>(smem + SB);  // [MROWS][D]
+  // ---------------------------------------------------------------- prologue: q -> f16, staged in the last stage
+  __half* q16 = reinterpret_cast<__half*>(smem + (S - 1) * SB);  // [MROWS][D]
   for (int g = warp; g < MROWS; g += NW) {
     float v[4] = {0.f, 0.f, 0.f, 0.f};
     if (g < HQ) {
@@ -228,8 +240,13 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
         make_uint4(*reinterpret_cast<const uint32_t*>(r0), *reinterpret_cast<const uint32_t*>(r1),
                    *reinterpret_cast<const uint32_t*>(r0 + 2), *reinterpret_cast<const uint32_t*>(r1 + 2));
   }
-  fence_proxy_async();  // the q staging lives in stage 1, which TMA refills after the first barrier
+  fence_proxy_async();  // the q staging lives in the last stage, which TMA fills right after this barrier
   __syncthreads();
+  if (tid == 0 && S - 1 < ntiles) {
+    cur_page = pt[cur_pg];
+    issue(S - 1);
+  }
+  if (tid == 0 && S < ntiles) cur_page = pt[cur_pg];  // the page of the next refill, loaded a tile ahead
 
   // ---------------------------------------------------------------- per-thread shared offsets
   const int qd = warp & 3, oct = warp >> 2;
@@ -237,10 +254,10 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   const int oX1 = qd * BAND + swz(8 * oct + r, 64 + 16 * c);
   const int oQA = pl.off_qa + qd * (MT * 2 * 512) + lane * 16;
   const int oSW = pl.off_sm + qd * PLANE + (r * TT + ((8 * oct + 2 * c) ^ (8 * ((r >> 1) & 1)))) * 4;
-  const int vc = tid >> 6, vdp = tid & 63;  // vmean split: pairs vc, vc + 4; d = 2vdp, 2vdp + 1
-  const int oV0 = pl.mean_bytes + (vdp >> 4) * BAND + swz(2 * vc, (vdp & 15) * 8);  // token 2vc; +8 at +1024
-  const int oV1 = pl.mean_bytes + (vdp >> 4) * BAND + swz(2 * vc + 1, (vdp & 15) * 8);
-  const int oVW = pl.off_vm + (74 * vc + 9 * (vdp >> 3) + (vdp & 7)) * 16;
+  const int vt = tid & 15, vu = tid >> 4;  // vmean split: token vt, d in [8vu, 8vu+8)
+  const int oV0 = pl.mean_bytes + (vu >> 2) * BAND + swz(vt, (vu & 3) * 32);  // vmean, stage-relative
+  const int oV1 = pl.mean_bytes + (vu >> 2) * BAND + swz(vt, (vu & 3) * 32 + 16);
+  const int oVW = pl.off_vm + vt * 256 + ((vu ^ (vt & 7)) << 4);
   const int hbK = h * GB + c * (GB / 4);
   const int oK = 2 * pl.mean_bytes + (hbK >> 7) * BAND + swz(r, hbK & 127);  // row r; row r + 8 at +1024
   const int oK2 = 2 * pl.mean_bytes + (hbK >> 7) * BAND + swz(r, (hbK & 127) + 16);  // 8-bit second half
@@ -249,28 +266,48 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   const int qx = 8 * ((qrow >> 1) & 1);
   const int oS0 = pl.off_sm + (qrow * TT + ((2 * c) ^ qx)) * 4, oS1 = pl.off_sm + (qrow * TT + ((8 + 2 * c) ^ qx)) * 4;
   const int oM = 2 * pl.side_bytes + 2 * c * pl.trow + 8 * h;  // kmeta of token 2c; vmeta at + meta_bytes
-  const int oVR = pl.off_vm + (74 * c + 9 * r) * 16;           // split vmean chunk (c, r, 0)
+  const int oPW = pl.off_p + qrow * 32 + 4 * c;                 // P row of q head qrow: chunk k at ((k ^ pch) << 4)
+  const int pch = (qrow >> 2) & 1;
   const int hbV = h * GB + 2 * r * BITS;
   const int oC0 = 2 * pl.mean_bytes + pl.codes_bytes + (hbV >> 7) * BAND + swz(2 * c, hbV & 127);  // token 2c
   const int oC1 = 2 * pl.mean_bytes + pl.codes_bytes + (hbV >> 7) * BAND + swz(2 * c + 1, hbV & 127);
+  // PV mean piece (warp = d slice 16w .. 16w+15): ldmatrix lane addresses
+  const uint32_t aPA = su32(smem + pl.off_p) + ((lane & 7) + 8 * ((lane >> 3) & 1)) * 32 +
+                       (((lane >> 4) ^ (((lane & 7) >> 2) & 1)) << 4);  // + 512 per q tile
+  const uint32_t aVB = su32(smem + pl.off_vm) + ((lane & 7) + 8 * ((lane >> 3) & 1)) * 256 +
+                       (((2 * warp + (lane >> 4)) ^ (lane & 7)) << 4);  // + VMPART for lo
 
-  float oc[8][4];  // O_h^T: rows d (16r + 2mt, +1), cols n = 2c, 2c+1 (q heads h*G + n)
+  float oc[8][4];      // PV code term O_h^T: rows d (16r + 2mt, +1), cols n = 2c, 2c+1 (q heads h*G + n)
+  float om[2][MT][4];  // PV mean piece: rows q (16mt + r, +8), cols d = 16w + 8j + 2c (+1)
 #pragma unroll
   for (int i = 0; i < 8; ++i) oc[i][0] = oc[i][1] = oc[i][2] = oc[i][3] = 0.f;
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) om[j][mt][0] = om[j][mt][1] = om[j][mt][2] = om[j][mt][3] = 0.f;
   const float NEG_INF = -__int_as_float(0x7f800000);
-  // rows r >= G carry the mean-term logits of q head h*G (finite); their columns are never stored
+  // rows r >= G carry the mean-term logits of q head h*G (finite); their P is never stored
   float m_run = NEG_INF, l_run = 0.f, bp_run = 0.f, sp_run = 0.f;
   const float sl2 = a.scale * 1.4426950408889634f;
 
-  auto body = [&](auto slot_c, int it) {
-    constexpr int SL = decltype(slot_c)::value;
-    constexpr int ST = SL * SB;  // this tile's stage
+  auto body = [&](auto stage_c, int it) {
+    constexpr int STG = decltype(stage_c)::value;
+    constexpr int ST = STG * SB;  // this tile's stage
     const int t0 = t_begin + it * TT;
     const int nv = min(TT, t_end - t0);
     const bool tail = nv < TT;
-    mbar_wait(&full[SL], (it >> 1) & 1);
+    mbar_wait(&full[STG], uint32_t(it / S) & 1u);
+    if (a.diag == 1) {  // diagnostics: pipeline only
+      __syncthreads();
+      __syncthreads();
+      if (tid == 0 && it + S < ntiles) {
+        issue(STG);
+        if (it + S + 1 < ntiles && a.diag != 2) cur_page = pt[cur_pg];
+      }
+      return;
+    }
 
-    // ------------------------------------------------------------ X1: QK mean piece -> S_mean plane qd
+    // ------------------------------------------------------------ A: QK mean piece -> S_mean plane qd
     {
       float acc[MT][4];
 #pragma unroll
@@ -298,31 +335,9 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int e = 0; e < 2; ++e)
-          sh<float2>(smem, oSW + SL * pl.sm_slot + (16 * mt + 8 * e) * TT * 4) = make_float2(acc[mt][2 * e], acc[mt][2 * e + 1]);
+          sh<float2>(smem, oSW + (16 * mt + 8 * e) * TT * 4) = make_float2(acc[mt][2 * e], acc[mt][2 * e + 1]);
     }
-    // ------------------------------------------------------------ X2: vmean -> f16 hi / lo fragment chunks
-    {  // words (pair vc | vc + 4, d = 2vdp | 2vdp + 1); a word holds tokens (2p, 2p + 1)
-      const float2 x0 = sh<float2>(smem, ST + oV0), x1 = sh<float2>(smem, ST + oV1);
-      const float2 x8 = sh<float2>(smem, ST + oV0 + 1024), x9 = sh<float2>(smem, ST + oV1 + 1024);
-      uint4 hi, lo;
-      split_h2(x0.x, x1.x, hi.x, lo.x);
-      split_h2(x0.y, x1.y, hi.y, lo.y);
-      split_h2(x8.x, x9.x, hi.z, lo.z);
-      split_h2(x8.y, x9.y, hi.w, lo.w);
-      if (tail) {  // rows past the sequence may hold anything: zero their halves
-        const uint32_t k0 = (2 * vc < nv ? 0x0000FFFFu : 0u) | (2 * vc + 1 < nv ? 0xFFFF0000u : 0u);
-        const uint32_t k8 = (2 * vc + 8 < nv ? 0x0000FFFFu : 0u) | (2 * vc + 9 < nv ? 0xFFFF0000u : 0u);
-        hi.x &= k0; hi.y &= k0; hi.z &= k8; hi.w &= k8;
-        lo.x &= k0; lo.y &= k0; lo.z &= k8; lo.w &= k8;
-      }
-      sh<uint4>(smem, oVW + SL * 2 * VMP) = hi;
-      sh<uint4>(smem, oVW + SL * 2 * VMP + VMP) = lo;
-    }
-    __syncthreads();  // ---- the barrier: S_mean / split vmean complete; tile it-1 fully consumed
-    if (tid == 0 && it + 1 < ntiles) {
-      issue(1 - SL);
-      if (it + 2 < ntiles) cur_page = pt[cur_pg];  // a late page-table load here would stall the next barrier
-    }
+    __syncthreads();  // ---- barrier 1: S_mean complete; the previous tile's P and split vmean are consumed
 
     // ------------------------------------------------------------ c: QK code term (q on M) + logits
     float x[2][2];  // logits (log2 units) of q head h*G + r for tokens 8nt + 2c + e
@@ -356,8 +371,8 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
       float sm[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const float2 v0 = sh<float2>(smem, oS0 + SL * pl.sm_slot + k * PLANE);
-        const float2 v1 = sh<float2>(smem, oS1 + SL * pl.sm_slot + k * PLANE);
+        const float2 v0 = sh<float2>(smem, oS0 + k * PLANE);
+        const float2 v1 = sh<float2>(smem, oS1 + k * PLANE);
         sm[0][0] += v0.x;
         sm[0][1] += v0.y;
         sm[1][0] += v1.x;
@@ -421,6 +436,11 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
         const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&bq1));
         ssum = (f0.x + f0.y) + (f1.x + f1.y);
       }
+      if (live) {  // P (f16) for the PV mean piece, corr for its rescale
+        sh<uint32_t>(smem, oPW + ((0 ^ pch) << 4)) = bp0;
+        sh<uint32_t>(smem, oPW + ((1 ^ pch) << 4)) = bp1;
+        if (c == 0) sh<float>(smem, pl.off_corr + 4 * qrow) = corr;
+      }
       l_run = fmaf(l_run, corr, lsum);
       bp_run = fmaf(bp_run, corr, bsum);
       sp_run = fmaf(sp_run, corr, ssum);
@@ -435,15 +455,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
         }
       }
     }
-    // ------------------------------------------------------------ e: PV (d on M): vmean hi, lo (P) + codes (P')
-#pragma unroll
-    for (int part = 0; part < 2; ++part)
-#pragma unroll
-      for (int mt = 0; mt < 8; ++mt) {
-        const uint4 w = sh<uint4>(smem, oVR + SL * 2 * VMP + part * VMP + 16 * mt);
-        const uint32_t af[4] = {w.x, w.y, w.z, w.w};
-        mma(oc[mt], af, bp0, bp1);
-      }
+    // ------------------------------------------------------------ PV code term (d on M)
     if (BITS == 4) {
       const uint2 w0 = sh<uint2>(smem, ST + oC0), w1 = sh<uint2>(smem, ST + oC1);
       const uint2 w2 = sh<uint2>(smem, ST + oC0 + 1024), w3 = sh<uint2>(smem, ST + oC1 + 1024);
@@ -503,10 +515,64 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
         mma(oc[mt], af, bq0, bq1);
       }
     }
+    // ------------------------------------------------------------ this warp's share of the vmean split
+    {  // token vt, d = 8vu .. 8vu+7 -> f16 hi / lo rows [tok][d] (16-B chunk vu at vu ^ (vt & 7))
+      const float4 x0 = sh<float4>(smem, ST + oV0), x1 = sh<float4>(smem, ST + oV1);
+      uint4 hi, lo;
+      split_h2(x0.x, x0.y, hi.x, lo.x);
+      split_h2(x0.z, x0.w, hi.y, lo.y);
+      split_h2(x1.x, x1.y, hi.z, lo.z);
+      split_h2(x1.z, x1.w, hi.w, lo.w);
+      if (tail && vt >= nv) hi = lo = make_uint4(0u, 0u, 0u, 0u);  // rows past the sequence may hold anything
+      sh<uint4>(smem, oVW) = hi;
+      sh<uint4>(smem, oVW + VMPART) = lo;
+    }
+    __syncthreads();  // ---- barrier 2: P, corr and the split vmean complete; this tile's stage is free
+    if (tid == 0 && it + S < ntiles) {
+      issue(STG);
+      // (a late page-table load here would stall the next barrier; diag 2 re-reads one L2-resident page)
+      if (it + S + 1 < ntiles && a.diag != 2) cur_page = pt[cur_pg];
+    }
+    // ------------------------------------------------------------ C: PV mean piece (d slice of this warp)
+    {
+      float cr[MT][2];
+      bool any = false;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        cr[mt][0] = sh<float>(smem, pl.off_corr + 4 * (16 * mt + r));
+        cr[mt][1] = sh<float>(smem, pl.off_corr + 4 * (16 * mt + r + 8));
+        any |= (cr[mt][0] != 1.f) || (cr[mt][1] != 1.f);
+      }
+      if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            om[j][mt][0] *= cr[mt][0];
+            om[j][mt][1] *= cr[mt][0];
+            om[j][mt][2] *= cr[mt][1];
+            om[j][mt][3] *= cr[mt][1];
+          }
+      }
+      uint32_t bh[4], bl[4];
+      ldsm_x4_t(bh, aVB);
+      ldsm_x4_t(bl, aVB + VMPART);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        uint32_t pa[4];
+        ldsm_x4(pa, aPA + mt * 512);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) mma(om[j][mt], pa, bh[2 * j], bh[2 * j + 1]);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) mma(om[j][mt], pa, bl[2 * j], bl[2 * j + 1]);
+      }
+    }
   };
-  for (int it = 0; it < ntiles; it += 2) {
+  for (int it = 0; it < ntiles; it += S) {
     body(std::integral_constant<int, 0>{}, it);
     if (it + 1 < ntiles) body(std::integral_constant<int, 1>{}, it + 1);
+    if constexpr (S == 3)
+      if (it + 2 < ntiles) body(std::integral_constant<int, 2>{}, it + 2);
   }
 
   // ------------------------------------------------------------------ epilogue
@@ -526,6 +592,20 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   }
   constexpr int PR = D + 4;  // park row (padded)
   float* park = reinterpret_cast<float*>(smem);  // [HQ][PR]
+  // 1) mean term: rows q = 16mt + r (+8), cols d = 16w + 8j + 2c (+1)
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int q = 16 * mt + r + 8 * e;
+      if (q < HQ)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          *reinterpret_cast<float2*>(park + q * PR + 16 * warp + 8 * j + 2 * c) =
+              make_float2(om[j][mt][2 * e], om[j][mt][2 * e + 1]);
+    }
+  __syncthreads();
+  // 2) code term minus its bias: rows d = 16r + 2mt (+1), cols n = 2c (+1)
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
     const int n = 2 * c + e;
@@ -534,13 +614,13 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
       float* row = park + (h * G + n) * PR + 16 * r;
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt) {
-        row[2 * mt] = oc[mt][e] - pv_bias<BITS>(mt, 0) * sp;
-        row[2 * mt + 1] = oc[mt][2 + e] - pv_bias<BITS>(mt, 1) * sp;
+        row[2 * mt] += oc[mt][e] - pv_bias<BITS>(mt, 0) * sp;
+        row[2 * mt + 1] += oc[mt][2 + e] - pv_bias<BITS>(mt, 1) * sp;
       }
     }
   }
   __syncthreads();
-  // write the split slot (natural-log LSE units for K3)
+  // 3) write the split slot (natural-log LSE units for K3)
   const float LN2 = 0.6931471805599453f;
   for (int i = tid; i < HQ * D; i += NTHR) {
     const int g = i / D, d = i - g * D;
@@ -558,7 +638,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
 
 bool v8_supported(const tada_page_layout& L, int Hq) {
   if (L.head_dim != 128 || L.heads != 8 || !(L.bits == 2 || L.bits == 4 || L.bits == 8)) return false;
-  if (!(Hq == 8 || Hq == 16 || Hq == 32)) return false;
+  if (!(Hq == 8 || Hq == 16 || Hq == 32 || Hq == 64)) return false;
   if (L.page_tokens % v8::TT != 0) return false;
   return v8::make_plan(L.group_bytes, Hq).ok;
 }
@@ -589,7 +669,8 @@ static int launch_v8_b(const AttnArgs& a, int batch, cudaStream_t st) {
   switch (a.Hq) {
     case 8: return launch_v8_t<BITS, 8>(a, batch, st);
     case 16: return launch_v8_t<BITS, 16>(a, batch, st);
-    default: return launch_v8_t<BITS, 32>(a, batch, st);
+    case 32: return launch_v8_t<BITS, 32>(a, batch, st);
+    default: return launch_v8_t<BITS, 64>(a, batch, st);
   }
 }
 
