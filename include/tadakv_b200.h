@@ -124,6 +124,29 @@ int tada_quant_append(const tada_page_layout* layout, uint8_t* pool, const void*
                       const int32_t* dst_start, int64_t dst_offset, int32_t* err_flag,
                       void* stream);
 
+/* ---------------------------------------------------------------- RoPE
+ * apply_rope / rotate_heads (tensor.py:63-105): rotate every adjacent (2j, 2j+1) pair of each
+ * [n_tok][heads][head_dim] row of token t by position positions[t]; out is f32. rope_cs is the
+ * host-built table [rope_rows][head_dim/2] of f32 (cos, sin) pairs, made exactly like tensor.py:84-88
+ * (f64 angles, np.cos/np.sin, cast to f32); the rotation is bit-identical to numpy's
+ * f32(e*c - o*s), f32(e*s + o*c). Positions outside [0, rope_rows) set bit 1 of err_flag. */
+int tada_apply_rope(const void* x, int32_t dtype, int64_t n_tok, int32_t heads, int32_t head_dim,
+                    const int32_t* positions, const float* rope_cs, int32_t rope_rows, float* out,
+                    int32_t* err_flag, void* stream);
+
+/* K1 with the keys rotated in registers before the mean: append_fused's key path
+ * (model.py:167-183 = rotate_heads + append_tokens) without the rotated keys ever reaching HBM.
+ * positions: device int32 [batch][pos_stride], token i of sequence b at positions[b * pos_stride + i].
+ * Values are appended as given. Needs heads 8, head_dim 128, bits 2/4/8 and 16-byte aligned rows,
+ * else TADA_ERR_CONFIG (compose tada_apply_rope + tada_quant_append). Bit-identical to that
+ * composition. */
+int tada_quant_append_rope(const tada_page_layout* layout, uint8_t* pool, const void* src_k,
+                           const void* src_v, int32_t dtype, int32_t batch, int64_t n_tok,
+                           int64_t src_seq_stride, const int32_t* page_table, int32_t pt_stride,
+                           const int32_t* dst_start, int64_t dst_offset, const int32_t* positions,
+                           int64_t pos_stride, const float* rope_cs, int32_t rope_rows,
+                           int32_t* err_flag, void* stream);
+
 /* Residual-buffer write (cache.py:174-175): token i of sequence b is copied (as f32)
  * to res[(b * res_seq_stride + pos[b] + pos_offset + i)][heads][head_dim]. */
 int tada_residual_write(float* res_k, float* res_v, int64_t res_seq_stride, int32_t heads,

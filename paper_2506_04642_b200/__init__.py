@@ -3,7 +3,8 @@
 Drop-in for the hot-path subset of the reference package ``tadakv``
 (pkg/src/tadakv/__init__.py:10-50): quantize / dequantize, mean centering,
 the compressed layer cache (append / reconstruct / TADAKV1), decode attention,
-and the per-layer PrecisionPlan.  Compute runs in libtadakv_b200.so
+the per-layer PrecisionPlan, and rotary keys fused into the append
+(apply_rope / rotate_heads / append_fused, tensor.py:63-105, model.py:167-183).  Compute runs in libtadakv_b200.so
 (hand-written sm_100a CUDA behind a C ABI, include/tadakv_b200.h); there is no
 CPU fallback.  ``PagedKVCache`` is the batched multi-layer production store.
 """
@@ -31,6 +32,7 @@ from .errors import (
     TadaError,
 )
 from .paged import PagedKVCache
+from .rope import append_fused, append_rope, apply_rope, rope_table, rotate_heads
 from .shard import ShardedKVCache, ShardPlan
 from .quant import (
     QuantizedDeviation,
@@ -52,7 +54,7 @@ __version__ = "0.1.0"
 __all__ = [
     "AttentionOutput", "BlockSpec", "BudgetInfeasibleError", "CapacityError", "CompressedLayerCache", "ConfigError",
     "DataError", "FormatError", "ModelConfig", "PagedKVCache", "PrecisionPlan", "QuantizedDeviation", "RopeParams",
-    "ShapeError", "ShardPlan", "ShardedKVCache", "StateError", "TadaError", "actual_bytes_per_token", "attend_naive", "attend_streaming",
+    "ShapeError", "ShardPlan", "append_fused", "append_rope", "apply_rope", "rope_table", "rotate_heads", "ShardedKVCache", "StateError", "TadaError", "actual_bytes_per_token", "attend_naive", "attend_streaming",
     "bytes_per_group", "concat_deviations", "dequantize_groups", "dequantize_tensor", "deserialize_cache",
     "direct_quantize_baseline", "empty_deviation", "kv_head_index", "mean_center", "memory_ratio", "pack_codes",
     "quantize_group", "quantize_tensor", "serialize_cache", "unpack_codes", "validate_bits", "__version__",

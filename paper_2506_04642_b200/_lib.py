@@ -60,6 +60,9 @@ SIGNATURES = {
     "tada_mean_center": (I32, [P, I32, I64, I32, I32, P, P, P, P]),
     "tada_quant_append": (I32, [C.POINTER(PageLayout), P, P, P, I32, I32, I64, I64, P, I32, P, I64, P, P]),
     "tada_residual_write": (I32, [P, P, I64, I32, I32, P, P, I32, I32, I64, I64, P, I32, P]),
+    "tada_apply_rope": (I32, [P, I32, I64, I32, I32, P, P, I32, P, P, P]),
+    "tada_quant_append_rope": (I32, [C.POINTER(PageLayout), P, P, P, I32, I32, I64, I64, P, I32, P, I64, P, I64, P,
+                                     I32, P, P]),
     "tada_residual_append": (I32, [P, P, I64, I32, I32, P, P, I32, I32, I64, I64, P, P]),
     "tada_lengths_add": (I32, [P, I32, I32, P]),
     "tada_gather_compressed": (I32, [C.POINTER(PageLayout), P, P, I64, I32, P, P, P, P, P]),

@@ -266,6 +266,11 @@ struct AppendArgs {
   int tt;  // tokens per tile
   int tiles_per_seq;
   bool vec_ok;
+  // fused RoPE of the keys: rope_cs[pos][j] = (cos, sin) f32, positions[b * pos_stride + i]
+  const float* rope_cs;
+  int rope_rows;
+  const int32_t* positions;
+  int64_t pos_stride;
 };
 
 template <typename T, int NCH>
@@ -464,7 +469,7 @@ __device__ __forceinline__ float redux_max(float v) {
 constexpr int K1_RING = 3;
 __device__ __forceinline__ uint32_t k1_su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
-template <typename T, int BITS, int MINB>
+template <typename T, int BITS, int MINB, bool ROPE>
 __global__ void __launch_bounds__(256, MINB) quant_append_fast_kernel(AppendArgs a, int tpw, int page_shift) {
   constexpr int H = 8, D = 128, GB = D * BITS / 8;
   constexpr uint32_t ROWB = H * D * sizeof(T);  // bytes of one token's rows
@@ -514,6 +519,22 @@ __global__ void __launch_bounds__(256, MINB) quant_append_fast_kernel(AppendArgs
     float x[H][4];
 #pragma unroll
     for (int h = 0; h < H; ++h) load4(src + h * D, x[h]);
+    if (ROPE && side == 0) {  // rotate the keys in registers (tensor.py:84-89); lane l holds pairs 2l, 2l+1
+      int p = a.positions[int64_t(b) * a.pos_stride + i];
+      if (p < 0 || p >= a.rope_rows) {  // the host validates positions; this guards device-side ones
+        if (lane == 0 && a.err) atomicOr(a.err, 2);
+        p = 0;
+      }
+      const float4 cs = *reinterpret_cast<const float4*>(a.rope_cs + int64_t(p) * D + 4 * lane);
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        const float e0 = x[h][0], o0 = x[h][1], e1 = x[h][2], o1 = x[h][3];
+        x[h][0] = __fsub_rn(__fmul_rn(e0, cs.x), __fmul_rn(o0, cs.y));
+        x[h][1] = __fadd_rn(__fmul_rn(e0, cs.y), __fmul_rn(o0, cs.x));
+        x[h][2] = __fsub_rn(__fmul_rn(e1, cs.z), __fmul_rn(o1, cs.w));
+        x[h][3] = __fadd_rn(__fmul_rn(e1, cs.w), __fmul_rn(o1, cs.z));
+      }
+    }
     // mean: f64 sequential head sum from +0.0, /H (exact for H = 8), RN to f32
     float mean[4];
     bool bad = false;
@@ -649,8 +670,12 @@ static int launch_append(const AppendArgs& a, int batch, size_t smem, cudaStream
     const int shift = (P & (P - 1)) == 0 ? __builtin_ctz(unsigned(P)) : -1;
     const size_t smem = size_t(8) * K1_RING * 8 * 128 * sizeof(T) + 8 * K1_RING * 8;
     // 3 CTAs per SM (80 registers, a few spills) measured faster than 2 (no spills): 3686 vs 3470 GB/s
-    auto k = a.L.bits == 2 ? quant_append_fast_kernel<T, 2, 3>
-                           : (a.L.bits == 4 ? quant_append_fast_kernel<T, 4, 3> : quant_append_fast_kernel<T, 8, 3>);
+    auto k = a.rope_cs ? (a.L.bits == 2 ? quant_append_fast_kernel<T, 2, 3, true>
+                                        : (a.L.bits == 4 ? quant_append_fast_kernel<T, 4, 3, true>
+                                                         : quant_append_fast_kernel<T, 8, 3, true>))
+                       : (a.L.bits == 2 ? quant_append_fast_kernel<T, 2, 3, false>
+                                        : (a.L.bits == 4 ? quant_append_fast_kernel<T, 4, 3, false>
+                                                         : quant_append_fast_kernel<T, 8, 3, false>));
     if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string("quant_append smem: ") + cudaGetErrorString(e));
@@ -658,6 +683,7 @@ static int launch_append(const AppendArgs& a, int batch, size_t smem, cudaStream
     k<<<grid, 256, smem, st>>>(a, tpw, shift);
     return check_launch("quant_append_fast");
   }
+  if (a.rope_cs) return fail(TADA_ERR_CONFIG, "fused RoPE append needs 16-byte aligned rows (compose apply_rope + quant_append)");
   if (D <= 128) return launch_append_n<T, 1>(a, batch, smem, st);
   if (D <= 256) return launch_append_n<T, 2>(a, batch, smem, st);
   if (D <= 512) return launch_append_n<T, 4>(a, batch, smem, st);
@@ -768,10 +794,13 @@ int tada_mean_center(const void* x, int32_t dtype, int64_t tokens, int32_t heads
   return check_launch("mean_center");
 }
 
-int tada_quant_append(const tada_page_layout* layout, uint8_t* pool, const void* src_k, const void* src_v,
-                      int32_t dtype, int32_t batch, int64_t n_tok, int64_t src_seq_stride, const int32_t* page_table,
-                      int32_t pt_stride, const int32_t* dst_start, int64_t dst_offset, int32_t* err_flag,
-                      void* stream) {
+}  // extern "C"
+
+static int quant_append_impl(const tada_page_layout* layout, uint8_t* pool, const void* src_k, const void* src_v,
+                             int32_t dtype, int32_t batch, int64_t n_tok, int64_t src_seq_stride,
+                             const int32_t* page_table, int32_t pt_stride, const int32_t* dst_start, int64_t dst_offset,
+                             int32_t* err_flag, const float* rope_cs, int32_t rope_rows, const int32_t* positions,
+                             int64_t pos_stride, void* stream) {
   if (!layout) return fail(TADA_ERR_CONFIG, "null layout");
   if (!valid_dtype(dtype)) return fail(TADA_ERR_CONFIG, "dtype must be f32 or bf16");
   if (batch < 0 || n_tok < 0 || src_seq_stride < n_tok) return fail(TADA_ERR_SHAPE, "bad batch/token geometry");
@@ -789,6 +818,10 @@ int tada_quant_append(const tada_page_layout* layout, uint8_t* pool, const void*
   a.dst_start = dst_start;
   a.dst_offset = dst_offset;
   a.err = err_flag;
+  a.rope_cs = rope_cs;
+  a.rope_rows = rope_rows;
+  a.positions = positions;
+  a.pos_stride = pos_stride;
   const int row = layout->heads * layout->head_dim;
   const size_t per_tok = size_t(row + layout->head_dim) * 4;
   int tt = int((32 * 1024) / per_tok);
@@ -804,6 +837,30 @@ int tada_quant_append(const tada_page_layout* layout, uint8_t* pool, const void*
              (layout->group_bytes % 4 == 0 || layout->bits <= 4);
   return dtype == TADA_F32 ? launch_append<float>(a, batch, smem, S(stream))
                            : launch_append<__nv_bfloat16>(a, batch, smem, S(stream));
+}
+
+extern "C" {
+
+int tada_quant_append(const tada_page_layout* layout, uint8_t* pool, const void* src_k, const void* src_v,
+                      int32_t dtype, int32_t batch, int64_t n_tok, int64_t src_seq_stride, const int32_t* page_table,
+                      int32_t pt_stride, const int32_t* dst_start, int64_t dst_offset, int32_t* err_flag,
+                      void* stream) {
+  return quant_append_impl(layout, pool, src_k, src_v, dtype, batch, n_tok, src_seq_stride, page_table, pt_stride,
+                           dst_start, dst_offset, err_flag, nullptr, 0, nullptr, 0, stream);
+}
+
+int tada_quant_append_rope(const tada_page_layout* layout, uint8_t* pool, const void* src_k, const void* src_v,
+                           int32_t dtype, int32_t batch, int64_t n_tok, int64_t src_seq_stride,
+                           const int32_t* page_table, int32_t pt_stride, const int32_t* dst_start, int64_t dst_offset,
+                           const int32_t* positions, int64_t pos_stride, const float* rope_cs, int32_t rope_rows,
+                           int32_t* err_flag, void* stream) {
+  if (!layout) return fail(TADA_ERR_CONFIG, "null layout");
+  if (!(layout->head_dim == 128 && layout->heads == 8 && (layout->bits == 2 || layout->bits == 4 || layout->bits == 8)))
+    return fail(TADA_ERR_CONFIG, "fused RoPE append needs heads 8, head_dim 128, bits 2/4/8 (compose apply_rope + "
+                                 "quant_append otherwise)");
+  if (!positions || !rope_cs || rope_rows <= 0 || pos_stride < n_tok) return fail(TADA_ERR_SHAPE, "bad rope arguments");
+  return quant_append_impl(layout, pool, src_k, src_v, dtype, batch, n_tok, src_seq_stride, page_table, pt_stride,
+                           dst_start, dst_offset, err_flag, rope_cs, rope_rows, positions, pos_stride, stream);
 }
 
 int tada_residual_write(float* res_k, float* res_v, int64_t res_seq_stride, int32_t heads, int32_t head_dim,

@@ -197,6 +197,81 @@ class PagedKVCache:
         self._add(self.comp_len, self.comp_host, layer, ncomp)
         self._add(self.res_len, self.res_host, layer, keep - r)
 
+    def _quant_append_rope(self, layer: int, src_k, src_v, dtype: int, n_tok: int, src_stride: int, dst_offset: int,
+                           pos: torch.Tensor, table: torch.Tensor):
+        call("tada_quant_append_rope", self._layout_ptr(layer), self.pools[layer].data_ptr(), src_k, src_v, dtype,
+             self.B, n_tok, src_stride, self.page_table.data_ptr(), self.page_table.shape[1],
+             self.comp_len[layer].data_ptr(), dst_offset, pos.data_ptr(), pos.shape[1], table.data_ptr(),
+             int(table.shape[0]), self.err.ptr, _dev.stream())
+
+    def _rotate(self, k: torch.Tensor, pos: torch.Tensor, table: torch.Tensor) -> torch.Tensor:
+        """[B, n, H, D] keys -> rotated f32 copy (tada_apply_rope), positions [B, n]."""
+        kc = k.contiguous()
+        out = torch.empty(kc.shape, dtype=torch.float32, device=self.dev)
+        n_rows = kc.shape[0] * kc.shape[1]
+        if n_rows:
+            call("tada_apply_rope", kc.data_ptr(), _dev.dtype_code(kc), n_rows, self.H, self.D,
+                 pos.contiguous().data_ptr(), table.data_ptr(), int(table.shape[0]), out.data_ptr(), self.err.ptr,
+                 _dev.stream())
+        return out
+
+    def append_rope(self, layer: int, k: torch.Tensor, v: torch.Tensor, pos: torch.Tensor, n_pos: int,
+                    rope) -> None:
+        """Append pre-RoPE keys (rotated on the fly) and values ``[batch, n, heads, head_dim]``.
+
+        ``pos``: device int32 ``[batch, n]`` (validated by the caller, max < n_pos).  The rows that reach
+        the compressed region go through K1 with the rotation fused (``tada_quant_append_rope``); rows
+        that stay in the residual buffer are rotated by ``tada_apply_rope`` first (cache.py:174-180
+        policy as in :meth:`append`).  Bit-identical to rotating first and calling :meth:`append`.
+        """
+        from .rope import rope_table
+
+        if k.ndim != 4 or tuple(k.shape[2:]) != (self.H, self.D) or k.shape[0] != self.B:
+            raise ShapeError(f"keys must be ({self.B}, tokens, {self.H}, {self.D}), got {tuple(k.shape)}")
+        if tuple(v.shape) != tuple(k.shape):
+            raise ShapeError(f"values shape {tuple(v.shape)} does not match keys shape {tuple(k.shape)}")
+        n = int(k.shape[1])
+        if tuple(pos.shape) != (self.B, n):
+            raise ShapeError(f"positions must be ({self.B}, {n}), got {tuple(pos.shape)}")
+        if n == 0:
+            return
+        table = rope_table(rope, n_pos)
+        pos = pos.to(device=self.dev, dtype=torch.int32).contiguous()
+        k = k.contiguous()
+        v = v.contiguous()
+        if k.dtype not in (torch.float32, torch.bfloat16) or v.dtype != k.dtype:
+            k, v = k.float(), v.float()
+        bits = self.layouts[layer].bits
+        if not (self.H == 8 and self.D == 128 and bits in (2, 4, 8)):
+            self.append(layer, self._rotate(k, pos, table), v.float())  # generic geometry: compose
+            return
+        dt = _dev.dtype_code(k)
+        C = self._uniform(self.comp_host, layer)
+        r = self._uniform(self.res_host, layer)
+        R = self.R
+        if R == 0:
+            self._ensure_pages(C + n)
+            self._quant_append_rope(layer, k.data_ptr(), v.data_ptr(), dt, n, n, 0, pos, table)
+            self._add(self.comp_len, self.comp_host, layer, n)
+            return
+        total = r + n
+        ncomp = (total // R) * R
+        if ncomp == 0:  # no flush: rotated rows go to the residual buffer
+            self.append(layer, self._rotate(k, pos, table), v.float())
+            return
+        self._ensure_pages(C + ncomp)
+        if r:  # the buffered residual rows (already rotated) are the oldest tokens of the flushed blocks
+            self._quant_append(layer, self.res_k[layer].data_ptr(), self.res_v[layer].data_ptr(), 0, r,
+                               self.res_k[layer].shape[1], 0)
+        n_new = ncomp - r
+        self._quant_append_rope(layer, k.data_ptr(), v.data_ptr(), dt, n_new, n, r, pos, table)
+        keep = total - ncomp
+        if keep:
+            k_keep = self._rotate(k[:, n_new:], pos[:, n_new:], table)
+            self._residual_write(layer, k_keep, v[:, n_new:].float().contiguous(), 0, keep, -r)
+        self._add(self.comp_len, self.comp_host, layer, ncomp)
+        self._add(self.res_len, self.res_host, layer, keep - r)
+
     def check_errors(self) -> None:
         """Raise DataError if any kernel saw a non-finite input since the last check (synchronising)."""
         if self.err.raised():

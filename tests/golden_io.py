@@ -61,3 +61,32 @@ def load():
 def keys(prefix):
     _, cases = load()
     return sorted(k for k in cases if k.startswith(prefix))
+
+
+# ---------------------------------------------------------------------- RoPE row (make_golden_rope.py)
+ROPE_AF_CHUNKS = (130, 1, 1, 6)  # prefill (crosses R = 128), two decode steps, a chunk
+
+
+def rope_af_inputs(case: int, bits: int, R: int, h=8, d=128):
+    """Per chunk: (k_pre [n, h, d], v [n, h, d], positions), bf16-gridded, for af<case>.
+
+    append_fused (model.py:167-183) is rotate_heads + (x_norm @ w_v) + append_tokens; the fixture feeds
+    the value rows directly (the BLAS projection's summation order is host-specific)."""
+    rng = np.random.default_rng(8100 + 7 * case + bits + R)
+    out, start = [], 0
+    for cnt in ROPE_AF_CHUNKS:
+        k_pre = bf16_round(rng.normal(size=(cnt, h, d)).astype(F32))
+        v = bf16_round(rng.normal(size=(cnt, h, d)).astype(F32))
+        out.append((k_pre, v, np.arange(start, start + cnt, dtype=np.int64)))
+        start += cnt
+    return out
+
+
+def load_rope():
+    """(arrays, manifest-cases) from tests/golden/rope.npz + rope_manifest.json."""
+    if "r" not in _CACHE:
+        arrays = dict(np.load(os.path.join(GOLDEN_DIR, "rope.npz")))
+        with open(os.path.join(GOLDEN_DIR, "rope_manifest.json")) as f:
+            cases = json.load(f)["cases"]
+        _CACHE["r"] = (arrays, cases)
+    return _CACHE["r"]
