@@ -31,6 +31,7 @@ from .errors import (
     StateError,
     TadaError,
 )
+from .decoder import ToyDecoder
 from .paged import PagedKVCache
 from .rope import append_fused, append_rope, apply_rope, rope_table, rotate_heads
 from .shard import ShardedKVCache, ShardPlan
@@ -54,7 +55,7 @@ __version__ = "0.1.0"
 __all__ = [
     "AttentionOutput", "BlockSpec", "BudgetInfeasibleError", "CapacityError", "CompressedLayerCache", "ConfigError",
     "DataError", "FormatError", "ModelConfig", "PagedKVCache", "PrecisionPlan", "QuantizedDeviation", "RopeParams",
-    "ShapeError", "ShardPlan", "append_fused", "append_rope", "apply_rope", "rope_table", "rotate_heads", "ShardedKVCache", "StateError", "TadaError", "actual_bytes_per_token", "attend_naive", "attend_streaming",
+    "ShapeError", "ShardPlan", "ToyDecoder", "append_fused", "append_rope", "apply_rope", "rope_table", "rotate_heads", "ShardedKVCache", "StateError", "TadaError", "actual_bytes_per_token", "attend_naive", "attend_streaming",
     "bytes_per_group", "concat_deviations", "dequantize_groups", "dequantize_tensor", "deserialize_cache",
     "direct_quantize_baseline", "empty_deviation", "kv_head_index", "mean_center", "memory_ratio", "pack_codes",
     "quantize_group", "quantize_tensor", "serialize_cache", "unpack_codes", "validate_bits", "__version__",

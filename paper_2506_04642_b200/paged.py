@@ -205,12 +205,12 @@ class PagedKVCache:
              int(table.shape[0]), self.err.ptr, _dev.stream())
 
     def _rotate(self, k: torch.Tensor, pos: torch.Tensor, table: torch.Tensor) -> torch.Tensor:
-        """[B, n, H, D] keys -> rotated f32 copy (tada_apply_rope), positions [B, n]."""
+        """[B, n, heads, D] rows -> rotated f32 copy (tada_apply_rope), positions [B, n] (any head count)."""
         kc = k.contiguous()
         out = torch.empty(kc.shape, dtype=torch.float32, device=self.dev)
         n_rows = kc.shape[0] * kc.shape[1]
         if n_rows:
-            call("tada_apply_rope", kc.data_ptr(), _dev.dtype_code(kc), n_rows, self.H, self.D,
+            call("tada_apply_rope", kc.data_ptr(), _dev.dtype_code(kc), n_rows, kc.shape[2], kc.shape[3],
                  pos.contiguous().data_ptr(), table.data_ptr(), int(table.shape[0]), out.data_ptr(), self.err.ptr,
                  _dev.stream())
         return out
