@@ -148,11 +148,24 @@ class ToyDecoder:
         self.position = n
         return self._mm(self._rmsnorm(x, w["final_norm"]), w["lm_head"])
 
+    def reset(self, cfg: ModelConfig | None = None) -> None:
+        """Fresh empty caches (optionally for another plan / residual length of the same geometry):
+        ``new_caches`` (model.py:163-164); the device weights are kept."""
+        if cfg is not None:
+            if (cfg.num_layers, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim) != (
+                    self.cfg.num_layers, self.cfg.num_q_heads, self.cfg.num_kv_heads, self.cfg.head_dim):
+                raise ConfigError("reset() keeps the weights: the geometry must not change")
+            self.cfg = cfg
+        c = self.cfg
+        self.store = PagedKVCache(c.num_layers, c.num_kv_heads, c.head_dim, c.plan.bits_per_layer, c.residual_length,
+                                  batch=self.B, page_tokens=self.page_tokens, max_tokens=self.max_seq_len)
+        self.position = 0
+
     # ------------------------------------------------------------------ decode (model.py:257-289)
     def decode_step(self, token_ids, position: int) -> torch.Tensor:
         """Append one token per sequence at ``position`` and return next-token logits ``[B, vocab]``."""
         if self.store is None:
-            raise DataError("decode_step needs a prefilled cache")
+            self.reset()
         ids = self._ids(np.asarray(token_ids).reshape(self.B, 1))
         if position != self.position:
             raise DataError(f"the caches hold {self.position} tokens but position is {position}")
