@@ -282,6 +282,106 @@ __global__ void __launch_bounds__(kCombThreads) combine_residual_kernel(AttnArgs
   }
 }
 
+// K3 for head_dim 128: one warp per (q head, sequence), lane l owning d = 4l .. 4l+3; warp reductions only
+// (no CTA barriers), every independent global load issued before its consumers.
+__global__ void __launch_bounds__(256) combine_residual_warp_kernel(AttnArgs a, int n_rows) {
+  constexpr int D = 128, U = 8;
+  extern __shared__ __align__(16) float csm[];  // [8 warps][res_seq_stride] residual logits
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int row = blockIdx.x * 8 + wib;  // b * Hq + gq
+  if (row >= n_rows) return;
+  const int Hq = a.Hq, H = a.L.heads, G = Hq / H, S = a.splits;
+  const int b = row / Hq, gq = row - b * Hq, h = gq / G;
+  const int R = a.res_len[b];
+  float* pr = csm + wib * a.res_seq_stride;
+  const float NEG_INF = -__int_as_float(0x7f800000);
+  float q[4];
+  if (a.q_dtype == TADA_F32) load4(reinterpret_cast<const float*>(a.q) + int64_t(row) * D + 4 * lane, q);
+  else load4(reinterpret_cast<const __nv_bfloat16*>(a.q) + int64_t(row) * D + 4 * lane, q);
+  const float* ml = a.part_ml + int64_t(row) * a.slots * 2;
+  const float* pa = a.part_acc + int64_t(row) * a.slots * D + 4 * lane;
+  // split (m, l): lane s holds split s (s < 32); larger S loops
+  float mx = NEG_INF;
+  for (int s2 = lane; s2 < S; s2 += 32)
+    if (ml[2 * s2 + 1] > 0.f) mx = fmaxf(mx, ml[2 * s2]);
+  // residual logits, four tokens per round (independent shuffle trees)
+  const int64_t rbase = int64_t(b) * a.res_seq_stride;
+  for (int t0 = 0; t0 < R; t0 += 4) {
+    float dot[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      dot[u] = 0.f;
+      if (t0 + u < R) {
+        const float4 k4 = *reinterpret_cast<const float4*>(a.res_k + ((rbase + t0 + u) * H + h) * D + 4 * lane);
+        dot[u] = __fmaf_rn(q[3], k4.w, __fmaf_rn(q[2], k4.z, __fmaf_rn(q[1], k4.y, __fmaf_rn(q[0], k4.x, 0.f))));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], o);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (t0 + u < R) {
+        const float sv = __fmul_rn(dot[u], a.scale);
+        if (lane == 0) pr[t0 + u] = sv;
+        mx = fmaxf(mx, sv);
+      }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const float M = mx;
+  __syncwarp();
+  // weighted sums: splits (weights broadcast from the lane that read them), then residual rows
+  float acc[4] = {0.f, 0.f, 0.f, 0.f}, lsum = 0.f;
+  for (int s0 = 0; s0 < S; s0 += 32) {
+    const int s2 = s0 + lane;
+    float w = 0.f;
+    if (s2 < S && ml[2 * s2 + 1] > 0.f) {
+      w = expf(ml[2 * s2] - M);
+      lsum += w * ml[2 * s2 + 1];
+    }
+    const int n = min(32, S - s0);
+    for (int j0 = 0; j0 < n; j0 += U) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        v[u] = j0 + u < n ? *reinterpret_cast<const float4*>(pa + int64_t(s0 + j0 + u) * D) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float wu = __shfl_sync(0xffffffffu, w, (j0 + u) & 31);
+        acc[0] = fmaf(wu, v[u].x, acc[0]);
+        acc[1] = fmaf(wu, v[u].y, acc[1]);
+        acc[2] = fmaf(wu, v[u].z, acc[2]);
+        acc[3] = fmaf(wu, v[u].w, acc[3]);
+      }
+    }
+  }
+  for (int t0 = 0; t0 < R; t0 += U) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      v[u] = t0 + u < R ? *reinterpret_cast<const float4*>(a.res_v + ((rbase + t0 + u) * H + h) * D + 4 * lane)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float p = t0 + u < R ? expf(pr[t0 + u] - M) : 0.f;
+      if (lane == 0) lsum += p;
+      acc[0] = fmaf(p, v[u].x, acc[0]);
+      acc[1] = fmaf(p, v[u].y, acc[1]);
+      acc[2] = fmaf(p, v[u].z, acc[2]);
+      acc[3] = fmaf(p, v[u].w, acc[3]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+  const float inv = 1.f / lsum;
+  const int64_t qi = int64_t(row) * D + 4 * lane;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) store_any(a.out, a.out_dtype, qi + e, acc[e] * inv);
+  if (lane == 0 && a.lse_out) a.lse_out[row] = M + logf(lsum);
+}
+
 static int launch_combine_residual(const AttnArgs& a, int batch, cudaStream_t st) {
   if (a.L.head_dim * 2 > kCombThreads * 2 || a.L.head_dim % 4) return fail(TADA_ERR_CONFIG, "combine needs head_dim % 4 == 0");
   const size_t smem = (size_t(a.L.head_dim) * 3 + size_t(a.res_seq_stride) + size_t(a.splits) + 8) * 4;
@@ -289,6 +389,17 @@ static int launch_combine_residual(const AttnArgs& a, int batch, cudaStream_t st
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(combine_residual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string("combine smem: ") + cudaGetErrorString(e));
+  }
+  if (a.L.head_dim == 128) {
+    const int rows = a.Hq * batch;
+    const size_t wsm = size_t(8) * a.res_seq_stride * 4;
+    if (wsm > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(combine_residual_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(wsm));
+      if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string("combine smem: ") + cudaGetErrorString(e));
+    }
+    combine_residual_warp_kernel<<<(rows + 7) / 8, 256, wsm, st>>>(a, rows);
+    return check_launch("decode_attn_combine_residual");
   }
   combine_residual_kernel<<<dim3(a.Hq, batch), kCombThreads, smem, st>>>(a);
   return check_launch("decode_attn_combine_residual");
