@@ -157,3 +157,32 @@ def test_precision_ordering():
             errs[b].append(float(np.linalg.norm(m.attend_naive(q, cache, cfg_for(4, 2, 16, 0, b)).output - exact)))
     med = [float(np.median(errs[b])) for b in (2, 4, 8, 16)]
     assert med[0] >= med[1] >= med[2] >= med[3]
+
+
+@pytest.mark.parametrize("bits", [2, 4, 8])
+@pytest.mark.parametrize("hq", [32, 64])
+@pytest.mark.parametrize("regime", ["shared", "head"])
+def test_fast_outlier_regimes(bits, hq, regime):
+    """Large means (analysis.py:37-57 shared outlier channels, x8) and head-specific outliers (one head's
+    channel x40, so the mean and the deviations are both large): the f16 hi + lo mean terms and the
+    16-bit fixed-point q keep the tensor-core kernels within 2e-3 of the reference (scaled by |out|max)."""
+    m = tk()
+    rng = np.random.default_rng(300 + bits + hq)
+    B, T, H, D = 2, 900, 8, 128
+    k = np.stack([orc.outlier_activations(rng, T, H, D) for _ in range(B)])
+    v = np.stack([orc.outlier_activations(rng, T, H, D) for _ in range(B)])
+    if regime == "head":
+        k[:, :, 3, 17] *= 40.0
+        v[:, :, 5, 90] *= 40.0
+    k, v = orc.bf16_round(k.astype(np.float32)), orc.bf16_round(v.astype(np.float32))
+    q = orc.bf16_round((rng.normal(size=(B, hq, D)) * 2.0).astype(np.float32))
+    store = m.PagedKVCache(1, H, D, (bits,), 128, batch=B, page_tokens=64, max_tokens=T + 1, shuffle_pages=True)
+    store.append(0, torch.from_numpy(k).cuda().bfloat16(), torch.from_numpy(v).cuda().bfloat16())
+    want = []
+    for b in range(B):
+        st = orc.LayerState(H, D, bits, 128)
+        orc.append(st, k[b], v[b])
+        want.append(orc.attend(q[b], st, hq)[0])
+    want = np.stack(want)
+    out = _fast_or_skip(store, torch.from_numpy(q).cuda(), out_dtype=torch.float32)
+    assert np.abs(out.cpu().numpy() - want).max() <= 2e-3 * max(1.0, float(np.abs(want).max()))
