@@ -3,6 +3,9 @@
 
 #include <cuda.h>
 
+#include <atomic>
+#include <string>
+
 #include "tada_common.cuh"
 
 namespace tada {
@@ -48,6 +51,20 @@ __device__ __forceinline__ void split_range(int n, int splits, int s, int align,
 struct alignas(64) TmaMaps {
   CUtensorMap m[2][3];
 };
+
+// Raise a kernel's dynamic shared-memory limit once per device (thread-safe; `done` is a per-kernel bitmask
+// of devices already configured).
+template <typename Kern>
+int ensure_smem(Kern kern, int bytes, std::atomic<uint64_t>& done, const char* what) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return fail(TADA_ERR_CUDA, "cudaGetDevice failed");
+  const uint64_t bit = uint64_t(1) << dev;
+  if (done.load(std::memory_order_acquire) & bit) return TADA_OK;
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string(what) + " smem: " + cudaGetErrorString(e));
+  done.fetch_or(bit, std::memory_order_acq_rel);
+  return TADA_OK;
+}
 
 // Fast path (tensor-core grouped-head contraction); returns TADA_ERR_CONFIG if the
 // geometry is unsupported so the caller can fall back to the generic kernel.

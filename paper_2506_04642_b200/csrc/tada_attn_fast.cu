@@ -801,12 +801,8 @@ template <int BITS, int HQ, int TT>
 static int launch_fast_tt(const AttnArgs& a, int batch, cudaStream_t st) {
   constexpr fast::Plan pl = fast::make_plan(8, BITS * 128 / 8, HQ, TT);
   auto kern = fast::attn_fast_kernel<BITS, HQ, TT>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.total);
-    if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string("attn_fast smem: ") + cudaGetErrorString(e));
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> smem_set{0};  // per instantiation, per device
+  if (const int rc0 = ensure_smem(kern, pl.total, smem_set, "attn_fast"); rc0 != TADA_OK) return rc0;
   TmaMaps maps;
   const int rc = get_tma_maps(a, &maps, TT);
   if (rc != TADA_OK) return rc;

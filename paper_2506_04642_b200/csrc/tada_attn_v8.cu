@@ -650,12 +650,8 @@ static int launch_v8_t(const AttnArgs& a, int batch, cudaStream_t st) {
     return fail(TADA_ERR_CONFIG, "decode_attn_v8: geometry does not fit two stages");
   } else {
     auto kern = v8::attn_v8_kernel<BITS, HQ>;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.total);
-      if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string("attn_v8 smem: ") + cudaGetErrorString(e));
-      attr_set = true;
-    }
+    static std::atomic<uint64_t> smem_set{0};  // per instantiation, per device
+    if (const int rc0 = ensure_smem(kern, pl.total, smem_set, "attn_v8"); rc0 != TADA_OK) return rc0;
     TmaMaps maps;
     const int rc = get_tma_maps(a, &maps, v8::TT);
     if (rc != TADA_OK) return rc;
