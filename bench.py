@@ -286,11 +286,12 @@ def run_ours(args):
         k_all = ks[s] if k_in is None else k_in
         v_all = vs[s] if v_in is None else v_in
         for layer in range(L):
-            store.append(layer, k_all[layer], v_all[layer])
             if record:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e0.record()
-            store.attend(layer, q_all[layer], out=outs[layer], num_splits=splits[PLAN[layer]], mode=args.mode)
+            # one decode step of the layer: append (residual row, or flush through K1) + K2/K3
+            store.append_attend(layer, q_all[layer], k_all[layer], v_all[layer], out=outs[layer],
+                                num_splits=splits[PLAN[layer]], mode=args.mode)
             if record:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record()

@@ -218,6 +218,21 @@ int tada_combine_lse(const float* o_parts, const float* lse_parts, int32_t n_par
 /* Split count for this layer's kernel on the current device: the fewest whole waves of resident
  * CTAs (SM count x CTAs per SM of the instantiation that will run) whose last wave is >= 90% full,
  * with >= 256 tokens per split. */
+/* One decode step of a layer in one call: append_tokens of one new token that stays in the residual
+ * buffer (no flush: r_prev + 1 < residual_length; cache.py:174-175) followed by attend_streaming
+ * (attention.py:103-151). new_k / new_v: [batch][heads][head_dim] (f32 or bf16), already rotated.
+ * The K3 combine attends the new row straight from the input, stores it (as f32) at residual row
+ * r_prev of every sequence and sets res_len[b] = r_prev + 1 (r_prev: the host-known, batch-uniform
+ * residual count before the step). Needs the tensor-core path (head_dim 128), else TADA_ERR_CONFIG
+ * with nothing enqueued. Results equal tada_residual_append + tada_decode_attn. */
+int tada_decode_attn_append(const tada_page_layout* layout, const uint8_t* pool, const void* q,
+                            int32_t q_dtype, int32_t batch, int32_t num_q_heads,
+                            const int32_t* page_table, int32_t pt_stride, const int32_t* comp_len,
+                            int32_t* res_len, float* res_k, float* res_v, int64_t res_seq_stride,
+                            float scale, int32_t num_splits, void* workspace, void* out,
+                            int32_t out_dtype, int32_t mode, const void* new_k, const void* new_v,
+                            int32_t new_dtype, int32_t r_prev, void* stream);
+
 int32_t tada_decode_attn_plan_splits(const tada_page_layout* layout, int32_t num_q_heads, int32_t batch,
                                      int64_t max_tokens);
 

@@ -72,6 +72,8 @@ SIGNATURES = {
                                I32, I32, P]),
     "tada_decode_attn_lse": (I32, [C.POINTER(PageLayout), P, P, I32, I32, I32, P, I32, P, P, P, P, I64, F, I32, P,
                                    P, I32, I32, P, P]),
+    "tada_decode_attn_append": (I32, [C.POINTER(PageLayout), P, P, I32, I32, I32, P, I32, P, P, P, P, I64, C.c_float,
+                                      I32, P, P, I32, I32, P, P, I32, I32, P]),
     "tada_combine_lse": (I32, [P, P, I32, I64, I32, P, I32, P, P]),
     "tada_decode_attn_suggest_splits": (I32, [I32, I64, I32]),
     "tada_decode_attn_plan_splits": (I32, [C.POINTER(PageLayout), I32, I32, I64]),

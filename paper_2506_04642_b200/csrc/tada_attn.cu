@@ -292,8 +292,24 @@ __global__ void __launch_bounds__(256) combine_residual_warp_kernel(AttnArgs a, 
   if (row >= n_rows) return;
   const int Hq = a.Hq, H = a.L.heads, G = Hq / H, S = a.splits;
   const int b = row / Hq, gq = row - b * Hq, h = gq / G;
-  const int R = a.res_len[b];
+  // fused decode step: the residual holds r_prev rows plus this step's row, read from the input
+  const bool fused = a.new_k != nullptr;
+  const int R = fused ? a.r_prev + 1 : a.res_len[b];
+  const int r_new = fused ? a.r_prev : -1;
   float* pr = csm + wib * a.res_seq_stride;
+  auto new_row = [&](const void* src) {  // this lane's 4 columns of the new row of head h, as f32
+    float x[4];
+    const int64_t off = (int64_t(b) * H + h) * D + 4 * lane;
+    if (a.new_dtype == TADA_F32) load4(reinterpret_cast<const float*>(src) + off, x);
+    else load4(reinterpret_cast<const __nv_bfloat16*>(src) + off, x);
+    return make_float4(x[0], x[1], x[2], x[3]);
+  };
+  if (fused && gq % G == 0) {  // one warp per (sequence, KV head) stores the row for later steps
+    const int64_t dst = ((int64_t(b) * a.res_seq_stride + r_new) * H + h) * D + 4 * lane;
+    *reinterpret_cast<float4*>(const_cast<float*>(a.res_k) + dst) = new_row(a.new_k);
+    *reinterpret_cast<float4*>(const_cast<float*>(a.res_v) + dst) = new_row(a.new_v);
+    if (gq == 0 && lane == 0) const_cast<int32_t*>(a.res_len)[b] = r_new + 1;
+  }
   const float NEG_INF = -__int_as_float(0x7f800000);
   float q[4];
   if (a.q_dtype == TADA_F32) load4(reinterpret_cast<const float*>(a.q) + int64_t(row) * D + 4 * lane, q);
@@ -312,7 +328,8 @@ __global__ void __launch_bounds__(256) combine_residual_warp_kernel(AttnArgs a, 
     for (int u = 0; u < 4; ++u) {
       dot[u] = 0.f;
       if (t0 + u < R) {
-        const float4 k4 = *reinterpret_cast<const float4*>(a.res_k + ((rbase + t0 + u) * H + h) * D + 4 * lane);
+        const float4 k4 = t0 + u == r_new ? new_row(a.new_k)
+                                          : *reinterpret_cast<const float4*>(a.res_k + ((rbase + t0 + u) * H + h) * D + 4 * lane);
         dot[u] = __fmaf_rn(q[3], k4.w, __fmaf_rn(q[2], k4.z, __fmaf_rn(q[1], k4.y, __fmaf_rn(q[0], k4.x, 0.f))));
       }
     }
@@ -361,8 +378,9 @@ __global__ void __launch_bounds__(256) combine_residual_warp_kernel(AttnArgs a, 
     float4 v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      v[u] = t0 + u < R ? *reinterpret_cast<const float4*>(a.res_v + ((rbase + t0 + u) * H + h) * D + 4 * lane)
-                        : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[u] = t0 + u >= R ? make_float4(0.f, 0.f, 0.f, 0.f)
+                         : (t0 + u == r_new ? new_row(a.new_v)
+                                            : *reinterpret_cast<const float4*>(a.res_v + ((rbase + t0 + u) * H + h) * D + 4 * lane));
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const float p = t0 + u < R ? expf(pr[t0 + u] - M) : 0.f;
@@ -474,7 +492,9 @@ static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool,
                             int32_t batch, int32_t num_q_heads, const int32_t* page_table, int32_t pt_stride,
                             const int32_t* comp_len, const int32_t* res_len, const float* res_k, const float* res_v,
                             int64_t res_seq_stride, float scale, int32_t num_splits, void* workspace, void* out,
-                            int32_t out_dtype, int32_t mode, float* lse_out, void* stream) {
+                            int32_t out_dtype, int32_t mode, float* lse_out, void* stream,
+                            const void* new_k = nullptr, const void* new_v = nullptr, int32_t new_dtype = 0,
+                            int32_t r_prev = 0) {
   if (!layout) return fail(TADA_ERR_CONFIG, "null layout");
   if (q_dtype != TADA_F32 && q_dtype != TADA_BF16) return fail(TADA_ERR_CONFIG, "q dtype must be f32 or bf16");
   if (out_dtype != TADA_F32 && out_dtype != TADA_BF16) return fail(TADA_ERR_CONFIG, "out dtype must be f32 or bf16");
@@ -511,6 +531,10 @@ static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool,
   a.out_dtype = out_dtype;
   a.q_dtype = q_dtype;
   a.lse_out = lse_out;
+  a.new_k = new_k;
+  a.new_v = new_v;
+  a.new_dtype = new_dtype;
+  a.r_prev = r_prev;
   {
     static const int diag = getenv("TADA_ATTN_DIAG") ? atoi(getenv("TADA_ATTN_DIAG")) : 0;
     a.diag = diag;
@@ -548,6 +572,24 @@ int tada_decode_attn_lse(const tada_page_layout* layout, const uint8_t* pool, co
   if (!lse_out) return fail(TADA_ERR_SHAPE, "null lse buffer");
   return decode_attn_impl(layout, pool, q, q_dtype, batch, num_q_heads, page_table, pt_stride, comp_len, res_len, res_k,
                           res_v, res_seq_stride, scale, num_splits, workspace, out, out_dtype, mode, lse_out, stream);
+}
+
+int tada_decode_attn_append(const tada_page_layout* layout, const uint8_t* pool, const void* q, int32_t q_dtype,
+                            int32_t batch, int32_t num_q_heads, const int32_t* page_table, int32_t pt_stride,
+                            const int32_t* comp_len, int32_t* res_len, float* res_k, float* res_v,
+                            int64_t res_seq_stride, float scale, int32_t num_splits, void* workspace, void* out,
+                            int32_t out_dtype, int32_t mode, const void* new_k, const void* new_v, int32_t new_dtype,
+                            int32_t r_prev, void* stream) {
+  if (!layout) return fail(TADA_ERR_CONFIG, "null layout");
+  if (mode == 1 || !fast_supported(*layout, num_q_heads) || layout->head_dim != 128)
+    return fail(TADA_ERR_CONFIG, "fused decode step needs the tensor-core attention path (head_dim 128)");
+  if (!new_k || !new_v || !res_k || !res_v) return fail(TADA_ERR_SHAPE, "null buffer");
+  if (new_dtype != TADA_F32 && new_dtype != TADA_BF16) return fail(TADA_ERR_CONFIG, "new row dtype must be f32 or bf16");
+  if (r_prev < 0 || r_prev + 1 > res_seq_stride)
+    return fail(TADA_ERR_CONFIG, "the new row does not fit the residual buffer (flush first)");
+  return decode_attn_impl(layout, pool, q, q_dtype, batch, num_q_heads, page_table, pt_stride, comp_len, res_len, res_k,
+                          res_v, res_seq_stride, scale, num_splits, workspace, out, out_dtype, mode == 0 ? 2 : mode,
+                          nullptr, stream, new_k, new_v, new_dtype, r_prev);
 }
 
 int tada_combine_lse(const float* o_parts, const float* lse_parts, int32_t n_parts, int64_t rows, int32_t head_dim,

@@ -30,6 +30,12 @@ struct AttnArgs {
   void* out;
   int out_dtype;
   int q_dtype;
+  // decode-step fusion (tada_decode_attn_append): the step's new K/V row [batch][heads][head_dim] is attended
+  // by K3 directly and written to residual row r_prev (whose count K3 then sets to r_prev + 1)
+  const void* new_k;
+  const void* new_v;
+  int new_dtype;
+  int r_prev;
   int diag;  // diagnostics only (env TADA_ATTN_DIAG): 1 = TMA ring without compute, 2 = compute on one L2-resident page
   float* lse_out;  // optional [B][Hq]: natural-log sum-exp of the scaled logits (cross-rank merge)
 };

@@ -325,6 +325,48 @@ class PagedKVCache:
              out.data_ptr(), _dev.dtype_code(out), mode, _dev.stream())
         return out
 
+    def append_attend(self, layer: int, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                      out: torch.Tensor | None = None, out_dtype=torch.float32, num_splits: int | None = None,
+                      mode: int = 0, scale: float | None = None) -> torch.Tensor:
+        """One decode step of a layer: :meth:`append` of one token per sequence (``k``, ``v``:
+        ``[batch, 1, heads, head_dim]``, rotated) then :meth:`attend` — model.py:280-281.
+
+        When the token stays in the residual buffer (no flush) and the layer runs on the tensor-core
+        path, both happen in one call (``tada_decode_attn_append``: K3 attends the new row straight from
+        the input and stores it); otherwise this is exactly append() + attend()."""
+        from ._lib import load
+
+        fused_ok = (k.ndim == 4 and k.shape[1] == 1 and tuple(v.shape) == tuple(k.shape) and self.R > 0
+                    and mode != 1 and k.dtype in (torch.float32, torch.bfloat16) and v.dtype == k.dtype
+                    and q.ndim == 3 and q.shape[0] == self.B and q.shape[2] == self.D and q.shape[1] % self.H == 0)
+        if fused_ok:
+            C = self._uniform(self.comp_host, layer)
+            r = self._uniform(self.res_host, layer)
+            fused_ok = C > 0 and r + 1 < self.R
+        if not fused_ok:
+            self.append(layer, k, v)
+            return self.attend(layer, q, out=out, out_dtype=out_dtype, num_splits=num_splits, mode=mode, scale=scale)
+        hq = int(q.shape[1])
+        if q.dtype not in (torch.float32, torch.bfloat16):
+            q = q.float()
+        q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+        splits = num_splits or self.suggest_splits(layer, hq)
+        ws = self.workspace(hq, splits)
+        if out is None:
+            out = torch.empty((self.B, hq, self.D), dtype=out_dtype, device=self.dev)
+        sc = np.float32(1.0 / math.sqrt(self.D)) if scale is None else np.float32(scale)
+        rc = load().tada_decode_attn_append(
+            self._layout_ptr(layer), self.pools[layer].data_ptr(), q.data_ptr(), _dev.dtype_code(q), self.B, hq,
+            self.page_table.data_ptr(), self.page_table.shape[1], self.comp_len[layer].data_ptr(),
+            self.res_len[layer].data_ptr(), self.res_k[layer].data_ptr(), self.res_v[layer].data_ptr(),
+            self.res_k[layer].shape[1], float(sc), splits, _dev.ptr(ws), out.data_ptr(), _dev.dtype_code(out), mode,
+            k.data_ptr(), v.data_ptr(), _dev.dtype_code(k), r, _dev.stream())
+        if rc != 0:  # geometry without the tensor-core path: nothing was enqueued
+            self.append(layer, k, v)
+            return self.attend(layer, q, out=out, out_dtype=out_dtype, num_splits=num_splits, mode=mode, scale=scale)
+        self.res_host[layer] += 1
+        return out
+
     def attend_lse(self, layer: int, q: torch.Tensor, num_splits: int | None = None, mode: int = 0,
                    scale: float | None = None) -> tuple[torch.Tensor, torch.Tensor]:
         """Like :meth:`attend` (f32 out) and also the log-sum-exp ``[batch, Hq]`` of the scaled logits.

@@ -186,3 +186,29 @@ def test_fast_outlier_regimes(bits, hq, regime):
     want = np.stack(want)
     out = _fast_or_skip(store, torch.from_numpy(q).cuda(), out_dtype=torch.float32)
     assert np.abs(out.cpu().numpy() - want).max() <= 2e-3 * max(1.0, float(np.abs(want).max()))
+
+
+@pytest.mark.parametrize("bits,hq", [(4, 32), (2, 64), (8, 32), (4, 8)])
+def test_append_attend_fused_equals_append_then_attend(bits, hq):
+    """PagedKVCache.append_attend (K3 attends and stores the step's row) == append() + attend(), output bits
+    and cache state, across decode steps that cross the residual flush (R = 8)."""
+    m = tk()
+    B, T, H, D, R = 3, 300, 8, 128, 8
+    rng = np.random.default_rng(70 + bits + hq)
+    k0 = torch.from_numpy(orc.bf16_round(rng.normal(size=(B, T, H, D)).astype(np.float32))).cuda().bfloat16()
+    v0 = torch.from_numpy(orc.bf16_round(rng.normal(size=(B, T, H, D)).astype(np.float32))).cuda().bfloat16()
+    a = m.PagedKVCache(1, H, D, (bits,), R, batch=B, page_tokens=64, max_tokens=T + 64)
+    b = m.PagedKVCache(1, H, D, (bits,), R, batch=B, page_tokens=64, max_tokens=T + 64)
+    a.append(0, k0, v0)
+    b.append(0, k0, v0)
+    for step in range(20):
+        k = torch.from_numpy(rng.normal(size=(B, 1, H, D)).astype(np.float32)).cuda().bfloat16()
+        v = torch.from_numpy(rng.normal(size=(B, 1, H, D)).astype(np.float32)).cuda().bfloat16()
+        q = torch.from_numpy(rng.normal(size=(B, hq, D)).astype(np.float32)).cuda().bfloat16()
+        want = (a.append(0, k, v), a.attend(0, q, out_dtype=torch.bfloat16, num_splits=5))[1]
+        got = b.append_attend(0, q, k, v, out_dtype=torch.bfloat16, num_splits=5)
+        assert torch.equal(got, want), step
+        assert a.lengths(0, 0) == b.lengths(0, 0)
+    r = a.lengths(0)[1]
+    assert torch.equal(a.res_k[0][:, :r], b.res_k[0][:, :r]) and torch.equal(a.res_v[0][:, :r], b.res_v[0][:, :r])
+    assert torch.equal(a.res_len[0], b.res_len[0]) and torch.equal(a.comp_len[0], b.comp_len[0])
