@@ -405,10 +405,10 @@ def run_ours(args):
                          "frac_of_8tbs_spec": achieved / 8000.0, "per_width": per_width,
                          "all_layers_gbs": attn_bytes / (attn_ms / 1e3) / 1e9,
                          "alg_bytes_per_step": step_bytes, "attn_ms_per_step": attn_ms / steps,
-                         # effective KV bytes streamed per decoded token (all layers, one sequence), and the
+                         # effective KV bytes streamed per decoded token (all layers, one sequence; step_bytes is this rank's), and the
                          # same as a fraction of a bf16 K/V cache's 2*H*D*2 bytes per token per layer
-                         "kv_bytes_per_decoded_token": step_bytes / (B * world),
-                         "kv_bytes_vs_bf16": step_bytes / (B * world) / (L * T * 2 * H * D * 2)},
+                         "kv_bytes_per_decoded_token": step_bytes / B,
+                         "kv_bytes_vs_bf16": step_bytes / B / (L * T * 2 * H * D * 2)},
             "quant_append": {"value": quant_append_gbs, "unit": "GB/s", "frac": quant_append_gbs / peak,
                              "workload": f"prefill bulk quantize-append 32k tokens x batch {B} x 32 layers (config 3 "
                                          f"shape per sequence)", "ms_per_layer": statistics.median(qa_ms)},
