@@ -45,8 +45,9 @@ __host__ __device__ constexpr int up1k(int x) { return (x + 1023) / 1024 * 1024;
 
 struct Plan {
   int mean_bytes, codes_bytes, meta_bytes, side_bytes, stage_bytes, stages, trow;
-  int off_vm, off_sm, off_p, off_corr, off_qa, off_bar, total;
+  int off_vm, off_sm, off_p, off_corr, off_qa, off_qi, off_bar, total;
   bool ok;
+  bool qi_smem;  // the IMMA q fragments live in shared memory (frees 16 registers) when there is room
 };
 
 // [stage 0 .. S-1] | VM [hi, lo][16 tok][256 B] | SM [4 planes][MROWS][16] f32 | P [MROWS][16] f16 |
@@ -75,6 +76,9 @@ __host__ __device__ constexpr Plan make_plan(int gb, int HQ) {
   off += up128(mrows * 4);
   p.off_qa = off;
   off += 4 * mt * 2 * 512;
+  p.off_qi = off;
+  p.qi_smem = off + 8 * 4 * 512 + 128 <= kBudget;
+  if (p.qi_smem) off += 8 * 4 * 512;  // [warp][k-step][lane] uint4
   p.off_bar = off;
   off += 128;
   p.total = off;
@@ -229,6 +233,10 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
     isum += __shfl_xor_sync(0xffffffffu, isum, 1);
     isum += __shfl_xor_sync(0xffffffffu, isum, 2);
     qs = sq * float(isum);
+    if (pl.qi_smem)
+#pragma unroll
+      for (int s = 0; s < 4; ++s)
+        sh<uint4>(smem, pl.off_qi + (warp * 4 + s) * 512 + lane * 16) = make_uint4(qA[s][0], qA[s][1], qA[s][2], qA[s][3]);
   }
   // QK mean A fragments of every piece, lane-major: [quarter qd][mt][ks][lane]; q rows 16mt + r (+8),
   // k-step ks slots (2c, 2c+1 | 2c+8, 2c+9) <-> d = 32qd + 16ks + 4c + (0, 1 | 2, 3)
@@ -253,6 +261,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   const int oX0 = qd * BAND + swz(8 * oct + r, 16 * c);  // kmean, stage-relative
   const int oX1 = qd * BAND + swz(8 * oct + r, 64 + 16 * c);
   const int oQA = pl.off_qa + qd * (MT * 2 * 512) + lane * 16;
+  const int oQI = pl.off_qi + warp * 4 * 512 + lane * 16;
   const int oSW = pl.off_sm + qd * PLANE + (r * TT + ((8 * oct + 2 * c) ^ (8 * ((r >> 1) & 1)))) * 4;
   const int vt = tid & 15, vu = tid >> 4;  // vmean split: token vt, d in [8vu, 8vu+8)
   const int oV0 = pl.mean_bytes + (vu >> 2) * BAND + swz(vt, (vu & 3) * 32);  // vmean, stage-relative
@@ -364,8 +373,15 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
       int acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
-        imma_su(acc[0], qA[s], qk_quad<BITS>(wa, s, 0), qk_quad<BITS>(wa, s, 1));
-        imma_su(acc[1], qA[s], qk_quad<BITS>(wb, s, 0), qk_quad<BITS>(wb, s, 1));
+        uint32_t A[4];
+        if (pl.qi_smem) {
+          const uint4 f = sh<uint4>(smem, oQI + s * 512);
+          A[0] = f.x; A[1] = f.y; A[2] = f.z; A[3] = f.w;
+        } else {
+          A[0] = qA[s][0]; A[1] = qA[s][1]; A[2] = qA[s][2]; A[3] = qA[s][3];
+        }
+        imma_su(acc[0], A, qk_quad<BITS>(wa, s, 0), qk_quad<BITS>(wa, s, 1));
+        imma_su(acc[1], A, qk_quad<BITS>(wb, s, 0), qk_quad<BITS>(wb, s, 1));
       }
       // S_mean of (q row, tokens 2c, 2c+1 | 8+2c, 9+2c): the 4 d-quarter planes
       float sm[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
