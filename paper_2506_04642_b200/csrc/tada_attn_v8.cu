@@ -39,6 +39,10 @@ constexpr int D = 128, H = 8, TT = 16, NW = 8, NTHR = 256;
 constexpr int BAND = TT * 128;       // bytes of one 128-B-wide swizzled band of a tile region
 constexpr int VMPART = TT * D * 2;   // one f16 part (hi or lo) of the split vmean: [16 tok][256 B]
 constexpr int kBudget = 113 * 1024;  // two CTAs per SM
+#ifndef TADA_V8_MAXS
+#define TADA_V8_MAXS 2  // measured: the x3 unroll of a 3-stage ring costs more (register pressure) than the depth buys
+#endif
+constexpr int MAXS = TADA_V8_MAXS;  // deepest TMA ring (2 or 3 stages)
 
 __host__ __device__ constexpr int up128(int x) { return (x + 127) / 128 * 128; }
 __host__ __device__ constexpr int up1k(int x) { return (x + 1023) / 1024 * 1024; }
@@ -64,7 +68,7 @@ __host__ __device__ constexpr Plan make_plan(int gb, int HQ) {
   p.side_bytes = p.mean_bytes + p.codes_bytes;
   p.stage_bytes = up1k(2 * p.side_bytes + 2 * p.meta_bytes);
   const int tail = 2 * VMPART + 4 * mrows * TT * 4 + mrows * TT * 2 + up128(mrows * 4) + 4 * mt * 2 * 512 + 128;
-  p.stages = (3 * p.stage_bytes + tail <= kBudget) ? 3 : ((2 * p.stage_bytes + tail <= kBudget) ? 2 : 0);
+  p.stages = (MAXS >= 3 && 3 * p.stage_bytes + tail <= kBudget) ? 3 : ((2 * p.stage_bytes + tail <= kBudget) ? 2 : 0);
   int off = p.stages * p.stage_bytes;
   p.off_vm = off;
   off += 2 * VMPART;
