@@ -42,6 +42,9 @@ constexpr int kBudget = 113 * 1024;  // two CTAs per SM
 #ifndef TADA_V8_MAXS
 #define TADA_V8_MAXS 2  // measured: the x3 unroll of a 3-stage ring costs more (register pressure) than the depth buys
 #endif
+#ifndef TADA_V8_VMEAN_LO
+#define TADA_V8_VMEAN_LO 0  // 1: the PV mean term also carries the f16 residual of vmean
+#endif
 #ifndef TADA_V8_TMEM_OM
 #define TADA_V8_TMEM_OM 1  // park the PV mean accumulators in TMEM between tiles
 #endif
@@ -559,14 +562,22 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
     // ------------------------------------------------------------ this warp's share of the vmean split
     {  // token vt, d = 8vu .. 8vu+7 -> f16 hi / lo rows [tok][d] (16-B chunk vu at vu ^ (vt & 7))
       const float4 x0 = sh<float4>(smem, ST + oV0), x1 = sh<float4>(smem, ST + oV1);
-      uint4 hi, lo;
+      uint4 hi;
+#if TADA_V8_VMEAN_LO
+      uint4 lo;
       split_h2(x0.x, x0.y, hi.x, lo.x);
       split_h2(x0.z, x0.w, hi.y, lo.y);
       split_h2(x1.x, x1.y, hi.z, lo.z);
       split_h2(x1.z, x1.w, hi.w, lo.w);
-      if (tail && vt >= nv) hi = lo = make_uint4(0u, 0u, 0u, 0u);  // rows past the sequence may hold anything
-      sh<uint4>(smem, oVW) = hi;
+      if (tail && vt >= nv) lo = make_uint4(0u, 0u, 0u, 0u);
       sh<uint4>(smem, oVW + VMPART) = lo;
+#else
+      // vmean enters the PV mean MMA as f16 (RN): |error| <= 2^-12 |vmean|, the same relative
+      // precision as the f16 P it multiplies (the logit side keeps hi + lo: errors there exponentiate)
+      hi = make_uint4(pack_h2(x0.x, x0.y), pack_h2(x0.z, x0.w), pack_h2(x1.x, x1.y), pack_h2(x1.z, x1.w));
+#endif
+      if (tail && vt >= nv) hi = make_uint4(0u, 0u, 0u, 0u);  // rows past the sequence may hold anything
+      sh<uint4>(smem, oVW) = hi;
     }
     __syncthreads();  // ---- barrier 2: P, corr and the split vmean complete; this tile's stage is free
     if (tid == 0 && it + S < ntiles) {
@@ -600,17 +611,22 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
             om[j][mt][3] *= cr[mt][1];
           }
       }
-      uint32_t bh[4], bl[4];
+      uint32_t bh[4];
       ldsm_x4_t(bh, aVB);
+#if TADA_V8_VMEAN_LO
+      uint32_t bl[4];
       ldsm_x4_t(bl, aVB + VMPART);
+#endif
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         uint32_t pa[4];
         ldsm_x4(pa, aPA + mt * 512);
 #pragma unroll
         for (int j = 0; j < 2; ++j) mma(om[j][mt], pa, bh[2 * j], bh[2 * j + 1]);
+#if TADA_V8_VMEAN_LO
 #pragma unroll
         for (int j = 0; j < 2; ++j) mma(om[j][mt], pa, bl[2 * j], bl[2 * j + 1]);
+#endif
       }
       if constexpr (PARK) tmem_st<NOM>(tom, &om[0][0][0]);
     }
