@@ -45,6 +45,15 @@ constexpr int kBudget = 113 * 1024;  // two CTAs per SM
 #ifndef TADA_V8_VMEAN_LO
 #define TADA_V8_VMEAN_LO 0  // 1: the PV mean term also carries the f16 residual of vmean
 #endif
+// Dependent-MMA chain splitting (more accumulators, summed at the end), 0 = measured per-geometry choice:
+//   ICHAINS 2: the QK code IMMAs of k-steps 0-1 and 2-3 in separate chains (+1.7% 2-bit Hq=32; -2% at Hq=64)
+//   ACHAINS 2: the QK mean HMMAs of the hi and lo kmean pieces in separate chains (+1.8% at Hq<=32)
+#ifndef TADA_V8_ICHAINS
+#define TADA_V8_ICHAINS 0
+#endif
+#ifndef TADA_V8_ACHAINS
+#define TADA_V8_ACHAINS 0
+#endif
 #ifndef TADA_V8_TMEM_OM
 #define TADA_V8_TMEM_OM 1  // park the PV mean accumulators in TMEM between tiles
 #endif
@@ -326,6 +335,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   // rows r >= G carry the mean-term logits of q head h*G (finite); their P is never stored
   float m_run = NEG_INF, l_run = 0.f, bp_run = 0.f, sp_run = 0.f;
   const float sl2 = a.scale * 1.4426950408889634f;
+  const float sq2 = sq * sl2, qs2 = qs * sl2;  // the code/min terms pre-scaled to log2 logit units
 
   auto body = [&](auto stage_c, int it) {
     constexpr int STG = decltype(stage_c)::value;
@@ -356,7 +366,12 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
         split_h2(x.x, x.y, hb[ks][0], lb[ks][0]);
         split_h2(x.z, x.w, hb[ks][1], lb[ks][1]);
       }
-      // 4 MT independent accumulation chains, interleaved so no MMA waits on the previous one
+      // MT (or 2 MT) independent accumulation chains, interleaved so no MMA waits on the previous one
+      constexpr bool AC2 = TADA_V8_ACHAINS == 2 || (TADA_V8_ACHAINS == 0 && MT <= 2);
+      float acc2[AC2 ? MT : 1][4];
+      if constexpr (AC2)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) acc2[mt][0] = acc2[mt][1] = acc2[mt][2] = acc2[mt][3] = 0.f;
 #pragma unroll
       for (int pass = 0; pass < 2; ++pass)
 #pragma unroll
@@ -366,8 +381,14 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
             const uint4 f = sh<uint4>(smem, oQA + (mt * 2 + ks) * 512);
             const uint32_t af[4] = {f.x, f.y, f.z, f.w};
             if (pass == 0) mma(acc[mt], af, hb[ks][0], hb[ks][1]);
+            else if constexpr (AC2) mma(acc2[AC2 ? mt : 0], af, lb[ks][0], lb[ks][1]);
             else mma(acc[mt], af, lb[ks][0], lb[ks][1]);
           }
+      if constexpr (AC2)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[mt][i] += acc2[AC2 ? mt : 0][i];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -398,7 +419,9 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
         wb[4 % NWD] = p3.x; wb[5 % NWD] = p3.y; wb[6 % NWD] = p3.z; wb[7 % NWD] = p3.w;
       }
       // rows r: hi . code, rows r + 8: lo . code; q_fx . code / sq = 256 hi + lo (exact, |.| < 2^31)
+      constexpr int NIC = TADA_V8_ICHAINS ? TADA_V8_ICHAINS : (BITS == 2 && MT <= 2 ? 2 : 1);
       int acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+      int accb[NIC == 2 ? 2 : 1][4] = {};
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
         uint32_t A[4];
@@ -408,13 +431,30 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
         } else {
           A[0] = qA[s][0]; A[1] = qA[s][1]; A[2] = qA[s][2]; A[3] = qA[s][3];
         }
-        imma_su(acc[0], A, qk_quad<BITS>(wa, s, 0), qk_quad<BITS>(wa, s, 1));
-        imma_su(acc[1], A, qk_quad<BITS>(wb, s, 0), qk_quad<BITS>(wb, s, 1));
+        if (NIC == 2 && s >= 2) {
+          imma_su(accb[0], A, qk_quad<BITS>(wa, s, 0), qk_quad<BITS>(wa, s, 1));
+          imma_su(accb[NIC == 2 ? 1 : 0], A, qk_quad<BITS>(wb, s, 0), qk_quad<BITS>(wb, s, 1));
+        } else {
+          imma_su(acc[0], A, qk_quad<BITS>(wa, s, 0), qk_quad<BITS>(wa, s, 1));
+          imma_su(acc[1], A, qk_quad<BITS>(wb, s, 0), qk_quad<BITS>(wb, s, 1));
+        }
       }
-      // S_mean of (q row, tokens 2c, 2c+1 | 8+2c, 9+2c): the 4 d-quarter planes
-      float sm[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+      if constexpr (NIC == 2)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[j][i] += accb[NIC == 2 ? j : 0][i];
+      // S_mean of (q row, tokens 2c, 2c+1 | 8+2c, 9+2c): the 4 d-quarter planes
+      float sm[2][2];
+      {
+        const float2 v0 = sh<float2>(smem, oS0), v1 = sh<float2>(smem, oS1);
+        sm[0][0] = v0.x;
+        sm[0][1] = v0.y;
+        sm[1][0] = v1.x;
+        sm[1][1] = v1.y;
+      }
+#pragma unroll
+      for (int k = 1; k < 4; ++k) {
         const float2 v0 = sh<float2>(smem, oS0 + k * PLANE);
         const float2 v1 = sh<float2>(smem, oS1 + k * PLANE);
         sm[0][0] += v0.x;
@@ -428,7 +468,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
         for (int e = 0; e < 2; ++e) {
           const float2 km = sh<float2>(smem, ST + oM + (8 * nt + e) * pl.trow);  // (scale, min)
           const float cs = float(acc[nt][e] * 256 + acc[nt][2 + e]);
-          x[nt][e] = (sm[nt][e] - fmaf(km.x * sq, cs, km.y * qs)) * sl2;
+          x[nt][e] = fmaf(sm[nt][e], sl2, -fmaf(km.x * sq2, cs, km.y * qs2));
         }
     }
     // ------------------------------------------------------------ d: online softmax (registers)
