@@ -79,7 +79,7 @@ def attn_alg_bytes(bits: int, batch: int, ctx_c: int, ctx_r: int) -> int:
 
 def attn_kernel_name(bits: int, hq: int) -> str:
     """The tensor-core decode kernel tada_decode_attn dispatches for this geometry (tada_attn.cu)."""
-    if bits in (2, 4) and hq in (8, 16, 32):
+    if bits in (2, 4) and hq in (8, 16, 32, 64):
         return f"attn_v8_kernel<{bits},{hq}>"
     return f"attn_fast_kernel<{bits},{hq},{16 if bits != 8 else 32}>"
 
@@ -408,7 +408,7 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic,
                          "kernel": f"decode attention K2+K3 (tada_decode_attn), {dom}-bit layers: {attn_kernel_name(dom, HQ)}"
-                                   f" + combine_residual_kernel",
+                                   f" + combine_pair_kernel (K3)",
                          "alg_bytes_per_launch": attn_alg_bytes(dom, B, T, 1), "peak_source": peak_kind,
                          "frac_of_8tbs_spec": achieved / 8000.0, "per_width": per_width,
                          "all_layers_gbs": attn_bytes / (attn_ms / 1e3) / 1e9,

@@ -282,142 +282,168 @@ __global__ void __launch_bounds__(kCombThreads) combine_residual_kernel(AttnArgs
   }
 }
 
-// K3 for head_dim 128: one warp per (q head, sequence), lane l owning d = 4l .. 4l+3; warp reductions only
-// (no CTA barriers), every independent global load issued before its consumers.
-__global__ void __launch_bounds__(256) combine_residual_warp_kernel(AttnArgs a, int n_rows) {
+// K3 for head_dim 128: two warps per (q head, sequence), lane l owning d = 4l .. 4l+3.  Warp 0 of the
+// pair merges the split partials, warp 1 attends the residual rows (and stores this step's new row);
+// each runs an online softmax over batches of 8 rows whose global loads are all issued before their
+// consumers, and the halves meet in shared memory with one rescale.  (The previous one-warp version
+// walked ~10 dependent global round trips per row: ml, keys by fours, partials, values.)
+__global__ void __launch_bounds__(256) combine_pair_kernel(AttnArgs a, int n_rows) {
   constexpr int D = 128, U = 8;
-  extern __shared__ __align__(16) float csm[];  // [8 warps][res_seq_stride] residual logits
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int row = blockIdx.x * 8 + wib;  // b * Hq + gq
-  if (row >= n_rows) return;
+  __shared__ float rx[4][D + 4];  // residual half of each pair: acc[D], m, l
+  const float NEG_INF = -__int_as_float(0x7f800000);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, pair = wib >> 1, role = wib & 1;
+  const int row = blockIdx.x * 4 + pair;  // b * Hq + gq
+  const bool active = row < n_rows;
   const int Hq = a.Hq, H = a.L.heads, G = Hq / H, S = a.splits;
   const int b = row / Hq, gq = row - b * Hq, h = gq / G;
-  // fused decode step: the residual holds r_prev rows plus this step's row, read from the input
-  const bool fused = a.new_k != nullptr;
-  const int R = fused ? a.r_prev + 1 : a.res_len[b];
-  const int r_new = fused ? a.r_prev : -1;
-  float* pr = csm + wib * a.res_seq_stride;
-  auto new_row = [&](const void* src) {  // this lane's 4 columns of the new row of head h, as f32
-    float x[4];
-    const int64_t off = (int64_t(b) * H + h) * D + 4 * lane;
-    if (a.new_dtype == TADA_F32) load4(reinterpret_cast<const float*>(src) + off, x);
-    else load4(reinterpret_cast<const __nv_bfloat16*>(src) + off, x);
-    return make_float4(x[0], x[1], x[2], x[3]);
-  };
-  if (fused && gq % G == 0) {  // one warp per (sequence, KV head) stores the row for later steps
-    const int64_t dst = ((int64_t(b) * a.res_seq_stride + r_new) * H + h) * D + 4 * lane;
-    *reinterpret_cast<float4*>(const_cast<float*>(a.res_k) + dst) = new_row(a.new_k);
-    *reinterpret_cast<float4*>(const_cast<float*>(a.res_v) + dst) = new_row(a.new_v);
-    if (gq == 0 && lane == 0) const_cast<int32_t*>(a.res_len)[b] = r_new + 1;
-  }
-  const float NEG_INF = -__int_as_float(0x7f800000);
-  float q[4];
-  if (a.q_dtype == TADA_F32) load4(reinterpret_cast<const float*>(a.q) + int64_t(row) * D + 4 * lane, q);
-  else load4(reinterpret_cast<const __nv_bfloat16*>(a.q) + int64_t(row) * D + 4 * lane, q);
-  const float* ml = a.part_ml + int64_t(row) * a.slots * 2;
-  const float* pa = a.part_acc + int64_t(row) * a.slots * D + 4 * lane;
-  // split (m, l): lane s holds split s (s < 32); larger S loops
-  float mx = NEG_INF;
-  for (int s2 = lane; s2 < S; s2 += 32)
-    if (ml[2 * s2 + 1] > 0.f) mx = fmaxf(mx, ml[2 * s2]);
-  // residual logits, four tokens per round (independent shuffle trees)
-  const int64_t rbase = int64_t(b) * a.res_seq_stride;
-  for (int t0 = 0; t0 < R; t0 += 4) {
-    float dot[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      dot[u] = 0.f;
-      if (t0 + u < R) {
-        const float4 k4 = t0 + u == r_new ? new_row(a.new_k)
-                                          : *reinterpret_cast<const float4*>(a.res_k + ((rbase + t0 + u) * H + h) * D + 4 * lane);
-        dot[u] = __fmaf_rn(q[3], k4.w, __fmaf_rn(q[2], k4.z, __fmaf_rn(q[1], k4.y, __fmaf_rn(q[0], k4.x, 0.f))));
+  float acc[4] = {0.f, 0.f, 0.f, 0.f}, m_run = NEG_INF, l_run = 0.f;
+  if (active && role == 0) {  // ---- split partials (natural-log (m, l) per slot)
+    const float* ml = a.part_ml + int64_t(row) * a.slots * 2;
+    const float* pa = a.part_acc + int64_t(row) * a.slots * D + 4 * lane;
+    for (int s0 = 0; s0 < S; s0 += 32) {
+      const int s2 = s0 + lane, n = min(32, S - s0);
+      float m = NEG_INF, l = 0.f;
+      if (s2 < S) {
+        m = ml[2 * s2];
+        l = ml[2 * s2 + 1];
       }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int u = 0; u < 4; ++u) dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], o);
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (t0 + u < R) {
-        const float sv = __fmul_rn(dot[u], a.scale);
-        if (lane == 0) pr[t0 + u] = sv;
-        mx = fmaxf(mx, sv);
-      }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  const float M = mx;
-  __syncwarp();
-  // weighted sums: splits (weights broadcast from the lane that read them), then residual rows
-  float acc[4] = {0.f, 0.f, 0.f, 0.f}, lsum = 0.f;
-  for (int s0 = 0; s0 < S; s0 += 32) {
-    const int s2 = s0 + lane;
-    float w = 0.f;
-    if (s2 < S && ml[2 * s2 + 1] > 0.f) {
-      w = expf(ml[2 * s2] - M);
-      lsum += w * ml[2 * s2 + 1];
-    }
-    const int n = min(32, S - s0);
-    for (int j0 = 0; j0 < n; j0 += U) {
       float4 v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        v[u] = j0 + u < n ? *reinterpret_cast<const float4*>(pa + int64_t(s0 + j0 + u) * D) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[u] = u < n ? *reinterpret_cast<const float4*>(pa + int64_t(s0 + u) * D) : make_float4(0.f, 0.f, 0.f, 0.f);
+      float mc = l > 0.f ? m : NEG_INF;
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const float wu = __shfl_sync(0xffffffffu, w, (j0 + u) & 31);
-        acc[0] = fmaf(wu, v[u].x, acc[0]);
-        acc[1] = fmaf(wu, v[u].y, acc[1]);
-        acc[2] = fmaf(wu, v[u].z, acc[2]);
-        acc[3] = fmaf(wu, v[u].w, acc[3]);
+      for (int o = 16; o > 0; o >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+      const float mn = fmaxf(m_run, mc);
+      if (mn == NEG_INF) continue;  // every slot of this chunk (and before) is empty
+      const float cf = m_run == NEG_INF ? 0.f : expf(m_run - mn);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[e] *= cf;
+      l_run *= cf;
+      m_run = mn;
+      const float w = l > 0.f ? expf(m - mn) : 0.f;
+      l_run += w * l;  // lane-partial; reduced below
+      for (int j0 = 0; j0 < n; j0 += U) {
+        float4 nv[U];
+        const bool more = j0 + U < n;
+        if (more)
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            nv[u] = j0 + U + u < n ? *reinterpret_cast<const float4*>(pa + int64_t(s0 + j0 + U + u) * D)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const float wu = __shfl_sync(0xffffffffu, w, (j0 + u) & 31);
+          acc[0] = fmaf(wu, v[u].x, acc[0]);
+          acc[1] = fmaf(wu, v[u].y, acc[1]);
+          acc[2] = fmaf(wu, v[u].z, acc[2]);
+          acc[3] = fmaf(wu, v[u].w, acc[3]);
+        }
+        if (more)
+#pragma unroll
+          for (int u = 0; u < U; ++u) v[u] = nv[u];
       }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l_run += __shfl_xor_sync(0xffffffffu, l_run, o);
   }
-  for (int t0 = 0; t0 < R; t0 += U) {
-    float4 v[U];
+  if (active && role == 1) {  // ---- residual rows (raw f32; this step's row read from the input)
+    const bool fused = a.new_k != nullptr;
+    const int R = fused ? a.r_prev + 1 : a.res_len[b];
+    const int r_new = fused ? a.r_prev : -1;
+    auto new_row = [&](const void* src) {  // this lane's 4 columns of the new row of head h, as f32
+      float x[4];
+      const int64_t off = (int64_t(b) * H + h) * D + 4 * lane;
+      if (a.new_dtype == TADA_F32) load4(reinterpret_cast<const float*>(src) + off, x);
+      else load4(reinterpret_cast<const __nv_bfloat16*>(src) + off, x);
+      return make_float4(x[0], x[1], x[2], x[3]);
+    };
+    if (fused && gq % G == 0) {  // one warp per (sequence, KV head) stores the row for later steps
+      const int64_t dst = ((int64_t(b) * a.res_seq_stride + r_new) * H + h) * D + 4 * lane;
+      *reinterpret_cast<float4*>(const_cast<float*>(a.res_k) + dst) = new_row(a.new_k);
+      *reinterpret_cast<float4*>(const_cast<float*>(a.res_v) + dst) = new_row(a.new_v);
+      if (gq == 0 && lane == 0) const_cast<int32_t*>(a.res_len)[b] = r_new + 1;
+    }
+    float q[4];
+    if (a.q_dtype == TADA_F32) load4(reinterpret_cast<const float*>(a.q) + int64_t(row) * D + 4 * lane, q);
+    else load4(reinterpret_cast<const __nv_bfloat16*>(a.q) + int64_t(row) * D + 4 * lane, q);
+    const int64_t rbase = int64_t(b) * a.res_seq_stride;
+    for (int t0 = 0; t0 < R; t0 += U) {
+      float4 k4[U], v4[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      v[u] = t0 + u >= R ? make_float4(0.f, 0.f, 0.f, 0.f)
-                         : (t0 + u == r_new ? new_row(a.new_v)
-                                            : *reinterpret_cast<const float4*>(a.res_v + ((rbase + t0 + u) * H + h) * D + 4 * lane));
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + u;
+        const int64_t o = ((rbase + t) * H + h) * D + 4 * lane;
+        k4[u] = t >= R ? make_float4(0.f, 0.f, 0.f, 0.f)
+                       : (t == r_new ? new_row(a.new_k) : *reinterpret_cast<const float4*>(a.res_k + o));
+        v4[u] = t >= R ? make_float4(0.f, 0.f, 0.f, 0.f)
+                       : (t == r_new ? new_row(a.new_v) : *reinterpret_cast<const float4*>(a.res_v + o));
+      }
+      float sv[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const float p = t0 + u < R ? expf(pr[t0 + u] - M) : 0.f;
-      if (lane == 0) lsum += p;
-      acc[0] = fmaf(p, v[u].x, acc[0]);
-      acc[1] = fmaf(p, v[u].y, acc[1]);
-      acc[2] = fmaf(p, v[u].z, acc[2]);
-      acc[3] = fmaf(p, v[u].w, acc[3]);
+      for (int u = 0; u < U; ++u)
+        sv[u] = __fmaf_rn(q[3], k4[u].w, __fmaf_rn(q[2], k4[u].z, __fmaf_rn(q[1], k4[u].y, __fmaf_rn(q[0], k4[u].x, 0.f))));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < U; ++u) sv[u] += __shfl_xor_sync(0xffffffffu, sv[u], o);
+      float bm = NEG_INF;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        sv[u] = t0 + u < R ? __fmul_rn(sv[u], a.scale) : NEG_INF;
+        bm = fmaxf(bm, sv[u]);
+      }
+      const float mn = fmaxf(m_run, bm);  // finite: every batch has a valid row
+      const float cf = m_run == NEG_INF ? 0.f : expf(m_run - mn);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[e] *= cf;
+      l_run *= cf;
+      m_run = mn;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float p = t0 + u < R ? expf(sv[u] - mn) : 0.f;
+        l_run += p;
+        acc[0] = fmaf(p, v4[u].x, acc[0]);
+        acc[1] = fmaf(p, v4[u].y, acc[1]);
+        acc[2] = fmaf(p, v4[u].z, acc[2]);
+        acc[3] = fmaf(p, v4[u].w, acc[3]);
+      }
+    }
+    *reinterpret_cast<float4*>(&rx[pair][4 * lane]) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    if (lane == 0) {
+      rx[pair][D] = m_run;
+      rx[pair][D + 1] = l_run;
     }
   }
+  __syncthreads();
+  if (active && role == 0) {  // ---- merge the halves
+    const float mr = rx[pair][D], lr = rx[pair][D + 1];
+    const float M = fmaxf(m_run, mr);
+    const float fs = m_run == NEG_INF ? 0.f : expf(m_run - M), fr = mr == NEG_INF ? 0.f : expf(mr - M);
+    const float L = l_run * fs + lr * fr;
+    const float inv = 1.f / L;
+    const float4 ar = *reinterpret_cast<const float4*>(&rx[pair][4 * lane]);
+    const float o[4] = {acc[0] * fs + ar.x * fr, acc[1] * fs + ar.y * fr, acc[2] * fs + ar.z * fr,
+                        acc[3] * fs + ar.w * fr};
+    const int64_t qi = int64_t(row) * D + 4 * lane;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-  const float inv = 1.f / lsum;
-  const int64_t qi = int64_t(row) * D + 4 * lane;
-#pragma unroll
-  for (int e = 0; e < 4; ++e) store_any(a.out, a.out_dtype, qi + e, acc[e] * inv);
-  if (lane == 0 && a.lse_out) a.lse_out[row] = M + logf(lsum);
+    for (int e = 0; e < 4; ++e) store_any(a.out, a.out_dtype, qi + e, o[e] * inv);
+    if (lane == 0 && a.lse_out) a.lse_out[row] = M + logf(L);
+  }
 }
 
 static int launch_combine_residual(const AttnArgs& a, int batch, cudaStream_t st) {
   if (a.L.head_dim * 2 > kCombThreads * 2 || a.L.head_dim % 4) return fail(TADA_ERR_CONFIG, "combine needs head_dim % 4 == 0");
+  if (a.L.head_dim == 128) {  // any residual length: the pair kernel streams the rows
+    const int rows = a.Hq * batch;
+    combine_pair_kernel<<<(rows + 3) / 4, 256, 0, st>>>(a, rows);
+    return check_launch("decode_attn_combine_residual");
+  }
   const size_t smem = (size_t(a.L.head_dim) * 3 + size_t(a.res_seq_stride) + size_t(a.splits) + 8) * 4;
   if (smem > 220 * 1024) return fail(TADA_ERR_CONFIG, "residual_length too large for the combine kernel");
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(combine_residual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string("combine smem: ") + cudaGetErrorString(e));
-  }
-  if (a.L.head_dim == 128) {
-    const int rows = a.Hq * batch;
-    const size_t wsm = size_t(8) * a.res_seq_stride * 4;
-    if (wsm > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(combine_residual_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(wsm));
-      if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string("combine smem: ") + cudaGetErrorString(e));
-    }
-    combine_residual_warp_kernel<<<(rows + 7) / 8, 256, wsm, st>>>(a, rows);
-    return check_launch("decode_attn_combine_residual");
   }
   combine_residual_kernel<<<dim3(a.Hq, batch), kCombThreads, smem, st>>>(a);
   return check_launch("decode_attn_combine_residual");
