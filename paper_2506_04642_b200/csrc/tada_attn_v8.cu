@@ -179,7 +179,11 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   // per-warp rescale flags instead of a corr scan in phase C: +2.5% at Hq=64, -1..2% at Hq<=32 (measured)
   constexpr bool FLAGS = MT >= 4;
   constexpr int NOM = 8 * MT;
-  constexpr uint32_t TCOLS = 2 * NOM < 32 ? 32u : uint32_t(2 * NOM);
+  // QTM: where shared memory has no room for the IMMA q fragments (4-bit Hq=64) they are parked in TMEM
+  // too (16 columns per thread after the om block) instead of occupying 16 registers in the loop
+  constexpr bool QTM = PARK && !pl.qi_smem;
+  constexpr int TUSED = 2 * NOM + (QTM ? 32 : 0);
+  constexpr uint32_t TCOLS = TUSED <= 32 ? 32u : (TUSED <= 64 ? 64u : (TUSED <= 128 ? 128u : 256u));
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + pl.off_bar + 64);
   if constexpr (PARK) {
     if (warp == 0) tmem_alloc(tslot, TCOLS);
@@ -192,6 +196,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
     tbase = *tslot;
     tom = tbase + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * NOM);
   }
+  const uint32_t tq = tbase + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(2 * NOM + (warp >> 2) * 16);
 
   // TMA producer (thread 0): tile `it` -> stage it % S, three copies (means, codes, metas; both sides).
   // The (page, row) cursor advances by TT rows per tile (P is a multiple of TT): no divisions in the loop.
@@ -271,6 +276,15 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
     isum += __shfl_xor_sync(0xffffffffu, isum, 1);
     isum += __shfl_xor_sync(0xffffffffu, isum, 2);
     qs = sq * float(isum);
+    if constexpr (QTM) {
+      float qf[16];
+#pragma unroll
+      for (int s = 0; s < 4; ++s)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) qf[4 * s + i] = __uint_as_float(qA[s][i]);
+      tmem_st<16>(tq, qf);
+      tmem_wait_st();
+    }
     if (pl.qi_smem)
 #pragma unroll
       for (int s = 0; s < 4; ++s)
@@ -423,6 +437,11 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
       // rows r: hi . code, rows r + 8: lo . code; q_fx . code / sq = 256 hi + lo (exact, |.| < 2^31)
       constexpr int NIC = TADA_V8_ICHAINS ? TADA_V8_ICHAINS : (BITS == 2 && MT <= 2 ? 2 : 1);
       int acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+      float qf[QTM ? 16 : 1];
+      if constexpr (QTM) {
+        tmem_ld<16>(tq, qf);
+        tmem_wait_ld();
+      }
       int accb[NIC == 2 ? 2 : 1][4] = {};
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
@@ -431,7 +450,12 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
           const uint4 f = sh<uint4>(smem, oQI + s * 512);
           A[0] = f.x; A[1] = f.y; A[2] = f.z; A[3] = f.w;
         } else {
-          A[0] = qA[s][0]; A[1] = qA[s][1]; A[2] = qA[s][2]; A[3] = qA[s][3];
+          if constexpr (QTM) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) A[i] = __float_as_uint(qf[QTM ? 4 * s + i : 0]);
+          } else {
+            A[0] = qA[s][0]; A[1] = qA[s][1]; A[2] = qA[s][2]; A[3] = qA[s][3];
+          }
         }
         if (NIC == 2 && s >= 2) {
           imma_su(accb[0], A, qk_quad<BITS>(wa, s, 0), qk_quad<BITS>(wa, s, 1));
