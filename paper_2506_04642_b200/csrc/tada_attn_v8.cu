@@ -54,9 +54,6 @@ constexpr int kBudget = 113 * 1024;  // two CTAs per SM
 #ifndef TADA_V8_ACHAINS
 #define TADA_V8_ACHAINS 0
 #endif
-#ifndef TADA_V8_TMEM_OC
-#define TADA_V8_TMEM_OC 0  // 1: park the PV code accumulators in TMEM outside the PV code MMAs
-#endif
 #ifndef TADA_V8_TMEM_OM
 #define TADA_V8_TMEM_OM 1  // park the PV mean accumulators in TMEM between tiles
 #endif
@@ -185,11 +182,11 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   // QTM: where shared memory has no room for the IMMA q fragments (4-bit Hq=64) they are parked in TMEM
   // too (16 columns per thread after the om block) instead of occupying 16 registers in the loop
   constexpr bool QTM = PARK && !pl.qi_smem;
-  // OCTM: the PV code accumulators (oc, 32 floats) parked in TMEM outside the PV code MMAs
-  constexpr bool OCTM = TADA_V8_TMEM_OC != 0;
-  constexpr bool USE_TM = PARK || OCTM;
+  // (The PV code accumulators oc are NOT parked: their TMEM round trip sits on phase B's critical path,
+  // measured -1..2% at every geometry.)
+  constexpr bool USE_TM = PARK;
   // TMEM columns of one lane (warps w and w+4 share lane quarter w%4; column blocks by w/4)
-  constexpr int C_Q = PARK ? 2 * NOM : 0, C_OC = C_Q + (QTM ? 32 : 0), TUSED = C_OC + (OCTM ? 64 : 0);
+  constexpr int C_Q = 2 * NOM, TUSED = C_Q + (QTM ? 32 : 0);
   constexpr uint32_t TCOLS = TUSED <= 32 ? 32u : (TUSED <= 64 ? 64u : (TUSED <= 128 ? 128u : 256u));
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + pl.off_bar + 64);
   if constexpr (USE_TM) {
@@ -205,7 +202,6 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   const uint32_t tlane = tbase + (uint32_t(32 * (warp & 3)) << 16);
   const uint32_t tom = tlane + uint32_t((warp >> 2) * NOM);
   const uint32_t tq = tlane + uint32_t(C_Q + (warp >> 2) * 16);
-  const uint32_t toc = tlane + uint32_t(C_OC + (warp >> 2) * 32);
 
   // TMA producer (thread 0): tile `it` -> stage it % S, three copies (means, codes, metas; both sides).
   // The (page, row) cursor advances by TT rows per tile (P is a multiple of TT): no divisions in the loop.
@@ -356,7 +352,6 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) om[j][mt][0] = om[j][mt][1] = om[j][mt][2] = om[j][mt][3] = 0.f;
   if constexpr (PARK) tmem_st<NOM>(tom, &om[0][0][0]);
-  if constexpr (OCTM) tmem_st<32>(toc, &oc[0][0]);
   const float NEG_INF = -__int_as_float(0x7f800000);
   // rows r >= G carry the mean-term logits of q head h*G (finite); their P is never stored
   float m_run = NEG_INF, l_run = 0.f, bp_run = 0.f, sp_run = 0.f;
@@ -566,11 +561,6 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
       l_run = fmaf(l_run, corr, lsum);
       bp_run = fmaf(bp_run, corr, bsum);
       sp_run = fmaf(sp_run, corr, ssum);
-      if constexpr (OCTM) {
-        tmem_wait_st();
-        tmem_ld<32>(toc, &oc[0][0]);
-        tmem_wait_ld();
-      }
       if (resc) {  // columns n = 2c, 2c+1 of oc belong to the softmax rows of lanes 4n
         const float c0 = __shfl_sync(0xffffffffu, corr, 8 * c), c1 = __shfl_sync(0xffffffffu, corr, 8 * c + 4);
 #pragma unroll
@@ -642,7 +632,6 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
         mma(oc[mt], af, bq0, bq1);
       }
     }
-    if constexpr (OCTM) tmem_st<32>(toc, &oc[0][0]);
     // ------------------------------------------------------------ this warp's share of the vmean split
     {  // token vt, d = 8vu .. 8vu+7 -> f16 hi / lo rows [tok][d] (16-B chunk vu at vu ^ (vt & 7))
       const float4 x0 = sh<float4>(smem, ST + oV0), x1 = sh<float4>(smem, ST + oV1);
@@ -757,7 +746,6 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   if constexpr (USE_TM) {
     tmem_wait_st();
     if constexpr (PARK) tmem_ld<NOM>(tom, &om[0][0][0]);
-    if constexpr (OCTM) tmem_ld<32>(toc, &oc[0][0]);
     tmem_wait_ld();
     tc_fence_before();  // the __syncthreads below orders every warp's last TMEM read before the dealloc
   }
