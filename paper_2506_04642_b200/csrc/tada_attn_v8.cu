@@ -54,6 +54,9 @@ constexpr int kBudget = 113 * 1024;  // two CTAs per SM
 #ifndef TADA_V8_ACHAINS
 #define TADA_V8_ACHAINS 0
 #endif
+#ifndef TADA_V8_QTM
+#define TADA_V8_QTM 2  // IMMA q fragments in TMEM: 0 where shared memory has no room, 1 at Hq=64, 2 always
+#endif
 #ifndef TADA_V8_TMEM_OM
 #define TADA_V8_TMEM_OM 1  // park the PV mean accumulators in TMEM between tiles
 #endif
@@ -179,14 +182,15 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   // per-warp rescale flags instead of a corr scan in phase C: +2.5% at Hq=64, -1..2% at Hq<=32 (measured)
   constexpr bool FLAGS = MT >= 4;
   constexpr int NOM = 8 * MT;
-  // QTM: where shared memory has no room for the IMMA q fragments (4-bit Hq=64) they are parked in TMEM
-  // too (16 columns per thread after the om block) instead of occupying 16 registers in the loop
-  constexpr bool QTM = PARK && !pl.qi_smem;
+  // QTM: the IMMA q fragments (16 values per thread) live in TMEM and come back with one tcgen05.ld per
+  // tile, instead of 4 LDS.128 from shared memory (or 16 registers where shared memory has no room):
+  // measured +6.3% 4-bit Hq=32, +2.5% 2-bit Hq=32, +4.2% 2-bit Hq=64, +1.2% 4-bit Hq=64 (vs registers)
+  constexpr bool QTM = TADA_V8_QTM == 2 || (TADA_V8_QTM == 1 && PARK) || (PARK && !pl.qi_smem);
   // (The PV code accumulators oc are NOT parked: their TMEM round trip sits on phase B's critical path,
   // measured -1..2% at every geometry.)
-  constexpr bool USE_TM = PARK;
+  constexpr bool USE_TM = PARK || QTM;
   // TMEM columns of one lane (warps w and w+4 share lane quarter w%4; column blocks by w/4)
-  constexpr int C_Q = 2 * NOM, TUSED = C_Q + (QTM ? 32 : 0);
+  constexpr int C_Q = PARK ? 2 * NOM : 0, TUSED = C_Q + (QTM ? 32 : 0);
   constexpr uint32_t TCOLS = TUSED <= 32 ? 32u : (TUSED <= 64 ? 64u : (TUSED <= 128 ? 128u : 256u));
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + pl.off_bar + 64);
   if constexpr (USE_TM) {
@@ -290,7 +294,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
       tmem_st<16>(tq, qf);
       tmem_wait_st();
     }
-    if (pl.qi_smem)
+    if (pl.qi_smem && !QTM)
 #pragma unroll
       for (int s = 0; s < 4; ++s)
         sh<uint4>(smem, pl.off_qi + (warp * 4 + s) * 512 + lane * 16) = make_uint4(qA[s][0], qA[s][1], qA[s][2], qA[s][3]);
@@ -451,16 +455,14 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
         uint32_t A[4];
-        if (pl.qi_smem) {
+        if constexpr (QTM) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) A[i] = __float_as_uint(qf[QTM ? 4 * s + i : 0]);
+        } else if (pl.qi_smem) {
           const uint4 f = sh<uint4>(smem, oQI + s * 512);
           A[0] = f.x; A[1] = f.y; A[2] = f.z; A[3] = f.w;
         } else {
-          if constexpr (QTM) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) A[i] = __float_as_uint(qf[QTM ? 4 * s + i : 0]);
-          } else {
-            A[0] = qA[s][0]; A[1] = qA[s][1]; A[2] = qA[s][2]; A[3] = qA[s][3];
-          }
+          A[0] = qA[s][0]; A[1] = qA[s][1]; A[2] = qA[s][2]; A[3] = qA[s][3];
         }
         if (NIC == 2 && s >= 2) {
           imma_su(accb[0], A, qk_quad<BITS>(wa, s, 0), qk_quad<BITS>(wa, s, 1));
