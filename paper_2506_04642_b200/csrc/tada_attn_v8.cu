@@ -57,6 +57,9 @@ constexpr int kBudget = 113 * 1024;  // two CTAs per SM
 #ifndef TADA_V8_QTM
 #define TADA_V8_QTM 2  // IMMA q fragments in TMEM: 0 where shared memory has no room, 1 at Hq=64, 2 always
 #endif
+#ifndef TADA_V8_QATM
+#define TADA_V8_QATM 0  // QK mean q fragments in TMEM: 0 = at Hq<=32 (measured +0.9%; -1% at Hq=64), 1 always, -1 never
+#endif
 #ifndef TADA_V8_TMEM_OM
 #define TADA_V8_TMEM_OM 1  // park the PV mean accumulators in TMEM between tiles
 #endif
@@ -188,9 +191,12 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   constexpr bool QTM = TADA_V8_QTM == 2 || (TADA_V8_QTM == 1 && PARK) || (PARK && !pl.qi_smem);
   // (The PV code accumulators oc are NOT parked: their TMEM round trip sits on phase B's critical path,
   // measured -1..2% at every geometry.)
-  constexpr bool USE_TM = PARK || QTM;
+  // QATM: the QK mean A fragments of this warp's d quarter (8*MT values) in TMEM too, one tcgen05.ld per
+  // tile instead of 2*MT LDS.128
+  constexpr bool QATM = TADA_V8_QATM == 1 || (TADA_V8_QATM == 0 && MT <= 2);
+  constexpr bool USE_TM = PARK || QTM || QATM;
   // TMEM columns of one lane (warps w and w+4 share lane quarter w%4; column blocks by w/4)
-  constexpr int C_Q = PARK ? 2 * NOM : 0, TUSED = C_Q + (QTM ? 32 : 0);
+  constexpr int C_Q = PARK ? 2 * NOM : 0, C_QA = C_Q + (QTM ? 32 : 0), TUSED = C_QA + (QATM ? 16 * MT : 0);
   constexpr uint32_t TCOLS = TUSED <= 32 ? 32u : (TUSED <= 64 ? 64u : (TUSED <= 128 ? 128u : 256u));
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + pl.off_bar + 64);
   if constexpr (USE_TM) {
@@ -206,6 +212,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   const uint32_t tlane = tbase + (uint32_t(32 * (warp & 3)) << 16);
   const uint32_t tom = tlane + uint32_t((warp >> 2) * NOM);
   const uint32_t tq = tlane + uint32_t(C_Q + (warp >> 2) * 16);
+  const uint32_t tqa = tlane + uint32_t(C_QA + (warp >> 2) * 8 * MT);
 
   // TMA producer (thread 0): tile `it` -> stage it % S, three copies (means, codes, metas; both sides).
   // The (page, row) cursor advances by TT rows per tile (P is a multiple of TT): no divisions in the loop.
@@ -316,6 +323,19 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
     issue(S - 1);
   }
   if (tid == 0 && S < ntiles) cur_page = pt[cur_pg];  // the page of the next refill, loaded a tile ahead
+  if constexpr (QATM) {  // this warp's d quarter of the QK mean A fragments -> TMEM
+    float v[8 * MT];
+#pragma unroll
+    for (int f = 0; f < 2 * MT; ++f) {
+      const uint4 x = sh<uint4>(smem, pl.off_qa + (warp & 3) * (MT * 2 * 512) + f * 512 + lane * 16);
+      v[4 * f] = __uint_as_float(x.x);
+      v[4 * f + 1] = __uint_as_float(x.y);
+      v[4 * f + 2] = __uint_as_float(x.z);
+      v[4 * f + 3] = __uint_as_float(x.w);
+    }
+    tmem_st<8 * MT>(tqa, v);
+    tmem_wait_st();
+  }
 
   // ---------------------------------------------------------------- per-thread shared offsets
   const int qd = warp & 3, oct = warp >> 2;
@@ -391,6 +411,11 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
         split_h2(x.x, x.y, hb[ks][0], lb[ks][0]);
         split_h2(x.z, x.w, hb[ks][1], lb[ks][1]);
       }
+      float qa[QATM ? 8 * MT : 1];
+      if constexpr (QATM) {
+        tmem_ld<QATM ? 8 * MT : 8>(tqa, qa);
+        tmem_wait_ld();
+      }
       // MT (or 2 MT) independent accumulation chains, interleaved so no MMA waits on the previous one
       constexpr bool AC2 = TADA_V8_ACHAINS == 2 || (TADA_V8_ACHAINS == 0 && MT <= 2);
       float acc2[AC2 ? MT : 1][4];
@@ -403,8 +428,14 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
         for (int ks = 0; ks < 2; ++ks)
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) {
-            const uint4 f = sh<uint4>(smem, oQA + (mt * 2 + ks) * 512);
-            const uint32_t af[4] = {f.x, f.y, f.z, f.w};
+            uint32_t af[4];
+            if constexpr (QATM) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) af[i] = __float_as_uint(qa[QATM ? 4 * (mt * 2 + ks) + i : 0]);
+            } else {
+              const uint4 f = sh<uint4>(smem, oQA + (mt * 2 + ks) * 512);
+              af[0] = f.x; af[1] = f.y; af[2] = f.z; af[3] = f.w;
+            }
             if (pass == 0) mma(acc[mt], af, hb[ks][0], hb[ks][1]);
             else if constexpr (AC2) mma(acc2[AC2 ? mt : 0], af, lb[ks][0], lb[ks][1]);
             else mma(acc[mt], af, lb[ks][0], lb[ks][1]);
