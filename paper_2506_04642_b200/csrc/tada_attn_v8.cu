@@ -60,6 +60,9 @@ constexpr int kBudget = 113 * 1024;  // two CTAs per SM
 #ifndef TADA_V8_QATM
 #define TADA_V8_QATM 0  // QK mean q fragments in TMEM: 0 = at Hq<=32 (measured +0.9%; -1% at Hq=64), 1 always, -1 never
 #endif
+#ifndef TADA_V8_OFTM
+#define TADA_V8_OFTM 1  // phase B's per-thread shared offsets parked in TMEM, reloaded per tile (+0.8..2.5%)
+#endif
 #ifndef TADA_V8_TMEM_OM
 #define TADA_V8_TMEM_OM 1  // park the PV mean accumulators in TMEM between tiles
 #endif
@@ -194,9 +197,10 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   // QATM: the QK mean A fragments of this warp's d quarter (8*MT values) in TMEM too, one tcgen05.ld per
   // tile instead of 2*MT LDS.128
   constexpr bool QATM = TADA_V8_QATM == 1 || (TADA_V8_QATM == 0 && MT <= 2);
-  constexpr bool USE_TM = PARK || QTM || QATM;
+  constexpr bool USE_TM = PARK || QTM || QATM || TADA_V8_OFTM;
   // TMEM columns of one lane (warps w and w+4 share lane quarter w%4; column blocks by w/4)
-  constexpr int C_Q = PARK ? 2 * NOM : 0, C_QA = C_Q + (QTM ? 32 : 0), TUSED = C_QA + (QATM ? 16 * MT : 0);
+  constexpr int C_Q = PARK ? 2 * NOM : 0, C_QA = C_Q + (QTM ? 32 : 0), C_OF = C_QA + (QATM ? 16 * MT : 0);
+  constexpr int TUSED = C_OF + (TADA_V8_OFTM ? 32 : 0);
   constexpr uint32_t TCOLS = TUSED <= 32 ? 32u : (TUSED <= 64 ? 64u : (TUSED <= 128 ? 128u : 256u));
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + pl.off_bar + 64);
   if constexpr (USE_TM) {
@@ -213,6 +217,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   const uint32_t tom = tlane + uint32_t((warp >> 2) * NOM);
   const uint32_t tq = tlane + uint32_t(C_Q + (warp >> 2) * 16);
   const uint32_t tqa = tlane + uint32_t(C_QA + (warp >> 2) * 8 * MT);
+  const uint32_t tof = tlane + uint32_t(C_OF + (warp >> 2) * 16);
 
   // TMA producer (thread 0): tile `it` -> stage it % S, three copies (means, codes, metas; both sides).
   // The (page, row) cursor advances by TT rows per tile (P is a multiple of TT): no divisions in the loop.
@@ -361,6 +366,16 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   const int hbV = h * GB + 2 * r * BITS;
   const int oC0 = 2 * pl.mean_bytes + pl.codes_bytes + (hbV >> 7) * BAND + swz(2 * c, hbV & 127);  // token 2c
   const int oC1 = 2 * pl.mean_bytes + pl.codes_bytes + (hbV >> 7) * BAND + swz(2 * c + 1, hbV & 127);
+#if TADA_V8_OFTM
+  {  // phase B's shared offsets -> TMEM (reloaded per tile: their registers are free outside phase B)
+    float v[16];
+    const int o[12] = {oK, oK2, oS0, oS1, oM, oPW, oC0, oC1, oV0, oV1, oVW, pch};
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __int_as_float(i < 12 ? o[i] : 0);
+    tmem_st<16>(tof, v);
+    tmem_wait_st();
+  }
+#endif
   // PV mean piece (warp = d slice 16w .. 16w+15): ldmatrix lane addresses
   const uint32_t aPA = su32(smem + pl.off_p) + ((lane & 7) + 8 * ((lane >> 3) & 1)) * 32 +
                        (((lane >> 4) ^ (((lane & 7) >> 2) & 1)) << 4);  // + 512 per q tile
@@ -452,6 +467,15 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
           sh<float2>(smem, oSW + (16 * mt + 8 * e) * TT * 4) = make_float2(acc[mt][2 * e], acc[mt][2 * e + 1]);
     }
     __syncthreads();  // ---- barrier 1: S_mean complete; the previous tile's P and split vmean are consumed
+#if TADA_V8_OFTM
+    float ofv[16];
+    tmem_ld<16>(tof, ofv);
+    tmem_wait_ld();
+    const int oK = __float_as_int(ofv[0]), oK2 = __float_as_int(ofv[1]), oS0 = __float_as_int(ofv[2]);
+    const int oS1 = __float_as_int(ofv[3]), oM = __float_as_int(ofv[4]), oPW = __float_as_int(ofv[5]);
+    const int oC0 = __float_as_int(ofv[6]), oC1 = __float_as_int(ofv[7]), oV0 = __float_as_int(ofv[8]);
+    const int oV1 = __float_as_int(ofv[9]), oVW = __float_as_int(ofv[10]), pch = __float_as_int(ofv[11]);
+#endif
 
     // ------------------------------------------------------------ c: QK code term (q on M) + logits
     float x[2][2];  // logits (log2 units) of q head h*G + r for tokens 8nt + 2c + e
