@@ -61,7 +61,7 @@ constexpr int kBudget = 113 * 1024;  // two CTAs per SM
 #define TADA_V8_QATM 0  // QK mean q fragments in TMEM: 0 = at Hq<=32 (measured +0.9%; -1% at Hq=64), 1 always, -1 never
 #endif
 #ifndef TADA_V8_OFTM
-#define TADA_V8_OFTM 1  // phase B's per-thread shared offsets parked in TMEM, reloaded per tile (+0.8..2.5%)
+#define TADA_V8_OFTM 2  // per-thread shared offsets in TMEM, reloaded per phase: 1 = phase B only (+0.8..2.5%), 2 = + phases A/C and the logit constants (+0.1..2.3% more)
 #endif
 #ifndef TADA_V8_TMEM_OM
 #define TADA_V8_TMEM_OM 1  // park the PV mean accumulators in TMEM between tiles
@@ -200,7 +200,8 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   constexpr bool USE_TM = PARK || QTM || QATM || TADA_V8_OFTM;
   // TMEM columns of one lane (warps w and w+4 share lane quarter w%4; column blocks by w/4)
   constexpr int C_Q = PARK ? 2 * NOM : 0, C_QA = C_Q + (QTM ? 32 : 0), C_OF = C_QA + (QATM ? 16 * MT : 0);
-  constexpr int TUSED = C_OF + (TADA_V8_OFTM ? 32 : 0);
+  constexpr int C_OF2 = C_OF + (TADA_V8_OFTM ? 32 : 0);  // phase A / C offsets (OFTM 2): 8 per warp
+  constexpr int TUSED = C_OF2 + (TADA_V8_OFTM >= 2 ? 16 : 0);
   constexpr uint32_t TCOLS = TUSED <= 32 ? 32u : (TUSED <= 64 ? 64u : (TUSED <= 128 ? 128u : 256u));
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + pl.off_bar + 64);
   if constexpr (USE_TM) {
@@ -218,6 +219,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   const uint32_t tq = tlane + uint32_t(C_Q + (warp >> 2) * 16);
   const uint32_t tqa = tlane + uint32_t(C_QA + (warp >> 2) * 8 * MT);
   const uint32_t tof = tlane + uint32_t(C_OF + (warp >> 2) * 16);
+  const uint32_t tof2 = tlane + uint32_t(C_OF2 + (warp >> 2) * 8);
 
   // TMA producer (thread 0): tile `it` -> stage it % S, three copies (means, codes, metas; both sides).
   // The (page, row) cursor advances by TT rows per tile (P is a multiple of TT): no divisions in the loop.
@@ -366,16 +368,6 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   const int hbV = h * GB + 2 * r * BITS;
   const int oC0 = 2 * pl.mean_bytes + pl.codes_bytes + (hbV >> 7) * BAND + swz(2 * c, hbV & 127);  // token 2c
   const int oC1 = 2 * pl.mean_bytes + pl.codes_bytes + (hbV >> 7) * BAND + swz(2 * c + 1, hbV & 127);
-#if TADA_V8_OFTM
-  {  // phase B's shared offsets -> TMEM (reloaded per tile: their registers are free outside phase B)
-    float v[16];
-    const int o[12] = {oK, oK2, oS0, oS1, oM, oPW, oC0, oC1, oV0, oV1, oVW, pch};
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __int_as_float(i < 12 ? o[i] : 0);
-    tmem_st<16>(tof, v);
-    tmem_wait_st();
-  }
-#endif
   // PV mean piece (warp = d slice 16w .. 16w+15): ldmatrix lane addresses
   const uint32_t aPA = su32(smem + pl.off_p) + ((lane & 7) + 8 * ((lane >> 3) & 1)) * 32 +
                        (((lane >> 4) ^ (((lane & 7) >> 2) & 1)) << 4);  // + 512 per q tile
@@ -396,6 +388,27 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   float m_run = NEG_INF, l_run = 0.f, bp_run = 0.f, sp_run = 0.f;
   const float sl2 = a.scale * 1.4426950408889634f;
   const float sq2 = sq * sl2, qs2 = qs * sl2;  // the code/min terms pre-scaled to log2 logit units
+#if TADA_V8_OFTM
+  {  // phase B's shared offsets -> TMEM (reloaded per tile: their registers are free outside phase B)
+    float v[16];
+    const int o[12] = {oK, oK2, oS0, oS1, oM, oPW, oC0, oC1, oV0, oV1, oVW, pch};
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __int_as_float(i < 12 ? o[i] : 0);
+#if TADA_V8_OFTM >= 2
+    v[12] = sq2;
+    v[13] = qs2;
+    {
+      float w[8];
+      const int o2[6] = {oX0, oX1, oQA, oSW, int(aPA), int(aVB)};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[i] = __int_as_float(i < 6 ? o2[i] : 0);
+      tmem_st<8>(tof2, w);
+    }
+#endif
+    tmem_st<16>(tof, v);
+    tmem_wait_st();
+  }
+#endif
 
   auto body = [&](auto stage_c, int it) {
     constexpr int STG = decltype(stage_c)::value;
@@ -416,6 +429,13 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
 
     // ------------------------------------------------------------ A: QK mean piece -> S_mean plane qd
     {
+#if TADA_V8_OFTM >= 2
+      float ofa[4];
+      tmem_ld<4>(tof2, ofa);
+      tmem_wait_ld();
+      const int oX0 = __float_as_int(ofa[0]), oX1 = __float_as_int(ofa[1]);
+      const int oQA = __float_as_int(ofa[2]), oSW = __float_as_int(ofa[3]);
+#endif
       float acc[MT][4];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
@@ -475,6 +495,9 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
     const int oS1 = __float_as_int(ofv[3]), oM = __float_as_int(ofv[4]), oPW = __float_as_int(ofv[5]);
     const int oC0 = __float_as_int(ofv[6]), oC1 = __float_as_int(ofv[7]), oV0 = __float_as_int(ofv[8]);
     const int oV1 = __float_as_int(ofv[9]), oVW = __float_as_int(ofv[10]), pch = __float_as_int(ofv[11]);
+#if TADA_V8_OFTM >= 2
+    const float sq2 = ofv[12], qs2 = ofv[13];
+#endif
 #endif
 
     // ------------------------------------------------------------ c: QK code term (q on M) + logits
@@ -717,6 +740,12 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
     }
     // ------------------------------------------------------------ C: PV mean piece (d slice of this warp)
     {
+#if TADA_V8_OFTM >= 2
+      float ofc[2];
+      tmem_ld<2>(tof2 + 4, ofc);
+      tmem_wait_ld();
+      const uint32_t aPA = __float_as_uint(ofc[0]), aVB = __float_as_uint(ofc[1]);
+#endif
       // FLAGS: one 8-byte read of the per-warp rescale flags (rare after the first tiles) decides whether
       // to touch corr at all; otherwise every thread reads its rows' corr and the warp votes
       float cr[MT][2];

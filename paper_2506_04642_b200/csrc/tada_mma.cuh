@@ -68,8 +68,13 @@ __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.
     "f"(v[o + 6]), "f"(v[o + 7])
 template <int N>
 __device__ __forceinline__ void tmem_ld(uint32_t taddr, float* v) {
-  static_assert(N == 8 || N == 16 || N == 32, "tmem_ld width");
-  if constexpr (N == 8) {
+  static_assert(N == 2 || N == 4 || N == 8 || N == 16 || N == 32, "tmem_ld width");
+  if constexpr (N == 2) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=f"(v[0]), "=f"(v[1]) : "r"(taddr));
+  } else if constexpr (N == 4) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "r"(taddr));
+  } else if constexpr (N == 8) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : TADA_R8(v, 0) : "r"(taddr));
   } else if constexpr (N == 16) {
