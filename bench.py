@@ -414,11 +414,15 @@ def run_ours(args):
     d2h = out_h.numel() * 2
     store.check_errors()
 
-    traffic = None
+    # dram bytes per launch of the dominant kernel from its ncu --set full capture (tools/make_profiles.py),
+    # taken at B=16 x 32k compressed tokens: the same per-launch bytes as configs 2, 4 (4 x 128k) and 5
+    traffic, traffic_src = None, None
     prof = os.path.join(ROOT, "profiles", "attn_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("traffic_bytes_per_launch")
+            for e in json.load(open(prof)).get("entries", []):
+                if e["bits"] == dom and e["hq"] == HQ and B * T == 16 * 32768:
+                    traffic, traffic_src = e["traffic_bytes_per_launch"], e["source"]
         except Exception:
             traffic = None
 
@@ -437,7 +441,7 @@ def run_ours(args):
                        "kernel_mode": args.mode, "l2": "cache 35 GB/GPU >> 126 MB L2 (no flush needed)"},
             "hbm_gbs": step_bytes / (ms_per_step / 1e3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic,
+                         "traffic": traffic, "traffic_source": traffic_src,
                          "kernel": f"decode attention K2+K3 (tada_decode_attn), {dom}-bit layers: {attn_kernel_name(dom, HQ)}"
                                    f" + combine_pair_kernel (K3)",
                          "alg_bytes_per_launch": attn_alg_bytes(dom, B, T, 1), "peak_source": peak_kind,

@@ -25,9 +25,15 @@ if [[ $what == bench || $what == all ]]; then
   timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 fi
 if [[ $what == prof || $what == all ]]; then
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:${PROF_KERNEL:-attn_v8} -s 3 -c 1 \
-    -o gpurun_out/attn4 -f python tools/attn_bench.py --bits ${PROF_BITS:-4} --iters 2 > gpurun_out/prof.log 2>&1
-  echo "prof rc=$?" >> gpurun_out/prof.log
+  # the dominant kernel of each bench config: 4-bit Hq=32 (config 2), 2-bit Hq=32 (config 4), 4-bit Hq=64 (config 5)
+  : > gpurun_out/prof.log
+  for cfg in ${PROF_CFGS:-4:32 2:32 4:64}; do
+    bits=${cfg%%:*}; hq=${cfg#*:}
+    timeout 600 ncu --set full --clock-control none --import-source on -k regex:${PROF_KERNEL:-attn_v8} -s 3 -c 1 \
+      -o gpurun_out/attn_b${bits}_h${hq} -f python tools/attn_bench.py --bits $bits --hq $hq --iters 2 >> gpurun_out/prof.log 2>&1
+    echo "prof $cfg rc=$?" >> gpurun_out/prof.log
+  done
+  cp gpurun_out/attn_b4_h32.ncu-rep gpurun_out/attn4.ncu-rep 2>/dev/null
 fi
 if [[ $what == ncu || $what == all ]]; then
   # skip prefill (2 launches/layer) + 3 warm-up steps (3 launches/layer/step), list 2 steps

@@ -1,8 +1,10 @@
 """Copy the judged evidence from gpurun_out/ (scratch) into profiles/ (tracked).
 
 python tools/make_profiles.py <tag>
-  gpurun_out/attn4.ncu-rep  -> profiles/<tag>_attn4_ncu.txt (headline metrics, stalls, opcode mix, hot lines)
-                               profiles/attn_traffic.json   (dram bytes per launch, read by bench.py)
+  gpurun_out/attn_b<bits>_h<hq>.ncu-rep (4:32, 2:32, 4:64)
+                            -> profiles/<tag>_attn4_ncu.txt / <tag>_attn_b2_h32_ncu.txt / <tag>_attn_b4_h64_ncu.txt
+                               (headline metrics, stalls, opcode mix, hot lines)
+                               profiles/attn_traffic.json   (dram bytes per launch per instantiation, read by bench.py)
   gpurun_out/launches.csv   -> profiles/<tag>_launches.csv + profiles/<tag>_launches.txt
   gpurun_out/bench.log      -> profiles/<tag>_bench.json (the bench line)
 """
@@ -26,15 +28,21 @@ def run(*cmd):
 def main():
     tag = sys.argv[1]
     os.makedirs(PROF, exist_ok=True)
-    rep = os.path.join(OUT, "attn4.ncu-rep")
-    if os.path.exists(rep):
-        tiles = 16 * 32768 // 16  # 16-token tiles of attn_v8_kernel<4,32>
+    entries = []
+    for bits, hq in ((4, 32), (2, 32), (4, 64)):
+        rep = os.path.join(OUT, f"attn_b{bits}_h{hq}.ncu-rep")
+        if not os.path.exists(rep) and (bits, hq) == (4, 32):
+            rep = os.path.join(OUT, "attn4.ncu-rep")  # older single-capture sessions
+        if not os.path.exists(rep):
+            continue
+        name = "attn4" if (bits, hq) == (4, 32) else f"attn_b{bits}_h{hq}"
+        tiles = 16 * 32768 // 16  # 16-token tiles of attn_v8_kernel<bits,hq> at B=16, T=32768
         txt = run("tools/ncu_summary.py", rep, str(tiles))
         txt += "\n--- per source line (top 40 by instructions + stalls)\n"
         txt += run("tools/ncu_lines.py", rep, "paper_2506_04642_b200/csrc/tada_attn_v8.cu", "40", str(tiles))
-        open(os.path.join(PROF, f"{tag}_attn4_ncu.txt"), "w").write(
+        open(os.path.join(PROF, f"{tag}_{name}_ncu.txt"), "w").write(
             "ncu --set full --clock-control none --import-source on -k regex:attn_v8 -s 3 -c 1 "
-            "python tools/attn_bench.py --bits 4 (B=16, T=32768, Hq=32, H=8, D=128)\n\n" + txt)
+            f"python tools/attn_bench.py --bits {bits} --hq {hq} (B=16, T=32768, Hq={hq}, H=8, D=128)\n\n" + txt)
         raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
         rows = list(csv.reader(io.StringIO(raw)))
         d = dict(zip(rows[0], rows[2]))
@@ -44,12 +52,14 @@ def main():
             v = float(d[k])
             return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit[k]]
 
-        traffic = nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum")
-        json.dump({"traffic_bytes_per_launch": traffic, "kernel": "attn_v8_kernel<4,32>",
-                   "shape": "B=16, T=32768 compressed, Hq=32, H=8, D=128, 4-bit",
-                   "alg_bytes_per_launch": 16 * (32768 * 2 * (4 * 128 + 8 * 64 + 64) + 2 * 32 * 128 * 2),
-                   "source": f"profiles/{tag}_attn4_ncu.txt"}, open(os.path.join(PROF, "attn_traffic.json"), "w"),
-                  indent=1)
+        gb = 128 * bits // 8
+        entries.append({"kernel": f"attn_v8_kernel<{bits},{hq}>", "bits": bits, "hq": hq,
+                        "traffic_bytes_per_launch": nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum"),
+                        "shape": f"B=16, T=32768 compressed, Hq={hq}, H=8, D=128, {bits}-bit",
+                        "alg_bytes_per_launch": 16 * (32768 * 2 * (4 * 128 + 8 * gb + 64) + 2 * hq * 128 * 2),
+                        "source": f"profiles/{tag}_{name}_ncu.txt"})
+    if entries:
+        json.dump({"entries": entries}, open(os.path.join(PROF, "attn_traffic.json"), "w"), indent=1)
     k1 = os.path.join(OUT, "k1.ncu-rep")
     if os.path.exists(k1):
         open(os.path.join(PROF, f"{tag}_k1_ncu.txt"), "w").write(
