@@ -58,7 +58,7 @@ constexpr int kBudget = 113 * 1024;  // two CTAs per SM
 #define TADA_V8_QTM 2  // IMMA q fragments in TMEM: 0 where shared memory has no room, 1 at Hq=64, 2 always
 #endif
 #ifndef TADA_V8_QATM
-#define TADA_V8_QATM 0  // QK mean q fragments in TMEM: 0 = at Hq<=32 (measured +0.9%; -1% at Hq=64), 1 always, -1 never
+#define TADA_V8_QATM 1  // QK mean q fragments in TMEM: 1 always (+0.8..5.6%), 0 = Hq<=32 only, -1 never
 #endif
 #ifndef TADA_V8_OFTM
 #define TADA_V8_OFTM 2  // per-thread shared offsets in TMEM, reloaded per phase: 1 = phase B only (+0.8..2.5%), 2 = + phases A/C and the logit constants (+0.1..2.3% more)
@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   // TMEM columns of one lane (warps w and w+4 share lane quarter w%4; column blocks by w/4)
   constexpr int C_Q = PARK ? 2 * NOM : 0, C_QA = C_Q + (QTM ? 32 : 0), C_OF = C_QA + (QATM ? 16 * MT : 0);
   constexpr int C_OF2 = C_OF + (TADA_V8_OFTM ? 32 : 0);  // phase A / C offsets (OFTM 2): 8 per warp
+  // (the running softmax state stays in registers: parking it cost 2%, measured)
   constexpr int TUSED = C_OF2 + (TADA_V8_OFTM >= 2 ? 16 : 0);
   constexpr uint32_t TCOLS = TUSED <= 32 ? 32u : (TUSED <= 64 ? 64u : (TUSED <= 128 ? 128u : 256u));
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + pl.off_bar + 64);

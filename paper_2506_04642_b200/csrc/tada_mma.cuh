@@ -88,8 +88,12 @@ __device__ __forceinline__ void tmem_ld(uint32_t taddr, float* v) {
 }
 template <int N>
 __device__ __forceinline__ void tmem_st(uint32_t taddr, const float* v) {
-  static_assert(N == 8 || N == 16 || N == 32, "tmem_st width");
-  if constexpr (N == 8) {
+  static_assert(N == 4 || N == 8 || N == 16 || N == 32, "tmem_st width");
+  if constexpr (N == 4) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "f"(v[0]), "f"(v[1]),
+                 "f"(v[2]), "f"(v[3])
+                 : "memory");
+  } else if constexpr (N == 8) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
                  ::"r"(taddr), TADA_W8(v, 0) : "memory");
   } else if constexpr (N == 16) {
