@@ -282,17 +282,19 @@ __global__ void __launch_bounds__(kCombThreads) combine_residual_kernel(AttnArgs
   }
 }
 
-// K3 for head_dim 128: two warps per (q head, sequence), lane l owning d = 4l .. 4l+3.  Warp 0 of the
-// pair merges the split partials, warp 1 attends the residual rows (and stores this step's new row);
-// each runs an online softmax over batches of 8 rows whose global loads are all issued before their
-// consumers, and the halves meet in shared memory with one rescale.  (The previous one-warp version
-// walked ~10 dependent global round trips per row: ml, keys by fours, partials, values.)
+// K3 for head_dim 128: four warps per (q head, sequence), lane l owning d = 4l .. 4l+3.  Warp 0 of the
+// group merges the split partials, warps 1..3 attend the residual rows (batches of 8 rows round-robin;
+// warp 1 also stores this step's new row); each runs an online softmax whose global loads are all issued
+// before their consumers, and the four parts meet in shared memory with one rescale.  The residual grows
+// by a row per decode step (up to R = 128 between flushes), so its batches are spread over three warps.
+// (The first one-warp version walked ~10 dependent global round trips per row.)
 __global__ void __launch_bounds__(256) combine_pair_kernel(AttnArgs a, int n_rows) {
-  constexpr int D = 128, U = 8;
-  __shared__ float rx[4][D + 4];  // residual half of each pair: acc[D], m, l
+  constexpr int D = 128, U = 8, RW = 3;  // RW residual warps per row
+  __shared__ float rx[2][RW][D + 4];      // residual parts of each row: acc[D], m, l
   const float NEG_INF = -__int_as_float(0x7f800000);
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, pair = wib >> 1, role = wib & 1;
-  const int row = blockIdx.x * 4 + pair;  // b * Hq + gq
+  pdl_enter();  // no global reads above this line
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, pair = wib >> 2, role = wib & 3;
+  const int row = blockIdx.x * 2 + pair;  // b * Hq + gq
   const bool active = row < n_rows;
   const int Hq = a.Hq, H = a.L.heads, G = Hq / H, S = a.splits;
   const int b = row / Hq, gq = row - b * Hq, h = gq / G;
@@ -347,7 +349,8 @@ __global__ void __launch_bounds__(256) combine_pair_kernel(AttnArgs a, int n_row
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) l_run += __shfl_xor_sync(0xffffffffu, l_run, o);
   }
-  if (active && role == 1) {  // ---- residual rows (raw f32; this step's row read from the input)
+  if (active && role >= 1) {  // ---- residual rows (raw f32; this step's row read from the input)
+    const int rw = role - 1;
     const bool fused = a.new_k != nullptr;
     const int R = fused ? a.r_prev + 1 : a.res_len[b];
     const int r_new = fused ? a.r_prev : -1;
@@ -358,7 +361,7 @@ __global__ void __launch_bounds__(256) combine_pair_kernel(AttnArgs a, int n_row
       else load4(reinterpret_cast<const __nv_bfloat16*>(src) + off, x);
       return make_float4(x[0], x[1], x[2], x[3]);
     };
-    if (fused && gq % G == 0) {  // one warp per (sequence, KV head) stores the row for later steps
+    if (fused && gq % G == 0 && rw == 0) {  // one warp per (sequence, KV head) stores the row for later steps
       const int64_t dst = ((int64_t(b) * a.res_seq_stride + r_new) * H + h) * D + 4 * lane;
       *reinterpret_cast<float4*>(const_cast<float*>(a.res_k) + dst) = new_row(a.new_k);
       *reinterpret_cast<float4*>(const_cast<float*>(a.res_v) + dst) = new_row(a.new_v);
@@ -368,7 +371,7 @@ __global__ void __launch_bounds__(256) combine_pair_kernel(AttnArgs a, int n_row
     if (a.q_dtype == TADA_F32) load4(reinterpret_cast<const float*>(a.q) + int64_t(row) * D + 4 * lane, q);
     else load4(reinterpret_cast<const __nv_bfloat16*>(a.q) + int64_t(row) * D + 4 * lane, q);
     const int64_t rbase = int64_t(b) * a.res_seq_stride;
-    for (int t0 = 0; t0 < R; t0 += U) {
+    for (int t0 = U * rw; t0 < R; t0 += U * RW) {
       float4 k4[U], v4[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -409,22 +412,32 @@ __global__ void __launch_bounds__(256) combine_pair_kernel(AttnArgs a, int n_row
         acc[3] = fmaf(p, v4[u].w, acc[3]);
       }
     }
-    *reinterpret_cast<float4*>(&rx[pair][4 * lane]) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    *reinterpret_cast<float4*>(&rx[pair][rw][4 * lane]) = make_float4(acc[0], acc[1], acc[2], acc[3]);
     if (lane == 0) {
-      rx[pair][D] = m_run;
-      rx[pair][D + 1] = l_run;
+      rx[pair][rw][D] = m_run;  // -inf with l = 0 when this warp had no rows
+      rx[pair][rw][D + 1] = l_run;
     }
   }
   __syncthreads();
-  if (active && role == 0) {  // ---- merge the halves
-    const float mr = rx[pair][D], lr = rx[pair][D + 1];
-    const float M = fmaxf(m_run, mr);
-    const float fs = m_run == NEG_INF ? 0.f : expf(m_run - M), fr = mr == NEG_INF ? 0.f : expf(mr - M);
-    const float L = l_run * fs + lr * fr;
+  if (active && role == 0) {  // ---- merge the parts
+    float M = m_run;
+#pragma unroll
+    for (int w = 0; w < RW; ++w) M = fmaxf(M, rx[pair][w][D]);
+    const float fs = m_run == NEG_INF ? 0.f : expf(m_run - M);
+    float L = l_run * fs;
+    float o[4] = {acc[0] * fs, acc[1] * fs, acc[2] * fs, acc[3] * fs};
+#pragma unroll
+    for (int w = 0; w < RW; ++w) {
+      const float mr = rx[pair][w][D];
+      const float fr = mr == NEG_INF ? 0.f : expf(mr - M);
+      L += rx[pair][w][D + 1] * fr;
+      const float4 ar = *reinterpret_cast<const float4*>(&rx[pair][w][4 * lane]);
+      o[0] += ar.x * fr;
+      o[1] += ar.y * fr;
+      o[2] += ar.z * fr;
+      o[3] += ar.w * fr;
+    }
     const float inv = 1.f / L;
-    const float4 ar = *reinterpret_cast<const float4*>(&rx[pair][4 * lane]);
-    const float o[4] = {acc[0] * fs + ar.x * fr, acc[1] * fs + ar.y * fr, acc[2] * fs + ar.z * fr,
-                        acc[3] * fs + ar.w * fr};
     const int64_t qi = int64_t(row) * D + 4 * lane;
 #pragma unroll
     for (int e = 0; e < 4; ++e) store_any(a.out, a.out_dtype, qi + e, o[e] * inv);
@@ -436,7 +449,8 @@ static int launch_combine_residual(const AttnArgs& a, int batch, cudaStream_t st
   if (a.L.head_dim * 2 > kCombThreads * 2 || a.L.head_dim % 4) return fail(TADA_ERR_CONFIG, "combine needs head_dim % 4 == 0");
   if (a.L.head_dim == 128) {  // any residual length: the pair kernel streams the rows
     const int rows = a.Hq * batch;
-    combine_pair_kernel<<<(rows + 3) / 4, 256, 0, st>>>(a, rows);
+    const cudaError_t e = launch_maybe_pdl(combine_pair_kernel, dim3((rows + 1) / 2), dim3(256), 0, st, a, rows);
+    if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string("decode_attn_combine: ") + cudaGetErrorString(e));
     return check_launch("decode_attn_combine_residual");
   }
   const size_t smem = (size_t(a.L.head_dim) * 3 + size_t(a.res_seq_stride) + size_t(a.splits) + 8) * 4;
@@ -467,6 +481,14 @@ static int launch_generic(const AttnArgs& a, int batch, cudaStream_t st) {
   }
   kern<<<dim3(a.splits, batch), 256, smem, st>>>(a);
   return check_launch("decode_attn_generic");
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TADA_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 }  // namespace tada

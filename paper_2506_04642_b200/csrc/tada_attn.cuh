@@ -60,6 +60,35 @@ struct alignas(64) TmaMaps {
 
 // Raise a kernel's dynamic shared-memory limit once per device (thread-safe; `done` is a per-kernel bitmask
 // of devices already configured).
+// Programmatic dependent launch (PDL): decode launches K2 -> K3 -> next layer's K2 back to back.  Each
+// is launched with programmatic stream serialization and, at entry, lets its dependent launch and then
+// waits for its prerequisites (griddepcontrol.wait: previous grid complete, its writes visible) before
+// any global read, so only the launch and CTA ramp overlap the previous kernel's tail, never data.
+// TADA_PDL=0 in the environment turns it off (A/B).
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+bool pdl_enabled();
+template <typename Kern, typename... Args>
+cudaError_t launch_maybe_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  if (!pdl_enabled()) {
+    kern<<<grid, block, smem, st>>>(args...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <typename Kern>
 int ensure_smem(Kern kern, int bytes, std::atomic<uint64_t>& done, const char* what) {
   int dev = 0;

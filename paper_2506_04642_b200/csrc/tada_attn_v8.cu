@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   float* qmax = reinterpret_cast<float*>(smem + (S - 1) * SB + MROWS * D * 2);  // [MROWS], prologue only
   float* red = reinterpret_cast<float*>(smem + pl.off_vm);                     // [3][HQ] epilogue (l, Σp·vmin, m)
 
+  pdl_enter();  // no global reads above this line
   const int C = a.comp_len[b];
   int t_begin, t_end;
   split_range(C, a.splits, split, TT, t_begin, t_end);
@@ -905,7 +906,8 @@ static int launch_v8_t(const AttnArgs& a, int batch, cudaStream_t st) {
     TmaMaps maps;
     const int rc = get_tma_maps(a, &maps, v8::TT);
     if (rc != TADA_OK) return rc;
-    kern<<<dim3(a.splits, batch), v8::NTHR, pl.total, st>>>(a, maps);
+    const cudaError_t e = launch_maybe_pdl(kern, dim3(a.splits, batch), dim3(v8::NTHR), size_t(pl.total), st, a, maps);
+    if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string("decode_attn_v8: ") + cudaGetErrorString(e));
     return check_launch("decode_attn_v8");
   }
 }
