@@ -293,18 +293,22 @@ def run_ours(args):
         q_all = qs[s] if q_in is None else q_in
         k_all = ks[s] if k_in is None else k_in
         v_all = vs[s] if v_in is None else v_in
+        group = None  # record=True: one event pair per run of consecutive same-width layers
         for layer in range(L):
-            if record:
-                e0 = torch.cuda.Event(enable_timing=True)
-                e0.record()
+            if record and (layer == 0 or PLAN[layer] != PLAN[layer - 1]):
+                group = [torch.cuda.Event(enable_timing=True), None, 0, PLAN[layer], 0]
+                group[0].record()
             # one decode step of the layer: append (residual row, or flush through K1) + K2/K3
             store.append_attend(layer, q_all[layer], k_all[layer], v_all[layer], out=outs[layer],
                                 num_splits=splits[PLAN[layer]], mode=args.mode)
             if record:
-                e1 = torch.cuda.Event(enable_timing=True)
-                e1.record()
                 c, r = store.lengths(layer)
-                attn_events.append((e0, e1, attn_alg_bytes(PLAN[layer], B, c, r), PLAN[layer]))
+                group[2] += attn_alg_bytes(PLAN[layer], B, c, r)
+                group[4] += 1
+                if layer == L - 1 or PLAN[layer + 1] != PLAN[layer]:
+                    group[1] = torch.cuda.Event(enable_timing=True)
+                    group[1].record()
+                    attn_events.append(tuple(group))
         if world > 1:
             dist.all_gather_into_tensor(gathered, outs)
 
@@ -401,14 +405,15 @@ def run_ours(args):
     barrier()
     ms_per_step = ms / steps
     value = B * world * steps / (ms / 1e3)
-    attn_ms = sum(e0.elapsed_time(e1) for e0, e1, _, _ in attn_events)
-    attn_bytes = sum(b for _, _, b, _ in attn_events)
+    attn_ms = sum(e0.elapsed_time(e1) for e0, e1, _, _, _ in attn_events)
+    attn_bytes = sum(b for _, _, b, _, _ in attn_events)
     step_bytes = attn_bytes / steps
     per_width = {}
     for bits in sorted(set(PLAN)):
-        ev = [(e0.elapsed_time(e1), nb) for e0, e1, nb, wb in attn_events if wb == bits]
-        per_width[str(bits)] = {"gbs": sum(nb for _, nb in ev) / (sum(t for t, _ in ev) / 1e3) / 1e9,
-                                "us_per_launch": 1e3 * sum(t for t, _ in ev) / len(ev), "layers": PLAN.count(bits)}
+        ev = [(e0.elapsed_time(e1), nb, n) for e0, e1, nb, wb, n in attn_events if wb == bits]
+        per_width[str(bits)] = {"gbs": sum(nb for _, nb, _ in ev) / (sum(t for t, _, _ in ev) / 1e3) / 1e9,
+                                "us_per_launch": 1e3 * sum(t for t, _, _ in ev) / sum(n for _, _, n in ev),
+                                "layers": PLAN.count(bits)}
     dom = max(set(PLAN), key=PLAN.count)  # the dominant kernel: the 4-bit instantiation (22 of 32 layers)
     achieved = per_width[str(dom)]["gbs"]
     peak, peak_kind = peaks()

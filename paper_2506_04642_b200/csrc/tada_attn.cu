@@ -12,6 +12,10 @@
 
 #include "tada_attn.cuh"
 
+#ifndef TADA_K3_KV
+#define TADA_K3_KV 1  // 0: the per-q-head combine_pair_kernel for every G (A/B)
+#endif
+
 namespace tada {
 
 template <int BITS>
@@ -445,8 +449,247 @@ __global__ void __launch_bounds__(256) combine_pair_kernel(AttnArgs a, int n_row
   }
 }
 
+// K3 for head_dim 128 and G = Hq/H in {1, 2, 4, 8}: one CTA per (sequence, KV head), G + 4 warps.
+//  * warps 0..G-1: the split partials of q head h*G + w (natural-log (m, l) per slot), online merge;
+//  * warps G..G+3: the residual rows, 32 per warp and round (lane = row): each lane takes the full
+//    128-d dot of its row with all G q rows (broadcast from shared memory), so a K/V row is read once
+//    for the whole head group and no shuffle trees are needed; then lane = 4 d columns for P.V, the
+//    weights broadcast by shuffle.  Every load of a round is independent: ~one round trip per 32 rows,
+//    flat in the residual length up to 128 rows (the previous per-q-head kernel grew by a round trip
+//    per 24 rows, and read each row G times).
+//  * the parts meet in shared memory; warp w writes q head h*G + w.
+// In a fused decode step the new row is read from the input and residual warp 0 stores it.
+template <int G>
+__global__ void __launch_bounds__((G + 4) * 32) combine_kv_kernel(AttnArgs a) {
+  constexpr int D = 128, RWN = 4, U = 8;
+  __shared__ __align__(16) float qsm[G][D];
+  __shared__ __align__(16) float rpart[RWN][G][D];
+  __shared__ float rml[RWN][G][2];
+  const float NEG_INF = -__int_as_float(0x7f800000);
+  pdl_enter();  // no global reads above this line
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int h = blockIdx.x, b = blockIdx.y, H = a.L.heads, Hq = a.Hq, S = a.splits;
+  const bool fused = a.new_k != nullptr;
+  const int R = fused ? a.r_prev + 1 : a.res_len[b];
+  const int r_new = fused ? a.r_prev : -1;
+  if (warp >= G) {  // the residual warps stage the q rows (named barrier 1: the split warps start at once)
+    for (int i = threadIdx.x - G * 32; i < G * D; i += RWN * 32) {
+      const int g = i / D, d = i - (i / D) * D;
+      const int64_t qi = (int64_t(b) * Hq + h * G + g) * D + d;
+      qsm[g][d] = a.q_dtype == TADA_F32 ? reinterpret_cast<const float*>(a.q)[qi]
+                                        : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(a.q)[qi]);
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(RWN * 32) : "memory");
+  }
+  float acc[4] = {0.f, 0.f, 0.f, 0.f}, m_run = NEG_INF, l_run = 0.f;
+  if (warp < G) {  // ---- split partials of q head h*G + warp
+    const int row = b * Hq + h * G + warp;
+    const float* ml = a.part_ml + int64_t(row) * a.slots * 2;
+    const float* pa = a.part_acc + int64_t(row) * a.slots * D + 4 * lane;
+    for (int s0 = 0; s0 < S; s0 += 32) {
+      const int s2 = s0 + lane, n = min(32, S - s0);
+      float m = NEG_INF, l = 0.f;
+      if (s2 < S) {
+        m = ml[2 * s2];
+        l = ml[2 * s2 + 1];
+      }
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        v[u] = u < n ? *reinterpret_cast<const float4*>(pa + int64_t(s0 + u) * D) : make_float4(0.f, 0.f, 0.f, 0.f);
+      float mc = l > 0.f ? m : NEG_INF;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+      const float mn = fmaxf(m_run, mc);
+      if (mn == NEG_INF) continue;
+      const float cf = m_run == NEG_INF ? 0.f : expf(m_run - mn);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[e] *= cf;
+      l_run *= cf;
+      m_run = mn;
+      const float w = l > 0.f ? expf(m - mn) : 0.f;
+      l_run += w * l;
+      for (int j0 = 0; j0 < n; j0 += U) {
+        float4 nv[U];
+        const bool more = j0 + U < n;
+        if (more)
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            nv[u] = j0 + U + u < n ? *reinterpret_cast<const float4*>(pa + int64_t(s0 + j0 + U + u) * D)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const float wu = __shfl_sync(0xffffffffu, w, (j0 + u) & 31);
+          acc[0] = fmaf(wu, v[u].x, acc[0]);
+          acc[1] = fmaf(wu, v[u].y, acc[1]);
+          acc[2] = fmaf(wu, v[u].z, acc[2]);
+          acc[3] = fmaf(wu, v[u].w, acc[3]);
+        }
+        if (more)
+#pragma unroll
+          for (int u = 0; u < U; ++u) v[u] = nv[u];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l_run += __shfl_xor_sync(0xffffffffu, l_run, o);
+  } else {  // ---- residual rows
+    const int rw = warp - G;
+    const int64_t rbase = int64_t(b) * a.res_seq_stride;
+    const int64_t nrow = (int64_t(b) * H + h) * D;  // this head's new row in the step input
+    if (fused && rw == 0) {  // store the step's row for later steps
+      float x[4];
+      const int64_t dst = ((rbase + r_new) * H + h) * D + 4 * lane;
+      if (a.new_dtype == TADA_F32) load4(reinterpret_cast<const float*>(a.new_k) + nrow + 4 * lane, x);
+      else load4(reinterpret_cast<const __nv_bfloat16*>(a.new_k) + nrow + 4 * lane, x);
+      *reinterpret_cast<float4*>(const_cast<float*>(a.res_k) + dst) = make_float4(x[0], x[1], x[2], x[3]);
+      if (a.new_dtype == TADA_F32) load4(reinterpret_cast<const float*>(a.new_v) + nrow + 4 * lane, x);
+      else load4(reinterpret_cast<const __nv_bfloat16*>(a.new_v) + nrow + 4 * lane, x);
+      *reinterpret_cast<float4*>(const_cast<float*>(a.res_v) + dst) = make_float4(x[0], x[1], x[2], x[3]);
+      if (h == 0 && lane == 0) const_cast<int32_t*>(a.res_len)[b] = r_new + 1;
+    }
+    float racc[G][4], rm[G], rl[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      racc[g][0] = racc[g][1] = racc[g][2] = racc[g][3] = 0.f;
+      rm[g] = NEG_INF;
+      rl[g] = 0.f;
+    }
+    for (int c0 = 32 * rw; c0 < R; c0 += 32 * RWN) {
+      const int t = c0 + lane;
+      const bool valid = t < R;
+      float sc[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) sc[g] = 0.f;
+      if (valid) {  // logits of row t (lane) against the G q rows
+        if (t == r_new) {
+#pragma unroll 4
+          for (int j = 0; j < D; j += 4) {
+            float x[4];
+            if (a.new_dtype == TADA_F32) load4(reinterpret_cast<const float*>(a.new_k) + nrow + j, x);
+            else load4(reinterpret_cast<const __nv_bfloat16*>(a.new_k) + nrow + j, x);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              const float4 qv = *reinterpret_cast<const float4*>(&qsm[g][j]);
+              sc[g] = __fmaf_rn(qv.w, x[3], __fmaf_rn(qv.z, x[2], __fmaf_rn(qv.y, x[1], __fmaf_rn(qv.x, x[0], sc[g]))));
+            }
+          }
+        } else {
+          const float* kr = a.res_k + ((rbase + t) * H + h) * D;
+#pragma unroll 8
+          for (int j = 0; j < D; j += 4) {
+            const float4 k4 = *reinterpret_cast<const float4*>(kr + j);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              const float4 qv = *reinterpret_cast<const float4*>(&qsm[g][j]);
+              sc[g] = __fmaf_rn(qv.w, k4.w, __fmaf_rn(qv.z, k4.z, __fmaf_rn(qv.y, k4.y, __fmaf_rn(qv.x, k4.x, sc[g]))));
+            }
+          }
+        }
+      }
+      float p[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float sv = valid ? __fmul_rn(sc[g], a.scale) : NEG_INF;
+        float bm = sv;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+        const float mn = fmaxf(rm[g], bm);  // finite: lane 0 of every round holds a valid row
+        const float cf = rm[g] == NEG_INF ? 0.f : expf(rm[g] - mn);
+        racc[g][0] *= cf;
+        racc[g][1] *= cf;
+        racc[g][2] *= cf;
+        racc[g][3] *= cf;
+        rl[g] *= cf;
+        rm[g] = mn;
+        p[g] = valid ? expf(sv - mn) : 0.f;
+        rl[g] += p[g];  // lane-partial; reduced below
+      }
+      const int nr = min(32, R - c0);
+      for (int u0 = 0; u0 < nr; u0 += U) {  // P.V: lane = columns 4*lane .. +3
+        float4 v4[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int tt = c0 + u0 + u;
+          if (u0 + u >= nr) {
+            v4[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          } else if (tt == r_new) {
+            float x[4];
+            if (a.new_dtype == TADA_F32) load4(reinterpret_cast<const float*>(a.new_v) + nrow + 4 * lane, x);
+            else load4(reinterpret_cast<const __nv_bfloat16*>(a.new_v) + nrow + 4 * lane, x);
+            v4[u] = make_float4(x[0], x[1], x[2], x[3]);
+          } else {
+            v4[u] = *reinterpret_cast<const float4*>(a.res_v + ((rbase + tt) * H + h) * D + 4 * lane);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const float pu = __shfl_sync(0xffffffffu, p[g], (u0 + u) & 31);
+            racc[g][0] = fmaf(pu, v4[u].x, racc[g][0]);
+            racc[g][1] = fmaf(pu, v4[u].y, racc[g][1]);
+            racc[g][2] = fmaf(pu, v4[u].z, racc[g][2]);
+            racc[g][3] = fmaf(pu, v4[u].w, racc[g][3]);
+          }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) rl[g] += __shfl_xor_sync(0xffffffffu, rl[g], o);
+      *reinterpret_cast<float4*>(&rpart[rw][g][4 * lane]) = make_float4(racc[g][0], racc[g][1], racc[g][2], racc[g][3]);
+      if (lane == 0) {
+        rml[rw][g][0] = rm[g];  // -inf with l = 0 when this warp had no rows
+        rml[rw][g][1] = rl[g];
+      }
+    }
+  }
+  __syncthreads();
+  if (warp < G) {  // ---- merge the parts of q head h*G + warp
+    float M = m_run;
+#pragma unroll
+    for (int w = 0; w < RWN; ++w) M = fmaxf(M, rml[w][warp][0]);
+    const float fs = m_run == NEG_INF ? 0.f : expf(m_run - M);
+    float L = l_run * fs;
+    float o[4] = {acc[0] * fs, acc[1] * fs, acc[2] * fs, acc[3] * fs};
+#pragma unroll
+    for (int w = 0; w < RWN; ++w) {
+      const float mr = rml[w][warp][0];
+      const float fr = mr == NEG_INF ? 0.f : expf(mr - M);
+      L += rml[w][warp][1] * fr;
+      const float4 ar = *reinterpret_cast<const float4*>(&rpart[w][warp][4 * lane]);
+      o[0] += ar.x * fr;
+      o[1] += ar.y * fr;
+      o[2] += ar.z * fr;
+      o[3] += ar.w * fr;
+    }
+    const float inv = 1.f / L;
+    const int row = b * Hq + h * G + warp;
+    const int64_t qi = int64_t(row) * D + 4 * lane;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) store_any(a.out, a.out_dtype, qi + e, o[e] * inv);
+    if (lane == 0 && a.lse_out) a.lse_out[row] = M + logf(L);
+  }
+}
+
 static int launch_combine_residual(const AttnArgs& a, int batch, cudaStream_t st) {
   if (a.L.head_dim * 2 > kCombThreads * 2 || a.L.head_dim % 4) return fail(TADA_ERR_CONFIG, "combine needs head_dim % 4 == 0");
+  if (a.L.head_dim == 128 && TADA_K3_KV) {  // any residual length: the rows stream through 4 warps per KV head
+    const int G = a.Hq / a.L.heads;
+    const dim3 grid(a.L.heads, batch);
+    cudaError_t e = cudaErrorInvalidValue;
+    switch (G) {
+      case 1: e = launch_maybe_pdl(combine_kv_kernel<1>, grid, dim3(5 * 32), 0, st, a); break;
+      case 2: e = launch_maybe_pdl(combine_kv_kernel<2>, grid, dim3(6 * 32), 0, st, a); break;
+      case 4: e = launch_maybe_pdl(combine_kv_kernel<4>, grid, dim3(8 * 32), 0, st, a); break;
+      case 8: e = launch_maybe_pdl(combine_kv_kernel<8>, grid, dim3(12 * 32), 0, st, a); break;
+      default: break;
+    }
+    if (G == 1 || G == 2 || G == 4 || G == 8) {
+      if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string("decode_attn_combine: ") + cudaGetErrorString(e));
+      return check_launch("decode_attn_combine_residual");
+    }
+  }
   if (a.L.head_dim == 128) {  // any residual length: the pair kernel streams the rows
     const int rows = a.Hq * batch;
     const cudaError_t e = launch_maybe_pdl(combine_pair_kernel, dim3((rows + 1) / 2), dim3(256), 0, st, a, rows);
