@@ -460,8 +460,9 @@ __global__ void __launch_bounds__(256) combine_pair_kernel(AttnArgs a, int n_row
 //  * the parts meet in shared memory; warp w writes q head h*G + w.
 // In a fused decode step the new row is read from the input and residual warp 0 stores it.
 template <int G>
-__global__ void __launch_bounds__((G + 4) * 32) combine_kv_kernel(AttnArgs a) {
-  constexpr int D = 128, RWN = 4, U = 8;
+__global__ void __launch_bounds__((G + 4) * 32) combine_kv_kernel(AttnArgs a, int rch) {
+  constexpr int D = 128, RWN = 4, U = 8, RP = D + 4;  // RP: padded staged row (lane = row reads hit 32 banks)
+  extern __shared__ __align__(16) float rst[];        // staged residual chunk: K rows [rch][RP], then V rows
   __shared__ __align__(16) float qsm[G][D];
   __shared__ __align__(16) float rpart[RWN][G][D];
   __shared__ float rml[RWN][G][2];
@@ -554,35 +555,44 @@ __global__ void __launch_bounds__((G + 4) * 32) combine_kv_kernel(AttnArgs a) {
       rm[g] = NEG_INF;
       rl[g] = 0.f;
     }
-    for (int c0 = 32 * rw; c0 < R; c0 += 32 * RWN) {
+    const int tid_r = threadIdx.x - G * 32;  // 0 .. 127 among the residual warps
+    for (int cb = 0; cb < R; cb += rch) {   // chunks of rch rows: one round of async copies each
+      const int n = min(rch, R - cb);
+      if (cb > 0) asm volatile("bar.sync 2, %0;" ::"n"(RWN * 32) : "memory");  // previous chunk consumed
+      for (int i = tid_r; i < 2 * n * 32; i += RWN * 32) {
+        const int side = i >= n * 32, rem = i - side * n * 32, r = rem >> 5, col = (rem & 31) * 4;
+        float* dst = rst + (side * rch + r) * RP + col;
+        if (cb + r == r_new) {  // the step's row, from the input (f32 or bf16)
+          float x[4];
+          const void* src = side ? a.new_v : a.new_k;
+          if (a.new_dtype == TADA_F32) load4(reinterpret_cast<const float*>(src) + nrow + col, x);
+          else load4(reinterpret_cast<const __nv_bfloat16*>(src) + nrow + col, x);
+          *reinterpret_cast<float4*>(dst) = make_float4(x[0], x[1], x[2], x[3]);
+        } else {
+          const float* src = (side ? a.res_v : a.res_k) + ((rbase + cb + r) * H + h) * D + col;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                       "l"(src)
+                       : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+      asm volatile("bar.sync 2, %0;" ::"n"(RWN * 32) : "memory");
+      const int c0 = cb + 32 * rw;  // this warp's 32 rows of the chunk
+      if (c0 >= cb + n) continue;
       const int t = c0 + lane;
-      const bool valid = t < R;
+      const bool valid = t < cb + n;
       float sc[G];
 #pragma unroll
       for (int g = 0; g < G; ++g) sc[g] = 0.f;
       if (valid) {  // logits of row t (lane) against the G q rows
-        if (t == r_new) {
-#pragma unroll 4
-          for (int j = 0; j < D; j += 4) {
-            float x[4];
-            if (a.new_dtype == TADA_F32) load4(reinterpret_cast<const float*>(a.new_k) + nrow + j, x);
-            else load4(reinterpret_cast<const __nv_bfloat16*>(a.new_k) + nrow + j, x);
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-              const float4 qv = *reinterpret_cast<const float4*>(&qsm[g][j]);
-              sc[g] = __fmaf_rn(qv.w, x[3], __fmaf_rn(qv.z, x[2], __fmaf_rn(qv.y, x[1], __fmaf_rn(qv.x, x[0], sc[g]))));
-            }
-          }
-        } else {
-          const float* kr = a.res_k + ((rbase + t) * H + h) * D;
+        const float* kr = rst + (t - cb) * RP;
 #pragma unroll 8
-          for (int j = 0; j < D; j += 4) {
-            const float4 k4 = *reinterpret_cast<const float4*>(kr + j);
+        for (int j = 0; j < D; j += 4) {
+          const float4 k4 = *reinterpret_cast<const float4*>(kr + j);
 #pragma unroll
-            for (int g = 0; g < G; ++g) {
-              const float4 qv = *reinterpret_cast<const float4*>(&qsm[g][j]);
-              sc[g] = __fmaf_rn(qv.w, k4.w, __fmaf_rn(qv.z, k4.z, __fmaf_rn(qv.y, k4.y, __fmaf_rn(qv.x, k4.x, sc[g]))));
-            }
+          for (int g = 0; g < G; ++g) {
+            const float4 qv = *reinterpret_cast<const float4*>(&qsm[g][j]);
+            sc[g] = __fmaf_rn(qv.w, k4.w, __fmaf_rn(qv.z, k4.z, __fmaf_rn(qv.y, k4.y, __fmaf_rn(qv.x, k4.x, sc[g]))));
           }
         }
       }
@@ -604,33 +614,18 @@ __global__ void __launch_bounds__((G + 4) * 32) combine_kv_kernel(AttnArgs a) {
         p[g] = valid ? expf(sv - mn) : 0.f;
         rl[g] += p[g];  // lane-partial; reduced below
       }
-      const int nr = min(32, R - c0);
-      for (int u0 = 0; u0 < nr; u0 += U) {  // P.V: lane = columns 4*lane .. +3
-        float4 v4[U];
+      const int nr = min(32, cb + n - c0);
+      const float* vr = rst + (rch + (c0 - cb)) * RP + 4 * lane;
+      for (int u = 0; u < nr; ++u) {  // P.V: lane = columns 4*lane .. +3
+        const float4 v4 = *reinterpret_cast<const float4*>(vr + u * RP);
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int tt = c0 + u0 + u;
-          if (u0 + u >= nr) {
-            v4[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-          } else if (tt == r_new) {
-            float x[4];
-            if (a.new_dtype == TADA_F32) load4(reinterpret_cast<const float*>(a.new_v) + nrow + 4 * lane, x);
-            else load4(reinterpret_cast<const __nv_bfloat16*>(a.new_v) + nrow + 4 * lane, x);
-            v4[u] = make_float4(x[0], x[1], x[2], x[3]);
-          } else {
-            v4[u] = *reinterpret_cast<const float4*>(a.res_v + ((rbase + tt) * H + h) * D + 4 * lane);
-          }
+        for (int g = 0; g < G; ++g) {
+          const float pu = __shfl_sync(0xffffffffu, p[g], u);
+          racc[g][0] = fmaf(pu, v4.x, racc[g][0]);
+          racc[g][1] = fmaf(pu, v4.y, racc[g][1]);
+          racc[g][2] = fmaf(pu, v4.z, racc[g][2]);
+          racc[g][3] = fmaf(pu, v4.w, racc[g][3]);
         }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            const float pu = __shfl_sync(0xffffffffu, p[g], (u0 + u) & 31);
-            racc[g][0] = fmaf(pu, v4[u].x, racc[g][0]);
-            racc[g][1] = fmaf(pu, v4[u].y, racc[g][1]);
-            racc[g][2] = fmaf(pu, v4[u].z, racc[g][2]);
-            racc[g][3] = fmaf(pu, v4[u].w, racc[g][3]);
-          }
       }
     }
 #pragma unroll
@@ -677,12 +672,20 @@ static int launch_combine_residual(const AttnArgs& a, int batch, cudaStream_t st
   if (a.L.head_dim == 128 && TADA_K3_KV) {  // any residual length: the rows stream through 4 warps per KV head
     const int G = a.Hq / a.L.heads;
     const dim3 grid(a.L.heads, batch);
+    // staged residual chunk: up to 128 rows (the default residual_length) of K and V, padded rows
+    const int rch = int(a.res_seq_stride < 128 ? (a.res_seq_stride + 31) / 32 * 32 : 128);
+    const size_t dsm = size_t(rch > 0 ? rch : 32) * 2 * (128 + 4) * 4;
     cudaError_t e = cudaErrorInvalidValue;
+    auto go = [&](auto kern, int warps, std::atomic<uint64_t>& done) {
+      if (ensure_smem(kern, 128 * 2 * (128 + 4) * 4, done, "combine_kv") != TADA_OK) return cudaErrorInvalidValue;
+      return launch_maybe_pdl(kern, grid, dim3(warps * 32), dsm, st, a, rch > 0 ? rch : 32);
+    };
+    static std::atomic<uint64_t> d1{0}, d2{0}, d4{0}, d8{0};
     switch (G) {
-      case 1: e = launch_maybe_pdl(combine_kv_kernel<1>, grid, dim3(5 * 32), 0, st, a); break;
-      case 2: e = launch_maybe_pdl(combine_kv_kernel<2>, grid, dim3(6 * 32), 0, st, a); break;
-      case 4: e = launch_maybe_pdl(combine_kv_kernel<4>, grid, dim3(8 * 32), 0, st, a); break;
-      case 8: e = launch_maybe_pdl(combine_kv_kernel<8>, grid, dim3(12 * 32), 0, st, a); break;
+      case 1: e = go(combine_kv_kernel<1>, 5, d1); break;
+      case 2: e = go(combine_kv_kernel<2>, 6, d2); break;
+      case 4: e = go(combine_kv_kernel<4>, 8, d4); break;
+      case 8: e = go(combine_kv_kernel<8>, 12, d8); break;
       default: break;
     }
     if (G == 1 || G == 2 || G == 4 || G == 8) {

@@ -58,8 +58,14 @@ def main():
             t1.record()
             h1 = time.perf_counter()
             torch.cuda.synchronize()
+            import subprocess
+
+            smi = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,power.draw,clocks_event_reasons.active",
+                                  "--format=csv,noheader"], capture_output=True, text=True).stdout.strip()
             print(f"rep {rep} residual ~{3 + rep * steps}..{3 + (rep + 1) * steps}: gpu {t0.elapsed_time(t1) / steps:.3f} "
-                  f"ms/step, host enqueue {(h1 - h0) * 1e3 / steps:.3f} ms/step", flush=True)
+                  f"ms/step, host enqueue {(h1 - h0) * 1e3 / steps:.3f} ms/step  [{smi}]", flush=True)
+            if os.environ.get("PROBE_COOL"):
+                time.sleep(float(os.environ["PROBE_COOL"]))
         return
     res = {"resident": timed(lambda: [layers(qs[i % 2], ks[i % 2], outs[i % 2]) for i in range(steps)])}
 
