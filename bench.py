@@ -247,7 +247,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     B = B_PER_GPU
     steps, warm = args.steps, args.warmup
-    max_tokens = T + R + 3 * steps + warm + 16  # timed + instrumented + e2e passes
+    max_tokens = T + R + 2 * steps + warm + 16  # timed + e2e passes
     store = tk.PagedKVCache(L, H, D, PLAN, R, batch=B, page_tokens=64, max_tokens=max_tokens, shuffle_pages=True,
                             seed=rank)
     gen = torch.Generator(device=dev)
@@ -331,7 +331,7 @@ def run_ours(args):
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record()
         for i in range(steps):
-            step(warm + i)
+            step(warm + i, record=True)  # one event pair per run of same-width layers (roofline per width)
         t1.record()
         barrier()
         wall1 = time.time()
@@ -397,11 +397,6 @@ def run_ours(args):
     main.wait_stream(d2h_s)
     main.wait_stream(h2d_s)
     t1.record()
-    barrier()
-    # per-layer CUDA events for the roofline's per-width kernel times, in a separate pass of the same
-    # steps after the e2e pass (events between kernels would otherwise sit inside the timed regions)
-    for i in range(steps):
-        step(warm + 2 * steps + i, record=True)
     barrier()
     ms_per_step = ms / steps
     value = B * world * steps / (ms / 1e3)
