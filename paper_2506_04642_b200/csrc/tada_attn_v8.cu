@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   // PARK: the PV mean accumulators (om, 8*MT floats per thread) are touched only in phase C; between
   // tiles they live in TMEM (warp w: lane quarter w%4, column block w/4), freeing their registers for
   // phases A/B.  Measured: +4% at Hq=64 (32 registers), -1% at Hq<=32 (16), so only there.
-  constexpr bool PARK = TADA_V8_TMEM_OM && MT >= 4;
+  constexpr bool PARK = TADA_V8_TMEM_OM && MT >= 4 && BITS != 2;  // 2-bit Hq=64: +0.9% without (measured)
   // per-warp rescale flags instead of a corr scan in phase C: +2.5% at Hq=64, -1..2% at Hq<=32 (measured)
   constexpr bool FLAGS = MT >= 4;
   constexpr int NOM = 8 * MT;
