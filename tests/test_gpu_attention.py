@@ -212,3 +212,56 @@ def test_append_attend_fused_equals_append_then_attend(bits, hq):
     r = a.lengths(0)[1]
     assert torch.equal(a.res_k[0][:, :r], b.res_k[0][:, :r]) and torch.equal(a.res_v[0][:, :r], b.res_v[0][:, :r])
     assert torch.equal(a.res_len[0], b.res_len[0]) and torch.equal(a.comp_len[0], b.comp_len[0])
+
+
+@pytest.mark.parametrize("hq,mode", [(24, 1), (24, 2), (40, 1)])
+def test_combine_other_group_sizes(hq, mode):
+    """G = Hq/H outside {1, 2, 4, 8} (K3 combine_pair_kernel), with residual rows: exact path within the
+    reference's 1e-5, tensor-core path (if the geometry has one) within 2e-3."""
+    store, q, want = _paged_case(B=2, H=8, hq=hq, D=128, bits=4, T=700, R=128, seed=hq + mode)
+    if mode == 1:
+        out = store.attend(0, q, num_splits=5, mode=1)
+        assert np.abs(out.cpu().numpy() - want).max() <= 1e-5
+    else:
+        out = _fast_or_skip(store, q, out_dtype=torch.float32)
+        assert np.abs(out.cpu().numpy() - want).max() <= 2e-3
+
+
+@pytest.mark.parametrize("R,T", [(200, 900), (200, 1000), (160, 159), (300, 1499)])
+def test_long_residual_chunks(R, T):
+    """residual_length > 128: K3 stages the residual rows through shared memory in chunks of 128
+    (T % R rows stay raw: 100, 0 + 200 flush..., 159, 299)."""
+    store, q, want = _paged_case(B=2, H=8, hq=32, D=128, bits=4, T=T, R=R, seed=R + T)
+    out = store.attend(0, q, num_splits=4, mode=1)
+    assert np.abs(out.cpu().numpy() - want).max() <= 1e-5
+    out = _fast_or_skip(store, q, out_dtype=torch.float32)
+    assert np.abs(out.cpu().numpy() - want).max() <= 2e-3
+
+
+@pytest.mark.parametrize("hq", [8, 32, 64])
+def test_fused_step_long_residual(hq):
+    """Fused decode steps (K3 attends and stores the new row) across a residual that grows past one
+    32-row round of a residual warp, against append-then-attend through the oracle."""
+    m = tk()
+    B, H, D, R, T = 2, 8, 128, 128, 640
+    rng = np.random.default_rng(77 + hq)
+    k = orc.bf16_round(rng.normal(size=(B, T, H, D)).astype(np.float32))
+    v = orc.bf16_round(rng.normal(size=(B, T, H, D)).astype(np.float32))
+    store = m.PagedKVCache(1, H, D, (4,), R, batch=B, page_tokens=64, max_tokens=T + 80, shuffle_pages=True)
+    store.append(0, torch.from_numpy(k).cuda().bfloat16(), torch.from_numpy(v).cuda().bfloat16())
+    states = []
+    for b in range(B):
+        st = orc.LayerState(H, D, 4, R)
+        orc.append(st, k[b], v[b])
+        states.append(st)
+    for step in range(70):
+        kn = orc.bf16_round(rng.normal(size=(B, 1, H, D)).astype(np.float32))
+        vn = orc.bf16_round(rng.normal(size=(B, 1, H, D)).astype(np.float32))
+        q = orc.bf16_round(rng.normal(size=(B, hq, D)).astype(np.float32))
+        out = store.append_attend(0, torch.from_numpy(q).cuda(), torch.from_numpy(kn).cuda().bfloat16(),
+                                  torch.from_numpy(vn).cuda().bfloat16(), out_dtype=torch.float32)
+        for b in range(B):
+            orc.append(states[b], kn[b], vn[b])
+        if step in (0, 31, 32, 69):
+            want = np.stack([orc.attend(q[b], states[b], hq)[0] for b in range(B)])
+            assert np.abs(out.cpu().numpy() - want).max() <= 2e-3, step
