@@ -452,7 +452,7 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "traffic_source": traffic_src,
                          "kernel": f"decode attention K2+K3 (tada_decode_attn), {dom}-bit layers: {attn_kernel_name(dom, HQ)}"
-                                   f" + combine_pair_kernel (K3)",
+                                   f" + combine_kv_kernel (K3)",
                          "alg_bytes_per_launch": attn_alg_bytes(dom, B, T, 1), "peak_source": peak_kind,
                          "frac_of_8tbs_spec": achieved / 8000.0, "per_width": per_width,
                          "all_layers_gbs": attn_bytes / (attn_ms / 1e3) / 1e9,

@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
       }
       // MT (or 2 MT) independent accumulation chains, interleaved so no MMA waits on the previous one
       constexpr bool AC2 = TADA_V8_ACHAINS == 2 || (TADA_V8_ACHAINS == 0 && MT <= 2);
-      float acc2[AC2 ? MT : 1][4];
+      [[maybe_unused]] float acc2[AC2 ? MT : 1][4];
       if constexpr (AC2)
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) acc2[mt][0] = acc2[mt][1] = acc2[mt][2] = acc2[mt][3] = 0.f;
