@@ -467,6 +467,9 @@ __device__ __forceinline__ float redux_max(float v) {
 // ring with cp.async.bulk + an mbarrier per slot, so the next rows are in flight while the
 // current one is quantized (the kernel is otherwise latency-bound on its global loads).
 constexpr int K1_RING = 3;
+#ifndef TADA_K1_PAGE_CACHE
+#define TADA_K1_PAGE_CACHE 1  // page base pointer reloaded on page change only
+#endif
 __device__ __forceinline__ uint32_t k1_su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
 template <typename T, int BITS, int MINB, bool ROPE>
@@ -509,6 +512,10 @@ __global__ void __launch_bounds__(256, MINB) quant_append_fast_kernel(AppendArgs
     pg = page_shift >= 0 ? (c >> page_shift) : c / P;
     row = int(c - pg * P);
   }
+#if TADA_K1_PAGE_CACHE
+  // the page base changes once every P tokens: load the page-table entry only then
+  uint8_t* page = i_begin < i_end ? a.pool + int64_t(pt[pg]) * a.L.page_bytes : nullptr;
+#endif
   for (int64_t i = i_begin; i < i_end; ++i) {
     asm volatile(
         "{\n.reg .pred p;\nK1_WAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra K1_WAIT_%=;\n}\n" ::"r"(
@@ -574,7 +581,9 @@ __global__ void __launch_bounds__(256, MINB) quant_append_fast_kernel(AppendArgs
       my_s = group_scale(my_mn, my_mx, BITS);
       my_inv = (my_s >= 0x1p-100f && my_s <= 0x1p100f) ? __frcp_rn(my_s) : 0.f;
     }
+#if !TADA_K1_PAGE_CACHE
     uint8_t* page = a.pool + int64_t(pt[pg]) * a.L.page_bytes;
+#endif
     *reinterpret_cast<float4*>(reinterpret_cast<float*>(page + a.L.off_mean[side]) + row * D + 4 * lane) =
         make_float4(mean[0], mean[1], mean[2], mean[3]);
     if (lane < H)
@@ -644,6 +653,9 @@ __global__ void __launch_bounds__(256, MINB) quant_append_fast_kernel(AppendArgs
     if (++row == P) {
       row = 0;
       ++pg;
+#if TADA_K1_PAGE_CACHE
+      if (i + 1 < i_end) page = a.pool + int64_t(pt[pg]) * a.L.page_bytes;
+#endif
     }
   }
 }
