@@ -63,6 +63,9 @@ constexpr int kBudget = 113 * 1024;  // two CTAs per SM
 #ifndef TADA_V8_OFTM
 #define TADA_V8_OFTM 2  // per-thread shared offsets in TMEM, reloaded per phase: 1 = phase B only (+0.8..2.5%), 2 = + phases A/C and the logit constants (+0.1..2.3% more)
 #endif
+#ifndef TADA_V8_PPS
+#define TADA_V8_PPS 0.00390625f  // 2^-8
+#endif
 #ifndef TADA_V8_TMEM_OM
 #define TADA_V8_TMEM_OM 1  // park the PV mean accumulators in TMEM between tiles
 #endif
@@ -127,6 +130,10 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], uint32_t addr) {
 // is removed once at the end as bias * Σp'.  Fields sit at mantissa bit 4 or above (bias <= 64) for
 // 2/4-bit codes, so the biased f32 accumulation loses at most ~2^-17 of the code term (8-bit: bias
 // 1024 against codes up to 255).
+// P' = -p * vscale enters the PV code MMA as f16.  The lazy softmax lets p reach 2^8, so unscaled a group
+// scale above 256 (a 2-bit deviation range above 768, which outlier channels reach) would overflow f16 to
+// inf; P' is therefore stored times PPS = 2^-8 and the code term scaled back (exactly) in the epilogue.
+constexpr float PPS = TADA_V8_PPS;
 template <int BITS>
 __host__ __device__ constexpr float pv_bias(int mt, int half) {
   if (BITS == 8) return 1024.f;
@@ -619,7 +626,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
           if (tail && 8 * nt + 2 * c + e >= nv) {  // rows past the sequence may hold anything
             pp[nt][e] = 0.f;
           } else {
-            pp[nt][e] = -pe * vm.x;
+            pp[nt][e] = pe * (vm.x * -PPS);  // P' pre-scaled by 2^-8: f16-safe up to vscale 65504
             bsum = fmaf(pe, vm.y, bsum);
           }
         }
@@ -865,8 +872,8 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
       float* row = park + (h * G + n) * PR + 16 * r;
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt) {
-        row[2 * mt] += oc[mt][e] - pv_bias<BITS>(mt, 0) * sp;
-        row[2 * mt + 1] += oc[mt][2 + e] - pv_bias<BITS>(mt, 1) * sp;
+        row[2 * mt] += (oc[mt][e] - pv_bias<BITS>(mt, 0) * sp) * (1.f / PPS);
+        row[2 * mt + 1] += (oc[mt][2 + e] - pv_bias<BITS>(mt, 1) * sp) * (1.f / PPS);
       }
     }
   }

@@ -265,3 +265,31 @@ def test_fused_step_long_residual(hq):
         if step in (0, 31, 32, 69):
             want = np.stack([orc.attend(q[b], states[b], hq)[0] for b in range(B)])
             assert np.abs(out.cpu().numpy() - want).max() <= 2e-3, step
+
+
+@pytest.mark.parametrize("bits", [2, 4])
+@pytest.mark.parametrize("mag", [2000.0, 8000.0])
+def test_fast_extreme_value_range(bits, mag):
+    """A value channel at +-mag: group scales far above 256 (2-bit: ~5000).  P' = -p*vscale enters the
+    PV code MMA as f16; unscaled it overflowed to inf (NaN output) at 2-bit +-8000 — the kernel stores
+    it times 2^-8 and scales the code term back."""
+    m = tk()
+    rng = np.random.default_rng(5)
+    B, T, H, D, hq = 2, 700, 8, 128, 32
+    k = rng.normal(size=(B, T, H, D))
+    v = rng.normal(size=(B, T, H, D))
+    v[:, :, 3, 17] = rng.choice([-mag, mag], size=(B, T))
+    k[:, :, 2, 5] = rng.choice([-mag, mag], size=(B, T)) * 0.01
+    k, v = orc.bf16_round(k.astype(np.float32)), orc.bf16_round(v.astype(np.float32))
+    q = orc.bf16_round(rng.normal(size=(B, hq, D)).astype(np.float32))
+    store = m.PagedKVCache(1, H, D, (bits,), 128, batch=B, page_tokens=64, max_tokens=T + 1, shuffle_pages=True)
+    store.append(0, torch.from_numpy(k).cuda().bfloat16(), torch.from_numpy(v).cuda().bfloat16())
+    want = []
+    for b in range(B):
+        st = orc.LayerState(H, D, bits, 128)
+        orc.append(st, k[b], v[b])
+        want.append(orc.attend(q[b], st, hq)[0])
+    want = np.stack(want)
+    out = store.attend(0, torch.from_numpy(q).cuda(), mode=2, out_dtype=torch.float32).cpu().numpy()
+    assert np.isfinite(out).all()
+    assert np.abs(out - want).max() <= 2e-3 * max(1.0, float(np.abs(want).max()))
