@@ -52,6 +52,8 @@ CONFIGS = {
                      "(128 at 8 GPUs), uniform 4-bit"),
 }
 H, D, R = 8, 128, 128
+# --scaling strong: the global batch BASELINE.json quotes (config 5: 128 sequences, which fit only on 8 B200s)
+STRONG_GLOBAL_BATCH = {2: 16, 4: 4, 5: 128}
 L = HQ = T = B_PER_GPU = 0
 PLAN: list = []
 WORKLOAD = ""
@@ -153,80 +155,173 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------ CPU oracle leg
-def _cpu_worker(args):
-    """One host core: build oracle caches at T tokens for the plan's widths, then time attend on each `reps` times."""
-    seed, tokens, reps, hq, widths = args
-    os.environ["OMP_NUM_THREADS"] = os.environ["OPENBLAS_NUM_THREADS"] = "1"
+_CPU = {}  # per worker process: the oracle LayerStates it built (one per plan width) and their append times
+
+
+def _cpu_init(tokens: int, hq: int, widths: list) -> None:
+    """Worker initializer (one host core): build one oracle (sequence, layer) cache per width with the
+    reference's append_tokens policy (cache.py:154-180, R=128) at `tokens` tokens, timing each append —
+    the CPU quantize-append baseline (config 3's metric)."""
+    try:
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(1)
+    except Exception:
+        pass
     from oracle import tada_oracle as orc
 
-    rng = np.random.default_rng(seed)
-    times = {}
+    rng = np.random.default_rng(1000 + os.getpid() % 1000)
+    _CPU.update(states={}, append_s={}, hq=hq)
     for bits in widths:
         st = orc.LayerState(H, D, bits, R)
         k = orc.bf16_round(rng.normal(size=(tokens, H, D)).astype(np.float32))
         v = orc.bf16_round(rng.normal(size=(tokens, H, D)).astype(np.float32))
+        t0 = time.perf_counter()
         orc.append(st, k, v)
-        del k, v
-        q = orc.bf16_round(rng.normal(size=(hq, D)).astype(np.float32))
-        ts = []
-        for _ in range(reps):
-            t0 = time.perf_counter()
-            orc.attend(q, st, hq, block=64)
-            ts.append(time.perf_counter() - t0)
-        times[bits] = ts
-    return times
+        _CPU["append_s"][bits] = time.perf_counter() - t0
+        _CPU["states"][bits] = st
+    _CPU["q"] = orc.bf16_round(rng.normal(size=(hq, D)).astype(np.float32))
 
 
-def cpu_oracle_leg(reps: int, workers: int | None = None):
-    """Per-unit (1 sequence x 1 layer) attend times on `workers` cores in parallel -> decode tokens/s of the config.
+def _cpu_unit(_):
+    """One sampled step's share of one worker: attend (attention.py:103-151, block 64) over its cache of
+    each width once; returns the per-width unit times and the build-time append times."""
+    from oracle import tada_oracle as orc
 
-    The unit is timed at min(T, 32768) context and scaled linearly to T (attend is linear in T), so
-    the leg stays bounded for the 128k config.
-    """
-    cores = os.cpu_count() or 1
-    workers = workers or min(cores, 32)
-    tokens = min(T, 32768)
-    widths = sorted(set(PLAN), reverse=True)
-    ctx = mp.get_context("spawn")
-    with ctx.Pool(workers) as pool:
-        res = pool.map(_cpu_worker, [(1000 + i, tokens, reps, HQ, widths) for i in range(workers)])
-    per = {b: [t for r in res for t in r[b]] for b in widths}
-    med = {b: statistics.median(per[b]) * (T / tokens) for b in widths}
-    unit_mix = sum(med[b] for b in PLAN)  # one sequence through all layers, one core
-    step_s = unit_mix * B_PER_GPU / workers  # the batch spread over `workers` cores
-    alg = sum(attn_alg_bytes(b, 1, T, 0) for b in PLAN) * B_PER_GPU
-    return {
-        "tokens_per_s": B_PER_GPU / step_s, "step_s": step_s, "alg_gbs": alg / step_s / 1e9, "workers": workers,
-        "unit_s": {str(b): med[b] for b in med}, "per_step_samples": workers * len(widths),
-        "sample": f"{workers} workers x 1 (seq, layer) unit per width {widths} at T={tokens} x {reps} reps"
-                  + (f", scaled x{T // tokens} to T={T}" if T != tokens else "")
-                  + f"; step = {B_PER_GPU} seqs x {L} layers extrapolated linearly from the per-width medians",
-    }
+    times = {}
+    for bits, st in _CPU["states"].items():
+        t0 = time.perf_counter()
+        orc.attend(_CPU["q"], st, _CPU["hq"], block=64)
+        times[bits] = time.perf_counter() - t0
+    return times, dict(_CPU["append_s"]), os.getpid()
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+class CpuOracle:
+    """The CPU reference path (the numpy oracle port of tadakv, one process per host core) on a bounded
+    sample of the configured workload.
+
+    Setup (untimed): every worker appends `tokens` = min(T, 32768) tokens of bf16 K/V into one cache per
+    plan width (timed per worker: the CPU quantize-append GB/s).  One STEP = every worker attends one
+    (sequence, layer) unit of each width — workers x widths units, timed by the wall clock around the
+    parallel map.  Decode tokens/s = workers / (time to attend one sequence through all L layers of the
+    plan on one core), from the per-width median unit times (scaled linearly to T when T > tokens)."""
+
+    def __init__(self, workers: int | None = None):
+        self.workers = workers or min(os.cpu_count() or 1, 32)
+        self.tokens = min(T, 32768)
+        self.widths = sorted(set(PLAN), reverse=True)
+        for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ[var] = "1"  # inherited by the spawned workers before their numpy loads
+        self.pool = mp.get_context("spawn").Pool(self.workers, initializer=_cpu_init,
+                                                 initargs=(self.tokens, HQ, self.widths))
+        self.unit = {b: [] for b in self.widths}
+        self.append = {}
+        self.step_s = []
+
+    def step(self, timed: bool = True) -> float:
+        t0 = time.perf_counter()
+        res = self.pool.map(_cpu_unit, range(self.workers), chunksize=1)
+        dt = time.perf_counter() - t0
+        for times, app, pid in res:
+            self.append[pid] = app
+            if timed:
+                for b in self.widths:
+                    self.unit[b].append(times[b])
+        if timed:
+            self.step_s.append(dt)
+        return dt
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+    def summary(self) -> dict:
+        med = {b: statistics.median(self.unit[b]) * (T / self.tokens) for b in self.widths}
+        seq_s = sum(med[b] for b in PLAN)  # one sequence through all L layers on one core
+        tok_s = self.workers / seq_s
+        alg = sum(attn_alg_bytes(b, 1, T, 0) for b in PLAN)  # per decoded token
+        # quantize-append: bytes of config 3's accounting (bf16 K/V read + compressed write) per worker append
+        app_bytes = {b: 2 * self.tokens * H * D * 2 + 2 * self.tokens * tok_bytes(b) for b in self.widths}
+        app_s = {b: statistics.median([a[b] for a in self.append.values()]) for b in self.widths}
+        append_gbs = self.workers * sum(app_bytes.values()) / sum(app_s.values()) / 1e9
+        return {
+            "tokens_per_s": tok_s, "alg_gbs": tok_s * alg / 1e9, "workers": self.workers,
+            "unit_s": {str(b): med[b] for b in self.widths}, "steps_timed": len(self.step_s),
+            "ms_per_step": 1e3 * statistics.median(self.step_s) if self.step_s else None,
+            "append_gbs": append_gbs, "append_s_per_unit": {str(b): app_s[b] for b in self.widths},
+            "cpu_model": cpu_model(),
+            "sample": f"one step = {self.workers} processes (1 core each) x 1 (sequence, layer) attend per width "
+                      f"{self.widths} at T={self.tokens}" + (f" (scaled x{T // self.tokens} to T={T})" if T != self.tokens else "")
+                      + f"; tokens/s = {self.workers} / (sum over the {L} layers' per-width median unit times); "
+                      f"append_gbs = {self.workers} workers x one {self.tokens}-token append_tokens per width",
+        }
+
+
+def parity_sample(store, outs, q_all, seq: int):
+    """Checker (outside every timed region): the last timed step's bf16 output of one sampled sequence in
+    the first layer of each width vs the CPU oracle's attend (attention.py:103-151) over that layer's
+    exported compressed state — the same state the step attended (nothing was appended since).  Bar: the
+    north_star's 2e-3 max-abs (|out| << 1 for these N(0, 1) inputs)."""
+    from oracle import tada_oracle as orc
+
+    rows = {}
+    for bits in sorted(set(PLAN)):
+        layer = PLAN.index(bits)
+        ex = store.export(layer, seq)
+        st = orc.LayerState(H, D, bits, R)
+        st.kmean, st.vmean = ex["k_mean"].cpu().numpy(), ex["v_mean"].cpu().numpy()
+        for name in ("k_dev", "v_dev"):
+            d = ex[name].to_host()
+            rec = orc.Deviation(bits, d.num_tokens, d.num_heads, d.group_size, d.codes, np.asarray(d.scales),
+                                np.asarray(d.mins))
+            setattr(st, "kdev" if name == "k_dev" else "vdev", rec)
+        st.rk, st.rv = ex["residual_k"].cpu().numpy(), ex["residual_v"].cpu().numpy()
+        q = q_all[layer][seq].float().cpu().numpy()
+        want, _ = orc.attend(q, st, HQ)
+        got = outs[layer][seq].float().cpu().numpy()
+        rows[str(bits)] = {"layer": layer, "seq": seq, "tokens": st.compressed + st.r,
+                           "max_abs": float(np.abs(got - want).max()), "out_absmax": float(np.abs(want).max())}
+    worst = max(r["max_abs"] for r in rows.values())
+    return {"max_abs": worst, "bar": 2e-3, "pass": worst <= 2e-3, "per_width": rows,
+            "oracle": "oracle/tada_oracle.py attend over the exported state (bf16 output of the timed step)"}
 
 
 def run_reference(args):
+    """The reference arm: the CPU oracle port on this host's cores, K timed sampled steps after W warm-up
+    steps (rank 0 only under torchrun)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    reps = 1
-    warm = cpu_oracle_leg(reps=max(1, args.warmup // 3))  # builds + warms; counts toward warmup
-    times = []
-    last = warm
-    for _ in range(max(1, args.steps // 5)):
-        last = cpu_oracle_leg(reps=reps)
-        times.append(last["step_s"])
-    step_s = statistics.median(times)
-    v = B_PER_GPU / step_s
+    cpu = CpuOracle()
+    for _ in range(args.warmup):
+        cpu.step(timed=False)
+    for _ in range(args.steps):
+        cpu.step()
+    cpu.close()
+    s = cpu.summary()
+    v = s["tokens_per_s"]
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "steps": s["steps_timed"], "warmup": args.warmup, "ms_per_step": s["ms_per_step"], "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD + " (CPU oracle port, numpy)", "global_batch": B_PER_GPU, "seq_len": T,
-                   "parallelism": f"{last['workers']} host processes"},
-        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": last["workers"], "kind": "port",
-                         "sample": last["sample"]},
+                   "parallelism": f"{s['workers']} host processes"},
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": s["workers"], "kind": "port", "sample": s["sample"],
+                         "cpu_model": s["cpu_model"], "append_gbs": s["append_gbs"], "alg_gbs": s["alg_gbs"]},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "hbm_gbs_equiv": last["alg_gbs"],
+        "hbm_gbs_equiv": s["alg_gbs"], "unit_s": s["unit_s"],
+        "note": "ms_per_step is the wall time of one sampled step (see cpu_baseline.sample), not of a full decode step",
     }
     print(json.dumps(line), flush=True)
 
@@ -242,10 +337,27 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    comm = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm = {"backend": dist.get_backend(), "nranks": dist.get_world_size(),
+                "nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
+                "collective": "all_gather_into_tensor of the step's attention outputs (once per step, after the "
+                              "last layer); no collective inside the per-layer hot loop"}
+        print(f"[rank {rank}] NCCL communicator: {comm['nranks']} ranks, backend {comm['backend']}, "
+              f"NCCL {comm['nccl_version']}", file=sys.stderr, flush=True)
     dev = torch.device("cuda", local)
     B = B_PER_GPU
+    if args.scaling == "strong":  # the config's global batch split over the ranks
+        global_b = STRONG_GLOBAL_BATCH.get(args.config, B_PER_GPU)
+        if global_b % world:
+            raise SystemExit(f"strong scaling: global batch {global_b} is not divisible by {world} GPUs")
+        B = global_b // world
+    need = B * (T + R) * sum(2 * tok_bytes(b) for b in PLAN)  # this rank's compressed cache bytes
+    free = torch.cuda.mem_get_info(dev)[0]
+    if need > 0.97 * free:
+        raise SystemExit(f"config {args.config} x batch {B} per GPU needs ~{need / 1e9:.0f} GB of cache; "
+                         f"{free / 1e9:.0f} GB free on this GPU ({args.scaling} scaling at {world} GPUs)")
     steps, warm = args.steps, args.warmup
     max_tokens = T + R + 2 * steps + warm + 16  # timed + e2e passes
     store = tk.PagedKVCache(L, H, D, PLAN, R, batch=B, page_tokens=64, max_tokens=max_tokens, shuffle_pages=True,
@@ -338,6 +450,10 @@ def run_ours(args):
         time.sleep(0.1)
     gpu_launches = launch_count() - launches_before
     ms = t0.elapsed_time(t1)
+    parity = None
+    if not args.no_parity:  # the timed step's output vs the oracle (untimed; before e2e changes the state)
+        last = (warm + steps - 1) % nsets
+        parity = parity_sample(store, outs, qs[last], seq=(5 + rank) % B)
     if world > 1:
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -438,12 +554,16 @@ def run_ours(args):
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu:
-            c = cpu_oracle_leg(reps=1)
+            oracle_cpu = CpuOracle()
+            oracle_cpu.step()
+            oracle_cpu.close()
+            c = oracle_cpu.summary()
             cpu = {"value": c["tokens_per_s"], "unit": "tokens/s", "cores": c["workers"], "kind": "port",
-                   "sample": c["sample"], "alg_gbs": c["alg_gbs"]}
+                   "sample": c["sample"], "alg_gbs": c["alg_gbs"], "append_gbs": c["append_gbs"],
+                   "cpu_model": c["cpu_model"]}
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": steps, "warmup": warm,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "u8 codes / f32 means+scales, bf16 q/out", "data": "synthetic (torch.randn bf16, seeded)",
             "config": {"workload": WORKLOAD, "global_batch": B * world, "seq_len": T, "layers": L,
                        "parallelism": f"seq-shard x{world}", "num_splits": {str(k): v for k, v in splits.items()}, "page_tokens": 64,
@@ -468,10 +588,31 @@ def run_ours(args):
             "gpu_launches": gpu_launches,
             "clocks": clk.summary(wall0, wall1),
             "cpu_baseline": cpu,
+            "parity": parity,
+            "comm": comm if comm is None else dict(comm, bytes_per_step=int(gathered.numel()) * 2),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def self_launch(args) -> int:
+    """--gpus N > 1 without a launcher: re-exec under torch.distributed.run, one rank per GPU (127.0.0.1
+    rendezvous).  Fails (non-zero) when this box has fewer than N GPUs instead of running fewer ranks."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} CUDA devices, this box has {have}", file=sys.stderr)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -482,12 +623,22 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", type=int, default=0, help="attention kernel: 0 auto, 1 exact generic, 2 tensor-core")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle leg")
+    ap.add_argument("--no-parity", action="store_true", help="skip the post-run oracle check of the timed step")
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS),
                     help="BASELINE.json config (2 = headline; 4 = 128k 2-bit; 5 = 70B shape)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: the config's batch per GPU; strong: the config's global batch split over the GPUs "
+                         "(config 2: 16 sequences; config 5: 128)")
     args = ap.parse_args()
     use_config(args.config)
     if args.warmup < 3:
         args.warmup = 3
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "ours" and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args)
     else:

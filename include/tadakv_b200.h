@@ -124,6 +124,32 @@ int tada_quant_append(const tada_page_layout* layout, uint8_t* pool, const void*
                       const int32_t* dst_start, int64_t dst_offset, int32_t* err_flag,
                       void* stream);
 
+/* Device-planned K1 for a batch of sequences at different lengths (append_tokens, cache.py:154-180, per
+ * sequence): every sequence b appends n = seq_n ? seq_n[b] : n_new rows and its flush is planned on the
+ * device from res_len[b] (r < residual_length) — the first floor((r + n) / R) * R tokens of [its r
+ * residual rows, its new rows] are compressed at comp_len[b] onwards (R = residual_length; R = 0: all n
+ * new rows).  part 1 compresses the residual rows (src = the f32 residual buffer, src_seq_stride = its
+ * rows per sequence), part 2 the new rows (src = the step input; dst after the part-1 rows).  n_max bounds
+ * the rows of any sequence in this launch (grid size).  Lengths are not changed: tada_append_commit
+ * follows.  rope_cs / positions (part 2 only, nullable): the keys are rotated in registers as in
+ * tada_quant_append_rope. */
+int tada_quant_append_plan(const tada_page_layout* layout, uint8_t* pool, const void* src_k,
+                           const void* src_v, int32_t dtype, int32_t batch, int64_t n_max,
+                           int64_t src_seq_stride, const int32_t* page_table, int32_t pt_stride,
+                           const int32_t* comp_len, const int32_t* res_len, int32_t residual_length,
+                           int32_t n_new, const int32_t* seq_n, int32_t part, const int32_t* positions,
+                           int64_t pos_stride, const float* rope_cs, int32_t rope_rows,
+                           int32_t* err_flag, void* stream);
+
+/* The rest of that append, one CTA per sequence: the new rows that stay raw are stored (f32; keys rotated
+ * when rope_cs is given) at their residual rows, then comp_len[b] / res_len[b] advance by the plan. */
+int tada_append_commit(float* res_k, float* res_v, int64_t res_seq_stride, int32_t heads, int32_t head_dim,
+                       const void* src_k, const void* src_v, int32_t dtype, int32_t batch,
+                       int64_t src_seq_stride, int32_t n_new, const int32_t* seq_n,
+                       int32_t residual_length, int32_t* comp_len, int32_t* res_len,
+                       const int32_t* positions, int64_t pos_stride, const float* rope_cs,
+                       int32_t rope_rows, int32_t* err_flag, void* stream);
+
 /* ---------------------------------------------------------------- RoPE
  * apply_rope / rotate_heads (tensor.py:63-105): rotate every adjacent (2j, 2j+1) pair of each
  * [n_tok][heads][head_dim] row of token t by position positions[t]; out is f32. rope_cs is the
@@ -133,36 +159,6 @@ int tada_quant_append(const tada_page_layout* layout, uint8_t* pool, const void*
 int tada_apply_rope(const void* x, int32_t dtype, int64_t n_tok, int32_t heads, int32_t head_dim,
                     const int32_t* positions, const float* rope_cs, int32_t rope_rows, float* out,
                     int32_t* err_flag, void* stream);
-
-/* K1 with the keys rotated in registers before the mean: append_fused's key path
- * (model.py:167-183 = rotate_heads + append_tokens) without the rotated keys ever reaching HBM.
- * positions: device int32 [batch][pos_stride], token i of sequence b at positions[b * pos_stride + i].
- * Values are appended as given. Needs heads 8, head_dim 128, bits 2/4/8 and 16-byte aligned rows,
- * else TADA_ERR_CONFIG (compose tada_apply_rope + tada_quant_append). Bit-identical to that
- * composition. */
-int tada_quant_append_rope(const tada_page_layout* layout, uint8_t* pool, const void* src_k,
-                           const void* src_v, int32_t dtype, int32_t batch, int64_t n_tok,
-                           int64_t src_seq_stride, const int32_t* page_table, int32_t pt_stride,
-                           const int32_t* dst_start, int64_t dst_offset, const int32_t* positions,
-                           int64_t pos_stride, const float* rope_cs, int32_t rope_rows,
-                           int32_t* err_flag, void* stream);
-
-/* Residual-buffer write (cache.py:174-175): token i of sequence b is copied (as f32)
- * to res[(b * res_seq_stride + pos[b] + pos_offset + i)][heads][head_dim]. */
-int tada_residual_write(float* res_k, float* res_v, int64_t res_seq_stride, int32_t heads,
-                        int32_t head_dim, const void* src_k, const void* src_v, int32_t dtype,
-                        int32_t batch, int64_t n_tok, int64_t src_seq_stride, const int32_t* pos,
-                        int32_t pos_offset, void* stream);
-
-/* tada_residual_write at pos[b] (pos_offset 0) followed by pos[b] += n_tok, in one launch:
- * the no-flush branch of append_tokens (cache.py:174-175) for a decode step. */
-int tada_residual_append(float* res_k, float* res_v, int64_t res_seq_stride, int32_t heads,
-                         int32_t head_dim, const void* src_k, const void* src_v, int32_t dtype,
-                         int32_t batch, int64_t n_tok, int64_t src_seq_stride, int32_t* pos,
-                         void* stream);
-
-/* arr[b] += delta for b < batch (device-side length bookkeeping, graph-capturable). */
-int tada_lengths_add(int32_t* arr, int32_t batch, int32_t delta, void* stream);
 
 /* Export / import of one sequence's compressed region between the paged layout
  * and the reference's dense layout (k_mean, k_dev.codes/scales/mins, ...), used
@@ -215,24 +211,31 @@ int tada_decode_attn_lse(const tada_page_layout* layout, const uint8_t* pool, co
 int tada_combine_lse(const float* o_parts, const float* lse_parts, int32_t n_parts, int64_t rows,
                      int32_t head_dim, void* out, int32_t out_dtype, float* lse_out, void* stream);
 
+/* One decode step of a layer for a batch of sequences at ANY mix of lengths (ragged), graph-capturable:
+ * append_tokens of one token per sequence (cache.py:154-180) then attend_streaming (attention.py:103-151),
+ * every flush decision taken on the device from the sequence's own res_len (seq_plan):
+ *  - a sequence whose residual reaches residual_length compresses it and the new row (K1, two launches
+ *    over the flushing sequences: the residual rows, then the new row; k1_rows bounds the residual rows
+ *    any sequence may flush, residual_length - 1 under graph capture; k1_rows < 0 skips K1 when the caller
+ *    knows no sequence compresses a token this step; residual_length 0 compresses every new row);
+ *  - K2 attends comp_len[b] plus the tokens this step compresses;
+ *  - K3 attends the residual rows and, where no flush happened, the new row read from the input, stores
+ *    that row at residual row res_len[b], and the last K3 CTA of each sequence advances comp_len[b] /
+ *    res_len[b] (step_sync: device int32[batch] arrival counters, zero-initialised, left at zero).
+ * new_k / new_v: [batch][heads][head_dim] (f32 or bf16), already rotated. Needs the tensor-core path
+ * (head_dim 128), else TADA_ERR_CONFIG with nothing enqueued (compose tada_quant_append_plan +
+ * tada_append_commit + tada_decode_attn). Results equal that composition. */
+int tada_decode_step(const tada_page_layout* layout, uint8_t* pool, const void* q, int32_t q_dtype,
+                     int32_t batch, int32_t num_q_heads, const int32_t* page_table, int32_t pt_stride,
+                     int32_t* comp_len, int32_t* res_len, float* res_k, float* res_v,
+                     int64_t res_seq_stride, int32_t residual_length, const void* new_k, const void* new_v,
+                     int32_t new_dtype, int32_t k1_rows, int32_t* step_sync, float scale,
+                     int32_t num_splits, void* workspace, void* out, int32_t out_dtype, int32_t mode,
+                     int32_t* err_flag, void* stream);
+
 /* Split count for this layer's kernel on the current device: the fewest whole waves of resident
  * CTAs (SM count x CTAs per SM of the instantiation that will run) whose last wave is >= 90% full,
  * with >= 256 tokens per split. */
-/* One decode step of a layer in one call: append_tokens of one new token that stays in the residual
- * buffer (no flush: r_prev + 1 < residual_length; cache.py:174-175) followed by attend_streaming
- * (attention.py:103-151). new_k / new_v: [batch][heads][head_dim] (f32 or bf16), already rotated.
- * The K3 combine attends the new row straight from the input, stores it (as f32) at residual row
- * r_prev of every sequence and sets res_len[b] = r_prev + 1 (r_prev: the host-known, batch-uniform
- * residual count before the step). Needs the tensor-core path (head_dim 128), else TADA_ERR_CONFIG
- * with nothing enqueued. Results equal tada_residual_append + tada_decode_attn. */
-int tada_decode_attn_append(const tada_page_layout* layout, const uint8_t* pool, const void* q,
-                            int32_t q_dtype, int32_t batch, int32_t num_q_heads,
-                            const int32_t* page_table, int32_t pt_stride, const int32_t* comp_len,
-                            int32_t* res_len, float* res_k, float* res_v, int64_t res_seq_stride,
-                            float scale, int32_t num_splits, void* workspace, void* out,
-                            int32_t out_dtype, int32_t mode, const void* new_k, const void* new_v,
-                            int32_t new_dtype, int32_t r_prev, void* stream);
-
 int32_t tada_decode_attn_plan_splits(const tada_page_layout* layout, int32_t num_q_heads, int32_t batch,
                                      int64_t max_tokens);
 

@@ -32,7 +32,7 @@ from .errors import (
     TadaError,
 )
 from .decoder import ToyDecoder
-from .paged import PagedKVCache
+from .paged import DecodeGraph, PagedKVCache
 from .rope import append_fused, append_rope, apply_rope, rope_table, rotate_heads
 from .shard import ShardedKVCache, ShardPlan
 from .quant import (
@@ -54,7 +54,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "AttentionOutput", "BlockSpec", "BudgetInfeasibleError", "CapacityError", "CompressedLayerCache", "ConfigError",
-    "DataError", "FormatError", "ModelConfig", "PagedKVCache", "PrecisionPlan", "QuantizedDeviation", "RopeParams",
+    "DataError", "DecodeGraph", "FormatError", "ModelConfig", "PagedKVCache", "PrecisionPlan", "QuantizedDeviation", "RopeParams",
     "ShapeError", "ShardPlan", "ToyDecoder", "append_fused", "append_rope", "apply_rope", "rope_table", "rotate_heads", "ShardedKVCache", "StateError", "TadaError", "actual_bytes_per_token", "attend_naive", "attend_streaming",
     "bytes_per_group", "concat_deviations", "dequantize_groups", "dequantize_tensor", "deserialize_cache",
     "direct_quantize_baseline", "empty_deviation", "kv_head_index", "mean_center", "memory_ratio", "pack_codes",

@@ -12,11 +12,12 @@ import os
 from .errors import ConfigError, DataError, FormatError, ShapeError, StateError, TadaError
 
 LIB_NAME = "libtadakv_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("TADA_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 TADA_F32 = 0
 TADA_BF16 = 1
 
+TADA_ERR_CONFIG = 2
 _ERRORS = {1: ShapeError, 2: ConfigError, 3: DataError, 4: FormatError, 5: StateError}
 
 
@@ -59,12 +60,7 @@ SIGNATURES = {
     "tada_unpack_codes": (I32, [P, I64, I32, I32, P, I64, P, P]),
     "tada_mean_center": (I32, [P, I32, I64, I32, I32, P, P, P, P]),
     "tada_quant_append": (I32, [C.POINTER(PageLayout), P, P, P, I32, I32, I64, I64, P, I32, P, I64, P, P]),
-    "tada_residual_write": (I32, [P, P, I64, I32, I32, P, P, I32, I32, I64, I64, P, I32, P]),
     "tada_apply_rope": (I32, [P, I32, I64, I32, I32, P, P, I32, P, P, P]),
-    "tada_quant_append_rope": (I32, [C.POINTER(PageLayout), P, P, P, I32, I32, I64, I64, P, I32, P, I64, P, I64, P,
-                                     I32, P, P]),
-    "tada_residual_append": (I32, [P, P, I64, I32, I32, P, P, I32, I32, I64, I64, P, P]),
-    "tada_lengths_add": (I32, [P, I32, I32, P]),
     "tada_gather_compressed": (I32, [C.POINTER(PageLayout), P, P, I64, I32, P, P, P, P, P]),
     "tada_scatter_compressed": (I32, [C.POINTER(PageLayout), P, P, I64, I32, P, P, P, P, P]),
     "tada_decode_attn_workspace_bytes": (I64, [I32, I32, I32, I32]),
@@ -72,9 +68,12 @@ SIGNATURES = {
                                I32, I32, P]),
     "tada_decode_attn_lse": (I32, [C.POINTER(PageLayout), P, P, I32, I32, I32, P, I32, P, P, P, P, I64, F, I32, P,
                                    P, I32, I32, P, P]),
-    "tada_decode_attn_append": (I32, [C.POINTER(PageLayout), P, P, I32, I32, I32, P, I32, P, P, P, P, I64, C.c_float,
-                                      I32, P, P, I32, I32, P, P, I32, I32, P]),
     "tada_combine_lse": (I32, [P, P, I32, I64, I32, P, I32, P, P]),
+    "tada_quant_append_plan": (I32, [C.POINTER(PageLayout), P, P, P, I32, I32, I64, I64, P, I32, P, P, I32, I32, P,
+                                     I32, P, I64, P, I32, P, P]),
+    "tada_append_commit": (I32, [P, P, I64, I32, I32, P, P, I32, I32, I64, I32, P, I32, P, P, P, I64, P, I32, P, P]),
+    "tada_decode_step": (I32, [C.POINTER(PageLayout), P, P, I32, I32, I32, P, I32, P, P, P, P, I64, I32, P, P, I32,
+                               I32, P, F, I32, P, P, I32, I32, P, P]),
     "tada_decode_attn_suggest_splits": (I32, [I32, I64, I32]),
     "tada_decode_attn_plan_splits": (I32, [C.POINTER(PageLayout), I32, I32, I64]),
 }

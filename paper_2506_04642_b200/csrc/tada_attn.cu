@@ -355,9 +355,8 @@ __global__ void __launch_bounds__(256) combine_pair_kernel(AttnArgs a, int n_row
   }
   if (active && role >= 1) {  // ---- residual rows (raw f32; this step's row read from the input)
     const int rw = role - 1;
-    const bool fused = a.new_k != nullptr;
-    const int R = fused ? a.r_prev + 1 : a.res_len[b];
-    const int r_new = fused ? a.r_prev : -1;
+    int R, r_new;
+    residual_rows(a, b, R, r_new);
     auto new_row = [&](const void* src) {  // this lane's 4 columns of the new row of head h, as f32
       float x[4];
       const int64_t off = (int64_t(b) * H + h) * D + 4 * lane;
@@ -365,11 +364,11 @@ __global__ void __launch_bounds__(256) combine_pair_kernel(AttnArgs a, int n_row
       else load4(reinterpret_cast<const __nv_bfloat16*>(src) + off, x);
       return make_float4(x[0], x[1], x[2], x[3]);
     };
-    if (fused && gq % G == 0 && rw == 0) {  // one warp per (sequence, KV head) stores the row for later steps
+    if (r_new >= 0 && gq % G == 0 && rw == 0) {  // one warp per (sequence, KV head) stores the row for later steps
       const int64_t dst = ((int64_t(b) * a.res_seq_stride + r_new) * H + h) * D + 4 * lane;
       *reinterpret_cast<float4*>(const_cast<float*>(a.res_k) + dst) = new_row(a.new_k);
       *reinterpret_cast<float4*>(const_cast<float*>(a.res_v) + dst) = new_row(a.new_v);
-      if (gq == 0 && lane == 0) const_cast<int32_t*>(a.res_len)[b] = r_new + 1;
+      if (!a.step && gq == 0 && lane == 0) const_cast<int32_t*>(a.res_len)[b] = r_new + 1;
     }
     float q[4];
     if (a.q_dtype == TADA_F32) load4(reinterpret_cast<const float*>(a.q) + int64_t(row) * D + 4 * lane, q);
@@ -447,6 +446,10 @@ __global__ void __launch_bounds__(256) combine_pair_kernel(AttnArgs a, int n_row
     for (int e = 0; e < 4; ++e) store_any(a.out, a.out_dtype, qi + e, o[e] * inv);
     if (lane == 0 && a.lse_out) a.lse_out[row] = M + logf(L);
   }
+  if (a.step) {  // both rows of this CTA belong to one sequence (Hq is even: a multiple of 8 KV heads)
+    __syncthreads();
+    if (threadIdx.x == 0 && active) step_commit(a, b, Hq / 2);
+  }
 }
 
 // K3 for head_dim 128 and G = Hq/H in {1, 2, 4, 8}: one CTA per (sequence, KV head), G + 4 warps.
@@ -470,9 +473,8 @@ __global__ void __launch_bounds__((G + 4) * 32) combine_kv_kernel(AttnArgs a, in
   pdl_enter();  // no global reads above this line
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int h = blockIdx.x, b = blockIdx.y, H = a.L.heads, Hq = a.Hq, S = a.splits;
-  const bool fused = a.new_k != nullptr;
-  const int R = fused ? a.r_prev + 1 : a.res_len[b];
-  const int r_new = fused ? a.r_prev : -1;
+  int R, r_new;
+  residual_rows(a, b, R, r_new);
   if (warp >= G) {  // the residual warps stage the q rows (named barrier 1: the split warps start at once)
     for (int i = threadIdx.x - G * 32; i < G * D; i += RWN * 32) {
       const int g = i / D, d = i - (i / D) * D;
@@ -537,7 +539,7 @@ __global__ void __launch_bounds__((G + 4) * 32) combine_kv_kernel(AttnArgs a, in
     const int rw = warp - G;
     const int64_t rbase = int64_t(b) * a.res_seq_stride;
     const int64_t nrow = (int64_t(b) * H + h) * D;  // this head's new row in the step input
-    if (fused && rw == 0) {  // store the step's row for later steps
+    if (r_new >= 0 && rw == 0) {  // store the step's row for later steps
       float x[4];
       const int64_t dst = ((rbase + r_new) * H + h) * D + 4 * lane;
       if (a.new_dtype == TADA_F32) load4(reinterpret_cast<const float*>(a.new_k) + nrow + 4 * lane, x);
@@ -546,7 +548,7 @@ __global__ void __launch_bounds__((G + 4) * 32) combine_kv_kernel(AttnArgs a, in
       if (a.new_dtype == TADA_F32) load4(reinterpret_cast<const float*>(a.new_v) + nrow + 4 * lane, x);
       else load4(reinterpret_cast<const __nv_bfloat16*>(a.new_v) + nrow + 4 * lane, x);
       *reinterpret_cast<float4*>(const_cast<float*>(a.res_v) + dst) = make_float4(x[0], x[1], x[2], x[3]);
-      if (h == 0 && lane == 0) const_cast<int32_t*>(a.res_len)[b] = r_new + 1;
+      if (!a.step && h == 0 && lane == 0) const_cast<int32_t*>(a.res_len)[b] = r_new + 1;
     }
     float racc[G][4], rm[G], rl[G];
 #pragma unroll
@@ -664,6 +666,10 @@ __global__ void __launch_bounds__((G + 4) * 32) combine_kv_kernel(AttnArgs a, in
 #pragma unroll
     for (int e = 0; e < 4; ++e) store_any(a.out, a.out_dtype, qi + e, o[e] * inv);
     if (lane == 0 && a.lse_out) a.lse_out[row] = M + logf(L);
+  }
+  if (a.step) {  // the H CTAs of sequence b: the last one advances its lengths
+    __syncthreads();
+    if (threadIdx.x == 0) step_commit(a, b, gridDim.x);
   }
 }
 
@@ -788,7 +794,7 @@ static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool,
                             int64_t res_seq_stride, float scale, int32_t num_splits, void* workspace, void* out,
                             int32_t out_dtype, int32_t mode, float* lse_out, void* stream,
                             const void* new_k = nullptr, const void* new_v = nullptr, int32_t new_dtype = 0,
-                            int32_t r_prev = 0) {
+                            int32_t step_R = -1, int32_t* step_sync = nullptr) {
   if (!layout) return fail(TADA_ERR_CONFIG, "null layout");
   if (q_dtype != TADA_F32 && q_dtype != TADA_BF16) return fail(TADA_ERR_CONFIG, "q dtype must be f32 or bf16");
   if (out_dtype != TADA_F32 && out_dtype != TADA_BF16) return fail(TADA_ERR_CONFIG, "out dtype must be f32 or bf16");
@@ -828,7 +834,9 @@ static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool,
   a.new_k = new_k;
   a.new_v = new_v;
   a.new_dtype = new_dtype;
-  a.r_prev = r_prev;
+  a.step = step_R >= 0;
+  a.step_R = step_R;
+  a.step_sync = step_sync;
   {
     static const int diag = getenv("TADA_ATTN_DIAG") ? atoi(getenv("TADA_ATTN_DIAG")) : 0;
     a.diag = diag;
@@ -868,22 +876,38 @@ int tada_decode_attn_lse(const tada_page_layout* layout, const uint8_t* pool, co
                           res_v, res_seq_stride, scale, num_splits, workspace, out, out_dtype, mode, lse_out, stream);
 }
 
-int tada_decode_attn_append(const tada_page_layout* layout, const uint8_t* pool, const void* q, int32_t q_dtype,
-                            int32_t batch, int32_t num_q_heads, const int32_t* page_table, int32_t pt_stride,
-                            const int32_t* comp_len, int32_t* res_len, float* res_k, float* res_v,
-                            int64_t res_seq_stride, float scale, int32_t num_splits, void* workspace, void* out,
-                            int32_t out_dtype, int32_t mode, const void* new_k, const void* new_v, int32_t new_dtype,
-                            int32_t r_prev, void* stream) {
+int tada_decode_step(const tada_page_layout* layout, uint8_t* pool, const void* q, int32_t q_dtype, int32_t batch,
+                     int32_t num_q_heads, const int32_t* page_table, int32_t pt_stride, int32_t* comp_len,
+                     int32_t* res_len, float* res_k, float* res_v, int64_t res_seq_stride, int32_t residual_length,
+                     const void* new_k, const void* new_v, int32_t new_dtype, int32_t k1_rows, int32_t* step_sync,
+                     float scale, int32_t num_splits, void* workspace, void* out, int32_t out_dtype, int32_t mode,
+                     int32_t* err_flag, void* stream) {
   if (!layout) return fail(TADA_ERR_CONFIG, "null layout");
   if (mode == 1 || !fast_supported(*layout, num_q_heads) || layout->head_dim != 128)
-    return fail(TADA_ERR_CONFIG, "fused decode step needs the tensor-core attention path (head_dim 128)");
-  if (!new_k || !new_v || !res_k || !res_v) return fail(TADA_ERR_SHAPE, "null buffer");
+    return fail(TADA_ERR_CONFIG, "the fused decode step needs the tensor-core attention path (head_dim 128)");
+  if (!new_k || !new_v || !res_k || !res_v || !step_sync || !comp_len || !res_len) return fail(TADA_ERR_SHAPE, "null buffer");
   if (new_dtype != TADA_F32 && new_dtype != TADA_BF16) return fail(TADA_ERR_CONFIG, "new row dtype must be f32 or bf16");
-  if (r_prev < 0 || r_prev + 1 > res_seq_stride)
-    return fail(TADA_ERR_CONFIG, "the new row does not fit the residual buffer (flush first)");
+  if (residual_length < 0 || (residual_length > 0 && residual_length > res_seq_stride) ||
+      k1_rows > (residual_length > 0 ? residual_length - 1 : 0))
+    return fail(TADA_ERR_CONFIG, "residual buffer / flush rows out of range");
+  if (batch == 0) return TADA_OK;
+  // K1 for the sequences whose residual fills this step (each decides on the device): its residual rows,
+  // then the new row; k1_rows < 0 means the caller knows no sequence compresses a token this step
+  if (k1_rows > 0) {
+    const int rc = tada_quant_append_plan(layout, pool, res_k, res_v, TADA_F32, batch, k1_rows, res_seq_stride,
+                                          page_table, pt_stride, comp_len, res_len, residual_length, 1, nullptr, 1,
+                                          nullptr, 0, nullptr, 0, err_flag, stream);
+    if (rc != TADA_OK) return rc;
+  }
+  if (k1_rows >= 0) {
+    const int rc = tada_quant_append_plan(layout, pool, new_k, new_v, new_dtype, batch, 1, 1, page_table, pt_stride,
+                                          comp_len, res_len, residual_length, 1, nullptr, 2, nullptr, 0, nullptr, 0,
+                                          err_flag, stream);
+    if (rc != TADA_OK) return rc;
+  }
   return decode_attn_impl(layout, pool, q, q_dtype, batch, num_q_heads, page_table, pt_stride, comp_len, res_len, res_k,
                           res_v, res_seq_stride, scale, num_splits, workspace, out, out_dtype, mode == 0 ? 2 : mode,
-                          nullptr, stream, new_k, new_v, new_dtype, r_prev);
+                          nullptr, stream, new_k, new_v, new_dtype, residual_length, step_sync);
 }
 
 int tada_combine_lse(const float* o_parts, const float* lse_parts, int32_t n_parts, int64_t rows, int32_t head_dim,

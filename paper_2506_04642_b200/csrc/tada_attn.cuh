@@ -30,15 +30,55 @@ struct AttnArgs {
   void* out;
   int out_dtype;
   int q_dtype;
-  // decode-step fusion (tada_decode_attn_append): the step's new K/V row [batch][heads][head_dim] is attended
-  // by K3 directly and written to residual row r_prev (whose count K3 then sets to r_prev + 1)
+  // decode step (tada_decode_step): the step's new K/V row [batch][heads][head_dim], attended by K3 straight
+  // from the input and stored at the sequence's next residual row
   const void* new_k;
   const void* new_v;
   int new_dtype;
-  int r_prev;
   int diag;  // diagnostics only (env TADA_ATTN_DIAG): 1 = TMA ring without compute, 2 = compute on one L2-resident page
   float* lse_out;  // optional [B][Hq]: natural-log sum-exp of the scaled logits (cross-rank merge)
+  // device-planned decode step (tada_decode_step): one new row per sequence, residual_length step_R; each
+  // sequence's flush decision comes from its own res_len (seq_plan), K3 advances the lengths (step_sync:
+  // per-sequence arrival counters, zero between steps)
+  int step;
+  int step_R;
+  int32_t* step_sync;
 };
+
+// Compressed tokens K2 attends for sequence b: in a decode step, those a flush of this step adds too (K1
+// compressed them just before).
+__device__ __forceinline__ int comp_tokens(const AttnArgs& a, int b) {
+  return a.comp_len[b] + (a.step ? seq_plan(a.res_len[b], 1, a.step_R).ncomp : 0);
+}
+
+// K3 side of a decode step: how many residual rows sequence b attends and which of them
+// (r_new, or -1) is the step's new row read from the input.
+__device__ __forceinline__ void residual_rows(const AttnArgs& a, int b, int& rows, int& r_new) {
+  if (a.step) {
+    const int rb = a.res_len[b];
+    const SeqPlan p = seq_plan(rb, 1, a.step_R);
+    rows = p.res_after;
+    r_new = (a.step_R > 0 && p.ncomp == 0) ? rb : -1;
+  } else {
+    rows = a.res_len[b];
+    r_new = -1;
+  }
+}
+
+// Last of `ctas` CTAs of sequence b in a decode step's K3: advance its lengths (every CTA read them at
+// entry, before its arrival; the counter returns to zero for the next step).  Call from one thread after
+// the CTA's last global read of the lengths.
+__device__ __forceinline__ void step_commit(const AttnArgs& a, int b, int ctas) {
+  __threadfence();
+  const int old = atomicAdd(&a.step_sync[b], 1);
+  if (old == ctas - 1) {
+    const SeqPlan p = seq_plan(a.res_len[b], 1, a.step_R);
+    const_cast<int32_t*>(a.comp_len)[b] += p.ncomp;
+    const_cast<int32_t*>(a.res_len)[b] = p.res_after;
+    a.step_sync[b] = 0;
+    __threadfence();
+  }
+}
 
 __device__ __forceinline__ void store_any(void* out, int dtype, int64_t i, float v) {
   if (dtype == TADA_F32) reinterpret_cast<float*>(out)[i] = v;

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(TT * 16, TT == 16 ? 2 : 1) attn_fast_kernel(At
   float* qsum = reinterpret_cast<float*>(smem + pl.off_qsum);    // [HQ]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + pl.off_bar);
 
-  const int C = a.comp_len[b];
+  const int C = comp_tokens(a, b);
   int t_begin, t_end;
   split_range(C, a.splits, split, TT, t_begin, t_end);
   const int ntiles = t_end > t_begin ? (t_end - t_begin + TT - 1) / TT : 0;

@@ -66,6 +66,9 @@ constexpr int kBudget = 113 * 1024;  // two CTAs per SM
 #ifndef TADA_V8_PPS
 #define TADA_V8_PPS 0.00390625f  // 2^-8
 #endif
+#ifndef TADA_V8_RECENTER
+#define TADA_V8_RECENTER 32  // tiles between removals of the PV code bias from oc (power of 2; 0 = at the end only)
+#endif
 #ifndef TADA_V8_TMEM_OM
 #define TADA_V8_TMEM_OM 1  // park the PV mean accumulators in TMEM between tiles
 #endif
@@ -177,7 +180,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   float* red = reinterpret_cast<float*>(smem + pl.off_vm);                     // [3][HQ] epilogue (l, Σp·vmin, m)
 
   pdl_enter();  // no global reads above this line
-  const int C = a.comp_len[b];
+  const int C = comp_tokens(a, b);
   int t_begin, t_end;
   split_range(C, a.splits, split, TT, t_begin, t_end);
   const int ntiles = t_end > t_begin ? (t_end - t_begin + TT - 1) / TT : 0;
@@ -719,6 +722,28 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
         af[2] = lop_and_or(v, 0x00FF00FFu, 0x64006400u);
         af[3] = lop_and_or(v >> 8, 0x00FF00FFu, 0x64006400u);
         mma(oc[mt], af, bq0, bq1);
+      }
+    }
+    // ------------------------------------------------------------ re-centre the PV code accumulators
+    // oc holds bias * Σp' + Σp'·code: the biased f16 codes make |oc| up to ~40x the code term (2-bit), and the
+    // tensor core's f32 accumulation truncates (rounds toward zero) relative to |oc| on every MMA, so over
+    // thousands of tiles the error grows systematically (measured 4.2e-3 max-abs at 128k tokens, 2-bit).
+    // Every RC tiles the bias part (bias * column sums of the f16 P' the MMAs saw) is removed exactly enough
+    // in f32 and the running Σp' restarts, so each truncation acts on the small code term only.
+    if constexpr (TADA_V8_RECENTER > 0) {
+      if ((it & (TADA_V8_RECENTER - 1)) == TADA_V8_RECENTER - 1) {
+        float s = sp_run;
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        const float s0 = __shfl_sync(0xffffffffu, s, 8 * c), s1 = __shfl_sync(0xffffffffu, s, 8 * c + 4);
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+          oc[mt][0] = fmaf(-pv_bias<BITS>(mt, 0), s0, oc[mt][0]);
+          oc[mt][1] = fmaf(-pv_bias<BITS>(mt, 0), s1, oc[mt][1]);
+          oc[mt][2] = fmaf(-pv_bias<BITS>(mt, 1), s0, oc[mt][2]);
+          oc[mt][3] = fmaf(-pv_bias<BITS>(mt, 1), s1, oc[mt][3]);
+        }
+        sp_run = 0.f;
       }
     }
     // ------------------------------------------------------------ this warp's share of the vmean split

@@ -110,6 +110,38 @@ __device__ __forceinline__ uint32_t get_code(const uint8_t* grp, int e, int bits
   return (uint32_t(grp[bit >> 3]) >> (bit & 7)) & ((1u << bits) - 1u);
 }
 
+// ---------------------------------------------------------------- per-sequence append plan
+// The reference's append_tokens policy (cache.py:154-180) for ONE sequence, evaluated on the device from
+// its own residual count, so a batch of sequences at different lengths appends in the same launches (and
+// a decode step stays graph-capturable: no host-side branch on lengths).  r residual rows held (r < R),
+// n rows appended, residual_length R:
+//   R > 0: the first floor((r + n) / R) * R tokens of [residual rows, new rows] are compressed (flushes of
+//          whole R-blocks; quantization is per token, so one pass == the reference's block loop), the
+//          rest stay raw in the residual buffer;
+//   R = 0: the n new rows are compressed at once; residual rows (only a deserialized stream has any) stay.
+struct SeqPlan {
+  int ncomp;      // tokens this append compresses
+  int cnt_res;    // ... of which the residual buffer's first rows
+  int cnt_new;    // ... of which the first new rows
+  int res_after;  // residual rows afterwards
+};
+__host__ __device__ __forceinline__ SeqPlan seq_plan(int r, int n, int R) {
+  SeqPlan p;
+  if (R <= 0) {
+    p.ncomp = n;
+    p.cnt_res = 0;
+    p.cnt_new = n;
+    p.res_after = r;
+    return p;
+  }
+  const int total = r + n;
+  p.ncomp = total / R * R;
+  p.cnt_res = p.ncomp > 0 ? (r < p.ncomp ? r : p.ncomp) : 0;
+  p.cnt_new = p.ncomp - p.cnt_res;
+  p.res_after = total - p.ncomp;
+  return p;
+}
+
 // Warp reductions
 __device__ __forceinline__ float warp_min(float v) {
 #pragma unroll

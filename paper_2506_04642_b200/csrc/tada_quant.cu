@@ -271,7 +271,27 @@ struct AppendArgs {
   int rope_rows;
   const int32_t* positions;
   int64_t pos_stride;
+  // device-planned append (seq_plan): part 1 = the residual rows a flush compresses, part 2 = the new rows it
+  // compresses (dst at comp_len[b] + the residual rows); part 0 = the caller's n_tok rows at dst_start + offset
+  int part;
+  const int32_t* plan_res;  // res_len [B]
+  const int32_t* plan_n;    // optional per-sequence new-row counts [B]
+  int plan_n_new;           // new rows per sequence when plan_n is null
+  int plan_R;               // residual_length
 };
+
+// rows [0, count) of sequence b this launch compresses, and their destination offset after comp_len[b]
+__device__ __forceinline__ void append_part(const AppendArgs& a, int b, int64_t& count, int64_t& offset) {
+  if (a.part == 0) {
+    count = a.n_tok;
+    offset = a.dst_offset;
+    return;
+  }
+  const SeqPlan p = seq_plan(a.plan_res[b], a.plan_n ? a.plan_n[b] : a.plan_n_new, a.plan_R);
+  count = a.part == 1 ? p.cnt_res : p.cnt_new;
+  offset = a.part == 1 ? 0 : p.cnt_res;
+  if (count > a.n_tok) count = a.n_tok;  // the launch covers at most n_tok rows per sequence
+}
 
 template <typename T, int NCH>
 __global__ void __launch_bounds__(256) quant_append_kernel(AppendArgs a) {
@@ -280,7 +300,9 @@ __global__ void __launch_bounds__(256) quant_append_kernel(AppendArgs a) {
   const int side = blockIdx.y;
   const int b = blockIdx.x / a.tiles_per_seq;
   const int64_t i0 = int64_t(blockIdx.x % a.tiles_per_seq) * a.tt;
-  const int64_t rem = a.n_tok - i0;
+  int64_t count, offset;
+  append_part(a, b, count, offset);
+  const int64_t rem = count - i0;
   const int nt = int(rem < a.tt ? rem : a.tt);
   if (nt <= 0) return;
   const int row = H * D;
@@ -308,7 +330,7 @@ __global__ void __launch_bounds__(256) quant_append_kernel(AppendArgs a) {
   if (bad && a.err) atomicOr(a.err, 1);
   __syncthreads();
 
-  const int64_t c0 = a.dst_start[b] + a.dst_offset;
+  const int64_t c0 = a.dst_start[b] + offset;
   const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
   // B: means
   for (int e = threadIdx.x; e < nt * D; e += blockDim.x) {
@@ -336,52 +358,63 @@ __global__ void __launch_bounds__(256) quant_append_kernel(AppendArgs a) {
   }
 }
 
-// ------------------------------------------------------------------ residual write / lengths
-template <typename T>
-__global__ void residual_write_kernel(float* __restrict__ rk, float* __restrict__ rv, int64_t res_seq_stride, int row,
-                                      const T* __restrict__ sk, const T* __restrict__ sv, int64_t n_tok,
-                                      int64_t src_seq_stride, const int32_t* __restrict__ pos, int pos_offset,
-                                      int batch) {
-  const int64_t per_seq = n_tok * row;
-  const int64_t total = per_seq * batch * 2;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int side = int(i / (per_seq * batch));
-    const int64_t r = i - side * per_seq * batch;
-    const int b = int(r / per_seq);
-    const int64_t e = r - b * per_seq;
-    const T* s = side ? sv : sk;
-    float* d = side ? rv : rk;
-    const int64_t dst_tok = int64_t(b) * res_seq_stride + pos[b] + pos_offset;
-    d[dst_tok * row + e] = to_f32(s[int64_t(b) * src_seq_stride * row + e]);
-  }
-}
-
-// Residual append for the no-flush case (cache.py:174-175): one CTA per sequence copies its n_tok
-// rows to res[pos[b] ..] and then advances pos[b] by n_tok (the length update rides along, so a
-// decode step's append is one launch).
-template <typename T>
-__global__ void __launch_bounds__(256) residual_append_kernel(float* __restrict__ rk, float* __restrict__ rv,
-                                                              int64_t res_seq_stride, int row,
-                                                              const T* __restrict__ sk, const T* __restrict__ sv,
-                                                              int64_t n_tok, int64_t src_seq_stride, int32_t* pos) {
+// ------------------------------------------------------------------ append commit (residual rows + lengths)
+// Commit of a device-planned append (seq_plan), one CTA per sequence: the new rows that stay raw go to
+// the residual buffer (keys rotated here when a RoPE table is given, like tada_apply_rope), then the
+// sequence's lengths advance.  The CTA reads res_len[b] before anything writes it and is the only writer
+// of sequence b, so no other ordering is needed; it runs after the K1 parts that read the same plan.
+template <typename T, bool ROPE>
+__global__ void __launch_bounds__(256) append_commit_kernel(float* __restrict__ rk, float* __restrict__ rv,
+                                                            int64_t res_seq_stride, int H, int D,
+                                                            const T* __restrict__ sk, const T* __restrict__ sv,
+                                                            int64_t src_seq_stride, int n_new, const int32_t* plan_n,
+                                                            int R, int32_t* comp_len, int32_t* res_len,
+                                                            const int32_t* __restrict__ positions, int64_t pos_stride,
+                                                            const float* __restrict__ rope_cs, int rope_rows,
+                                                            int32_t* err) {
   const int b = blockIdx.x;
-  const int64_t p0 = pos[b];
-  const int64_t n = n_tok * row;
+  const int r = res_len[b];
+  const int n = plan_n ? plan_n[b] : n_new;
+  const SeqPlan p = seq_plan(r, n, R);
+  const bool flush = p.ncomp > 0;
+  const int src0 = R > 0 ? (flush ? p.cnt_new : 0) : 0;  // first new row kept raw
+  const int dst0 = flush ? 0 : r;                       // its residual row
+  const int rows = R > 0 ? (flush ? p.res_after : n) : 0;
+  const int row = H * D;
   const T* s0 = sk + int64_t(b) * src_seq_stride * row;
   const T* s1 = sv + int64_t(b) * src_seq_stride * row;
-  float* d0 = rk + (int64_t(b) * res_seq_stride + p0) * row;
-  float* d1 = rv + (int64_t(b) * res_seq_stride + p0) * row;
-  for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
-    d0[e] = to_f32(s0[e]);
-    d1[e] = to_f32(s1[e]);
+  float* d0 = rk + int64_t(b) * res_seq_stride * row;
+  float* d1 = rv + int64_t(b) * res_seq_stride * row;
+  const int64_t n_el = int64_t(rows) * row;
+  if (!ROPE) {
+    for (int64_t e = threadIdx.x; e < n_el; e += blockDim.x) {
+      d0[int64_t(dst0) * row + e] = to_f32(s0[int64_t(src0) * row + e]);
+      d1[int64_t(dst0) * row + e] = to_f32(s1[int64_t(src0) * row + e]);
+    }
+  } else {  // keys: one thread per (row, head, pair) with the reference's separately rounded products
+    const int half = D >> 1;
+    for (int64_t e = threadIdx.x; e < n_el / 2; e += blockDim.x) {
+      const int64_t t = e / (int64_t(H) * half);
+      const int j = int(e % half);
+      const int64_t el = 2 * e;  // = (t * H + h) * D + 2j
+      int ps = positions[int64_t(b) * pos_stride + src0 + t];
+      if (ps < 0 || ps >= rope_rows) {
+        if (err) atomicOr(err, 2);
+        ps = 0;
+      }
+      const float c = rope_cs[int64_t(ps) * D + 2 * j], sn = rope_cs[int64_t(ps) * D + 2 * j + 1];
+      const float x0 = to_f32(s0[int64_t(src0) * row + el]), x1 = to_f32(s0[int64_t(src0) * row + el + 1]);
+      d0[int64_t(dst0) * row + el] = __fsub_rn(__fmul_rn(x0, c), __fmul_rn(x1, sn));
+      d0[int64_t(dst0) * row + el + 1] = __fadd_rn(__fmul_rn(x0, sn), __fmul_rn(x1, c));
+      d1[int64_t(dst0) * row + el] = to_f32(s1[int64_t(src0) * row + el]);
+      d1[int64_t(dst0) * row + el + 1] = to_f32(s1[int64_t(src0) * row + el + 1]);
+    }
   }
   __syncthreads();
-  if (threadIdx.x == 0) pos[b] = int32_t(p0 + n_tok);
-}
-
-__global__ void lengths_add_kernel(int32_t* arr, int batch, int32_t delta) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < batch) arr[i] += delta;
+  if (threadIdx.x == 0) {
+    comp_len[b] += p.ncomp;
+    res_len[b] = p.res_after;
+  }
 }
 
 // ------------------------------------------------------------------ paged <-> dense (TADAKV1 export/import)
@@ -482,9 +515,11 @@ __global__ void __launch_bounds__(256, MINB) quant_append_fast_kernel(AppendArgs
   uint64_t* bars = reinterpret_cast<uint64_t*>(k1_smem + 8 * K1_RING * ROWB) + warp * K1_RING;
   const int side = blockIdx.y & 1, b = blockIdx.y >> 1;
   const int64_t i_begin = (int64_t(blockIdx.x) * 8 + warp) * tpw;
-  const int64_t i_end = min(a.n_tok, i_begin + tpw);
+  int64_t count, offset;
+  append_part(a, b, count, offset);
+  const int64_t i_end = min(count, i_begin + tpw);
   const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
-  const int64_t c0 = a.dst_start[b] + a.dst_offset;
+  const int64_t c0 = a.dst_start[b] + offset;
   const T* src_seq = reinterpret_cast<const T*>(a.src[side]) + int64_t(b) * a.src_seq_stride * (H * D);
   const int P = a.L.page_tokens;
   auto fetch = [&](int64_t i, int slot) {  // lane 0
@@ -812,7 +847,8 @@ static int quant_append_impl(const tada_page_layout* layout, uint8_t* pool, cons
                              int32_t dtype, int32_t batch, int64_t n_tok, int64_t src_seq_stride,
                              const int32_t* page_table, int32_t pt_stride, const int32_t* dst_start, int64_t dst_offset,
                              int32_t* err_flag, const float* rope_cs, int32_t rope_rows, const int32_t* positions,
-                             int64_t pos_stride, void* stream) {
+                             int64_t pos_stride, void* stream, int part = 0, const int32_t* plan_res = nullptr,
+                             const int32_t* plan_n = nullptr, int plan_n_new = 0, int plan_R = 0) {
   if (!layout) return fail(TADA_ERR_CONFIG, "null layout");
   if (!valid_dtype(dtype)) return fail(TADA_ERR_CONFIG, "dtype must be f32 or bf16");
   if (batch < 0 || n_tok < 0 || src_seq_stride < n_tok) return fail(TADA_ERR_SHAPE, "bad batch/token geometry");
@@ -834,6 +870,11 @@ static int quant_append_impl(const tada_page_layout* layout, uint8_t* pool, cons
   a.rope_rows = rope_rows;
   a.positions = positions;
   a.pos_stride = pos_stride;
+  a.part = part;
+  a.plan_res = plan_res;
+  a.plan_n = plan_n;
+  a.plan_n_new = plan_n_new;
+  a.plan_R = plan_R;
   const int row = layout->heads * layout->head_dim;
   const size_t per_tok = size_t(row + layout->head_dim) * 4;
   int tt = int((32 * 1024) / per_tok);
@@ -861,62 +902,55 @@ int tada_quant_append(const tada_page_layout* layout, uint8_t* pool, const void*
                            dst_start, dst_offset, err_flag, nullptr, 0, nullptr, 0, stream);
 }
 
-int tada_quant_append_rope(const tada_page_layout* layout, uint8_t* pool, const void* src_k, const void* src_v,
-                           int32_t dtype, int32_t batch, int64_t n_tok, int64_t src_seq_stride,
-                           const int32_t* page_table, int32_t pt_stride, const int32_t* dst_start, int64_t dst_offset,
-                           const int32_t* positions, int64_t pos_stride, const float* rope_cs, int32_t rope_rows,
-                           int32_t* err_flag, void* stream) {
+int tada_quant_append_plan(const tada_page_layout* layout, uint8_t* pool, const void* src_k, const void* src_v,
+                           int32_t dtype, int32_t batch, int64_t n_max, int64_t src_seq_stride,
+                           const int32_t* page_table, int32_t pt_stride, const int32_t* comp_len,
+                           const int32_t* res_len, int32_t residual_length, int32_t n_new, const int32_t* seq_n,
+                           int32_t part, const int32_t* positions, int64_t pos_stride, const float* rope_cs,
+                           int32_t rope_rows, int32_t* err_flag, void* stream) {
   if (!layout) return fail(TADA_ERR_CONFIG, "null layout");
-  if (!(layout->head_dim == 128 && layout->heads == 8 && (layout->bits == 2 || layout->bits == 4 || layout->bits == 8)))
-    return fail(TADA_ERR_CONFIG, "fused RoPE append needs heads 8, head_dim 128, bits 2/4/8 (compose apply_rope + "
-                                 "quant_append otherwise)");
-  if (!positions || !rope_cs || rope_rows <= 0 || pos_stride < n_tok) return fail(TADA_ERR_SHAPE, "bad rope arguments");
-  return quant_append_impl(layout, pool, src_k, src_v, dtype, batch, n_tok, src_seq_stride, page_table, pt_stride,
-                           dst_start, dst_offset, err_flag, rope_cs, rope_rows, positions, pos_stride, stream);
+  if (part != 1 && part != 2) return fail(TADA_ERR_CONFIG, "part must be 1 (residual rows) or 2 (new rows)");
+  if (!res_len) return fail(TADA_ERR_SHAPE, "null buffer");
+  if (residual_length < 0 || n_new < 0) return fail(TADA_ERR_SHAPE, "bad plan geometry");
+  if (rope_cs) {
+    if (part != 2) return fail(TADA_ERR_CONFIG, "only the new rows are rotated (residual rows are stored rotated)");
+    if (!(layout->head_dim == 128 && layout->heads == 8 && (layout->bits == 2 || layout->bits == 4 || layout->bits == 8)))
+      return fail(TADA_ERR_CONFIG, "fused RoPE append needs heads 8, head_dim 128, bits 2/4/8");
+    if (!positions || rope_rows <= 0 || pos_stride < n_max) return fail(TADA_ERR_SHAPE, "bad rope arguments");
+  }
+  return quant_append_impl(layout, pool, src_k, src_v, dtype, batch, n_max, src_seq_stride, page_table, pt_stride,
+                           comp_len, 0, err_flag, rope_cs, rope_rows, positions, pos_stride, stream, part, res_len,
+                           seq_n, n_new, residual_length);
 }
 
-int tada_residual_write(float* res_k, float* res_v, int64_t res_seq_stride, int32_t heads, int32_t head_dim,
-                        const void* src_k, const void* src_v, int32_t dtype, int32_t batch, int64_t n_tok,
-                        int64_t src_seq_stride, const int32_t* pos, int32_t pos_offset, void* stream) {
+int tada_append_commit(float* res_k, float* res_v, int64_t res_seq_stride, int32_t heads, int32_t head_dim,
+                       const void* src_k, const void* src_v, int32_t dtype, int32_t batch, int64_t src_seq_stride,
+                       int32_t n_new, const int32_t* seq_n, int32_t residual_length, int32_t* comp_len,
+                       int32_t* res_len, const int32_t* positions, int64_t pos_stride, const float* rope_cs,
+                       int32_t rope_rows, int32_t* err_flag, void* stream) {
   if (!valid_dtype(dtype)) return fail(TADA_ERR_CONFIG, "dtype must be f32 or bf16");
-  if (batch < 0 || n_tok < 0) return fail(TADA_ERR_SHAPE, "bad batch/token geometry");
-  if (batch == 0 || n_tok == 0) return TADA_OK;
-  const int row = heads * head_dim;
-  const int grid = grid_for(int64_t(batch) * n_tok * row * 2, 256);
-  if (dtype == TADA_F32)
-    residual_write_kernel<float><<<grid, 256, 0, S(stream)>>>(
-        res_k, res_v, res_seq_stride, row, reinterpret_cast<const float*>(src_k), reinterpret_cast<const float*>(src_v),
-        n_tok, src_seq_stride, pos, pos_offset, batch);
-  else
-    residual_write_kernel<__nv_bfloat16><<<grid, 256, 0, S(stream)>>>(
-        res_k, res_v, res_seq_stride, row, reinterpret_cast<const __nv_bfloat16*>(src_k),
-        reinterpret_cast<const __nv_bfloat16*>(src_v), n_tok, src_seq_stride, pos, pos_offset, batch);
-  return check_launch("residual_write");
-}
-
-int tada_residual_append(float* res_k, float* res_v, int64_t res_seq_stride, int32_t heads, int32_t head_dim,
-                         const void* src_k, const void* src_v, int32_t dtype, int32_t batch, int64_t n_tok,
-                         int64_t src_seq_stride, int32_t* pos, void* stream) {
-  if (!valid_dtype(dtype)) return fail(TADA_ERR_CONFIG, "dtype must be f32 or bf16");
-  if (batch < 0 || n_tok < 0) return fail(TADA_ERR_SHAPE, "bad batch/token geometry");
-  if (batch == 0 || n_tok == 0) return TADA_OK;
-  const int row = heads * head_dim;
-  if (dtype == TADA_F32)
-    residual_append_kernel<float><<<batch, 256, 0, S(stream)>>>(res_k, res_v, res_seq_stride, row,
-                                                                 reinterpret_cast<const float*>(src_k),
-                                                                 reinterpret_cast<const float*>(src_v), n_tok,
-                                                                 src_seq_stride, pos);
-  else
-    residual_append_kernel<__nv_bfloat16><<<batch, 256, 0, S(stream)>>>(
-        res_k, res_v, res_seq_stride, row, reinterpret_cast<const __nv_bfloat16*>(src_k),
-        reinterpret_cast<const __nv_bfloat16*>(src_v), n_tok, src_seq_stride, pos);
-  return check_launch("residual_append");
-}
-
-int tada_lengths_add(int32_t* arr, int32_t batch, int32_t delta, void* stream) {
-  if (batch <= 0) return TADA_OK;
-  lengths_add_kernel<<<(batch + 127) / 128, 128, 0, S(stream)>>>(arr, batch, delta);
-  return check_launch("lengths_add");
+  if (batch < 0 || n_new < 0 || heads <= 0 || head_dim <= 0 || residual_length < 0)
+    return fail(TADA_ERR_SHAPE, "bad append geometry");
+  if (batch == 0) return TADA_OK;
+  if (!comp_len || !res_len || (residual_length > 0 && (!res_k || !res_v || !src_k || !src_v)))
+    return fail(TADA_ERR_SHAPE, "null buffer");
+  if (rope_cs && (head_dim % 2 || !positions || rope_rows <= 0)) return fail(TADA_ERR_SHAPE, "bad rope arguments");
+  cudaStream_t st = S(stream);
+#define TADA_COMMIT(T, ROPE)                                                                                    \
+  append_commit_kernel<T, ROPE><<<batch, 256, 0, st>>>(res_k, res_v, res_seq_stride, heads, head_dim,             \
+                                                       reinterpret_cast<const T*>(src_k),                       \
+                                                       reinterpret_cast<const T*>(src_v), src_seq_stride, n_new, \
+                                                       seq_n, residual_length, comp_len, res_len, positions,     \
+                                                       pos_stride, rope_cs, rope_rows, err_flag)
+  if (dtype == TADA_F32) {
+    if (rope_cs) TADA_COMMIT(float, true);
+    else TADA_COMMIT(float, false);
+  } else {
+    if (rope_cs) TADA_COMMIT(__nv_bfloat16, true);
+    else TADA_COMMIT(__nv_bfloat16, false);
+  }
+#undef TADA_COMMIT
+  return check_launch("append_commit");
 }
 
 int tada_gather_compressed(const tada_page_layout* layout, const uint8_t* pool, const int32_t* page_row, int64_t n_tok,

@@ -24,7 +24,7 @@ import torch
 
 from . import _dev
 from .cache import ModelConfig, PrecisionPlan
-from .errors import CapacityError, ConfigError, DataError, ShapeError
+from .errors import CapacityError, ConfigError, DataError, ShapeError, StateError
 from .paged import PagedKVCache
 from .rope import _positions, rope_table
 
@@ -167,8 +167,8 @@ class ToyDecoder:
         if self.store is None:
             self.reset()
         ids = self._ids(np.asarray(token_ids).reshape(self.B, 1))
-        if position != self.position:
-            raise DataError(f"the caches hold {self.position} tokens but position is {position}")
+        if position != self.position:  # model.py:282-286
+            raise StateError(f"layer 0 cache holds {self.position} tokens but position is {position}")
         if position >= self.max_seq_len:
             raise CapacityError(f"position {position} exceeds max_seq_len {self.max_seq_len}")
         cfg, w, B = self.cfg, self.w, self.B

@@ -125,9 +125,21 @@ def append_rope(cache: CompressedLayerCache, k_pre_rope, v_new, positions, rope:
 def append_fused(cache: CompressedLayerCache, k_pre_rope, x_norm, w_v, positions, rope: RopeParams) -> None:
     """Rotate keys, project values and write both into the cache in one step (model.py:167-183).
 
-    The value projection ``x_norm @ w_v`` is an f32 GEMM on the GPU (cuBLAS, TF32 off); the rotated
-    keys exist only in registers of the fused append kernel.  Equal, byte for byte, to composing
-    rotate_heads / the same projection / append_tokens (AC8)."""
+    The value projection ``x_norm @ w_v`` is computed where its operands live: host numpy operands (the
+    reference API) get numpy's f32 matmul — the reference's own expression (model.py:181), so the cache is
+    byte-equal to composing rotate_heads / ``x_norm @ w_v`` / append_tokens by hand (AC8); device tensors
+    get an f32 cuBLAS GEMM (TF32 off).  Either way the projection is a library GEMM beside the path; the
+    rotated keys exist only in registers of the fused append kernel."""
+    if not (_dev.is_torch(x_norm) or _dev.is_torch(w_v)):
+        xh = np.ascontiguousarray(x_norm, dtype=np.float32)
+        wh = np.ascontiguousarray(w_v, dtype=np.float32)
+        if xh.ndim != 2 or wh.ndim != 2 or xh.shape[1] != wh.shape[0]:
+            raise ShapeError(f"cannot project {xh.shape} by {wh.shape}")
+        if wh.shape[1] != cache.num_kv_heads * cache.head_dim:
+            raise ShapeError(f"w_v must have {cache.num_kv_heads * cache.head_dim} columns, got {wh.shape[1]}")
+        v = (xh @ wh).reshape(xh.shape[0], cache.num_kv_heads, cache.head_dim)
+        append_rope(cache, k_pre_rope, v, positions, rope)
+        return
     xn = _dev.to_dev(x_norm, allow_bf16=False)
     wv = _dev.to_dev(w_v, allow_bf16=False)
     if xn.ndim != 2 or wv.ndim != 2 or xn.shape[1] != wv.shape[0]:

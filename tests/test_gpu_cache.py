@@ -198,3 +198,30 @@ def test_k1_fast_path_bit_exact(bits, kind, dtype):
             assert np.array_equal(np.asarray(got.scales).view(np.uint32), rec.scales.view(np.uint32))
             assert np.array_equal(np.asarray(got.mins), rec.mins)
             assert np.array_equal(ex[f"{side}_mean"].cpu().numpy().view(np.uint32), mean.view(np.uint32))
+
+
+def test_deserialize_untrusted_residual_header():
+    """A TADAKV1 header with a huge residual_length must not allocate B*R*H*D floats up front, and a
+    stream holding more raw rows than residual_length is accepted like the reference does; the next append
+    flushes them exactly as the reference's append_tokens would (cache.py:171-180)."""
+    import struct
+
+    m = tk()
+    rng = np.random.default_rng(3)
+    H, D = 2, 16
+    k = rng.normal(size=(9, H, D)).astype(np.float32)
+    v = rng.normal(size=(9, H, D)).astype(np.float32)
+    st = orc.LayerState(H, D, 4, 4)
+    orc.append(st, k[:7], v[:7])  # C = 4, r = 3
+    blob = orc.dump(st)
+    hdr = len(orc.MAGIC)
+    huge = blob[:hdr] + struct.pack("<IIBIQQ", H, D, 4, 0xFFFFFFFF, st.compressed, st.r) + blob[hdr + 29:]
+    cache = m.deserialize_cache(huge)  # no 2^32-row residual allocation
+    assert cache.total_tokens == 7 and m.serialize_cache(cache) == huge
+    # r = 3 raw rows with residual_length 2: the reference keeps them; its next append flushes 4
+    small = blob[:hdr] + struct.pack("<IIBIQQ", H, D, 4, 2, st.compressed, st.r) + blob[hdr + 29:]
+    cache = m.deserialize_cache(small)
+    ref = orc.load(small)
+    cache.append_tokens(k[7:], v[7:])
+    orc.append(ref, k[7:], v[7:])
+    assert m.serialize_cache(cache) == orc.dump(ref)

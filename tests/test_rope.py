@@ -122,8 +122,13 @@ def test_gpu_append_fused_equals_composition(bits, R):
         x_norm = rng.normal(size=(cnt, 64)).astype(np.float32)
         w_v = (rng.normal(size=(64, 1024)) * 0.1).astype(np.float32)
         pos = np.arange(start, start + cnt) + 1000
-        tk.append_fused(fused, k_pre, x_norm, w_v, pos, rope)
-        v = (torch.from_numpy(x_norm).cuda() @ torch.from_numpy(w_v).cuda()).reshape(cnt, 8, 128)
+        if start % 2:  # device operands: the projection is a cuBLAS GEMM on both sides
+            xd, wd = torch.from_numpy(x_norm).cuda(), torch.from_numpy(w_v).cuda()
+            tk.append_fused(fused, k_pre, xd, wd, pos, rope)
+            v = (xd @ wd).reshape(cnt, 8, 128)
+        else:  # host operands: numpy's f32 matmul on both sides, exactly the reference's AC8 composition
+            tk.append_fused(fused, k_pre, x_norm, w_v, pos, rope)
+            v = (x_norm @ w_v).reshape(cnt, 8, 128)
         composed.append_tokens(tk.rotate_heads(k_pre, pos, rope), v)
         start += cnt
     assert tk.serialize_cache(fused) == tk.serialize_cache(composed)

@@ -161,9 +161,11 @@ def test_gloo_batch_axis_gather_ragged():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("R", [0, 128])
-def test_gpu_sequence_axis_two_ranks_on_one_device(R):
-    """Both ranks of a 2-way sequence split on one GPU; the CUDA merge equals the 1-rank oracle."""
+@pytest.mark.parametrize("R,mode", [(0, 1), (128, 1), (0, 2), (128, 2)])
+def test_gpu_sequence_axis_two_ranks_on_one_device(R, mode):
+    """Both ranks of a 2-way sequence split on one GPU; the CUDA merge equals the 1-rank oracle.  mode 1:
+    the exact kernel (1e-5, the reference's streaming bar); mode 2: the tensor-core K2 + K3 that bench.py
+    times, whose per-rank (out, lse) partials merge within the north_star's 2e-3."""
     import paper_2506_04642_b200 as tk
     from paper_2506_04642_b200.shard import merge_partials
 
@@ -181,16 +183,16 @@ def test_gpu_sequence_axis_two_ranks_on_one_device(R):
             rk.append(0, kd[:, pos:pos + n], vd[:, pos:pos + n])
         pos += n
     qd = torch.from_numpy(q).cuda()[None]
-    parts = [rk.store.attend_lse(0, qd, mode=1) for rk in ranks]
+    parts = [rk.store.attend_lse(0, qd, mode=mode) for rk in ranks]
     o = torch.stack([p[0] for p in parts], dim=1)    # [1, 2, Hq, D]
     lse = torch.stack([p[1] for p in parts], dim=1)  # [1, 2, Hq]
     got = merge_partials(o, lse)[0].cpu().numpy()
     ref = orc.LayerState(H, D, bits, R)
     orc.append(ref, k, v)
     want, want_lse = orc.attend_lse(q, ref, Hq)
-    assert np.abs(got - want).max() <= 1e-5
+    assert np.abs(got - want).max() <= (1e-5 if mode == 1 else 2e-3)
     # each rank's lse matches the oracle on its own tokens
     for p, rk in zip(parts, ranks):
         st = _oracle_local_state(rk.plan, k, v, [300, 1, 1, 398], bits, R)
         _, l_r = orc.attend_lse(q, st, Hq)
-        assert np.abs(p[1][0].cpu().numpy() - l_r).max() <= 1e-4
+        assert np.abs(p[1][0].cpu().numpy() - l_r).max() <= (1e-4 if mode == 1 else 2e-3)
