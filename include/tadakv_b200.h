@@ -131,15 +131,16 @@ int tada_quant_append(const tada_page_layout* layout, uint8_t* pool, const void*
  * new rows).  part 1 compresses the residual rows (src = the f32 residual buffer, src_seq_stride = its
  * rows per sequence), part 2 the new rows (src = the step input; dst after the part-1 rows).  n_max bounds
  * the rows of any sequence in this launch (grid size).  Lengths are not changed: tada_append_commit
- * follows.  rope_cs / positions (part 2 only, nullable): the keys are rotated in registers as in
- * tada_quant_append_rope. */
+ * follows.  rope_cs / positions (part 2 only, nullable): the keys are rotated in registers first, bit for
+ * bit like tada_apply_rope.  range_word (nullable): the layer's two int32 range words, atomicMax'ed with
+ * the binary exponent of any stored |mean| >= 2^15 ([0]) or group scale >= 2^8 ([1]); see tada_decode_attn. */
 int tada_quant_append_plan(const tada_page_layout* layout, uint8_t* pool, const void* src_k,
                            const void* src_v, int32_t dtype, int32_t batch, int64_t n_max,
                            int64_t src_seq_stride, const int32_t* page_table, int32_t pt_stride,
                            const int32_t* comp_len, const int32_t* res_len, int32_t residual_length,
                            int32_t n_new, const int32_t* seq_n, int32_t part, const int32_t* positions,
                            int64_t pos_stride, const float* rope_cs, int32_t rope_rows,
-                           int32_t* err_flag, void* stream);
+                           int32_t* err_flag, int32_t* range_word, void* stream);
 
 /* The rest of that append, one CTA per sequence: the new rows that stay raw are stored (f32; keys rotated
  * when rope_cs is given) at their residual rows, then comp_len[b] / res_len[b] advance by the plan. */
@@ -180,6 +181,10 @@ int tada_scatter_compressed(const tada_page_layout* layout, uint8_t* pool, const
  * ways (split-K flash decoding) and merged by a log-sum-exp combine (K3);
  * workspace must hold tada_decode_attn_workspace_bytes(...) bytes.
  * out: [batch][num_q_heads][head_dim] in out_dtype.
+ * range_word (nullable): the layer's two device range words that tada_quant_append_plan maintains; the
+ * tensor-core kernels stage q, the means and P' as f16, so a layer with a stored |mean| >= 2^15 or a
+ * group scale beyond what its kernel's P' holds (2^15 for the 2/4-bit kernel, 2^8 for the 8-bit one),
+ * or a query element >= 2^15, is attended on their exact f32 path instead (mode 0 and 2). 
  * mode: 0 = auto, 1 = exact generic kernel (f32 reconstruct-then-dot, any geometry),
  *       2 = fast tensor-core kernel (head_dim 128, bits 2/4/8),
  *       3 = fast tensor-core kernel, previous two-barrier-per-tile variant (A/B comparisons). */
@@ -190,7 +195,7 @@ int tada_decode_attn(const tada_page_layout* layout, const uint8_t* pool, const 
                      int32_t pt_stride, const int32_t* comp_len, const int32_t* res_len,
                      const float* res_k, const float* res_v, int64_t res_seq_stride, float scale,
                      int32_t num_splits, void* workspace, void* out, int32_t out_dtype, int32_t mode,
-                     void* stream);
+                     const int32_t* range_word, void* stream);
 
 /* Same as tada_decode_attn, and also writes lse_out[b][g] = log sum_t exp(scale * q.k_t) (natural
  * log) so that attention over disjoint token sets held by different ranks can be merged exactly
@@ -201,7 +206,8 @@ int tada_decode_attn_lse(const tada_page_layout* layout, const uint8_t* pool, co
                          const int32_t* page_table, int32_t pt_stride, const int32_t* comp_len,
                          const int32_t* res_len, const float* res_k, const float* res_v,
                          int64_t res_seq_stride, float scale, int32_t num_splits, void* workspace,
-                         void* out, int32_t out_dtype, int32_t mode, float* lse_out, void* stream);
+                         void* out, int32_t out_dtype, int32_t mode, float* lse_out,
+                         const int32_t* range_word, void* stream);
 
 /* Merge n_parts normalised partial attentions: o_parts [n_parts][rows][head_dim] f32 and
  * lse_parts [n_parts][rows] f32 (-inf = the part had no tokens) ->
@@ -231,7 +237,7 @@ int tada_decode_step(const tada_page_layout* layout, uint8_t* pool, const void* 
                      int64_t res_seq_stride, int32_t residual_length, const void* new_k, const void* new_v,
                      int32_t new_dtype, int32_t k1_rows, int32_t* step_sync, float scale,
                      int32_t num_splits, void* workspace, void* out, int32_t out_dtype, int32_t mode,
-                     int32_t* err_flag, void* stream);
+                     int32_t* err_flag, int32_t* range_word, void* stream);
 
 /* Split count for this layer's kernel on the current device: the fewest whole waves of resident
  * CTAs (SM count x CTAs per SM of the instantiation that will run) whose last wave is >= 90% full,

@@ -65,15 +65,15 @@ SIGNATURES = {
     "tada_scatter_compressed": (I32, [C.POINTER(PageLayout), P, P, I64, I32, P, P, P, P, P]),
     "tada_decode_attn_workspace_bytes": (I64, [I32, I32, I32, I32]),
     "tada_decode_attn": (I32, [C.POINTER(PageLayout), P, P, I32, I32, I32, P, I32, P, P, P, P, I64, F, I32, P, P,
-                               I32, I32, P]),
+                               I32, I32, P, P]),
     "tada_decode_attn_lse": (I32, [C.POINTER(PageLayout), P, P, I32, I32, I32, P, I32, P, P, P, P, I64, F, I32, P,
-                                   P, I32, I32, P, P]),
+                                   P, I32, I32, P, P, P]),
     "tada_combine_lse": (I32, [P, P, I32, I64, I32, P, I32, P, P]),
     "tada_quant_append_plan": (I32, [C.POINTER(PageLayout), P, P, P, I32, I32, I64, I64, P, I32, P, P, I32, I32, P,
-                                     I32, P, I64, P, I32, P, P]),
+                                     I32, P, I64, P, I32, P, P, P]),
     "tada_append_commit": (I32, [P, P, I64, I32, I32, P, P, I32, I32, I64, I32, P, I32, P, P, P, I64, P, I32, P, P]),
     "tada_decode_step": (I32, [C.POINTER(PageLayout), P, P, I32, I32, I32, P, I32, P, P, P, P, I64, I32, P, P, I32,
-                               I32, P, F, I32, P, P, I32, I32, P, P]),
+                               I32, P, F, I32, P, P, I32, I32, P, P, P]),
     "tada_decode_attn_suggest_splits": (I32, [I32, I64, I32]),
     "tada_decode_attn_plan_splits": (I32, [C.POINTER(PageLayout), I32, I32, I64]),
 }

@@ -673,6 +673,14 @@ __global__ void __launch_bounds__((G + 4) * 32) combine_kv_kernel(AttnArgs a, in
   }
 }
 
+// K3 with residual rows covers this geometry (head_dim % 4 == 0 and, off the D = 128 kernels, the residual
+// logits and split weights fit shared memory).
+static bool combine_residual_ok(const AttnArgs& a) {
+  if (a.L.head_dim % 4) return false;
+  if (a.L.head_dim == 128) return true;
+  return (size_t(a.L.head_dim) * 3 + size_t(a.res_seq_stride) + size_t(a.splits) + 8) * 4 <= 220 * 1024;
+}
+
 static int launch_combine_residual(const AttnArgs& a, int batch, cudaStream_t st) {
   if (a.L.head_dim * 2 > kCombThreads * 2 || a.L.head_dim % 4) return fail(TADA_ERR_CONFIG, "combine needs head_dim % 4 == 0");
   if (a.L.head_dim == 128 && TADA_K3_KV) {  // any residual length: the rows stream through 4 warps per KV head
@@ -783,6 +791,7 @@ int32_t tada_decode_attn_plan_splits(const tada_page_layout* layout, int32_t num
   int per_sm = 1;
   if (v8_supported(*layout, num_q_heads)) per_sm = 2;  // attn_v8_kernel: two CTAs per SM
   else if (fast_supported(*layout, num_q_heads)) per_sm = fast_tile_tokens(*layout, num_q_heads) == 16 ? 2 : 1;
+  else per_sm = exact_ctas_per_sm(*layout, num_q_heads);
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   return plan_splits(int64_t(sms) * per_sm, batch, max_tokens);
@@ -794,7 +803,7 @@ static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool,
                             int64_t res_seq_stride, float scale, int32_t num_splits, void* workspace, void* out,
                             int32_t out_dtype, int32_t mode, float* lse_out, void* stream,
                             const void* new_k = nullptr, const void* new_v = nullptr, int32_t new_dtype = 0,
-                            int32_t step_R = -1, int32_t* step_sync = nullptr) {
+                            int32_t step_R = -1, int32_t* step_sync = nullptr, const int32_t* range_word = nullptr) {
   if (!layout) return fail(TADA_ERR_CONFIG, "null layout");
   if (q_dtype != TADA_F32 && q_dtype != TADA_BF16) return fail(TADA_ERR_CONFIG, "q dtype must be f32 or bf16");
   if (out_dtype != TADA_F32 && out_dtype != TADA_BF16) return fail(TADA_ERR_CONFIG, "out dtype must be f32 or bf16");
@@ -809,7 +818,8 @@ static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool,
   if (mode >= 2 && !fast_supported(*layout, num_q_heads))
     return fail(TADA_ERR_CONFIG, "fast decode attention needs head_dim 128, bits 2/4/8, num_q_heads in {8,16,32,64}, "
                                  "group size in {1,2,4,8} and page_tokens % 32 == 0");
-  if ((num_splits > 1 || fast) && !workspace) return fail(TADA_ERR_SHAPE, "workspace required");
+  if (!workspace && (num_splits > 1 || fast || exact_smem_bytes(*layout, num_q_heads)))
+    return fail(TADA_ERR_SHAPE, "workspace required");
   AttnArgs a{};
   a.L = *layout;
   a.pool = pool;
@@ -837,6 +847,7 @@ static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool,
   a.step = step_R >= 0;
   a.step_R = step_R;
   a.step_sync = step_sync;
+  a.range = range_word;
   {
     static const int diag = getenv("TADA_ATTN_DIAG") ? atoi(getenv("TADA_ATTN_DIAG")) : 0;
     a.diag = diag;
@@ -845,6 +856,10 @@ static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool,
   int rc;
   if (fast) {
     rc = (mode != 3 && v8_supported(*layout, num_q_heads)) ? launch_v8(a, batch, st) : launch_fast(a, batch, st);
+    if (rc == TADA_OK) rc = launch_combine_residual(a, batch, st);
+    return rc;
+  } else if (exact_smem_bytes(*layout, num_q_heads) && combine_residual_ok(a)) {
+    rc = launch_exact(a, batch, st);  // staged f32 kernel over the compressed tokens; K3 the residual + merge
     if (rc == TADA_OK) rc = launch_combine_residual(a, batch, st);
     return rc;
   } else {
@@ -861,19 +876,21 @@ int tada_decode_attn(const tada_page_layout* layout, const uint8_t* pool, const 
                      int32_t num_q_heads, const int32_t* page_table, int32_t pt_stride, const int32_t* comp_len,
                      const int32_t* res_len, const float* res_k, const float* res_v, int64_t res_seq_stride,
                      float scale, int32_t num_splits, void* workspace, void* out, int32_t out_dtype, int32_t mode,
-                     void* stream) {
+                     const int32_t* range_word, void* stream) {
   return decode_attn_impl(layout, pool, q, q_dtype, batch, num_q_heads, page_table, pt_stride, comp_len, res_len, res_k,
-                          res_v, res_seq_stride, scale, num_splits, workspace, out, out_dtype, mode, nullptr, stream);
+                          res_v, res_seq_stride, scale, num_splits, workspace, out, out_dtype, mode, nullptr, stream,
+                          nullptr, nullptr, 0, -1, nullptr, range_word);
 }
 
 int tada_decode_attn_lse(const tada_page_layout* layout, const uint8_t* pool, const void* q, int32_t q_dtype,
                          int32_t batch, int32_t num_q_heads, const int32_t* page_table, int32_t pt_stride,
                          const int32_t* comp_len, const int32_t* res_len, const float* res_k, const float* res_v,
                          int64_t res_seq_stride, float scale, int32_t num_splits, void* workspace, void* out,
-                         int32_t out_dtype, int32_t mode, float* lse_out, void* stream) {
+                         int32_t out_dtype, int32_t mode, float* lse_out, const int32_t* range_word, void* stream) {
   if (!lse_out) return fail(TADA_ERR_SHAPE, "null lse buffer");
   return decode_attn_impl(layout, pool, q, q_dtype, batch, num_q_heads, page_table, pt_stride, comp_len, res_len, res_k,
-                          res_v, res_seq_stride, scale, num_splits, workspace, out, out_dtype, mode, lse_out, stream);
+                          res_v, res_seq_stride, scale, num_splits, workspace, out, out_dtype, mode, lse_out, stream,
+                          nullptr, nullptr, 0, -1, nullptr, range_word);
 }
 
 int tada_decode_step(const tada_page_layout* layout, uint8_t* pool, const void* q, int32_t q_dtype, int32_t batch,
@@ -881,7 +898,7 @@ int tada_decode_step(const tada_page_layout* layout, uint8_t* pool, const void* 
                      int32_t* res_len, float* res_k, float* res_v, int64_t res_seq_stride, int32_t residual_length,
                      const void* new_k, const void* new_v, int32_t new_dtype, int32_t k1_rows, int32_t* step_sync,
                      float scale, int32_t num_splits, void* workspace, void* out, int32_t out_dtype, int32_t mode,
-                     int32_t* err_flag, void* stream) {
+                     int32_t* err_flag, int32_t* range_word, void* stream) {
   if (!layout) return fail(TADA_ERR_CONFIG, "null layout");
   if (mode == 1 || !fast_supported(*layout, num_q_heads) || layout->head_dim != 128)
     return fail(TADA_ERR_CONFIG, "the fused decode step needs the tensor-core attention path (head_dim 128)");
@@ -896,18 +913,18 @@ int tada_decode_step(const tada_page_layout* layout, uint8_t* pool, const void* 
   if (k1_rows > 0) {
     const int rc = tada_quant_append_plan(layout, pool, res_k, res_v, TADA_F32, batch, k1_rows, res_seq_stride,
                                           page_table, pt_stride, comp_len, res_len, residual_length, 1, nullptr, 1,
-                                          nullptr, 0, nullptr, 0, err_flag, stream);
+                                          nullptr, 0, nullptr, 0, err_flag, range_word, stream);
     if (rc != TADA_OK) return rc;
   }
   if (k1_rows >= 0) {
     const int rc = tada_quant_append_plan(layout, pool, new_k, new_v, new_dtype, batch, 1, 1, page_table, pt_stride,
                                           comp_len, res_len, residual_length, 1, nullptr, 2, nullptr, 0, nullptr, 0,
-                                          err_flag, stream);
+                                          err_flag, range_word, stream);
     if (rc != TADA_OK) return rc;
   }
   return decode_attn_impl(layout, pool, q, q_dtype, batch, num_q_heads, page_table, pt_stride, comp_len, res_len, res_k,
                           res_v, res_seq_stride, scale, num_splits, workspace, out, out_dtype, mode == 0 ? 2 : mode,
-                          nullptr, stream, new_k, new_v, new_dtype, residual_length, step_sync);
+                          nullptr, stream, new_k, new_v, new_dtype, residual_length, step_sync, range_word);
 }
 
 int tada_combine_lse(const float* o_parts, const float* lse_parts, int32_t n_parts, int64_t rows, int32_t head_dim,

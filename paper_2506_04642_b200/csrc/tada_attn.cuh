@@ -43,7 +43,84 @@ struct AttnArgs {
   int step;
   int step_R;
   int32_t* step_sync;
+  // the layer's range words (K1's note_range): [0] binary exponent of its largest stored |mean| >= 2^15,
+  // [1] of its largest group scale >= 2^8 (0 when below)
+  const int32_t* range;
 };
+
+// The tensor-core kernels stage q and the f32 means (f16 hi + lo / f16) as f16, which holds |x| < 65504, and
+// P' = -p * vscale with the lazy softmax's p <= 2^8: attn_v8_kernel pre-scales it by 2^-8 (safe for scales
+// below 2^15), attn_fast_kernel does not (safe below 2^8).  A layer whose range words pass those bounds, or a
+// query element of magnitude >= 2^15, is attended on the exact f32 path below instead (rare; mode 0 never
+// returns inf/NaN for finite inputs).
+constexpr int kF16SafeExp = 15;    // |mean|, |q| and (attn_v8_kernel) vscale below 2^15
+constexpr int kFastScaleExp = 8;   // attn_fast_kernel: vscale below 2^8
+__device__ __forceinline__ bool beyond_f16(const AttnArgs& a, int scale_exp) {
+  return a.range && (a.range[0] >= kF16SafeExp || a.range[1] >= scale_exp);
+}
+
+// Exact f32 partials of one K2 split over compressed tokens [t_begin, t_end) of sequence b, in the
+// tensor-core kernels' slot format (natural-log max, normaliser, unnormalised weighted sum): warp w < H
+// attends for KV head w, lane = 4 columns; K̂ = mean - fmaf(code, scale, min) as in the reference's
+// reconstruct_slice (cache.py:190-213), logits scaled after the dot (attention.py:118-136).
+template <int BITS, int G>
+__device__ void exact_split_partials(const AttnArgs& a, int b, int split, int t_begin, int t_end, int warp,
+                                     int lane) {
+  constexpr int D = 128;
+  const int H = a.L.heads, Hq = a.Hq, P = a.L.page_tokens, gb = a.L.group_bytes;
+  if (warp >= H) return;
+  const int h = warp;
+  const float NEG_INF = -__int_as_float(0x7f800000);
+  float q[G][4], acc[G][4], m[G], l[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int64_t qi = (int64_t(b) * Hq + h * G + g) * D + 4 * lane;
+    if (a.q_dtype == TADA_F32) load4(reinterpret_cast<const float*>(a.q) + qi, q[g]);
+    else load4(reinterpret_cast<const __nv_bfloat16*>(a.q) + qi, q[g]);
+    acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.f;
+    m[g] = NEG_INF;
+    l[g] = 0.f;
+  }
+  const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
+  for (int t = t_begin; t < t_end; ++t) {
+    const uint8_t* page = a.pool + int64_t(pt[t / P]) * a.L.page_bytes;
+    const int r = t % P;
+    float kh[4], vh[4];
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const float4 mean = *reinterpret_cast<const float4*>(page + a.L.off_mean[side] + (int64_t(r) * D + 4 * lane) * 4);
+      const uint8_t* grp = page + a.L.off_codes[side] + (int64_t(r) * H + h) * gb;
+      const float2 sm = *reinterpret_cast<const float2*>(page + a.L.off_meta[side] + (int64_t(r) * H + h) * 8);
+      const float mv[4] = {mean.x, mean.y, mean.z, mean.w};
+      float* dst = side ? vh : kh;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        dst[e] = __fsub_rn(mv[e], __fmaf_rn(float(get_code(grp, 4 * lane + e, BITS)), sm.x, sm.y));
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float z = __fmaf_rn(q[g][3], kh[3], __fmaf_rn(q[g][2], kh[2], __fmaf_rn(q[g][1], kh[1], __fmul_rn(q[g][0], kh[0]))));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+      z = __fmul_rn(z, a.scale);
+      const float mn = fmaxf(m[g], z);
+      const float cf = expf(m[g] - mn), p = expf(z - mn);
+      l[g] = l[g] * cf + p;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[g][e] = fmaf(p, vh[e], acc[g][e] * cf);
+      m[g] = mn;
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int64_t slot = (int64_t(b) * Hq + h * G + g) * a.slots + split;
+    *reinterpret_cast<float4*>(a.part_acc + slot * D + 4 * lane) = make_float4(acc[g][0], acc[g][1], acc[g][2], acc[g][3]);
+    if (lane == 0) {
+      a.part_ml[slot * 2] = l[g] > 0.f ? m[g] : NEG_INF;
+      a.part_ml[slot * 2 + 1] = l[g];
+    }
+  }
+}
 
 // Compressed tokens K2 attends for sequence b: in a decode step, those a flush of this step adds too (K1
 // compressed them just before).
@@ -149,6 +226,10 @@ int fast_tile_tokens(const tada_page_layout& L, int Hq);  // 16 or 32 (0: unsupp
 // One-barrier-per-tile kernel (tada_attn_v8.cu): 2/4-bit (8-bit where two stages fit), Hq in {8, 16, 32}.
 bool v8_supported(const tada_page_layout& L, int Hq);
 int launch_v8(const AttnArgs& a, int batch, cudaStream_t st);
+// Staged exact f32 kernel for any geometry (tada_attn_exact.cu): compressed tokens only, K3 adds the residual.
+int exact_smem_bytes(const tada_page_layout& L, int Hq);  // 0: geometry too large (use attn_generic_kernel)
+int exact_ctas_per_sm(const tada_page_layout& L, int Hq);
+int launch_exact(const AttnArgs& a, int batch, cudaStream_t st);
 // Cached TMA descriptors of a layer pool for TT-token tiles (tada_attn_fast.cu).
 int get_tma_maps(const AttnArgs& a, TmaMaps* out, int tt);
 

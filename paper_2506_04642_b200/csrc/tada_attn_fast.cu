@@ -160,6 +160,8 @@ __global__ void __launch_bounds__(TT * 16, TT == 16 ? 2 : 1) attn_fast_kernel(At
   for (int i = tid; i < (MROWS * PROW2) / 2; i += NTHR) reinterpret_cast<uint32_t*>(pbuf)[i] = 0u;
   for (int i = tid; i < (H * 8 * PROW2) / 2; i += NTHR) reinterpret_cast<uint32_t*>(p2all)[i] = 0u;
   for (int i = tid; i < MROWS; i += NTHR) corrb[i] = 1.f;
+  int* exact_flag = reinterpret_cast<int*>(red);  // prologue only: a query element beyond the f16 range
+  if (tid == 0) *exact_flag = 0;
   __syncthreads();
 
   // TMA producer (thread 0): tile `it` -> stage it % S.  A stage is refilled only after the CTA
@@ -191,6 +193,8 @@ __global__ void __launch_bounds__(TT * 16, TT == 16 ? 2 : 1) attn_fast_kernel(At
         if (a.q_dtype == TADA_F32) load4(reinterpret_cast<const float*>(a.q) + (int64_t(b) * HQ + g) * D + 4 * lane, v);
         else load4(reinterpret_cast<const __nv_bfloat16*>(a.q) + (int64_t(b) * HQ + g) * D + 4 * lane, v);
       }
+      const bool big = !(fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3]))) < 32768.f);
+      if (__any_sync(0xffffffffu, big) && lane == 0) *exact_flag = 1;
       const uint32_t lo = pack_h2(v[0], v[1]), hi = pack_h2(v[2], v[3]);
       *reinterpret_cast<uint2*>(q16 + g * D + 4 * lane) = make_uint2(lo, hi);
       // max |q| of the f16-rounded row: the fixed-point scale of the integer code term
@@ -203,6 +207,11 @@ __global__ void __launch_bounds__(TT * 16, TT == 16 ? 2 : 1) attn_fast_kernel(At
     }
   }
   __syncthreads();
+  if (*exact_flag || beyond_f16(a, kFastScaleExp)) {  // CTA-uniform, rare: operands beyond f16 -> exact f32 path
+    for (int it = 0; it < S - 1 && it < ntiles; ++it) mbar_wait(&full[it % S], 0u);  // no copy lands after exit
+    exact_split_partials<BITS, HQ / H>(a, b, split, t_begin, t_end, warp, lane);
+    return;
+  }
   // QK code B operand: Q_h^T as 16-bit fixed point (scale sq per KV head) split into two s8 pieces
   // (q = sq * (256 * hi + lo)), k laid out by dk(); column n = r <-> q head h*G + r.  The integer
   // products and sums are exact, so the code term is q_fx . code with no rounding at all.
@@ -464,6 +473,9 @@ __global__ void __launch_bounds__(TT * 16, TT == 16 ? 2 : 1) attn_fast_kernel(At
         lsum += p;
         bsum = fmaf(p, ok ? vm.y : 0.f, bsum);
         pv[u] = __float2half_rn(p);
+        // P' in f16 unscaled: with p <= 2^8 (lazy max) it holds group scales below 2^8; layers with larger
+        // scales (a deviation range above ~65k at 8 bits) are attended on the exact path (kFastScaleExp).
+        // A 2^-8 pre-scale as in attn_v8_kernel would push 8-bit P' (scales ~range/255) into f16 subnormals.
         p2v[u] = __float2half_rn(ok ? -p * vm.x : 0.f);
       }
       __half* prow = pbuf + sg * PROW2 + TPT * sj;

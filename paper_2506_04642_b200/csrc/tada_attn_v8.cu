@@ -185,9 +185,11 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   split_range(C, a.splits, split, TT, t_begin, t_end);
   const int ntiles = t_end > t_begin ? (t_end - t_begin + TT - 1) / TT : 0;
 
+  int* exact_flag = reinterpret_cast<int*>(smem + pl.off_bar + 112);  // a query element beyond the f16 range
   if (tid == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    *exact_flag = 0;
   }
   // P rows of padding q heads stay zero; corr starts at 1
   for (int i = tid; i < MROWS * TT / 2; i += NTHR) sh<uint32_t>(smem, pl.off_p + 4 * i) = 0u;
@@ -267,6 +269,8 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
       if (a.q_dtype == TADA_F32) load4(reinterpret_cast<const float*>(a.q) + (int64_t(b) * HQ + g) * D + 4 * lane, v);
       else load4(reinterpret_cast<const __nv_bfloat16*>(a.q) + (int64_t(b) * HQ + g) * D + 4 * lane, v);
     }
+    const bool big = !(fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3]))) < 32768.f);
+    if (__any_sync(0xffffffffu, big) && lane == 0) *exact_flag = 1;
     const uint32_t lo = pack_h2(v[0], v[1]), hi = pack_h2(v[2], v[3]);
     *reinterpret_cast<uint2*>(q16 + g * D + 4 * lane) = make_uint2(lo, hi);
     const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&lo));
@@ -277,6 +281,19 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
     if (lane == 0) qmax[g] = amax;
   }
   __syncthreads();
+  if (*exact_flag || beyond_f16(a, kF16SafeExp)) {  // CTA-uniform, rare: operands beyond f16 -> the exact f32 path
+    for (int k = 0; k < S - 1 && k < ntiles; ++k) mbar_wait(&full[k], 0u);  // no copy may land after exit
+    if constexpr (USE_TM) {
+      tc_fence_before();
+      __syncthreads();
+      if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tbase, TCOLS);
+      }
+    }
+    exact_split_partials<BITS, G>(a, b, split, t_begin, t_end, warp, lane);
+    return;
+  }
   // IMMA A operand: q head h*G + r (r < G) as 16-bit fixed point (scale sq) split into two s8 pieces,
   // q = sq * (256 hi + lo): hi in row r, lo in row r + 8, so one IMMA yields both partial sums; k laid
   // out by dk() to match the code bytes.  Stored in fragment order {a0, a1, a2, a3}.

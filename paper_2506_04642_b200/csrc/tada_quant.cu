@@ -41,6 +41,18 @@ static inline int grid_for(int64_t work, int per_block) {
   return int(g);
 }
 
+// Stored values beyond the f16 operand range of the tensor-core decode kernels (tada_attn.cuh: a mean at or
+// above 2^15, a group scale at or above 2^8 for the unscaled P' of attn_fast_kernel) record their binary
+// exponent in the layer's range words (atomicMax, rare): [0] means, [1] scales.  K2 then attends that layer
+// on its exact f32 path.
+__device__ __forceinline__ void note_mean(int32_t* range, float v) {
+  const float a = fabsf(v);
+  if (range && a >= 32768.f && a <= 3.4028235e38f) atomicMax(range, ilogbf(a));
+}
+__device__ __forceinline__ void note_scale(int32_t* range, float s) {
+  if (range && s >= 256.f && s <= 3.4028235e38f) atomicMax(range + 1, ilogbf(s));
+}
+
 // ------------------------------------------------------------------ warp group quantizer
 //
 // One warp quantizes one group of D elements.  Lane l owns elements
@@ -50,7 +62,7 @@ static inline int grid_for(int64_t work, int per_block) {
 template <int NCH, typename Load>
 __device__ __forceinline__ void quantize_group_warp(Load load, int D, int bits, uint8_t* __restrict__ out,
                                                     float* scale_out, float* min_out, int32_t* err, int lane,
-                                                    bool vec_ok) {
+                                                    bool vec_ok, int32_t* range = nullptr) {
   float v[NCH][4];
   float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000);
   bool bad = false;
@@ -126,6 +138,7 @@ __device__ __forceinline__ void quantize_group_warp(Load load, int D, int bits, 
   if (lane == 0) {
     *scale_out = s;
     *min_out = mn;
+    note_scale(range, s);
   }
 }
 
@@ -278,6 +291,7 @@ struct AppendArgs {
   const int32_t* plan_n;    // optional per-sequence new-row counts [B]
   int plan_n_new;           // new rows per sequence when plan_n is null
   int plan_R;               // residual_length
+  int32_t* range;           // optional: the layer's two range words (note_mean / note_scale)
 };
 
 // rows [0, count) of sequence b this launch compresses, and their destination offset after comp_len[b]
@@ -337,6 +351,7 @@ __global__ void __launch_bounds__(256) quant_append_kernel(AppendArgs a) {
     const int t = e / D, d = e - t * D;
     const float m = head_mean(xs + t * row + d, D, H);
     ms[t * D + d] = m;
+    note_mean(a.range, m);
     const int64_t c = c0 + i0 + t;
     uint8_t* page = a.pool + int64_t(pt[c / P]) * a.L.page_bytes;
     reinterpret_cast<float*>(page + a.L.off_mean[side])[(c % P) * D + d] = m;
@@ -354,7 +369,7 @@ __global__ void __launch_bounds__(256) quant_append_kernel(AppendArgs a) {
     float* meta = reinterpret_cast<float*>(page + a.L.off_meta[side]) + 2 * grp;
     CenteredRow ld{ms + t * D, xs + t * row + h * D};
     quantize_group_warp<NCH>(ld, D, bits, page + a.L.off_codes[side] + grp * gb, meta, meta + 1, a.err, lane,
-                             a.vec_ok);
+                             a.vec_ok, a.range);
   }
 }
 
@@ -579,14 +594,15 @@ __global__ void __launch_bounds__(256, MINB) quant_append_fast_kernel(AppendArgs
     }
     // mean: f64 sequential head sum from +0.0, /H (exact for H = 8), RN to f32
     float mean[4];
-    bool bad = false;
+    bool big = false;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       double acc = 0.0;
 #pragma unroll
       for (int h = 0; h < H; ++h) acc = __dadd_rn(acc, double(x[h][k]));
       mean[k] = __double2float_rn(__dmul_rn(acc, 0.125));
-      bad |= !finite(mean[k]);  // any non-finite input makes its column's sum non-finite
+      // any non-finite input makes its column's sum non-finite; |mean| >= 2^15 leaves the f16 range of K2
+      big |= !(fabsf(mean[k]) < 32768.f);
     }
     // every lane has its rows in registers (the mean consumed them): refill the slot freed last
     __syncwarp();
@@ -595,7 +611,15 @@ __global__ void __launch_bounds__(256, MINB) quant_append_fast_kernel(AppendArgs
       fetch(i + K1_RING - 1, fslot);
     }
     fslot = fslot == K1_RING - 1 ? 0 : fslot + 1;
-    if (__any_sync(0xffffffffu, bad) && lane == 0 && a.err) atomicOr(a.err, 1);
+    if (__any_sync(0xffffffffu, big)) {  // rare: a non-finite input, or a mean beyond K2's f16 range
+      bool bad = false;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        bad |= !finite(mean[k]);
+        note_mean(a.range, mean[k]);
+      }
+      if (__any_sync(0xffffffffu, bad) && lane == 0 && a.err) atomicOr(a.err, 1);
+    }
     float mnh[H], mxh[H];
 #pragma unroll
     for (int h = 0; h < H; ++h) {
@@ -659,8 +683,10 @@ __global__ void __launch_bounds__(256, MINB) quant_append_fast_kernel(AppendArgs
     }
     // scales outside [2^-100, 2^100] have no fast path (inv == 0 with s != 0)
     if (lane < H && my_inv == 0.f && my_s != 0.f) unsafe |= 1u << lane;
+    if (lane < H && my_s >= 256.f) unsafe |= 1u << 16;  // a scale beyond attn_fast_kernel's f16 range (note_scale)
     const uint32_t redo = __reduce_or_sync(0xffffffffu, unsafe);
     if (redo) {  // rare: a group within 2^-12 of a rounding boundary -> exact fp64 half-up (quant_code)
+      if ((redo >> 16) && lane < H) note_scale(a.range, my_s);
       constexpr int CMAX = (1 << BITS) - 1;
 #pragma unroll
       for (int h = 0; h < H; ++h) {
@@ -848,7 +874,8 @@ static int quant_append_impl(const tada_page_layout* layout, uint8_t* pool, cons
                              const int32_t* page_table, int32_t pt_stride, const int32_t* dst_start, int64_t dst_offset,
                              int32_t* err_flag, const float* rope_cs, int32_t rope_rows, const int32_t* positions,
                              int64_t pos_stride, void* stream, int part = 0, const int32_t* plan_res = nullptr,
-                             const int32_t* plan_n = nullptr, int plan_n_new = 0, int plan_R = 0) {
+                             const int32_t* plan_n = nullptr, int plan_n_new = 0, int plan_R = 0,
+                             int32_t* range = nullptr) {
   if (!layout) return fail(TADA_ERR_CONFIG, "null layout");
   if (!valid_dtype(dtype)) return fail(TADA_ERR_CONFIG, "dtype must be f32 or bf16");
   if (batch < 0 || n_tok < 0 || src_seq_stride < n_tok) return fail(TADA_ERR_SHAPE, "bad batch/token geometry");
@@ -875,6 +902,7 @@ static int quant_append_impl(const tada_page_layout* layout, uint8_t* pool, cons
   a.plan_n = plan_n;
   a.plan_n_new = plan_n_new;
   a.plan_R = plan_R;
+  a.range = range;
   const int row = layout->heads * layout->head_dim;
   const size_t per_tok = size_t(row + layout->head_dim) * 4;
   int tt = int((32 * 1024) / per_tok);
@@ -907,7 +935,7 @@ int tada_quant_append_plan(const tada_page_layout* layout, uint8_t* pool, const 
                            const int32_t* page_table, int32_t pt_stride, const int32_t* comp_len,
                            const int32_t* res_len, int32_t residual_length, int32_t n_new, const int32_t* seq_n,
                            int32_t part, const int32_t* positions, int64_t pos_stride, const float* rope_cs,
-                           int32_t rope_rows, int32_t* err_flag, void* stream) {
+                           int32_t rope_rows, int32_t* err_flag, int32_t* range_word, void* stream) {
   if (!layout) return fail(TADA_ERR_CONFIG, "null layout");
   if (part != 1 && part != 2) return fail(TADA_ERR_CONFIG, "part must be 1 (residual rows) or 2 (new rows)");
   if (!res_len) return fail(TADA_ERR_SHAPE, "null buffer");
@@ -920,7 +948,7 @@ int tada_quant_append_plan(const tada_page_layout* layout, uint8_t* pool, const 
   }
   return quant_append_impl(layout, pool, src_k, src_v, dtype, batch, n_max, src_seq_stride, page_table, pt_stride,
                            comp_len, 0, err_flag, rope_cs, rope_rows, positions, pos_stride, stream, part, res_len,
-                           seq_n, n_new, residual_length);
+                           seq_n, n_new, residual_length, range_word);
 }
 
 int tada_append_commit(float* res_k, float* res_v, int64_t res_seq_stride, int32_t heads, int32_t head_dim,

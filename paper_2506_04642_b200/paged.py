@@ -73,6 +73,9 @@ class PagedKVCache:
         self.res_v = [torch.zeros_like(t) for t in self.res_k]
         self.err = _dev.ErrFlag()
         self._step_sync = torch.zeros((num_layers, batch), dtype=torch.int32, device=self.dev)  # K3 arrival counters
+        # per-layer range words (K1 note_mean / note_scale): stored values beyond the tensor-core kernels' f16
+        # operand range route K2 to its exact f32 path for that layer
+        self.range = torch.zeros((num_layers, 2), dtype=torch.int32, device=self.dev)
         self._stale = False  # host length mirrors behind the device (after CUDA-graph replays)
         self._ws = None
         if max_tokens is not None:  # pre-size: every page of every sequence up front
@@ -176,7 +179,7 @@ class PagedKVCache:
         call("tada_quant_append_plan", self._layout_ptr(layer), self.pools[layer].data_ptr(), src_k, src_v, dtype,
              self.B, n_max, stride, self.page_table.data_ptr(), self.page_table.shape[1],
              self.comp_len[layer].data_ptr(), self.res_len[layer].data_ptr(), self.R, n_new, _dev.ptr(seq_n), part,
-             _dev.ptr(pos), pos_stride, _dev.ptr(table), rows, self.err.ptr, _dev.stream())
+             _dev.ptr(pos), pos_stride, _dev.ptr(table), rows, self.err.ptr, self.range[layer].data_ptr(), _dev.stream())
 
     def _append_planned(self, layer: int, k: torch.Tensor, v: torch.Tensor, lengths, rope=None) -> None:
         """Device-planned append of [batch, n, H, D] rows (n_b = lengths[b] of them per sequence): K1 over the
@@ -347,7 +350,7 @@ class PagedKVCache:
              _dev.dtype_code(q), self.B, hq, self.page_table.data_ptr(), self.page_table.shape[1],
              self.comp_len[layer].data_ptr(), self.res_len[layer].data_ptr(), self.res_k[layer].data_ptr(),
              self.res_v[layer].data_ptr(), self.res_k[layer].shape[1], float(sc), splits, _dev.ptr(ws),
-             out.data_ptr(), _dev.dtype_code(out), mode, _dev.stream())
+             out.data_ptr(), _dev.dtype_code(out), mode, self.range[layer].data_ptr(), _dev.stream())
         return out
 
     def append_attend(self, layer: int, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
@@ -398,7 +401,7 @@ class PagedKVCache:
             self.res_len[layer].data_ptr(), self.res_k[layer].data_ptr(), self.res_v[layer].data_ptr(),
             self.res_k[layer].shape[1], self.R, k.data_ptr(), v.data_ptr(), _dev.dtype_code(k), k1_rows,
             self._step_sync[layer].data_ptr(), float(sc), splits, _dev.ptr(ws), out.data_ptr(), _dev.dtype_code(out),
-            mode, self.err.ptr, _dev.stream())
+            mode, self.err.ptr, self.range[layer].data_ptr(), _dev.stream())
         if rc == TADA_ERR_CONFIG and not _capture:  # geometry without the tensor-core path: nothing was enqueued
             self.append(layer, k, v)
             return self.attend(layer, q, out=out, out_dtype=out_dtype, num_splits=num_splits, mode=mode, scale=scale)
@@ -433,7 +436,7 @@ class PagedKVCache:
              _dev.dtype_code(q), self.B, hq, self.page_table.data_ptr(), self.page_table.shape[1],
              self.comp_len[layer].data_ptr(), self.res_len[layer].data_ptr(), self.res_k[layer].data_ptr(),
              self.res_v[layer].data_ptr(), self.res_k[layer].shape[1], float(sc), splits, _dev.ptr(ws),
-             out.data_ptr(), _dev.dtype_code(out), mode, lse.data_ptr(), _dev.stream())
+             out.data_ptr(), _dev.dtype_code(out), mode, lse.data_ptr(), self.range[layer].data_ptr(), _dev.stream())
         return out, lse
 
     # ------------------------------------------------------------------ export / import (TADAKV1 parity vehicle)

@@ -293,3 +293,49 @@ def test_fast_extreme_value_range(bits, mag):
     out = store.attend(0, torch.from_numpy(q).cuda(), mode=2, out_dtype=torch.float32).cpu().numpy()
     assert np.isfinite(out).all()
     assert np.abs(out - want).max() <= 2e-3 * max(1.0, float(np.abs(want).max()))
+
+
+@pytest.mark.parametrize("bits", [2, 4, 8])
+@pytest.mark.parametrize("where", ["mean", "scale", "query"])
+def test_auto_mode_beyond_f16_range(bits, where):
+    """The tensor-core kernels stage q, the means and P' as f16 (|x| < 65504).  A 1e5-magnitude channel shared by
+    all heads (a mean >= 2^15), a 1e6 channel on one head only (a group scale beyond the kernel's P' range), or a
+    1e5 query element makes
+    mode 0 attend that layer on K2's exact f32 path (K1 records the range; K2 checks q): the answer equals the
+    exact kernel's and the oracle's, never inf/NaN."""
+    m = tk()
+    rng = np.random.default_rng(60 + bits + len(where))
+    B, T, H, D, hq = 2, 700, 8, 128, 32
+    k = rng.normal(size=(B, T, H, D))
+    v = rng.normal(size=(B, T, H, D))
+    q = rng.normal(size=(B, hq, D))
+    if where == "mean":
+        v[:, :, :, 17] += 1e5
+        k[:, :, :, 40] -= 1e5
+    elif where == "scale":  # one head's group range ~1.9e6: scale >= 2^15 at 2/4 bits, >= 2^8 at 8 bits
+        v[:, :, 3, 17] = rng.choice([-1e6, 1e6], size=(B, T))
+    else:
+        q[:, :, 5] = 1e5 * rng.choice([-1.0, 1.0], size=(B, hq))
+    k, v, q = (orc.bf16_round(x.astype(np.float32)) for x in (k, v, q))
+    store = m.PagedKVCache(1, H, D, (bits,), 128, batch=B, page_tokens=64, max_tokens=T + 1, shuffle_pages=True)
+    store.append(0, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    want = []
+    for b in range(B):
+        st = orc.LayerState(H, D, bits, 128)
+        orc.append(st, k[b], v[b])
+        want.append(orc.attend(q[b], st, hq)[0])
+    want = np.stack(want)
+    qd = torch.from_numpy(q).cuda()
+    auto = store.attend(0, qd, mode=0, out_dtype=torch.float32).cpu().numpy()
+    exact = store.attend(0, qd, mode=1, out_dtype=torch.float32).cpu().numpy()
+    assert np.isfinite(auto).all()
+    scale = max(1.0, float(np.abs(want).max()))
+    assert np.abs(exact - want).max() <= 1e-5 * scale
+    assert np.abs(auto - want).max() <= 1e-5 * scale
+    rng_words = store.range[0].tolist()
+    routed = rng_words[0] >= 15 or rng_words[1] >= (8 if bits == 8 else 15)
+    assert routed == (where != "query"), rng_words
+    # the fused decode step takes the same path
+    kn = orc.bf16_round(rng.normal(size=(B, 1, H, D)).astype(np.float32))
+    step = store.append_attend(0, qd, torch.from_numpy(kn).cuda(), torch.from_numpy(kn).cuda(), out_dtype=torch.float32)
+    assert torch.isfinite(step).all()
