@@ -72,7 +72,10 @@ constexpr int kBudget = 113 * 1024;  // two CTAs per SM
 #ifndef TADA_V8_TMEM_OM
 #define TADA_V8_TMEM_OM 1  // park the PV mean accumulators in TMEM between tiles
 #endif
-constexpr int MAXS = TADA_V8_MAXS;  // deepest TMA ring (2 or 3 stages)
+constexpr int MAXS = TADA_V8_MAXS;
+#ifndef TADA_V8_PIPE_S3
+#define TADA_V8_PIPE_S3 1  // the pipelined plan takes a third stage where it fits
+#endif  // deepest TMA ring (2 or 3 stages)
 
 __host__ __device__ constexpr int up128(int x) { return (x + 127) / 128 * 128; }
 __host__ __device__ constexpr int up1k(int x) { return (x + 1023) / 1024 * 1024; }
@@ -80,6 +83,7 @@ __host__ __device__ constexpr int up1k(int x) { return (x + 1023) / 1024 * 1024;
 struct Plan {
   int mean_bytes, codes_bytes, meta_bytes, side_bytes, stage_bytes, stages, trow;
   int off_vm, off_sm, off_p, off_corr, off_qa, off_qi, off_bar, total;
+  int vm_stride, sm_stride, p_stride, corr_stride;  // second buffer of each exchange region (pipelined plan)
   bool ok;
   bool qi_smem;  // the IMMA q fragments live in shared memory (frees 16 registers) when there is room
 };
@@ -88,7 +92,9 @@ struct Plan {
 // corr [MROWS] | QA [4 quarters][MT][2 k-steps][32 lanes] uint4 | mbarriers.  The prologue's q staging
 // and row maxima live in the last stage; the epilogue parks [HQ][D + 4] f32 over the stages and keeps
 // its (l, Σp·vmin, m) table in the then idle VM region.
-__host__ __device__ constexpr Plan make_plan(int gb, int HQ) {
+// Pipelined plan (pipe): two stages, and VM (hi only), SM, P and corr twice — tile i's phase B works on
+// buffer i & 1 while phase C of tile i - 1 and phase A of tile i + 1 use the other one.
+__host__ __device__ constexpr Plan make_plan(int gb, int HQ, bool pipe = false) {
   Plan p{};
   const int mrows = HQ >= 16 ? HQ : 16, mt = mrows / 16;
   p.trow = H * 8 + 16;  // meta box row: 16 B of TMA zero fill per row spread the banks
@@ -97,21 +103,29 @@ __host__ __device__ constexpr Plan make_plan(int gb, int HQ) {
   p.meta_bytes = TT * p.trow;
   p.side_bytes = p.mean_bytes + p.codes_bytes;
   p.stage_bytes = up1k(2 * p.side_bytes + 2 * p.meta_bytes);
-  const int tail = 2 * VMPART + 4 * mrows * TT * 4 + mrows * TT * 2 + up128(mrows * 4) + 4 * mt * 2 * 512 + 128;
-  p.stages = (MAXS >= 3 && 3 * p.stage_bytes + tail <= kBudget) ? 3 : ((2 * p.stage_bytes + tail <= kBudget) ? 2 : 0);
+  const int nb = pipe ? 2 : 1;
+  const int vmb = pipe ? VMPART : 2 * VMPART, smb = 4 * mrows * TT * 4, pb = mrows * TT * 2, cb = up128(mrows * 4);
+  const int qab = 4 * mt * 2 * 512;  // QA: prologue only; the pipelined plan stages it in the S_mean buffers
+  const int tail = nb * (vmb + smb + pb + cb) + (pipe ? 0 : qab) + 128;
+  p.stages = (((pipe && TADA_V8_PIPE_S3) || MAXS >= 3) && 3 * p.stage_bytes + tail <= kBudget) ? 3
+                                                                         : ((2 * p.stage_bytes + tail <= kBudget) ? 2 : 0);
   int off = p.stages * p.stage_bytes;
   p.off_vm = off;
-  off += 2 * VMPART;
+  p.vm_stride = pipe ? vmb : 0;
+  off += nb * vmb;
   p.off_sm = off;
-  off += 4 * mrows * TT * 4;
+  p.sm_stride = pipe ? smb : 0;
+  off += nb * smb;
   p.off_p = off;
-  off += mrows * TT * 2;
+  p.p_stride = pipe ? pb : 0;
+  off += nb * pb;
   p.off_corr = off;
-  off += up128(mrows * 4);
-  p.off_qa = off;
-  off += 4 * mt * 2 * 512;
+  p.corr_stride = pipe ? cb : 0;
+  off += nb * cb;
+  p.off_qa = pipe ? p.off_sm : off;
+  if (!pipe) off += qab;
   p.off_qi = off;
-  p.qi_smem = off + 8 * 4 * 512 + 128 <= kBudget;
+  p.qi_smem = !pipe && off + 8 * 4 * 512 + 128 <= kBudget;  // (the pipelined kernel keeps them in TMEM)
   if (p.qi_smem) off += 8 * 4 * 512;  // [warp][k-step][lane] uint4
   p.off_bar = off;
   off += 128;
@@ -119,6 +133,18 @@ __host__ __device__ constexpr Plan make_plan(int gb, int HQ) {
   p.ok = p.stages >= 2 && p.stage_bytes >= mrows * (D * 2 + 4) && p.stages * p.stage_bytes >= HQ * (D + 4) * 4 &&
          2 * VMPART >= 3 * HQ * 4;
   return p;
+}
+
+#ifndef TADA_V8_PIPE
+#define TADA_V8_PIPE 2  // pipelined schedule (one barrier per tile): 2 = 2-bit layers only, 1 = wherever it fits
+#endif
+// The pipelined schedule runs phase C of tile i - 1, phase B of tile i and phase A of tile i + 1 between two
+// consecutive barriers; it needs the doubled exchange buffers (make_plan(.., true)), and takes a third stage when
+// it fits (the refill of tile i + S is issued one interval after tile i was consumed).
+__host__ __device__ constexpr bool v8_pipe(int bits, int HQ) {
+  // measured (B=16, T=32k): 2-bit +4.4% (Hq=32) / +3% (Hq=16); 4-bit -0.6% (Hq=32) / -3.8% (Hq=8), where the
+  // shorter refill distance (tile i + 2 is loaded during interval i + 1, not a whole tile ahead) shows at HBM speed
+  return (TADA_V8_PIPE == 1 || (TADA_V8_PIPE == 2 && bits == 2)) && make_plan(bits * D / 8, HQ, true).ok;
 }
 
 __device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], uint32_t addr) {
@@ -167,7 +193,8 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   constexpr int MT = HQ >= 16 ? HQ / 16 : 1;  // 16-row q tiles of the shared mean terms
   constexpr int MROWS = MT * 16;
   constexpr int GB = BITS * D / 8;            // code bytes per (token, head)
-  constexpr Plan pl = make_plan(GB, HQ);
+  constexpr bool PIPE = v8_pipe(BITS, HQ);
+  constexpr Plan pl = make_plan(GB, HQ, PIPE);
   constexpr int S = pl.stages < 2 ? 2 : pl.stages;  // geometries with < 2 stages are never launched
   constexpr int SB = pl.stage_bytes;
   constexpr int PLANE = MROWS * TT * 4;
@@ -192,8 +219,14 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
     *exact_flag = 0;
   }
   // P rows of padding q heads stay zero; corr starts at 1
-  for (int i = tid; i < MROWS * TT / 2; i += NTHR) sh<uint32_t>(smem, pl.off_p + 4 * i) = 0u;
-  for (int i = tid; i < MROWS; i += NTHR) sh<float>(smem, pl.off_corr + 4 * i) = 1.f;
+  for (int i = tid; i < MROWS * TT / 2; i += NTHR) {
+    sh<uint32_t>(smem, pl.off_p + 4 * i) = 0u;
+    if (PIPE) sh<uint32_t>(smem, pl.off_p + pl.p_stride + 4 * i) = 0u;
+  }
+  for (int i = tid; i < MROWS; i += NTHR) {
+    sh<float>(smem, pl.off_corr + 4 * i) = 1.f;
+    if (PIPE) sh<float>(smem, pl.off_corr + pl.corr_stride + 4 * i) = 1.f;
+  }
   // PARK: the PV mean accumulators (om, 8*MT floats per thread) are touched only in phase C; between
   // tiles they live in TMEM (warp w: lane quarter w%4, column block w/4), freeing their registers for
   // phases A/B.  Measured: +4% at Hq=64 (32 registers), -1% at Hq<=32 (16), so only there.
@@ -210,6 +243,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   // QATM: the QK mean A fragments of this warp's d quarter (8*MT values) in TMEM too, one tcgen05.ld per
   // tile instead of 2*MT LDS.128
   constexpr bool QATM = TADA_V8_QATM == 1 || (TADA_V8_QATM == 0 && MT <= 2);
+  static_assert(!PIPE || (QTM && QATM), "the pipelined plan keeps the q fragments in TMEM (QA aliases S_mean)");
   constexpr bool USE_TM = PARK || QTM || QATM || TADA_V8_OFTM;
   // TMEM columns of one lane (warps w and w+4 share lane quarter w%4; column blocks by w/4)
   constexpr int C_Q = PARK ? 2 * NOM : 0, C_QA = C_Q + (QTM ? 32 : 0), C_OF = C_QA + (QATM ? 16 * MT : 0);
@@ -439,83 +473,82 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   }
 #endif
 
-  auto body = [&](auto stage_c, int it) {
-    constexpr int STG = decltype(stage_c)::value;
-    constexpr int ST = STG * SB;  // this tile's stage
-    const int t0 = t_begin + it * TT;
-    const int nv = min(TT, t_end - t0);
-    const bool tail = nv < TT;
-    mbar_wait(&full[STG], uint32_t(it / S) & 1u);
-    if (a.diag == 1) {  // diagnostics: pipeline only
-      __syncthreads();
-      __syncthreads();
-      if (tid == 0 && it + S < ntiles) {
-        issue(STG);
-        if (it + S + 1 < ntiles && a.diag != 2) cur_page = pt[cur_pg];
-      }
-      return;
-    }
-
-    // ------------------------------------------------------------ A: QK mean piece -> S_mean plane qd
-    {
+  // One tile's three phases.  STG = the tile's stage; BUF = the exchange buffer (S_mean, P, corr, flags, split
+  // vmean) the phase writes or reads (always 0 in the classic schedule).
+  using I0 = std::integral_constant<int, 0>;
+  using I1 = std::integral_constant<int, 1>;
+  // ------------------------------------------------------------ A: QK mean piece -> S_mean plane qd
+  auto phaseA = [&](auto stage_c, auto buf_c) {
+    const int ST = int(stage_c) * SB;
+    const int SMO = int(buf_c) * pl.sm_stride;
 #if TADA_V8_OFTM >= 2
-      float ofa[4];
-      tmem_ld<4>(tof2, ofa);
-      tmem_wait_ld();
-      const int oX0 = __float_as_int(ofa[0]), oX1 = __float_as_int(ofa[1]);
-      const int oQA = __float_as_int(ofa[2]), oSW = __float_as_int(ofa[3]);
+    float ofa[4];
+    tmem_ld<4>(tof2, ofa);
+    tmem_wait_ld();
+    const int oX0 = __float_as_int(ofa[0]), oX1 = __float_as_int(ofa[1]);
+    const int oQA = __float_as_int(ofa[2]), oSW = __float_as_int(ofa[3]);
 #endif
-      float acc[MT][4];
+    float acc[MT][4];
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
-      uint32_t hb[2][2], lb[2][2];  // B fragments (hi, lo) of both k-steps
+    for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
+    uint32_t hb[2][2], lb[2][2];  // B fragments (hi, lo) of both k-steps
 #pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        const float4 x = sh<float4>(smem, ST + (ks ? oX1 : oX0));
-        split_h2(x.x, x.y, hb[ks][0], lb[ks][0]);
-        split_h2(x.z, x.w, hb[ks][1], lb[ks][1]);
-      }
-      float qa[QATM ? 8 * MT : 1];
-      if constexpr (QATM) {
-        tmem_ld<QATM ? 8 * MT : 8>(tqa, qa);
-        tmem_wait_ld();
-      }
-      // MT (or 2 MT) independent accumulation chains, interleaved so no MMA waits on the previous one
-      constexpr bool AC2 = TADA_V8_ACHAINS == 2 || (TADA_V8_ACHAINS == 0 && MT <= 2);
-      [[maybe_unused]] float acc2[AC2 ? MT : 1][4];
-      if constexpr (AC2)
+    for (int ks = 0; ks < 2; ++ks) {
+      const float4 x = sh<float4>(smem, ST + (ks ? oX1 : oX0));
+      split_h2(x.x, x.y, hb[ks][0], lb[ks][0]);
+      split_h2(x.z, x.w, hb[ks][1], lb[ks][1]);
+    }
+    float qa[QATM ? 8 * MT : 1];
+    if constexpr (QATM) {
+      tmem_ld<QATM ? 8 * MT : 8>(tqa, qa);
+      tmem_wait_ld();
+    }
+    // MT (or 2 MT) independent accumulation chains, interleaved so no MMA waits on the previous one
+    constexpr bool AC2 = TADA_V8_ACHAINS == 2 || (TADA_V8_ACHAINS == 0 && MT <= 2);
+    [[maybe_unused]] float acc2[AC2 ? MT : 1][4];
+    if constexpr (AC2)
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) acc2[mt][0] = acc2[mt][1] = acc2[mt][2] = acc2[mt][3] = 0.f;
+      for (int mt = 0; mt < MT; ++mt) acc2[mt][0] = acc2[mt][1] = acc2[mt][2] = acc2[mt][3] = 0.f;
 #pragma unroll
-      for (int pass = 0; pass < 2; ++pass)
+    for (int pass = 0; pass < 2; ++pass)
 #pragma unroll
-        for (int ks = 0; ks < 2; ++ks)
+      for (int ks = 0; ks < 2; ++ks)
 #pragma unroll
-          for (int mt = 0; mt < MT; ++mt) {
-            uint32_t af[4];
-            if constexpr (QATM) {
+        for (int mt = 0; mt < MT; ++mt) {
+          uint32_t af[4];
+          if constexpr (QATM) {
 #pragma unroll
-              for (int i = 0; i < 4; ++i) af[i] = __float_as_uint(qa[QATM ? 4 * (mt * 2 + ks) + i : 0]);
-            } else {
-              const uint4 f = sh<uint4>(smem, oQA + (mt * 2 + ks) * 512);
-              af[0] = f.x; af[1] = f.y; af[2] = f.z; af[3] = f.w;
-            }
-            if (pass == 0) mma(acc[mt], af, hb[ks][0], hb[ks][1]);
-            else if constexpr (AC2) mma(acc2[AC2 ? mt : 0], af, lb[ks][0], lb[ks][1]);
-            else mma(acc[mt], af, lb[ks][0], lb[ks][1]);
+            for (int i = 0; i < 4; ++i) af[i] = __float_as_uint(qa[QATM ? 4 * (mt * 2 + ks) + i : 0]);
+          } else {
+            const uint4 f = sh<uint4>(smem, oQA + (mt * 2 + ks) * 512);
+            af[0] = f.x; af[1] = f.y; af[2] = f.z; af[3] = f.w;
           }
-      if constexpr (AC2)
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-          for (int i = 0; i < 4; ++i) acc[mt][i] += acc2[AC2 ? mt : 0][i];
+          if (pass == 0) mma(acc[mt], af, hb[ks][0], hb[ks][1]);
+          else if constexpr (AC2) mma(acc2[AC2 ? mt : 0], af, lb[ks][0], lb[ks][1]);
+          else mma(acc[mt], af, lb[ks][0], lb[ks][1]);
+        }
+    if constexpr (AC2)
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
-          sh<float2>(smem, oSW + (16 * mt + 8 * e) * TT * 4) = make_float2(acc[mt][2 * e], acc[mt][2 * e + 1]);
-    }
-    __syncthreads();  // ---- barrier 1: S_mean complete; the previous tile's P and split vmean are consumed
+        for (int i = 0; i < 4; ++i) acc[mt][i] += acc2[AC2 ? mt : 0][i];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        sh<float2>(smem, SMO + oSW + (16 * mt + 8 * e) * TT * 4) = make_float2(acc[mt][2 * e], acc[mt][2 * e + 1]);
+  };
+
+  // ------------------------------------------------------------ B: the warp's KV head (QK code term, softmax,
+  // PV code term) and its share of the vmean split.  MAYTAIL: the tile may be the split's partial last tile.
+  auto phaseB = [&](auto stage_c, auto buf_c, auto maytail_c, int it) {
+    const int ST = int(stage_c) * SB;
+    const int BUF = int(buf_c);
+    const int SMO = BUF * pl.sm_stride, PO = BUF * pl.p_stride, CO = BUF * pl.corr_stride, VO = BUF * pl.vm_stride;
+    constexpr bool MAYTAIL = decltype(maytail_c)::value;
+    const int t0 = t_begin + it * TT;
+    const int nv = MAYTAIL ? min(TT, t_end - t0) : TT;
+    const bool tail = MAYTAIL && nv < TT;
 #if TADA_V8_OFTM
     float ofv[16];
     tmem_ld<16>(tof, ofv);
@@ -587,7 +620,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
       // S_mean of (q row, tokens 2c, 2c+1 | 8+2c, 9+2c): the 4 d-quarter planes
       float sm[2][2];
       {
-        const float2 v0 = sh<float2>(smem, oS0), v1 = sh<float2>(smem, oS1);
+        const float2 v0 = sh<float2>(smem, SMO + oS0), v1 = sh<float2>(smem, SMO + oS1);
         sm[0][0] = v0.x;
         sm[0][1] = v0.y;
         sm[1][0] = v1.x;
@@ -595,8 +628,8 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
       }
 #pragma unroll
       for (int k = 1; k < 4; ++k) {
-        const float2 v0 = sh<float2>(smem, oS0 + k * PLANE);
-        const float2 v1 = sh<float2>(smem, oS1 + k * PLANE);
+        const float2 v0 = sh<float2>(smem, SMO + oS0 + k * PLANE);
+        const float2 v1 = sh<float2>(smem, SMO + oS1 + k * PLANE);
         sm[0][0] += v0.x;
         sm[0][1] += v0.y;
         sm[1][0] += v1.x;
@@ -661,12 +694,12 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
         ssum = (f0.x + f0.y) + (f1.x + f1.y);
       }
       if (live) {  // P (f16) for the PV mean piece, corr for its rescale
-        sh<uint32_t>(smem, oPW + ((0 ^ pch) << 4)) = bp0;
-        sh<uint32_t>(smem, oPW + ((1 ^ pch) << 4)) = bp1;
-        if (c == 0) sh<float>(smem, pl.off_corr + 4 * qrow) = corr;
+        sh<uint32_t>(smem, PO + oPW + ((0 ^ pch) << 4)) = bp0;
+        sh<uint32_t>(smem, PO + oPW + ((1 ^ pch) << 4)) = bp1;
+        if (c == 0) sh<float>(smem, CO + pl.off_corr + 4 * qrow) = corr;
       }
       if constexpr (FLAGS)
-        if (lane == 0) sh<uint8_t>(smem, pl.off_bar + 96 + warp) = resc ? 1 : 0;  // this warp's rescale flag
+        if (lane == 0) sh<uint8_t>(smem, pl.off_bar + 96 + 8 * BUF + warp) = resc ? 1 : 0;  // this warp's rescale flag
       l_run = fmaf(l_run, corr, lsum);
       bp_run = fmaf(bp_run, corr, bsum);
       sp_run = fmaf(sp_run, corr, ssum);
@@ -768,6 +801,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
       const float4 x0 = sh<float4>(smem, ST + oV0), x1 = sh<float4>(smem, ST + oV1);
       uint4 hi;
 #if TADA_V8_VMEAN_LO
+      static_assert(!PIPE, "the pipelined plan holds the hi part of the split vmean only");
       uint4 lo;
       split_h2(x0.x, x0.y, hi.x, lo.x);
       split_h2(x0.z, x0.w, hi.y, lo.y);
@@ -781,86 +815,166 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
       hi = make_uint4(pack_h2(x0.x, x0.y), pack_h2(x0.z, x0.w), pack_h2(x1.x, x1.y), pack_h2(x1.z, x1.w));
 #endif
       if (tail && vt >= nv) hi = make_uint4(0u, 0u, 0u, 0u);  // rows past the sequence may hold anything
-      sh<uint4>(smem, oVW) = hi;
-    }
-    __syncthreads();  // ---- barrier 2: P, corr and the split vmean complete; this tile's stage is free
-    if (tid == 0 && it + S < ntiles) {
-      issue(STG);
-      // (a late page-table load here would stall the next barrier; diag 2 re-reads one L2-resident page)
-      if (it + S + 1 < ntiles && a.diag != 2) cur_page = pt[cur_pg];
-    }
-    // ------------------------------------------------------------ C: PV mean piece (d slice of this warp)
-    {
-#if TADA_V8_OFTM >= 2
-      float ofc[2];
-      tmem_ld<2>(tof2 + 4, ofc);
-      tmem_wait_ld();
-      const uint32_t aPA = __float_as_uint(ofc[0]), aVB = __float_as_uint(ofc[1]);
-#endif
-      // FLAGS: one 8-byte read of the per-warp rescale flags (rare after the first tiles) decides whether
-      // to touch corr at all; otherwise every thread reads its rows' corr and the warp votes
-      float cr[MT][2];
-      bool any = false;
-      if constexpr (FLAGS) {
-        const uint2 fl = sh<uint2>(smem, pl.off_bar + 96);
-        any = (fl.x | fl.y) != 0u;  // CTA-uniform
-      } else {
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          cr[mt][0] = sh<float>(smem, pl.off_corr + 4 * (16 * mt + r));
-          cr[mt][1] = sh<float>(smem, pl.off_corr + 4 * (16 * mt + r + 8));
-          any |= (cr[mt][0] != 1.f) || (cr[mt][1] != 1.f);
-        }
-        any = __any_sync(0xffffffffu, any);
-      }
-      if constexpr (PARK) {
-        tmem_wait_st();
-        tmem_ld<NOM>(tom, &om[0][0][0]);
-        tmem_wait_ld();
-      }
-      if (any) {
-        if constexpr (FLAGS) {
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt) {
-            cr[mt][0] = sh<float>(smem, pl.off_corr + 4 * (16 * mt + r));
-            cr[mt][1] = sh<float>(smem, pl.off_corr + 4 * (16 * mt + r + 8));
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt) {
-            om[j][mt][0] *= cr[mt][0];
-            om[j][mt][1] *= cr[mt][0];
-            om[j][mt][2] *= cr[mt][1];
-            om[j][mt][3] *= cr[mt][1];
-          }
-      }
-      uint32_t bh[4];
-      ldsm_x4_t(bh, aVB);
-#if TADA_V8_VMEAN_LO
-      uint32_t bl[4];
-      ldsm_x4_t(bl, aVB + VMPART);
-#endif
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        uint32_t pa[4];
-        ldsm_x4(pa, aPA + mt * 512);
-#pragma unroll
-        for (int j = 0; j < 2; ++j) mma(om[j][mt], pa, bh[2 * j], bh[2 * j + 1]);
-#if TADA_V8_VMEAN_LO
-#pragma unroll
-        for (int j = 0; j < 2; ++j) mma(om[j][mt], pa, bl[2 * j], bl[2 * j + 1]);
-#endif
-      }
-      if constexpr (PARK) tmem_st<NOM>(tom, &om[0][0][0]);
+      sh<uint4>(smem, VO + oVW) = hi;
     }
   };
-  for (int it = 0; it < ntiles; it += S) {
-    body(std::integral_constant<int, 0>{}, it);
-    if (it + 1 < ntiles) body(std::integral_constant<int, 1>{}, it + 1);
-    if constexpr (S == 3)
-      if (it + 2 < ntiles) body(std::integral_constant<int, 2>{}, it + 2);
+
+  // ------------------------------------------------------------ C: PV mean piece (d slice of this warp)
+  auto phaseC = [&](auto buf_c) {
+    const int BUF = int(buf_c);
+    const int PO = BUF * pl.p_stride, CO = BUF * pl.corr_stride, VO = BUF * pl.vm_stride;
+#if TADA_V8_OFTM >= 2
+    float ofc[2];
+    tmem_ld<2>(tof2 + 4, ofc);
+    tmem_wait_ld();
+    const uint32_t aPA = __float_as_uint(ofc[0]), aVB = __float_as_uint(ofc[1]);
+#endif
+    // FLAGS: one 8-byte read of the per-warp rescale flags (rare after the first tiles) decides whether
+    // to touch corr at all; otherwise every thread reads its rows' corr and the warp votes
+    float cr[MT][2];
+    bool any = false;
+    if constexpr (FLAGS) {
+      const uint2 fl = sh<uint2>(smem, pl.off_bar + 96 + 8 * BUF);
+      any = (fl.x | fl.y) != 0u;  // CTA-uniform
+    } else {
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        cr[mt][0] = sh<float>(smem, CO + pl.off_corr + 4 * (16 * mt + r));
+        cr[mt][1] = sh<float>(smem, CO + pl.off_corr + 4 * (16 * mt + r + 8));
+        any |= (cr[mt][0] != 1.f) || (cr[mt][1] != 1.f);
+      }
+      any = __any_sync(0xffffffffu, any);
+    }
+    if constexpr (PARK) {
+      tmem_wait_st();
+      tmem_ld<NOM>(tom, &om[0][0][0]);
+      tmem_wait_ld();
+    }
+    if (any) {
+      if constexpr (FLAGS) {
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          cr[mt][0] = sh<float>(smem, CO + pl.off_corr + 4 * (16 * mt + r));
+          cr[mt][1] = sh<float>(smem, CO + pl.off_corr + 4 * (16 * mt + r + 8));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          om[j][mt][0] *= cr[mt][0];
+          om[j][mt][1] *= cr[mt][0];
+          om[j][mt][2] *= cr[mt][1];
+          om[j][mt][3] *= cr[mt][1];
+        }
+    }
+    uint32_t bh[4];
+    ldsm_x4_t(bh, aVB + VO);
+#if TADA_V8_VMEAN_LO
+    uint32_t bl[4];
+    ldsm_x4_t(bl, aVB + VMPART);
+#endif
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      uint32_t pa[4];
+      ldsm_x4(pa, aPA + PO + mt * 512);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) mma(om[j][mt], pa, bh[2 * j], bh[2 * j + 1]);
+#if TADA_V8_VMEAN_LO
+#pragma unroll
+      for (int j = 0; j < 2; ++j) mma(om[j][mt], pa, bl[2 * j], bl[2 * j + 1]);
+#endif
+    }
+    if constexpr (PARK) tmem_st<NOM>(tom, &om[0][0][0]);
+  };
+
+  if constexpr (!PIPE) {
+    // classic schedule: A | barrier | B | barrier, refill | C
+    auto body = [&](auto stage_c, int it) {
+      constexpr int STG = decltype(stage_c)::value;
+      mbar_wait(&full[STG], uint32_t(it / S) & 1u);
+      if (a.diag == 1) {  // diagnostics: pipeline only
+        __syncthreads();
+        __syncthreads();
+        if (tid == 0 && it + S < ntiles) {
+          issue(STG);
+          if (it + S + 1 < ntiles && a.diag != 2) cur_page = pt[cur_pg];
+        }
+        return;
+      }
+      phaseA(stage_c, I0{});
+      __syncthreads();  // ---- barrier 1: S_mean complete; the previous tile's P and split vmean are consumed
+      phaseB(stage_c, I0{}, std::true_type{}, it);
+      __syncthreads();  // ---- barrier 2: P, corr and the split vmean complete; this tile's stage is free
+      if (tid == 0 && it + S < ntiles) {
+        issue(STG);
+        // (a late page-table load here would stall the next barrier; diag 2 re-reads one L2-resident page)
+        if (it + S + 1 < ntiles && a.diag != 2) cur_page = pt[cur_pg];
+      }
+      phaseC(I0{});
+    };
+    for (int it = 0; it < ntiles; it += S) {
+      body(std::integral_constant<int, 0>{}, it);
+      if (it + 1 < ntiles) body(std::integral_constant<int, 1>{}, it + 1);
+      if constexpr (S == 3)
+        if (it + 2 < ntiles) body(std::integral_constant<int, 2>{}, it + 2);
+    }
+  } else {
+    // pipelined schedule (tile i in stage i % S, exchange buffer i & 1):
+    //   A(0) | barrier | { C(i-1), B(i), A(i+1) | barrier, refill stage i % S with tile i + S } for each i | C(last)
+    // One barrier per tile; the three phases are independent dependency chains the scheduler interleaves.  The
+    // loop is unrolled by U = 2S so stage, buffer and mbarrier parity are immediates (J = i mod U: stage J % S,
+    // buffer J & 1, parity (J / S) & 1 since U / S is even); the < U leftover tiles run one runtime-indexed copy.
+    constexpr int U = 2 * S;
+    auto step = [&](auto stg, auto buf, auto st1, auto buf1, uint32_t par1, auto maytail_c, int it) {
+      if (it > 0) phaseC(buf1);  // tile i - 1 used buffer (i - 1) & 1 = buf ^ 1
+      phaseB(stg, buf, maytail_c, it);
+      if (it + 1 < ntiles) {
+        mbar_wait(&full[int(st1)], par1);
+        phaseA(st1, buf1);
+      }
+      __syncthreads();  // ---- S_mean(i+1), P(i) and the split vmean(i) complete; stage i % S is free
+      if (tid == 0 && it + S < ntiles) {
+        issue(int(stg));
+        if (it + S + 1 < ntiles) cur_page = pt[cur_pg];
+      }
+    };
+    auto stepJ = [&](auto j_c, int it) {
+      constexpr int J = decltype(j_c)::value;
+      step(std::integral_constant<int, J % S>{}, std::integral_constant<int, J & 1>{},
+           std::integral_constant<int, (J + 1) % S>{}, std::integral_constant<int, (J + 1) & 1>{},
+           uint32_t(((J + 1) / S) & 1), std::false_type{}, it);
+    };
+    __syncthreads();  // the QA staging (aliased onto the S_mean buffers) is in TMEM in every warp
+    if (ntiles > 0) {
+      mbar_wait(&full[0], 0u);
+      phaseA(I0{}, I0{});
+    }
+    __syncthreads();
+    const int nfull = (t_end - t_begin) / TT;  // tiles with TT valid tokens (only the last may be partial)
+    int it = 0;
+    for (; it + U <= nfull; it += U) {
+      stepJ(std::integral_constant<int, 0>{}, it);
+      stepJ(std::integral_constant<int, 1>{}, it + 1);
+      stepJ(std::integral_constant<int, 2>{}, it + 2);
+      stepJ(std::integral_constant<int, 3>{}, it + 3);
+      if constexpr (U == 6) {
+        stepJ(std::integral_constant<int, U == 6 ? 4 : 0>{}, it + 4);
+        stepJ(std::integral_constant<int, U == 6 ? 5 : 0>{}, it + 5);
+      }
+    }
+    int st = 0;  // leftover tiles: it is a multiple of U here, so tile it sits in stage 0 at parity 0
+    uint32_t par = 0u;
+    auto step_rt = [&](auto maytail_c, int it) {
+      const int st1 = st + 1 == S ? 0 : st + 1;
+      const uint32_t par1 = st + 1 == S ? par ^ 1u : par;
+      step(st, it & 1, st1, (it & 1) ^ 1, par1, maytail_c, it);
+      st = st1;
+      par = par1;
+    };
+    for (; it < nfull; ++it) step_rt(std::false_type{}, it);
+    if (it < ntiles) step_rt(std::true_type{}, it);
+    if (ntiles > 0) phaseC((ntiles - 1) & 1);
   }
 
   // ------------------------------------------------------------------ epilogue
@@ -945,7 +1059,7 @@ bool v8_supported(const tada_page_layout& L, int Hq) {
 
 template <int BITS, int HQ>
 static int launch_v8_t(const AttnArgs& a, int batch, cudaStream_t st) {
-  constexpr v8::Plan pl = v8::make_plan(BITS * 128 / 8, HQ);
+  constexpr v8::Plan pl = v8::make_plan(BITS * 128 / 8, HQ, v8::v8_pipe(BITS, HQ));  // the kernel's own plan
   if constexpr (!pl.ok) {
     return fail(TADA_ERR_CONFIG, "decode_attn_v8: geometry does not fit two stages");
   } else {
