@@ -856,7 +856,7 @@ static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool,
   int rc;
   if (fast) {
     rc = (mode != 3 && v8_supported(*layout, num_q_heads)) ? launch_v8(a, batch, st) : launch_fast(a, batch, st);
-    if (rc == TADA_OK) rc = launch_combine_residual(a, batch, st);
+    if (rc == TADA_OK && a.diag != 3) rc = launch_combine_residual(a, batch, st);  // diag 3: K2 alone (timing only)
     return rc;
   } else if (exact_smem_bytes(*layout, num_q_heads) && combine_residual_ok(a)) {
     rc = launch_exact(a, batch, st);  // staged f32 kernel over the compressed tokens; K3 the residual + merge

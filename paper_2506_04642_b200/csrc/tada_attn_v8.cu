@@ -73,6 +73,12 @@ constexpr int kBudget = 113 * 1024;  // two CTAs per SM
 #define TADA_V8_TMEM_OM 1  // park the PV mean accumulators in TMEM between tiles
 #endif
 constexpr int MAXS = TADA_V8_MAXS;
+#ifndef TADA_V8_ORDER
+#define TADA_V8_ORDER 0  // pipelined interval order: 0 = C, B, A; 1 = the same with A's loads first; 2 = C, A, B
+#endif
+#ifndef TADA_V8_EARLYWAIT
+#define TADA_V8_EARLYWAIT 0  // pipelined: wait for the next tile's stage at the start of the interval
+#endif
 #ifndef TADA_V8_PIPE_S3
 #define TADA_V8_PIPE_S3 1  // the pipelined plan takes a third stage where it fits
 #endif  // deepest TMA ring (2 or 3 stages)
@@ -478,15 +484,26 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
   using I0 = std::integral_constant<int, 0>;
   using I1 = std::integral_constant<int, 1>;
   // ------------------------------------------------------------ A: QK mean piece -> S_mean plane qd
-  auto phaseA = [&](auto stage_c, auto buf_c) {
+  struct KMean {
+    float4 x0, x1;  // this thread's kmean B-fragment values (k-steps 0 and 1), f32
+  };
+  auto loadA = [&](auto stage_c) {
     const int ST = int(stage_c) * SB;
-    const int SMO = int(buf_c) * pl.sm_stride;
 #if TADA_V8_OFTM >= 2
-    float ofa[4];
-    tmem_ld<4>(tof2, ofa);
+    float ofa[2];
+    tmem_ld<2>(tof2, ofa);
     tmem_wait_ld();
     const int oX0 = __float_as_int(ofa[0]), oX1 = __float_as_int(ofa[1]);
-    const int oQA = __float_as_int(ofa[2]), oSW = __float_as_int(ofa[3]);
+#endif
+    return KMean{sh<float4>(smem, ST + oX0), sh<float4>(smem, ST + oX1)};
+  };
+  auto phaseA = [&](auto buf_c, const KMean& km) {
+    const int SMO = int(buf_c) * pl.sm_stride;
+#if TADA_V8_OFTM >= 2
+    float ofa[2];
+    tmem_ld<2>(tof2 + 2, ofa);
+    tmem_wait_ld();
+    const int oQA = __float_as_int(ofa[0]), oSW = __float_as_int(ofa[1]);
 #endif
     float acc[MT][4];
 #pragma unroll
@@ -494,7 +511,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
     uint32_t hb[2][2], lb[2][2];  // B fragments (hi, lo) of both k-steps
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks) {
-      const float4 x = sh<float4>(smem, ST + (ks ? oX1 : oX0));
+      const float4 x = ks ? km.x1 : km.x0;
       split_h2(x.x, x.y, hb[ks][0], lb[ks][0]);
       split_h2(x.z, x.w, hb[ks][1], lb[ks][1]);
     }
@@ -562,6 +579,29 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
 #endif
 #endif
 
+    // ------------------------------------------------------------ re-centre the PV code accumulators
+    // oc holds bias * Σp' + Σp'·code: the biased f16 codes make |oc| up to ~40x the code term (2-bit), and the
+    // tensor core's f32 accumulation truncates (rounds toward zero) relative to |oc| on every MMA, so over
+    // thousands of tiles the error grows systematically (measured 4.2e-3 max-abs at 128k tokens, 2-bit).
+    // Every RC tiles the bias part (bias * column sums of the f16 P' the MMAs saw) is removed exactly enough
+    // in f32 and the running Σp' restarts, so each truncation acts on the small code term only.
+    if constexpr (TADA_V8_RECENTER > 0) {
+      if (it > 0 && (it & (TADA_V8_RECENTER - 1)) == 0) {  // after every RC tiles (placed before this tile's
+        // QK work so the PV code term, the vmean split and phase A form one scheduling block)
+        float s = sp_run;
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        const float s0 = __shfl_sync(0xffffffffu, s, 8 * c), s1 = __shfl_sync(0xffffffffu, s, 8 * c + 4);
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+          oc[mt][0] = fmaf(-pv_bias<BITS>(mt, 0), s0, oc[mt][0]);
+          oc[mt][1] = fmaf(-pv_bias<BITS>(mt, 0), s1, oc[mt][1]);
+          oc[mt][2] = fmaf(-pv_bias<BITS>(mt, 1), s0, oc[mt][2]);
+          oc[mt][3] = fmaf(-pv_bias<BITS>(mt, 1), s1, oc[mt][3]);
+        }
+        sp_run = 0.f;
+      }
+    }
     // ------------------------------------------------------------ c: QK code term (q on M) + logits
     float x[2][2];  // logits (log2 units) of q head h*G + r for tokens 8nt + 2c + e
     {
@@ -774,28 +814,6 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
         mma(oc[mt], af, bq0, bq1);
       }
     }
-    // ------------------------------------------------------------ re-centre the PV code accumulators
-    // oc holds bias * Σp' + Σp'·code: the biased f16 codes make |oc| up to ~40x the code term (2-bit), and the
-    // tensor core's f32 accumulation truncates (rounds toward zero) relative to |oc| on every MMA, so over
-    // thousands of tiles the error grows systematically (measured 4.2e-3 max-abs at 128k tokens, 2-bit).
-    // Every RC tiles the bias part (bias * column sums of the f16 P' the MMAs saw) is removed exactly enough
-    // in f32 and the running Σp' restarts, so each truncation acts on the small code term only.
-    if constexpr (TADA_V8_RECENTER > 0) {
-      if ((it & (TADA_V8_RECENTER - 1)) == TADA_V8_RECENTER - 1) {
-        float s = sp_run;
-        s += __shfl_xor_sync(0xffffffffu, s, 1);
-        s += __shfl_xor_sync(0xffffffffu, s, 2);
-        const float s0 = __shfl_sync(0xffffffffu, s, 8 * c), s1 = __shfl_sync(0xffffffffu, s, 8 * c + 4);
-#pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-          oc[mt][0] = fmaf(-pv_bias<BITS>(mt, 0), s0, oc[mt][0]);
-          oc[mt][1] = fmaf(-pv_bias<BITS>(mt, 0), s1, oc[mt][1]);
-          oc[mt][2] = fmaf(-pv_bias<BITS>(mt, 1), s0, oc[mt][2]);
-          oc[mt][3] = fmaf(-pv_bias<BITS>(mt, 1), s1, oc[mt][3]);
-        }
-        sp_run = 0.f;
-      }
-    }
     // ------------------------------------------------------------ this warp's share of the vmean split
     {  // token vt, d = 8vu .. 8vu+7 -> f16 hi / lo rows [tok][d] (16-B chunk vu at vu ^ (vt & 7))
       const float4 x0 = sh<float4>(smem, ST + oV0), x1 = sh<float4>(smem, ST + oV1);
@@ -902,7 +920,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
         }
         return;
       }
-      phaseA(stage_c, I0{});
+      phaseA(I0{}, loadA(stage_c));
       __syncthreads();  // ---- barrier 1: S_mean complete; the previous tile's P and split vmean are consumed
       phaseB(stage_c, I0{}, std::true_type{}, it);
       __syncthreads();  // ---- barrier 2: P, corr and the split vmean complete; this tile's stage is free
@@ -927,12 +945,31 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
     // buffer J & 1, parity (J / S) & 1 since U / S is even); the < U leftover tiles run one runtime-indexed copy.
     constexpr int U = 2 * S;
     auto step = [&](auto stg, auto buf, auto st1, auto buf1, uint32_t par1, auto maytail_c, int it) {
+#if TADA_V8_ORDER == 1  // the next tile's kmean loads issued first, consumed after phase B
+      KMean km{};
+      if (it + 1 < ntiles) {
+        mbar_wait(&full[int(st1)], par1);
+        km = loadA(st1);
+      }
+      if (it > 0) phaseC(buf1);  // tile i - 1 used buffer (i - 1) & 1 = buf ^ 1
+      phaseB(stg, buf, maytail_c, it);
+      if (it + 1 < ntiles) phaseA(buf1, km);
+#elif TADA_V8_ORDER == 2  // C, A, B
+      if (it > 0) phaseC(buf1);
+      if (it + 1 < ntiles) {
+        mbar_wait(&full[int(st1)], par1);
+        phaseA(buf1, loadA(st1));
+      }
+      phaseB(stg, buf, maytail_c, it);
+#else
+      if (TADA_V8_EARLYWAIT && it + 1 < ntiles) mbar_wait(&full[int(st1)], par1);
       if (it > 0) phaseC(buf1);  // tile i - 1 used buffer (i - 1) & 1 = buf ^ 1
       phaseB(stg, buf, maytail_c, it);
       if (it + 1 < ntiles) {
-        mbar_wait(&full[int(st1)], par1);
-        phaseA(st1, buf1);
+        if (!TADA_V8_EARLYWAIT) mbar_wait(&full[int(st1)], par1);
+        phaseA(buf1, loadA(st1));
       }
+#endif
       __syncthreads();  // ---- S_mean(i+1), P(i) and the split vmean(i) complete; stage i % S is free
       if (tid == 0 && it + S < ntiles) {
         issue(int(stg));
@@ -948,7 +985,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
     __syncthreads();  // the QA staging (aliased onto the S_mean buffers) is in TMEM in every warp
     if (ntiles > 0) {
       mbar_wait(&full[0], 0u);
-      phaseA(I0{}, I0{});
+      phaseA(I0{}, loadA(I0{}));
     }
     __syncthreads();
     const int nfull = (t_end - t_begin) / TT;  // tiles with TT valid tokens (only the last may be partial)
