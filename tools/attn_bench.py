@@ -21,13 +21,14 @@ def main():
     ap.add_argument("--tokens", type=int, default=32768)
     ap.add_argument("--hq", type=int, default=32)
     ap.add_argument("--heads", type=int, default=8)
+    ap.add_argument("--dim", type=int, default=128)
     ap.add_argument("--mode", type=int, default=2)
     ap.add_argument("--splits", type=int, default=0)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--layers", type=int, default=4, help="distinct layer pools cycled (defeats L2)")
     ap.add_argument("--reps", type=int, default=5, help="timed repetitions; the median is reported")
     args = ap.parse_args()
-    B, T, H, D = args.batch, args.tokens, args.heads, 128
+    B, T, H, D = args.batch, args.tokens, args.heads, args.dim
     store = tk.PagedKVCache(args.layers, H, D, [args.bits] * args.layers, 128, batch=B, page_tokens=64,
                             max_tokens=T + 130, shuffle_pages=True)
     g = torch.Generator(device="cuda")
@@ -58,7 +59,7 @@ def main():
     c, r = store.lengths(0)
     tokb = 4 * D + H * (D * args.bits // 8) + 8 * H
     alg = B * (2 * c * tokb + 2 * r * H * D * 2 + 2 * args.hq * D * 2)
-    print(json.dumps({"bits": args.bits, "batch": B, "tokens": c + r, "hq": args.hq, "mode": args.mode,
+    print(json.dumps({"bits": args.bits, "batch": B, "tokens": c + r, "hq": args.hq, "heads": H, "dim": D, "mode": args.mode,
                       "splits": splits, "ms": ms, "ms_min": times[0], "alg_GBps": alg / ms / 1e6}))
 
 
