@@ -79,6 +79,30 @@ __device__ __forceinline__ float group_scale(float mn, float mx, int bits) {
   return s;
 }
 
+// group_scale with top = f32(f64 min + f64 cmax * f64 s) taken as one f32 FMA: cmax * s is exact in f64
+// (<= 32 significant bits) and the f64 sum is exact while 2^-19 * s <= |min| <= 2^26 * s (the binary exponents
+// then span <= 53 bits) or min == 0, so both are RN32 of the same exact value.  Other groups take the f64
+// sequence.
+__device__ __forceinline__ float group_scale_k1(float mn, float mx, int bits) {
+  if (mx == mn) return 0.f;  // quant.py:158
+  const double cmax = double((1 << bits) - 1);
+  const float cmaxf = float((1 << bits) - 1);
+  const double ycm = bits == 2 ? 1.0 / 3.0 : (bits == 4 ? 1.0 / 15.0 : (bits == 8 ? 1.0 / 255.0 : 1.0 / cmax));
+  const double mn64 = double(mn);
+  float s = __double2float_rn(div_cmax(__dsub_rn(double(mx), mn64), cmax, ycm));
+  const float am = fabsf(mn);
+  const bool fma_ok = mn == 0.f || (am >= s * 0x1p-19f && am <= s * 0x1p26f);
+#pragma unroll 1
+  for (int it = 0; it < 8; ++it) {
+    if (s == 0.f) break;  // np.where(scale == 0, 0, refined): a fixed point
+    const float top = fma_ok ? __fmaf_rn(cmaxf, s, mn) : __double2float_rn(__dadd_rn(mn64, __dmul_rn(cmax, double(s))));
+    const float r = __double2float_rn(div_cmax(__dsub_rn(double(top), mn64), cmax, ycm));
+    if (__float_as_uint(r) == __float_as_uint(s)) break;
+    s = r;
+  }
+  return s;
+}
+
 // code = clip(floor(f64(f64 x - f64 min) / f64 s + 0.5), 0, cmax)  (quant.py:169-173).
 // Fast path: an f32 estimate decides whenever it lies clearly away from a rounding
 // boundary (|err| <= ~2^-21.9 * y vs margin 2^-19 * y); otherwise the exact fp64

@@ -515,10 +515,207 @@ __device__ __forceinline__ float redux_max(float v) {
 // ring with cp.async.bulk + an mbarrier per slot, so the next rows are in flight while the
 // current one is quantized (the kernel is otherwise latency-bound on its global loads).
 constexpr int K1_RING = 3;
+#ifndef TADA_K1_RECOMP
+#define TADA_K1_RECOMP 0  // recompute nd = x - mean from the packed row on each use instead of holding it
+#endif
 #ifndef TADA_K1_PAGE_CACHE
 #define TADA_K1_PAGE_CACHE 1  // page base pointer reloaded on page change only
 #endif
 __device__ __forceinline__ uint32_t k1_su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+
+// K1 row of one token as held by lane l: elements 4l .. 4l+3 of each of the 8 heads.  bf16 rows stay packed:
+// cvt.f64.bf16 (F2F.F64.BF16) and the mixed-precision sub.f32.bf16 (FHADD) read the halves directly.
+struct K1RowBF16 {
+  uint32_t w[8][2];
+  __device__ __forceinline__ void load(const __nv_bfloat16* p) {
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      const uint2 x = *reinterpret_cast<const uint2*>(p + h * 128);
+      w[h][0] = x.x;
+      w[h][1] = x.y;
+    }
+  }
+  __device__ __forceinline__ double f64(int h, int k) const {
+    double r;
+    if (k & 1) asm("{.reg .b16 l, u; mov.b32 {l, u}, %1; cvt.f64.bf16 %0, u;}" : "=d"(r) : "r"(w[h][k >> 1]));
+    else asm("{.reg .b16 l, u; mov.b32 {l, u}, %1; cvt.f64.bf16 %0, l;}" : "=d"(r) : "r"(w[h][k >> 1]));
+    return r;
+  }
+  __device__ __forceinline__ float minus(int h, int k, float m) const {  // RN(x - m)
+    float r;
+    if (k & 1) asm("{.reg .b16 l, u; mov.b32 {l, u}, %2; sub.rn.f32.bf16 %0, u, %1;}" : "=f"(r) : "f"(m), "r"(w[h][k >> 1]));
+    else asm("{.reg .b16 l, u; mov.b32 {l, u}, %2; sub.rn.f32.bf16 %0, l, %1;}" : "=f"(r) : "f"(m), "r"(w[h][k >> 1]));
+    return r;
+  }
+};
+struct K1RowF32 {
+  float v[8][4];
+  __device__ __forceinline__ void load(const float* p) {
+#pragma unroll
+    for (int h = 0; h < 8; ++h) load4(p + h * 128, v[h]);
+  }
+  __device__ __forceinline__ void load(const __nv_bfloat16* p) {
+#pragma unroll
+    for (int h = 0; h < 8; ++h) load4(p + h * 128, v[h]);
+  }
+  __device__ __forceinline__ double f64(int h, int k) const { return double(v[h][k]); }
+  __device__ __forceinline__ float minus(int h, int k, float m) const { return __fsub_rn(v[h][k], m); }
+};
+template <typename T> struct K1Row { using type = K1RowF32; };
+template <> struct K1Row<__nv_bfloat16> { using type = K1RowBF16; };
+
+// negated deviations held in registers, or recomputed from the packed row on every use (TADA_K1_RECOMP)
+struct K1NdRegs {
+  float v[8][4];
+  __device__ __forceinline__ float operator()(int h, int k) const { return v[h][k]; }
+};
+template <typename Row>
+struct K1NdLazy {
+  Row x;
+  float m[4];
+  __device__ __forceinline__ float operator()(int h, int k) const { return x.minus(h, k, m[k]); }
+};
+
+// mean: f64 sequential head sum from +0.0, /H (exact for H = 8), RN to f32 (cache.py:109)
+template <typename Row>
+__device__ __forceinline__ void k1_mean(const Row& x, float (&mean)[4], bool& big) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    double acc = 0.0;
+#pragma unroll
+    for (int h = 0; h < 8; ++h) acc = __dadd_rn(acc, x.f64(h, k));
+    mean[k] = __double2float_rn(__dmul_rn(acc, 0.125));
+    big |= !(fabsf(mean[k]) < 32768.f);
+  }
+}
+// ... and nd = RN(x - mean)
+template <typename Row>
+__device__ __forceinline__ void k1_mean_dev(const Row& x, float (&mean)[4], float (&nd)[8][4], bool& big) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    double acc = 0.0;
+#pragma unroll
+    for (int h = 0; h < 8; ++h) acc = __dadd_rn(acc, x.f64(h, k));
+    mean[k] = __double2float_rn(__dmul_rn(acc, 0.125));
+    // any non-finite input makes its column's sum non-finite; |mean| >= 2^15 leaves the f16 range of K2
+    big |= !(fabsf(mean[k]) < 32768.f);
+  }
+#pragma unroll
+  for (int h = 0; h < 8; ++h)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) nd[h][k] = x.minus(h, k, mean[k]);
+}
+
+// The two bracket ends of 4 codes of one group, packed like pack_codes (LSB-first): t = RN(u * m + 2^23) holds
+// RN(u * m) in its low mantissa bits, and the bits above the code field are identical for both ends.
+template <int BITS, typename ND>
+__device__ __forceinline__ void k1_bracket(const ND& nd, int h, float ndmax, float ml, float mh, uint32_t& wl,
+                                           uint32_t& wh) {
+  uint32_t tl[4], th[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float u = __fsub_rn(ndmax, nd(h, k));  // RN(dev - min): dev = -nd, min = -ndmax (zero signs aside)
+    tl[k] = __float_as_uint(__fmaf_rn(u, ml, 8388608.f));
+    th[k] = __float_as_uint(__fmaf_rn(u, mh, 8388608.f));
+  }
+  if (BITS == 8) {
+    wl = prmt(prmt(tl[0], tl[1], 0x0040u), prmt(tl[2], tl[3], 0x0040u), 0x5410u);
+    wh = prmt(prmt(th[0], th[1], 0x0040u), prmt(th[2], th[3], 0x0040u), 0x5410u);
+  } else {  // code fields < 2^BITS: shifted adds keep the garbage above bit 4 * BITS
+    wl = (((tl[3] << BITS) + tl[2]) << (2 * BITS)) + ((tl[1] << BITS) + tl[0]);
+    wh = (((th[3] << BITS) + th[2]) << (2 * BITS)) + ((th[1] << BITS) + th[0]);
+  }
+}
+template <int BITS>
+__device__ __forceinline__ void k1_store_codes(uint8_t* dst, uint32_t w) {
+  if (BITS == 8) *reinterpret_cast<uint32_t*>(dst) = w;
+  else if (BITS == 4) *reinterpret_cast<uint16_t*>(dst) = uint16_t(w);
+  else *dst = uint8_t(w);
+}
+
+// One token of one side after its rows were read: group min / max, scales, codes and stores (K1 fast path).
+// ND yields the negated deviations nd(h, k) = RN(x - mean) of the lane's elements, from registers or recomputed.
+template <int BITS, typename ND>
+__device__ __forceinline__ void k1_token(const AppendArgs& a, const ND& nd, const float (&mean)[4], bool big,
+                                         uint8_t* page, int row, int side, int lane) {
+  constexpr int H = 8, D = 128, GB = D * BITS / 8;
+  if (__any_sync(0xffffffffu, big)) {  // rare: a non-finite input, or a mean beyond K2's f16 range
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      bad |= !finite(mean[k]);
+      note_mean(a.range, mean[k]);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0 && a.err) atomicOr(a.err, 1);
+  }
+  // group min / max of dev = -nd: one CREDUX each per head; +0.0 - y keeps the reference's +0.0 for zeros
+  float ndmax[H];  // max of nd = -(min of dev) per head (uniform across the warp)
+  float my_mn = 0.f, my_mx = 0.f;
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    ndmax[h] = redux_max(fmaxf(fmaxf(nd(h, 0), nd(h, 1)), fmaxf(nd(h, 2), nd(h, 3))));
+    const float lo = redux_min(fminf(fminf(nd(h, 0), nd(h, 1)), fminf(nd(h, 2), nd(h, 3))));
+    if (lane == h) {
+      my_mn = ndmax[h];
+      my_mx = lo;
+    }
+  }
+  my_mn = __fsub_rn(0.f, my_mn);  // group min / max of dev
+  my_mx = __fsub_rn(0.f, my_mx);
+  // Lane h < 8: group h's f64 scale with the reference's refinement, then the bracket multipliers.
+  // Codes (quant.py:169-173): code = floor(W + 1/2), W = (dev - min) / s in f64.  With u = RN32(dev - min),
+  // r = RN32(1 / s) and the multipliers r * (1 -+ 2^-22) rounded once more (relative error 2^-24 each, so
+  // 3 * 2^-24 < 2^-22 in total), u * r * (1 -+ 2^-22) lies strictly below / above W.  The two FFMAs t = RN(u * m + 2^23) round
+  // both bracket ends to integers in t's low mantissa bits; when they agree on every code of a group the
+  // common value is floor(W + 1/2) (W sits strictly inside (r - 1/2, r + 1/2)), otherwise the group is
+  // recomputed with the exact f64 half-up sequence (quant_code), which also decides every exact tie.
+  float my_s = 0.f, my_lo = 0.f, my_hi = 0.f;
+  bool special = false;
+  if (lane < H) {
+    my_s = group_scale_k1(my_mn, my_mx, BITS);
+    if (my_s >= 0x1p-100f && my_s <= 0x1p100f) {
+      const float r = __frcp_rn(my_s);
+      my_lo = __fmul_rn(r, 1.f - 0x1p-22f);
+      my_hi = __fmul_rn(r, 1.f + 0x1p-22f);
+    }
+    // no bracket outside [2^-100, 2^100] (codes forced to 0, then redone); scales beyond the f16 range of
+    // attn_fast_kernel are recorded (note_scale)
+    special = (my_s != 0.f && my_lo == 0.f) || my_s >= 256.f;
+  }
+  *reinterpret_cast<float4*>(reinterpret_cast<float*>(page + a.L.off_mean[side]) + row * D + 4 * lane) =
+      make_float4(mean[0], mean[1], mean[2], mean[3]);
+  if (lane < H)
+    *reinterpret_cast<float2*>(page + a.L.off_meta[side] + (row * H + lane) * 8) = make_float2(my_s, my_mn);
+  uint8_t* codes = page + a.L.off_codes[side] + row * (H * GB) + lane * (BITS / 2);
+  uint32_t diff = 0;
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    const float ml = __shfl_sync(0xffffffffu, my_lo, h), mh = __shfl_sync(0xffffffffu, my_hi, h);
+    uint32_t wl, wh;
+    k1_bracket<BITS>(nd, h, ndmax[h], ml, mh, wl, wh);
+    diff |= wl ^ wh;  // the constant bits above the fields cancel
+    k1_store_codes<BITS>(codes + h * GB, wl);
+  }
+  if (__any_sync(0xffffffffu, diff != 0 || special)) {  // rare: a code near a rounding boundary, or a special scale
+    if (special && my_s >= 256.f) note_scale(a.range, my_s);
+    constexpr int CMAX = (1 << BITS) - 1;
+#pragma unroll
+    for (int h = 0; h < H; ++h) {  // unrolled: nd stays in registers
+      const float ml = __shfl_sync(0xffffffffu, my_lo, h), mh = __shfl_sync(0xffffffffu, my_hi, h);
+      const float sh = __shfl_sync(0xffffffffu, my_s, h);
+      const bool sp = __shfl_sync(0xffffffffu, special && (my_s != 0.f && my_lo == 0.f), h);
+      uint32_t wl, wh;
+      k1_bracket<BITS>(nd, h, ndmax[h], ml, mh, wl, wh);
+      if (!__any_sync(0xffffffffu, wl != wh) && !sp) continue;
+      uint32_t w = 0;
+      if (sh != 0.f)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w |= quant_code(-nd(h, k), __fsub_rn(0.f, ndmax[h]), sh, 0.f, false, CMAX) << (BITS * k);
+      k1_store_codes<BITS>(codes + h * GB, w);
+    }
+  }
+}
 
 template <typename T, int BITS, int MINB, bool ROPE>
 __global__ void __launch_bounds__(256, MINB) quant_append_fast_kernel(AppendArgs a, int tpw, int page_shift) {
@@ -537,19 +734,23 @@ __global__ void __launch_bounds__(256, MINB) quant_append_fast_kernel(AppendArgs
   const int64_t c0 = a.dst_start[b] + offset;
   const T* src_seq = reinterpret_cast<const T*>(a.src[side]) + int64_t(b) * a.src_seq_stride * (H * D);
   const int P = a.L.page_tokens;
-  auto fetch = [&](int64_t i, int slot) {  // lane 0
-    const uint32_t bar = k1_su32(&bars[slot]);
+  // lane 0 copies the rows of the next token (fsrc, advanced per copy) into ring slot `slot`
+  const T* fsrc = src_seq + i_begin * (H * D);
+  const uint32_t ring_s = k1_su32(ring), bars_s = k1_su32(bars);
+  auto fetch = [&](int slot) {
+    const uint32_t bar = bars_s + 8 * slot;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(ROWB) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     k1_su32(ring + slot * (H * D))),
-                 "l"(src_seq + i * (H * D)), "r"(ROWB), "r"(bar)
+    asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     ring_s + slot * ROWB),
+                 "l"(fsrc), "r"(ROWB), "r"(bar)
                  : "memory");
+    fsrc += H * D;
   };
   if (lane == 0) {
     for (int k = 0; k < K1_RING; ++k)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(k1_su32(&bars[k])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int k = 0; k < K1_RING - 1 && i_begin + k < i_end; ++k) fetch(i_begin + k, k);
+    for (int k = 0; k < K1_RING - 1 && i_begin + k < i_end; ++k) fetch(k);
   }
   __syncwarp();
   // ring cursor (slot, phase parity) and page cursor (page index, row) advance incrementally
@@ -573,139 +774,50 @@ __global__ void __launch_bounds__(256, MINB) quant_append_fast_kernel(AppendArgs
         "r"(parity)
         : "memory");
     const T* src = ring + slot * (H * D) + 4 * lane;
-    float x[H][4];
-#pragma unroll
-    for (int h = 0; h < H; ++h) load4(src + h * D, x[h]);
-    if (ROPE && side == 0) {  // rotate the keys in registers (tensor.py:84-89); lane l holds pairs 2l, 2l+1
-      int p = a.positions[int64_t(b) * a.pos_stride + i];
-      if (p < 0 || p >= a.rope_rows) {  // the host validates positions; this guards device-side ones
-        if (lane == 0 && a.err) atomicOr(a.err, 2);
-        p = 0;
+    // every lane has its rows in registers: refill the slot freed last
+    auto refill = [&]() {
+      __syncwarp();
+      if (lane == 0 && i + K1_RING - 1 < i_end) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        fetch(fslot);
       }
-      const float4 cs = *reinterpret_cast<const float4*>(a.rope_cs + int64_t(p) * D + 4 * lane);
-#pragma unroll
-      for (int h = 0; h < H; ++h) {
-        const float e0 = x[h][0], o0 = x[h][1], e1 = x[h][2], o1 = x[h][3];
-        x[h][0] = __fsub_rn(__fmul_rn(e0, cs.x), __fmul_rn(o0, cs.y));
-        x[h][1] = __fadd_rn(__fmul_rn(e0, cs.y), __fmul_rn(o0, cs.x));
-        x[h][2] = __fsub_rn(__fmul_rn(e1, cs.z), __fmul_rn(o1, cs.w));
-        x[h][3] = __fadd_rn(__fmul_rn(e1, cs.w), __fmul_rn(o1, cs.z));
-      }
-    }
-    // mean: f64 sequential head sum from +0.0, /H (exact for H = 8), RN to f32
-    float mean[4];
+      fslot = fslot == K1_RING - 1 ? 0 : fslot + 1;
+    };
     bool big = false;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      double acc = 0.0;
-#pragma unroll
-      for (int h = 0; h < H; ++h) acc = __dadd_rn(acc, double(x[h][k]));
-      mean[k] = __double2float_rn(__dmul_rn(acc, 0.125));
-      // any non-finite input makes its column's sum non-finite; |mean| >= 2^15 leaves the f16 range of K2
-      big |= !(fabsf(mean[k]) < 32768.f);
-    }
-    // every lane has its rows in registers (the mean consumed them): refill the slot freed last
-    __syncwarp();
-    if (lane == 0 && i + K1_RING - 1 < i_end) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      fetch(i + K1_RING - 1, fslot);
-    }
-    fslot = fslot == K1_RING - 1 ? 0 : fslot + 1;
-    if (__any_sync(0xffffffffu, big)) {  // rare: a non-finite input, or a mean beyond K2's f16 range
-      bool bad = false;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        bad |= !finite(mean[k]);
-        note_mean(a.range, mean[k]);
-      }
-      if (__any_sync(0xffffffffu, bad) && lane == 0 && a.err) atomicOr(a.err, 1);
-    }
-    float mnh[H], mxh[H];
-#pragma unroll
-    for (int h = 0; h < H; ++h) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) x[h][k] = __fsub_rn(mean[k], x[h][k]);
-      mnh[h] = redux_min(fminf(fminf(x[h][0], x[h][1]), fminf(x[h][2], x[h][3])));
-      mxh[h] = redux_max(fmaxf(fmaxf(x[h][0], x[h][1]), fmaxf(x[h][2], x[h][3])));
-    }
-    float my_mn = 0.f, my_mx = 0.f;
-#pragma unroll
-    for (int h = 0; h < H; ++h)
-      if (lane == h) {
-        my_mn = mnh[h];
-        my_mx = mxh[h];
-      }
-    float my_s = 0.f, my_inv = 0.f;
-    if (lane < H) {
-      my_s = group_scale(my_mn, my_mx, BITS);
-      my_inv = (my_s >= 0x1p-100f && my_s <= 0x1p100f) ? __frcp_rn(my_s) : 0.f;
-    }
-#if !TADA_K1_PAGE_CACHE
-    uint8_t* page = a.pool + int64_t(pt[pg]) * a.L.page_bytes;
-#endif
-    *reinterpret_cast<float4*>(reinterpret_cast<float*>(page + a.L.off_mean[side]) + row * D + 4 * lane) =
-        make_float4(mean[0], mean[1], mean[2], mean[3]);
-    if (lane < H)
-      *reinterpret_cast<float2*>(page + a.L.off_meta[side] + (row * H + lane) * 8) = make_float2(my_s, my_mn);
-    uint8_t* codes = page + a.L.off_codes[side] + row * (H * GB) + lane * (BITS / 2);
-    // Fast path for every group at once (s == 0 has inv == 0: codes 0); one vote per token.
-    // P = u * inv with u = f32(dev - min), inv = RN(1/s) is within 2^-23 * P (relative) of the reference's
-    // f64 quotient W = (dev - min) / s, and P <= cmax + 1.  t = RN(P + 2^23) gives r = RN(P); e = P - r
-    // is recovered by one FMA.  Whenever |e| < 1/2 - margin with margin = 2^-21 * (cmax + 1) (4x the
-    // error bound) floor(W + 1/2) = r; otherwise the group is recomputed with the exact fp64 half-up
-    // sequence (quant_code), which also decides every exact tie like the reference.
-    constexpr float MARGIN = 0x1p-21f * float(1 << BITS);
-    uint32_t word[H];
-    uint32_t unsafe = 0;
-#pragma unroll
-    for (int h = 0; h < H; ++h) {
-      const float inv = __shfl_sync(0xffffffffu, my_inv, h);
-      const float mn = mnh[h];
-      float r[4], e[4];
-      uint32_t tb[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float u = __fsub_rn(x[h][k], mn);
-        const float t = __fmaf_rn(u, inv, 8388608.f);
-        r[k] = __fsub_rn(t, 8388608.f);
-        e[k] = __fmaf_rn(u, inv, -r[k]);
-        tb[k] = __float_as_uint(t);
-      }
-      const float emax = fmaxf(fmaxf(fabsf(e[0]), fabsf(e[1])), fmaxf(fabsf(e[2]), fabsf(e[3])));
-      unsafe |= uint32_t(emax >= 0.5f - MARGIN) << h;
-      if (BITS == 8) {
-        word[h] = prmt(prmt(tb[0], tb[1], 0x0040u), prmt(tb[2], tb[3], 0x0040u), 0x5410u);
-      } else {  // exact small-integer arithmetic in f32, read back through the magic add
-        constexpr float M1 = float(1 << BITS), M2 = M1 * M1, M3 = M2 * M1;
-        const float v = fmaf(r[3], M3, fmaf(r[2], M2, fmaf(r[1], M1, r[0])));
-        word[h] = __float_as_uint(__fadd_rn(v, 8388608.f));
-      }
-    }
-    // scales outside [2^-100, 2^100] have no fast path (inv == 0 with s != 0)
-    if (lane < H && my_inv == 0.f && my_s != 0.f) unsafe |= 1u << lane;
-    if (lane < H && my_s >= 256.f) unsafe |= 1u << 16;  // a scale beyond attn_fast_kernel's f16 range (note_scale)
-    const uint32_t redo = __reduce_or_sync(0xffffffffu, unsafe);
-    if (redo) {  // rare: a group within 2^-12 of a rounding boundary -> exact fp64 half-up (quant_code)
-      if ((redo >> 16) && lane < H) note_scale(a.range, my_s);
-      constexpr int CMAX = (1 << BITS) - 1;
-#pragma unroll
-      for (int h = 0; h < H; ++h) {
-        const float sh = __shfl_sync(0xffffffffu, my_s, h);
-        if ((redo >> h) & 1u) {
-          uint32_t w = 0;
-          if (sh != 0.f)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) w |= quant_code(x[h][k], mnh[h], sh, 0.f, false, CMAX) << (BITS * k);
-          word[h] = w;
+    if (!ROPE && TADA_K1_RECOMP) {
+      K1NdLazy<typename K1Row<T>::type> nd;
+      nd.x.load(src);
+      refill();
+      k1_mean(nd.x, nd.m, big);
+      k1_token<BITS>(a, nd, nd.m, big, page, row, side, lane);
+    } else {
+      float mean[4];
+      K1NdRegs nd;  // x - mean = -(mean - x): the negated deviations (dev = -nd exactly, cache.py:110)
+      if (ROPE && side == 0) {  // rotate the keys in registers (tensor.py:84-89); lane l holds pairs 2l, 2l+1
+        K1RowF32 x;
+        x.load(src);
+        int p = a.positions[int64_t(b) * a.pos_stride + i];
+        if (p < 0 || p >= a.rope_rows) {  // the host validates positions; this guards device-side ones
+          if (lane == 0 && a.err) atomicOr(a.err, 2);
+          p = 0;
         }
-      }
-    }
+        const float4 cs = *reinterpret_cast<const float4*>(a.rope_cs + int64_t(p) * D + 4 * lane);
 #pragma unroll
-    for (int h = 0; h < H; ++h) {
-      uint8_t* dst = codes + h * GB;
-      if (BITS == 8) *reinterpret_cast<uint32_t*>(dst) = word[h];
-      else if (BITS == 4) *reinterpret_cast<uint16_t*>(dst) = uint16_t(word[h]);
-      else *dst = uint8_t(word[h]);
+        for (int h = 0; h < H; ++h) {
+          const float e0 = x.v[h][0], o0 = x.v[h][1], e1 = x.v[h][2], o1 = x.v[h][3];
+          x.v[h][0] = __fsub_rn(__fmul_rn(e0, cs.x), __fmul_rn(o0, cs.y));
+          x.v[h][1] = __fadd_rn(__fmul_rn(e0, cs.y), __fmul_rn(o0, cs.x));
+          x.v[h][2] = __fsub_rn(__fmul_rn(e1, cs.z), __fmul_rn(o1, cs.w));
+          x.v[h][3] = __fadd_rn(__fmul_rn(e1, cs.w), __fmul_rn(o1, cs.z));
+        }
+        k1_mean_dev(x, mean, nd.v, big);
+      } else {
+        typename K1Row<T>::type x;
+        x.load(src);
+        k1_mean_dev(x, mean, nd.v, big);
+      }
+      refill();
+      k1_token<BITS>(a, nd, mean, big, page, row, side, lane);
     }
     if (++slot == K1_RING) {
       slot = 0;
