@@ -548,6 +548,18 @@ struct K1RowBF16 {
     else asm("{.reg .b16 l, u; mov.b32 {l, u}, %2; sub.rn.f32.bf16 %0, l, %1;}" : "=f"(r) : "f"(m), "r"(w[h][k >> 1]));
     return r;
   }
+  __device__ __forceinline__ float add_rd(int h, int k, float acc) const {  // RD(x + acc)
+    float r;
+    if (k & 1) asm("{.reg .b16 l, u; mov.b32 {l, u}, %2; add.rm.f32.bf16 %0, u, %1;}" : "=f"(r) : "f"(acc), "r"(w[h][k >> 1]));
+    else asm("{.reg .b16 l, u; mov.b32 {l, u}, %2; add.rm.f32.bf16 %0, l, %1;}" : "=f"(r) : "f"(acc), "r"(w[h][k >> 1]));
+    return r;
+  }
+  __device__ __forceinline__ float add_ru(int h, int k, float acc) const {  // RU(x + acc)
+    float r;
+    if (k & 1) asm("{.reg .b16 l, u; mov.b32 {l, u}, %2; add.rp.f32.bf16 %0, u, %1;}" : "=f"(r) : "f"(acc), "r"(w[h][k >> 1]));
+    else asm("{.reg .b16 l, u; mov.b32 {l, u}, %2; add.rp.f32.bf16 %0, l, %1;}" : "=f"(r) : "f"(acc), "r"(w[h][k >> 1]));
+    return r;
+  }
 };
 struct K1RowF32 {
   float v[8][4];
@@ -561,6 +573,8 @@ struct K1RowF32 {
   }
   __device__ __forceinline__ double f64(int h, int k) const { return double(v[h][k]); }
   __device__ __forceinline__ float minus(int h, int k, float m) const { return __fsub_rn(v[h][k], m); }
+  __device__ __forceinline__ float add_rd(int h, int k, float acc) const { return __fadd_rd(v[h][k], acc); }
+  __device__ __forceinline__ float add_ru(int h, int k, float acc) const { return __fadd_ru(v[h][k], acc); }
 };
 template <typename T> struct K1Row { using type = K1RowF32; };
 template <> struct K1Row<__nv_bfloat16> { using type = K1RowBF16; };
@@ -577,30 +591,56 @@ struct K1NdLazy {
   __device__ __forceinline__ float operator()(int h, int k) const { return x.minus(h, k, m[k]); }
 };
 
-// mean: f64 sequential head sum from +0.0, /H (exact for H = 8), RN to f32 (cache.py:109)
+// mean (cache.py:109): the reference sums the 8 heads in f64 from +0.0, divides by 8 (exact) and rounds to f32.
+// The f64 sum of 8 bf16/f32 values is exact unless their exponents span more than ~28 bits, so the mean is
+// RN32(S) / 8 for the exact sum S.  Two f32 sums rounded down and up bracket S; when they are equal, S is that
+// f32 value (every step was exact) and the mean is S * 0.125 (+0.0 restores the reference's +0.0 for zeros;
+// |S| >= 2^-120 keeps the scaling exact).  Other columns (rare: a wide exponent spread, or non-finite) take the
+// f64 sequence.  This keeps the F2F conversions off the XU pipe, which they saturated.
+template <typename Row>
+__device__ __forceinline__ double k1_col_sum64(const Row& x, int k) {
+  double acc = 0.0;
+#pragma unroll
+  for (int h = 0; h < 8; ++h) acc = __dadd_rn(acc, x.f64(h, k));
+  return acc;
+}
+#ifndef TADA_K1_F32_MEAN64
+#define TADA_K1_F32_MEAN64 1  // f32 rows (RoPE keys, residual flushes): the f64 sequence directly (measured +4.5% with RoPE)
+#endif
 template <typename Row>
 __device__ __forceinline__ void k1_mean(const Row& x, float (&mean)[4], bool& big) {
+  if (TADA_K1_F32_MEAN64 && sizeof(x) == sizeof(float) * 32) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      mean[k] = __double2float_rn(__dmul_rn(k1_col_sum64(x, k), 0.125));
+      big |= !(fabsf(mean[k]) < 32768.f);
+    }
+    return;
+  }
+  bool slow = false;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    double acc = 0.0;
+    float dn = 0.f, up = 0.f;
 #pragma unroll
-    for (int h = 0; h < 8; ++h) acc = __dadd_rn(acc, x.f64(h, k));
-    mean[k] = __double2float_rn(__dmul_rn(acc, 0.125));
-    big |= !(fabsf(mean[k]) < 32768.f);
+    for (int h = 0; h < 8; ++h) {
+      dn = x.add_rd(h, k, dn);
+      up = x.add_ru(h, k, up);
+    }
+    slow |= !(dn == up && (fabsf(dn) >= 0x1p-120f || dn == 0.f));
+    mean[k] = __fmaf_rn(dn, 0.125f, 0.f);
   }
+  if (__any_sync(0xffffffffu, slow)) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) mean[k] = __double2float_rn(__dmul_rn(k1_col_sum64(x, k), 0.125));
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) big |= !(fabsf(mean[k]) < 32768.f);
 }
 // ... and nd = RN(x - mean)
 template <typename Row>
 __device__ __forceinline__ void k1_mean_dev(const Row& x, float (&mean)[4], float (&nd)[8][4], bool& big) {
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    double acc = 0.0;
-#pragma unroll
-    for (int h = 0; h < 8; ++h) acc = __dadd_rn(acc, x.f64(h, k));
-    mean[k] = __double2float_rn(__dmul_rn(acc, 0.125));
-    // any non-finite input makes its column's sum non-finite; |mean| >= 2^15 leaves the f16 range of K2
-    big |= !(fabsf(mean[k]) < 32768.f);
-  }
+  // any non-finite input makes its column's sum non-finite; |mean| >= 2^15 leaves the f16 range of K2
+  k1_mean(x, mean, big);
 #pragma unroll
   for (int h = 0; h < 8; ++h)
 #pragma unroll
