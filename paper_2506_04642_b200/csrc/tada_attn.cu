@@ -753,13 +753,113 @@ bool pdl_enabled() {
 
 }  // namespace tada
 
+namespace tada {
+
+// ---------------------------------------------------------------- group-size remapping of the tensor-core path
+// The tensor-core kernels are instantiated for 8 KV heads and q-head groups G in {1, 2, 4, 8} (G <= 4 at 8-bit,
+// whose stages leave no room for 64 q heads).  Any other G runs in `passes` passes of up to gc q heads per KV
+// head: pass p takes q heads p*gc .. p*gc + n - 1 of every group, zero-padded to gp = 2^ceil(log2 n) rows
+// (a zero query row attends harmlessly and is dropped), then K2 + K3 as usual into staging buffers whose rows
+// go back to their places.  Each pass re-reads the layer's cache, so 8-bit layers with G > 4 cost 2x traffic.
+bool fast_map(const tada_page_layout& L, int Hq, FastMap* m) {
+  if (L.heads <= 0 || Hq <= 0 || Hq % L.heads) return false;
+  const int G = Hq / L.heads;
+  if (fast_supported(L, Hq)) {
+    *m = FastMap{1, G, G, G};
+    return true;
+  }
+  if (L.heads != 8 || L.head_dim != 128 || !(L.bits == 2 || L.bits == 4 || L.bits == 8)) return false;
+  const int gc = L.bits == 8 ? 4 : 8;
+  const int n0 = G < gc ? G : gc;
+  int gp = 1;
+  while (gp < n0) gp *= 2;
+  if (!fast_supported(L, 8 * gp)) return false;
+  *m = FastMap{(G + gc - 1) / gc, gc, gp, G};
+  return true;
+}
+
+template <typename T>
+__global__ void pad_q_kernel(const T* __restrict__ q, T* __restrict__ qp, int G, int j0, int n, int gp, int D,
+                             int64_t total) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int d = int(i % D);
+    const int64_t r = i / D;  // (b, h, j) row of the padded [B][8][gp] q
+    const int j = int(r % gp);
+    const int64_t bh = r / gp;  // b * 8 + h
+    qp[i] = j < n ? q[(bh * G + j0 + j) * D + d] : T(0.f);
+  }
+}
+
+template <typename T>
+__global__ void unpad_out_kernel(const T* __restrict__ op, const float* __restrict__ lp, T* __restrict__ out,
+                                 float* __restrict__ lse, int G, int j0, int n, int gp, int D, int64_t total) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int d = int(i % D);
+    const int64_t r = i / D;  // (b, h, j) row of the output, j < n
+    const int j = int(r % n);
+    const int64_t bh = r / n;
+    const int64_t src = bh * gp + j, dst = bh * G + j0 + j;
+    out[dst * D + d] = op[src * D + d];
+    if (lse && d == 0) lse[dst] = lp[src];
+  }
+}
+
+int launch_fast_mapped(const AttnArgs& a0, int batch, const FastMap& fm, int mode, void* workspace, cudaStream_t st) {
+  const int D = a0.L.head_dim, hq = 8 * fm.gp;
+  const int64_t rows = int64_t(batch) * hq;
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  const int64_t part_bytes = rows * a0.slots * (int64_t(D) + 2) * 4;
+  void* qp = ws + (part_bytes + 255) / 256 * 256;
+  void* op = reinterpret_cast<uint8_t*>(qp) + rows * D * 4;
+  float* lp = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(op) + rows * D * 4);
+  const bool qbf = a0.q_dtype == TADA_BF16, obf = a0.out_dtype == TADA_BF16;
+  for (int p = 0; p < fm.passes; ++p) {
+    const int j0 = p * fm.gc, n = fm.g - j0 < fm.gc ? fm.g - j0 : fm.gc;
+    AttnArgs a = a0;
+    a.Hq = hq;
+    a.q = qp;
+    a.out = op;
+    a.lse_out = a0.lse_out ? lp : nullptr;
+    a.part_acc = reinterpret_cast<float*>(ws);
+    a.part_ml = a.part_acc + rows * a.slots * D;
+    const int64_t tq = rows * D;
+    const int grid = int((tq + 255) / 256 < 148 * 16 ? (tq + 255) / 256 : 148 * 16);
+    if (qbf)
+      pad_q_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(a0.q), reinterpret_cast<__nv_bfloat16*>(qp),
+                                         fm.g, j0, n, fm.gp, D, tq);
+    else
+      pad_q_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(a0.q), reinterpret_cast<float*>(qp), fm.g, j0, n,
+                                         fm.gp, D, tq);
+    int rc = check_launch("decode_attn_pad_q");
+    if (rc != TADA_OK) return rc;
+    rc = (mode != 3 && v8_supported(a.L, hq)) ? launch_v8(a, batch, st) : launch_fast(a, batch, st);
+    if (rc == TADA_OK) rc = launch_combine_residual(a, batch, st);
+    if (rc != TADA_OK) return rc;
+    const int64_t to = int64_t(batch) * 8 * n * D;
+    const int g2 = int((to + 255) / 256 < 148 * 16 ? (to + 255) / 256 : 148 * 16);
+    if (obf)
+      unpad_out_kernel<<<g2, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(op), lp,
+                                           reinterpret_cast<__nv_bfloat16*>(a0.out), a0.lse_out, fm.g, j0, n, fm.gp, D, to);
+    else
+      unpad_out_kernel<<<g2, 256, 0, st>>>(reinterpret_cast<const float*>(op), lp, reinterpret_cast<float*>(a0.out),
+                                           a0.lse_out, fm.g, j0, n, fm.gp, D, to);
+    rc = check_launch("decode_attn_unpad");
+    if (rc != TADA_OK) return rc;
+  }
+  return TADA_OK;
+}
+
+}  // namespace tada
+
 using namespace tada;
 
 extern "C" {
 
 int64_t tada_decode_attn_workspace_bytes(int32_t batch, int32_t num_q_heads, int32_t head_dim, int32_t num_splits) {
-  // slots = splits + 1 (the tensor-core path puts the residual rows in an extra slot)
-  return int64_t(batch) * num_q_heads * (num_splits + 1) * (int64_t(head_dim) + 2) * 4;
+  // slots = splits + 1 (the tensor-core path puts the residual rows in an extra slot); a remapped group size
+  // (FastMap) runs with up to 2 * num_q_heads padded q heads and stages their q, outputs and lse here too
+  const int64_t direct = int64_t(batch) * num_q_heads * (num_splits + 1) * (int64_t(head_dim) + 2) * 4;
+  return 2 * direct + int64_t(batch) * 2 * num_q_heads * (2 * int64_t(head_dim) + 1) * 4 + 256;
 }
 
 // Split count for `slots` concurrently resident CTAs: the fewest whole waves whose last wave is
@@ -789,8 +889,10 @@ int32_t tada_decode_attn_plan_splits(const tada_page_layout* layout, int32_t num
                                      int64_t max_tokens) {
   if (!layout || num_q_heads <= 0) return 1;
   int per_sm = 1;
-  if (v8_supported(*layout, num_q_heads)) per_sm = 2;  // attn_v8_kernel: two CTAs per SM
-  else if (fast_supported(*layout, num_q_heads)) per_sm = fast_tile_tokens(*layout, num_q_heads) == 16 ? 2 : 1;
+  FastMap fm;
+  const int hq = fast_map(*layout, num_q_heads, &fm) ? 8 * fm.gp : num_q_heads;  // the instantiation that runs
+  if (v8_supported(*layout, hq)) per_sm = 2;  // attn_v8_kernel: two CTAs per SM
+  else if (fast_supported(*layout, hq)) per_sm = fast_tile_tokens(*layout, hq) == 16 ? 2 : 1;
   else per_sm = exact_ctas_per_sm(*layout, num_q_heads);
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -814,10 +916,13 @@ static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool,
   if (!q || !out || !comp_len || !res_len) return fail(TADA_ERR_SHAPE, "null buffer");
   if (mode < 0 || mode > 3)
     return fail(TADA_ERR_CONFIG, "mode must be 0 (auto), 1 (exact), 2 (fast) or 3 (fast, two-barrier kernel)");
-  const bool fast = mode >= 2 || (mode == 0 && fast_supported(*layout, num_q_heads));
-  if (mode >= 2 && !fast_supported(*layout, num_q_heads))
-    return fail(TADA_ERR_CONFIG, "fast decode attention needs head_dim 128, bits 2/4/8, num_q_heads in {8,16,32,64}, "
-                                 "group size in {1,2,4,8} and page_tokens % 32 == 0");
+  FastMap fm{};
+  const bool mapped = fast_map(*layout, num_q_heads, &fm);
+  const bool fast = mode >= 2 || (mode == 0 && mapped);
+  if (mode >= 2 && !mapped)
+    return fail(TADA_ERR_CONFIG, "fast decode attention needs 8 KV heads, head_dim 128, bits 2/4/8 and page_tokens % 32 == 0");
+  if (fast && !fm.direct() && step_R >= 0 && fm.passes > 1)
+    return fail(TADA_ERR_CONFIG, "the fused decode step runs in one pass (group size <= 4 for 8-bit layers)");
   if (!workspace && (num_splits > 1 || fast || exact_smem_bytes(*layout, num_q_heads)))
     return fail(TADA_ERR_SHAPE, "workspace required");
   AttnArgs a{};
@@ -854,6 +959,7 @@ static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool,
   }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int rc;
+  if (fast && !fm.direct()) return launch_fast_mapped(a, batch, fm, mode, workspace, st);
   if (fast) {
     rc = (mode != 3 && v8_supported(*layout, num_q_heads)) ? launch_v8(a, batch, st) : launch_fast(a, batch, st);
     if (rc == TADA_OK && a.diag != 3) rc = launch_combine_residual(a, batch, st);  // diag 3: K2 alone (timing only)
@@ -900,8 +1006,9 @@ int tada_decode_step(const tada_page_layout* layout, uint8_t* pool, const void* 
                      float scale, int32_t num_splits, void* workspace, void* out, int32_t out_dtype, int32_t mode,
                      int32_t* err_flag, int32_t* range_word, void* stream) {
   if (!layout) return fail(TADA_ERR_CONFIG, "null layout");
-  if (mode == 1 || !fast_supported(*layout, num_q_heads) || layout->head_dim != 128)
-    return fail(TADA_ERR_CONFIG, "the fused decode step needs the tensor-core attention path (head_dim 128)");
+  FastMap fm;
+  if (mode == 1 || !fast_map(*layout, num_q_heads, &fm) || fm.passes != 1 || layout->head_dim != 128)
+    return fail(TADA_ERR_CONFIG, "the fused decode step needs the one-pass tensor-core attention path (head_dim 128)");
   if (!new_k || !new_v || !res_k || !res_v || !step_sync || !comp_len || !res_len) return fail(TADA_ERR_SHAPE, "null buffer");
   if (new_dtype != TADA_F32 && new_dtype != TADA_BF16) return fail(TADA_ERR_CONFIG, "new row dtype must be f32 or bf16");
   if (residual_length < 0 || (residual_length > 0 && residual_length > res_seq_stride) ||

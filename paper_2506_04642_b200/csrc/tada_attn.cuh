@@ -221,6 +221,13 @@ int ensure_smem(Kern kern, int bytes, std::atomic<uint64_t>& done, const char* w
 // Fast path (tensor-core grouped-head contraction); returns TADA_ERR_CONFIG if the
 // geometry is unsupported so the caller can fall back to the generic kernel.
 bool fast_supported(const tada_page_layout& L, int Hq);
+// tensor-core head mapping: `passes` passes of up to gc q heads per KV head, each padded to gp rows (tada_attn.cu)
+struct FastMap {
+  int passes, gc, gp, g;
+  bool direct() const { return passes == 1 && gp == g; }
+};
+bool fast_map(const tada_page_layout& L, int Hq, FastMap* m);
+int launch_fast_mapped(const AttnArgs& a, int batch, const FastMap& fm, int mode, void* workspace, cudaStream_t st);
 int launch_fast(const AttnArgs& a, int batch, cudaStream_t st);
 int fast_tile_tokens(const tada_page_layout& L, int Hq);  // 16 or 32 (0: unsupported)
 // One-barrier-per-tile kernel (tada_attn_v8.cu): 2/4-bit (8-bit where two stages fit), Hq in {8, 16, 32}.

@@ -123,8 +123,10 @@ def _fast_or_skip(store, q, **kw):
 
 
 @pytest.mark.parametrize("bits", [2, 4, 8])
-@pytest.mark.parametrize("hq", [8, 16, 32, 64])
+@pytest.mark.parametrize("hq", [8, 16, 24, 32, 40, 48, 56, 64])
 def test_paged_batched_fast_bf16(bits, hq):
+    """Every group size 1..8 on the tensor-core path: G in {3, 5, 6, 7} run zero-padded to the next
+    instantiated group, 8-bit G > 4 in two passes (tada_attn.cu fast_map)."""
     store, q, want = _paged_case(B=4, H=8, hq=hq, D=128, bits=bits, T=1500, R=128, seed=10 + bits)
     out = _fast_or_skip(store, q.bfloat16(), out_dtype=torch.bfloat16)
     assert np.abs(out.float().cpu().numpy() - want).max() <= 2e-3
@@ -339,3 +341,42 @@ def test_auto_mode_beyond_f16_range(bits, where):
     kn = orc.bf16_round(rng.normal(size=(B, 1, H, D)).astype(np.float32))
     step = store.append_attend(0, qd, torch.from_numpy(kn).cuda(), torch.from_numpy(kn).cuda(), out_dtype=torch.float32)
     assert torch.isfinite(step).all()
+
+
+@pytest.mark.parametrize("bits,hq", [(4, 24), (2, 40), (8, 48), (8, 64), (4, 128)])
+def test_fast_mapped_lse_and_auto(bits, hq):
+    """Remapped group sizes (padding / two passes / G = 16) through attend_lse and mode 0: outputs within 2e-3
+    of the oracle, lse equal to the exact kernel's within 2e-3, mode 0 on the tensor-core path."""
+    m = tk()
+    store, q, want = _paged_case(B=3, H=8, hq=hq, D=128, bits=bits, T=700, R=128, seed=500 + bits + hq)
+    out, lse = store.attend_lse(0, q, mode=2)
+    assert np.abs(out.float().cpu().numpy() - want).max() <= 2e-3
+    out1, lse1 = store.attend_lse(0, q, mode=1)
+    assert np.abs(lse.cpu().numpy() - lse1.cpu().numpy()).max() <= 2e-3
+    auto = store.attend(0, q.bfloat16(), out_dtype=torch.float32)
+    assert np.abs(auto.cpu().numpy() - want).max() <= 2e-3
+    assert m is not None
+
+
+@pytest.mark.parametrize("bits,hq", [(4, 24), (8, 40), (8, 64)])
+def test_fused_step_mapped_geometry(bits, hq):
+    """append_attend at remapped group sizes (one pass: fused K3 step; two passes: the composition) equals
+    append() + attend() bit for bit across a residual flush."""
+    m = tk()
+    B, T, H, D, R = 2, 200, 8, 128, 8
+    rng = np.random.default_rng(90 + bits + hq)
+    k0 = torch.from_numpy(orc.bf16_round(rng.normal(size=(B, T, H, D)).astype(np.float32))).cuda().bfloat16()
+    v0 = torch.from_numpy(orc.bf16_round(rng.normal(size=(B, T, H, D)).astype(np.float32))).cuda().bfloat16()
+    a = m.PagedKVCache(1, H, D, (bits,), R, batch=B, page_tokens=64, max_tokens=T + 64)
+    b = m.PagedKVCache(1, H, D, (bits,), R, batch=B, page_tokens=64, max_tokens=T + 64)
+    a.append(0, k0, v0)
+    b.append(0, k0, v0)
+    for step in range(12):
+        q = torch.from_numpy(orc.bf16_round(rng.normal(size=(B, hq, D)).astype(np.float32))).cuda().bfloat16()
+        k1 = torch.from_numpy(orc.bf16_round(rng.normal(size=(B, 1, H, D)).astype(np.float32))).cuda().bfloat16()
+        v1 = torch.from_numpy(orc.bf16_round(rng.normal(size=(B, 1, H, D)).astype(np.float32))).cuda().bfloat16()
+        oa = a.append_attend(0, q, k1, v1, out_dtype=torch.float32)
+        b.append(0, k1, v1)
+        ob = b.attend(0, q, out_dtype=torch.float32)
+        assert torch.equal(oa, ob), f"step {step}"
+    assert a.lengths(0) == b.lengths(0)
