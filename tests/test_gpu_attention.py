@@ -1,9 +1,11 @@
 """GPU parity of decode attention (K2 split-K + K3 combine) vs the reference.
 
-Bars: exact generic kernel (f32 out) within 1e-5 of the reference's
-attend_streaming (the reference's own streaming-vs-naive tolerance,
-test_acceptance.py:150-178); the tensor-core kernel (bf16 out) within the
-north_star's 2e-3 max-abs.  Mirrors pkg/tests/test_attention.py (hot-path subset).
+Bars: exact kernels (f32 out) within 1e-5 of the reference's attend_streaming
+(the reference's own streaming-vs-naive tolerance, test_acceptance.py:150-178);
+the tensor-core kernels within the north_star's 2e-3 max-abs on randn-scale
+activations, and within 2e-3 * max(1, |out|max) — a RELATIVE bar — in the outlier
+regimes whose outputs exceed 1 (the f16 vmean; bf16 itself carries a
+2e-3 half-ulp at |out| = 1).  Mirrors pkg/tests/test_attention.py (hot-path subset).
 """
 
 import numpy as np

@@ -46,9 +46,12 @@ def test_host_only_entry_points():
     assert lay.page_bytes % 256 == 0 and lay.page_bytes >= offs[5] + 64 * 8 * 8
     with pytest.raises(_lib.ConfigError):
         _lib.page_layout(64, 8, 128, 3)
-    # partial slots = splits + 1 (the residual rows get their own slot on the tensor-core path)
-    assert lib.tada_decode_attn_workspace_bytes(16, 32, 128, 1) == 16 * 32 * 2 * 130 * 4
-    assert lib.tada_decode_attn_workspace_bytes(16, 32, 128, 8) == 16 * 32 * 9 * 130 * 4
+    # partial slots = splits + 1 (the residual rows get their own slot on the tensor-core path), doubled for
+    # the padded q heads of a remapped group size, plus their staged q / outputs / lse
+    def ws(b, hq, d, s):
+        return 2 * b * hq * (s + 1) * (d + 2) * 4 + b * 2 * hq * (2 * d + 1) * 4 + 256
+    assert lib.tada_decode_attn_workspace_bytes(16, 32, 128, 1) == ws(16, 32, 128, 1)
+    assert lib.tada_decode_attn_workspace_bytes(16, 32, 128, 8) == ws(16, 32, 128, 8)
     assert 1 <= lib.tada_decode_attn_suggest_splits(16, 32768, 64) <= 4096
     # argument validation happens before any device work
     rc = lib.tada_quantize_groups(None, 0, 10, 16, 3, None, None, None, None, None)
