@@ -475,12 +475,13 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
     __syncthreads();
     // ---- online softmax: warp per q head, lane = token (attention.py:139-147); P replaces the scores
     for (int g = warp; g < Hq; g += NTHR / 32) {
-      const float zz = lane < nv ? __fmul_rn(S[g * pl.PS + lane], a.scale) : NEG_INF;
+      const float zz = lane < nv ? __fmul_rn(S[g * pl.PS + (lane & (TT - 1))], a.scale) : NEG_INF;  // in-row index
       const float2 m0 = ml[g];
       const float m_new = fmaxf(m0.x, warp_max(zz));
       const float cf = expf(m0.x - m_new);
       const float p = lane < nv ? expf(zz - m_new) : 0.f;
       const float lsum = warp_sum(p);
+      __syncwarp();  // every lane's score read precedes the in-place P write
       if (lane < TT) S[g * pl.PS + lane] = p;
       if (lane == 0) {
         ml[g] = make_float2(m_new, m0.y * cf + lsum);

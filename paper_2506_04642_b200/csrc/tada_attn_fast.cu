@@ -207,7 +207,10 @@ __global__ void __launch_bounds__(TT * 16, TT == 16 ? 2 : 1) attn_fast_kernel(At
     }
   }
   __syncthreads();
-  if (*exact_flag || beyond_f16(a, kFastScaleExp)) {  // CTA-uniform, rare: operands beyond f16 -> exact f32 path
+  const bool to_exact = *exact_flag || beyond_f16(a, kFastScaleExp);
+  __syncthreads();  // every warp has read the flag: red[] (which it aliases) is written by the epilogue, which an
+                    // empty split reaches without another barrier
+  if (to_exact) {  // CTA-uniform, rare: operands beyond f16 -> exact f32 path
     for (int it = 0; it < S - 1 && it < ntiles; ++it) mbar_wait(&full[it % S], 0u);  // no copy lands after exit
     exact_split_partials<BITS, HQ / H>(a, b, split, t_begin, t_end, warp, lane);
     return;

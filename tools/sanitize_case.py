@@ -18,8 +18,10 @@ def main():
     ap.add_argument("--bits", type=int, default=4)
     ap.add_argument("--hq", type=int, default=32)
     ap.add_argument("--mode", type=int, default=2)
+    ap.add_argument("--heads", type=int, default=8)
+    ap.add_argument("--dim", type=int, default=128)
     args = ap.parse_args()
-    B, T, H, D, R = 2, 300, 8, 128, 8
+    B, T, H, D, R = 2, 300, args.heads, args.dim, 8
     rng = np.random.default_rng(1)
     k = torch.from_numpy(rng.normal(size=(B, T, H, D)).astype(np.float32)).cuda().bfloat16()
     v = torch.from_numpy(rng.normal(size=(B, T, H, D)).astype(np.float32)).cuda().bfloat16()
