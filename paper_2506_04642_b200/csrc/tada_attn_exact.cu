@@ -379,6 +379,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
   }
   for (int g = tid; g < Hq; g += NTHR) ml[g] = make_float2(NEG_INF, 0.f);
   const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
+  const int pshift = (P & (P - 1)) == 0 ? __ffs(P) - 1 : -1;
 
   // ---- staging of tile [t0, t0 + TT) into stage st (cp.async; tokens past t_end are not loaded): warp per
   // (side, token row), lanes over the row's 16-byte chunks
@@ -387,8 +388,9 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
     uint8_t* sb = smem + st * pl.sb;
     for (int r = warp; r < 2 * nv; r += NTHR / 32) {
       const int side = r & 1, t = r >> 1, tok = t0 + t;
-      const uint8_t* page = a.pool + int64_t(pt[tok / P]) * a.L.page_bytes;
-      const int row = tok % P;
+      const int pg = pshift >= 0 ? tok >> pshift : tok / P;  // page_tokens is a power of two in practice
+      const uint8_t* page = a.pool + int64_t(pt[pg]) * a.L.page_bytes;
+      const int row = tok - pg * P;
       const float* msrc = reinterpret_cast<const float*>(page + a.L.off_mean[side]) + int64_t(row) * D;
       float* mdst = reinterpret_cast<float*>(sb + (side ? pl.off_vm : pl.off_km)) + t * pl.RS;
       for (int c = lane; c < D / 4; c += 32) cp16(mdst + 4 * c, msrc + 4 * c);
