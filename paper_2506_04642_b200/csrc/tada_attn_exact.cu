@@ -467,30 +467,26 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
           }
         }
       }
+      // online softmax of the unit's q heads over the tile, in the same warp (attention.py:139-147): the two
+      // column halves hold the same sums after the shuffle, so lanes t and t + TT agree; P goes to shared memory
 #pragma unroll
       for (int g = 0; g < GT; ++g) {
         float z = z2[g].x + z2[g].y;
         z += __shfl_xor_sync(0xffffffffu, z, TT);
-        if (lane < TT) S[(g0 + g) * pl.PS + lane] = z;
+        const float zz = t < nv ? __fmul_rn(z, a.scale) : NEG_INF;
+        const float2 m0 = ml[g0 + g];
+        const float m_new = fmaxf(m0.x, warp_max(zz));
+        const float cf = expf(m0.x - m_new);
+        const float p = t < nv ? expf(zz - m_new) : 0.f;
+        const float lsum = warp_sum(lane < TT ? p : 0.f);
+        if (lane < TT) S[(g0 + g) * pl.PS + lane] = p;
+        if (lane == 0) {
+          ml[g0 + g] = make_float2(m_new, m0.y * cf + lsum);
+          corr[g0 + g] = cf;
+        }
       }
     }
-    __syncthreads();
-    // ---- online softmax: warp per q head, lane = token (attention.py:139-147); P replaces the scores
-    for (int g = warp; g < Hq; g += NTHR / 32) {
-      const float zz = lane < nv ? __fmul_rn(S[g * pl.PS + (lane & (TT - 1))], a.scale) : NEG_INF;  // in-row index
-      const float2 m0 = ml[g];
-      const float m_new = fmaxf(m0.x, warp_max(zz));
-      const float cf = expf(m0.x - m_new);
-      const float p = lane < nv ? expf(zz - m_new) : 0.f;
-      const float lsum = warp_sum(p);
-      __syncwarp();  // every lane's score read precedes the in-place P write
-      if (lane < TT) S[g * pl.PS + lane] = p;
-      if (lane == 0) {
-        ml[g] = make_float2(m_new, m0.y * cf + lsum);
-        corr[g] = cf;
-      }
-    }
-    __syncthreads();
+    __syncthreads();  // P and the rescale factors of every q head are in shared memory
     // ---- phase 2: acc = acc * corr + P · V̂ per (KV head, q chunk, 4 columns)
 #pragma unroll
     for (int i = 0; i < UPT; ++i) {
