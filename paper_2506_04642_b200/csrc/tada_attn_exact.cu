@@ -469,19 +469,36 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
       }
       // online softmax of the unit's q heads over the tile, in the same warp (attention.py:139-147): the two
       // column halves hold the same sums after the shuffle, so lanes t and t + TT agree; P goes to shared memory
+      // (the GT reductions interleaved: independent shuffle chains; 16-lane butterflies, the halves being equal)
+      float zz[GT], mx[GT], pe[GT], ls[GT];
 #pragma unroll
       for (int g = 0; g < GT; ++g) {
         float z = z2[g].x + z2[g].y;
         z += __shfl_xor_sync(0xffffffffu, z, TT);
-        const float zz = t < nv ? __fmul_rn(z, a.scale) : NEG_INF;
-        const float2 m0 = ml[g0 + g];
-        const float m_new = fmaxf(m0.x, warp_max(zz));
-        const float cf = expf(m0.x - m_new);
-        const float p = t < nv ? expf(zz - m_new) : 0.f;
-        const float lsum = warp_sum(lane < TT ? p : 0.f);
-        if (lane < TT) S[(g0 + g) * pl.PS + lane] = p;
+        zz[g] = t < nv ? __fmul_rn(z, a.scale) : NEG_INF;
+        mx[g] = zz[g];
+      }
+#pragma unroll
+      for (int o = TT / 2; o > 0; o >>= 1)
+#pragma unroll
+        for (int g = 0; g < GT; ++g) mx[g] = fmaxf(mx[g], __shfl_xor_sync(0xffffffffu, mx[g], o));
+#pragma unroll
+      for (int g = 0; g < GT; ++g) {
+        mx[g] = fmaxf(ml[g0 + g].x, mx[g]);
+        pe[g] = t < nv ? expf(zz[g] - mx[g]) : 0.f;
+        ls[g] = pe[g];
+      }
+#pragma unroll
+      for (int o = TT / 2; o > 0; o >>= 1)
+#pragma unroll
+        for (int g = 0; g < GT; ++g) ls[g] += __shfl_xor_sync(0xffffffffu, ls[g], o);
+#pragma unroll
+      for (int g = 0; g < GT; ++g) {
+        if (lane < TT) S[(g0 + g) * pl.PS + lane] = pe[g];
         if (lane == 0) {
-          ml[g0 + g] = make_float2(m_new, m0.y * cf + lsum);
+          const float2 m0 = ml[g0 + g];
+          const float cf = expf(m0.x - mx[g]);
+          ml[g0 + g] = make_float2(mx[g], m0.y * cf + ls[g]);
           corr[g0 + g] = cf;
         }
       }
