@@ -594,9 +594,8 @@ struct K1NdLazy {
 // mean (cache.py:109): the reference sums the 8 heads in f64 from +0.0, divides by 8 (exact) and rounds to f32.
 // The f64 sum of 8 bf16/f32 values is exact unless their exponents span more than ~28 bits, so the mean is
 // RN32(S) / 8 for the exact sum S.  Two f32 sums rounded down and up bracket S; when they are equal, S is that
-// f32 value (every step was exact) and the mean is S * 0.125 (+0.0 restores the reference's +0.0 for zeros;
-// |S| >= 2^-120 keeps the scaling exact).  Other columns (rare: a wide exponent spread, or non-finite) take the
-// f64 sequence.  This keeps the F2F conversions off the XU pipe, which they saturated.
+// f32 value (every step was exact) and the mean is S * 0.125 (|S| >= 2^-120 keeps the scaling exact).  Other
+// columns (rare: a wide exponent spread, an exact zero or tiny sum, or non-finite) take the f64 sequence.  This keeps the F2F conversions off the XU pipe, which they saturated.
 template <typename Row>
 __device__ __forceinline__ double k1_col_sum64(const Row& x, int k) {
   double acc = 0.0;
@@ -626,7 +625,7 @@ __device__ __forceinline__ void k1_mean(const Row& x, float (&mean)[4], bool& bi
       dn = x.add_rd(h, k, dn);
       up = x.add_ru(h, k, up);
     }
-    slow |= !(dn == up && (fabsf(dn) >= 0x1p-120f || dn == 0.f));
+    slow |= (dn != up) | !(fabsf(up) >= 0x1p-120f);  // inexact, tiny (zero included: conservative) or NaN
     mean[k] = __fmaf_rn(dn, 0.125f, 0.f);
   }
   if (__any_sync(0xffffffffu, slow)) {
@@ -690,17 +689,20 @@ __device__ __forceinline__ void k1_token(const AppendArgs& a, const ND& nd, cons
     if (__any_sync(0xffffffffu, bad) && lane == 0 && a.err) atomicOr(a.err, 1);
   }
   // group min / max of dev = -nd: one CREDUX each per head; +0.0 - y keeps the reference's +0.0 for zeros
-  float ndmax[H];  // max of nd = -(min of dev) per head (uniform across the warp)
-  float my_mn = 0.f, my_mx = 0.f;
+  float ndmax[H], ndmin[H];  // max / min of nd = -(min / max of dev) per head (uniform across the warp)
 #pragma unroll
   for (int h = 0; h < H; ++h) {
     ndmax[h] = redux_max(fmaxf(fmaxf(nd(h, 0), nd(h, 1)), fmaxf(nd(h, 2), nd(h, 3))));
-    const float lo = redux_min(fminf(fminf(nd(h, 0), nd(h, 1)), fminf(nd(h, 2), nd(h, 3))));
-    if (lane == h) {
-      my_mn = ndmax[h];
-      my_mx = lo;
-    }
+    ndmin[h] = redux_min(fminf(fminf(nd(h, 0), nd(h, 1)), fminf(nd(h, 2), nd(h, 3))));
   }
+  // lane h < 8 takes head h's pair: a three-level select tree on the lane bits
+  const bool l0 = lane & 1, l1 = lane & 2, l2 = lane & 4;
+  auto pick = [&](const float (&v)[H]) {
+    const float a0 = l0 ? v[1] : v[0], a1 = l0 ? v[3] : v[2], a2 = l0 ? v[5] : v[4], a3 = l0 ? v[7] : v[6];
+    const float b0 = l1 ? a1 : a0, b1 = l1 ? a3 : a2;
+    return l2 ? b1 : b0;
+  };
+  float my_mn = pick(ndmax), my_mx = pick(ndmin);
   my_mn = __fsub_rn(0.f, my_mn);  // group min / max of dev
   my_mx = __fsub_rn(0.f, my_mx);
   // Lane h < 8: group h's f64 scale with the reference's refinement, then the bracket multipliers.
