@@ -452,19 +452,19 @@ __global__ void __launch_bounds__(256) combine_pair_kernel(AttnArgs a, int n_row
   }
 }
 
-// K3 for head_dim 128 and G = Hq/H in {1, 2, 4, 8}: one CTA per (sequence, KV head), G + 4 warps.
+// K3 for head_dim 128 and G = Hq/H in {1, 2, 4, 8}: one CTA per (sequence, KV head), G + 8 warps.
 //  * warps 0..G-1: the split partials of q head h*G + w (natural-log (m, l) per slot), online merge;
-//  * warps G..G+3: the residual rows, 32 per warp and round (lane = row): each lane takes the full
-//    128-d dot of its row with all G q rows (broadcast from shared memory), so a K/V row is read once
-//    for the whole head group and no shuffle trees are needed; then lane = 4 d columns for P.V, the
-//    weights broadcast by shuffle.  Every load of a round is independent: ~one round trip per 32 rows,
-//    flat in the residual length up to 128 rows (the previous per-q-head kernel grew by a round trip
-//    per 24 rows, and read each row G times).
+//  * warps G..G+7: the residual rows, staged into shared memory by one round of 16-byte cp.async (up to 128
+//    rows per chunk), then 8 rows per warp and round with lane = (row, d quarter): each lane forms the 32-d
+//    partial dots of its row with all G q rows (broadcast), two shuffles join the quarters, so a K/V row is
+//    read once for the whole head group and the dependent FMA chains are 32 long; then lane = 4 d columns
+//    for P.V, the weights broadcast by shuffle.  (The lane = row variant with 4 warps ran its 128-long FMA
+//    chains on too few warps: 100 rows cost 7 us per layer.)
 //  * the parts meet in shared memory; warp w writes q head h*G + w.
 // In a fused decode step the new row is read from the input and residual warp 0 stores it.
 template <int G>
-__global__ void __launch_bounds__((G + 4) * 32) combine_kv_kernel(AttnArgs a, int rch) {
-  constexpr int D = 128, RWN = 4, U = 8, RP = D + 4;  // RP: padded staged row (lane = row reads hit 32 banks)
+__global__ void __launch_bounds__((G + 8) * 32) combine_kv_kernel(AttnArgs a, int rch) {
+  constexpr int D = 128, RWN = 8, U = 8, RP = D + 4;  // RP: padded staged row (8-row phases hit distinct banks)
   extern __shared__ __align__(16) float rst[];        // staged residual chunk: K rows [rch][RP], then V rows
   __shared__ __align__(16) float qsm[G][D];
   __shared__ __align__(16) float rpart[RWN][G][D];
@@ -557,7 +557,7 @@ __global__ void __launch_bounds__((G + 4) * 32) combine_kv_kernel(AttnArgs a, in
       rm[g] = NEG_INF;
       rl[g] = 0.f;
     }
-    const int tid_r = threadIdx.x - G * 32;  // 0 .. 127 among the residual warps
+    const int tid_r = threadIdx.x - G * 32;  // 0 .. 255 among the residual warps
     for (int cb = 0; cb < R; cb += rch) {   // chunks of rch rows: one round of async copies each
       const int n = min(rch, R - cb);
       if (cb > 0) asm volatile("bar.sync 2, %0;" ::"n"(RWN * 32) : "memory");  // previous chunk consumed
@@ -579,54 +579,62 @@ __global__ void __launch_bounds__((G + 4) * 32) combine_kv_kernel(AttnArgs a, in
       }
       asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
       asm volatile("bar.sync 2, %0;" ::"n"(RWN * 32) : "memory");
-      const int c0 = cb + 32 * rw;  // this warp's 32 rows of the chunk
-      if (c0 >= cb + n) continue;
-      const int t = c0 + lane;
-      const bool valid = t < cb + n;
-      float sc[G];
+      // rounds of 8 rows per warp: lane = (row r = lane & 7, d quarter dq = lane >> 3); an 8-lane phase reads 8
+      // rows of one quarter (row stride RP = 4 words mod 32: distinct banks), the quarters meet by two shuffles
+      const int r8 = lane & 7, dq = lane >> 3;
+      for (int c0 = cb + 8 * rw; c0 < cb + n; c0 += 8 * RWN) {
+        const int t = c0 + r8;
+        const bool valid = t < cb + n;
+        float sc[G];
 #pragma unroll
-      for (int g = 0; g < G; ++g) sc[g] = 0.f;
-      if (valid) {  // logits of row t (lane) against the G q rows
-        const float* kr = rst + (t - cb) * RP;
-#pragma unroll 8
-        for (int j = 0; j < D; j += 4) {
-          const float4 k4 = *reinterpret_cast<const float4*>(kr + j);
+        for (int g = 0; g < G; ++g) sc[g] = 0.f;
+        if (valid) {  // partial logits of row t over columns 32 dq .. 32 dq + 31
+          const float* kr = rst + (t - cb) * RP + 32 * dq;
 #pragma unroll
-          for (int g = 0; g < G; ++g) {
-            const float4 qv = *reinterpret_cast<const float4*>(&qsm[g][j]);
-            sc[g] = __fmaf_rn(qv.w, k4.w, __fmaf_rn(qv.z, k4.z, __fmaf_rn(qv.y, k4.y, __fmaf_rn(qv.x, k4.x, sc[g]))));
+          for (int j = 0; j < 32; j += 4) {
+            const float4 k4 = *reinterpret_cast<const float4*>(kr + j);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              const float4 qv = *reinterpret_cast<const float4*>(&qsm[g][32 * dq + j]);
+              sc[g] = __fmaf_rn(qv.w, k4.w, __fmaf_rn(qv.z, k4.z, __fmaf_rn(qv.y, k4.y, __fmaf_rn(qv.x, k4.x, sc[g]))));
+            }
           }
         }
-      }
-      float p[G];
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const float sv = valid ? __fmul_rn(sc[g], a.scale) : NEG_INF;
-        float bm = sv;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
-        const float mn = fmaxf(rm[g], bm);  // finite: lane 0 of every round holds a valid row
-        const float cf = rm[g] == NEG_INF ? 0.f : expf(rm[g] - mn);
-        racc[g][0] *= cf;
-        racc[g][1] *= cf;
-        racc[g][2] *= cf;
-        racc[g][3] *= cf;
-        rl[g] *= cf;
-        rm[g] = mn;
-        p[g] = valid ? expf(sv - mn) : 0.f;
-        rl[g] += p[g];  // lane-partial; reduced below
-      }
-      const int nr = min(32, cb + n - c0);
-      const float* vr = rst + (rch + (c0 - cb)) * RP + 4 * lane;
-      for (int u = 0; u < nr; ++u) {  // P.V: lane = columns 4*lane .. +3
-        const float4 v4 = *reinterpret_cast<const float4*>(vr + u * RP);
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-          const float pu = __shfl_sync(0xffffffffu, p[g], u);
-          racc[g][0] = fmaf(pu, v4.x, racc[g][0]);
-          racc[g][1] = fmaf(pu, v4.y, racc[g][1]);
-          racc[g][2] = fmaf(pu, v4.z, racc[g][2]);
-          racc[g][3] = fmaf(pu, v4.w, racc[g][3]);
+          sc[g] += __shfl_xor_sync(0xffffffffu, sc[g], 8);
+          sc[g] += __shfl_xor_sync(0xffffffffu, sc[g], 16);
+        }
+        float p[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const float sv = valid ? __fmul_rn(sc[g], a.scale) : NEG_INF;
+          float bm = sv;
+#pragma unroll
+          for (int o = 4; o > 0; o >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+          const float mn = fmaxf(rm[g], bm);  // finite: row c0 of every round is valid
+          const float cf = rm[g] == NEG_INF ? 0.f : expf(rm[g] - mn);
+          racc[g][0] *= cf;
+          racc[g][1] *= cf;
+          racc[g][2] *= cf;
+          racc[g][3] *= cf;
+          rl[g] *= cf;
+          rm[g] = mn;
+          p[g] = valid ? expf(sv - mn) : 0.f;
+          if (dq == 0) rl[g] += p[g];  // lane-partial over the quarter-0 lanes; reduced below
+        }
+        const int nr = min(8, cb + n - c0);
+        const float* vr = rst + (rch + (c0 - cb)) * RP + 4 * lane;
+        for (int u = 0; u < nr; ++u) {  // P.V: lane = columns 4*lane .. +3, row u's weight from lane u
+          const float4 v4 = *reinterpret_cast<const float4*>(vr + u * RP);
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const float pu = __shfl_sync(0xffffffffu, p[g], u);
+            racc[g][0] = fmaf(pu, v4.x, racc[g][0]);
+            racc[g][1] = fmaf(pu, v4.y, racc[g][1]);
+            racc[g][2] = fmaf(pu, v4.z, racc[g][2]);
+            racc[g][3] = fmaf(pu, v4.w, racc[g][3]);
+          }
         }
       }
     }
@@ -683,7 +691,7 @@ static bool combine_residual_ok(const AttnArgs& a) {
 
 static int launch_combine_residual(const AttnArgs& a, int batch, cudaStream_t st) {
   if (a.L.head_dim * 2 > kCombThreads * 2 || a.L.head_dim % 4) return fail(TADA_ERR_CONFIG, "combine needs head_dim % 4 == 0");
-  if (a.L.head_dim == 128 && TADA_K3_KV) {  // any residual length: the rows stream through 4 warps per KV head
+  if (a.L.head_dim == 128 && TADA_K3_KV) {  // any residual length: the rows stream through 8 warps per KV head
     const int G = a.Hq / a.L.heads;
     const dim3 grid(a.L.heads, batch);
     // staged residual chunk: up to 128 rows (the default residual_length) of K and V, padded rows
@@ -696,10 +704,10 @@ static int launch_combine_residual(const AttnArgs& a, int batch, cudaStream_t st
     };
     static std::atomic<uint64_t> d1{0}, d2{0}, d4{0}, d8{0};
     switch (G) {
-      case 1: e = go(combine_kv_kernel<1>, 5, d1); break;
-      case 2: e = go(combine_kv_kernel<2>, 6, d2); break;
-      case 4: e = go(combine_kv_kernel<4>, 8, d4); break;
-      case 8: e = go(combine_kv_kernel<8>, 12, d8); break;
+      case 1: e = go(combine_kv_kernel<1>, 9, d1); break;
+      case 2: e = go(combine_kv_kernel<2>, 10, d2); break;
+      case 4: e = go(combine_kv_kernel<4>, 12, d4); break;
+      case 8: e = go(combine_kv_kernel<8>, 16, d8); break;
       default: break;
     }
     if (G == 1 || G == 2 || G == 4 || G == 8) {
