@@ -518,6 +518,9 @@ constexpr int K1_RING = 3;
 #ifndef TADA_K1_RECOMP
 #define TADA_K1_RECOMP 0  // recompute nd = x - mean from the packed row on each use instead of holding it
 #endif
+#ifndef TADA_K1_MINB
+#define TADA_K1_MINB 3  // resident CTAs per SM the register allocation targets (3: 80 registers)
+#endif
 #ifndef TADA_K1_PAGE_CACHE
 #define TADA_K1_PAGE_CACHE 1  // page base pointer reloaded on page change only
 #endif
@@ -897,12 +900,12 @@ static int launch_append(const AppendArgs& a, int batch, size_t smem, cudaStream
     const int shift = (P & (P - 1)) == 0 ? __builtin_ctz(unsigned(P)) : -1;
     const size_t smem = size_t(8) * K1_RING * 8 * 128 * sizeof(T) + 8 * K1_RING * 8;
     // 3 CTAs per SM (80 registers, a few spills) measured faster than 2 (no spills): 3686 vs 3470 GB/s
-    auto k = a.rope_cs ? (a.L.bits == 2 ? quant_append_fast_kernel<T, 2, 3, true>
-                                        : (a.L.bits == 4 ? quant_append_fast_kernel<T, 4, 3, true>
-                                                         : quant_append_fast_kernel<T, 8, 3, true>))
-                       : (a.L.bits == 2 ? quant_append_fast_kernel<T, 2, 3, false>
-                                        : (a.L.bits == 4 ? quant_append_fast_kernel<T, 4, 3, false>
-                                                         : quant_append_fast_kernel<T, 8, 3, false>));
+    auto k = a.rope_cs ? (a.L.bits == 2 ? quant_append_fast_kernel<T, 2, TADA_K1_MINB, true>
+                                        : (a.L.bits == 4 ? quant_append_fast_kernel<T, 4, TADA_K1_MINB, true>
+                                                         : quant_append_fast_kernel<T, 8, TADA_K1_MINB, true>))
+                       : (a.L.bits == 2 ? quant_append_fast_kernel<T, 2, TADA_K1_MINB, false>
+                                        : (a.L.bits == 4 ? quant_append_fast_kernel<T, 4, TADA_K1_MINB, false>
+                                                         : quant_append_fast_kernel<T, 8, TADA_K1_MINB, false>));
     if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e != cudaSuccess) return fail(TADA_ERR_CUDA, std::string("quant_append smem: ") + cudaGetErrorString(e));
