@@ -392,6 +392,6 @@ def test_exact_kernel_geometries(H, hq, D, bits):
     every width, ragged tails and several splits: within the reference's 1e-5 streaming bar."""
     store, q, want = _paged_case(B=2, H=H, hq=hq, D=D, bits=bits, T=333, R=16, seed=700 + H + hq + D + bits,
                                  poison=True)
-    for splits in (1, 5):
+    for splits in (1, 5, 37):  # 37: splits of 16 tokens and empty ones
         out = store.attend(0, q, num_splits=splits, mode=1)
         assert np.abs(out.cpu().numpy() - want).max() <= 1e-5, f"splits {splits}"
