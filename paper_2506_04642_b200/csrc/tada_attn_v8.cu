@@ -63,6 +63,9 @@ constexpr int kBudget = 113 * 1024;  // two CTAs per SM
 #ifndef TADA_V8_OFTM
 #define TADA_V8_OFTM 2  // per-thread shared offsets in TMEM, reloaded per phase: 1 = phase B only (+0.8..2.5%), 2 = + phases A/C and the logit constants (+0.1..2.3% more)
 #endif
+#ifndef TADA_V8_KMEAN_LO
+#define TADA_V8_KMEAN_LO 1  // the QK mean piece with the f32 kmean as f16 hi + lo (0: hi only, one MMA pass)
+#endif
 #ifndef TADA_V8_PPS
 #define TADA_V8_PPS 0.00390625f  // 2^-8
 #endif
@@ -512,8 +515,13 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks) {
       const float4 x = ks ? km.x1 : km.x0;
-      split_h2(x.x, x.y, hb[ks][0], lb[ks][0]);
-      split_h2(x.z, x.w, hb[ks][1], lb[ks][1]);
+      if (TADA_V8_KMEAN_LO) {
+        split_h2(x.x, x.y, hb[ks][0], lb[ks][0]);
+        split_h2(x.z, x.w, hb[ks][1], lb[ks][1]);
+      } else {
+        hb[ks][0] = pack_h2(x.x, x.y);
+        hb[ks][1] = pack_h2(x.z, x.w);
+      }
     }
     float qa[QATM ? 8 * MT : 1];
     if constexpr (QATM) {
@@ -527,7 +535,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) acc2[mt][0] = acc2[mt][1] = acc2[mt][2] = acc2[mt][3] = 0.f;
 #pragma unroll
-    for (int pass = 0; pass < 2; ++pass)
+    for (int pass = 0; pass < (TADA_V8_KMEAN_LO ? 2 : 1); ++pass)
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks)
 #pragma unroll

@@ -461,6 +461,15 @@ class PagedKVCache:
         out["residual_v"] = self.res_v[layer][b, :r].clone()
         return out
 
+    def _note_range(self, layer: int, mean: torch.Tensor, scales: torch.Tensor) -> None:
+        """The range words K1 keeps (note_mean / note_scale in tada_quant.cu) for values that arrive by import:
+        the binary exponent of max |mean| when >= 2^15 and of max scale when >= 2^8, on the device (no sync)."""
+        for word, vals, floor in ((0, mean, 32768.0), (1, scales, 256.0)):
+            a = torch.nan_to_num(vals.float().abs().max(), nan=3.0e38, posinf=3.0e38)
+            e = (torch.frexp(a)[1] - 1).to(torch.int32)
+            e = torch.where(a >= floor, e, torch.zeros_like(e))
+            self.range[layer, word] = torch.maximum(self.range[layer, word], e)
+
     def load(self, layer: int, b: int, k_mean, v_mean, k_dev: QuantizedDeviation, v_dev: QuantizedDeviation,
              residual_k, residual_v) -> None:
         """Replace one (layer, sequence)'s contents from dense reference-layout arrays (deserialize path)."""
@@ -477,6 +486,7 @@ class PagedKVCache:
                 call("tada_scatter_compressed", self._layout_ptr(layer), self.pools[layer].data_ptr(),
                      self.page_table[b].contiguous().data_ptr(), C, side, m.data_ptr(), codes.data_ptr(),
                      scales.data_ptr(), mins.data_ptr(), _dev.stream())
+                self._note_range(layer, m, scales)
         if r:
             self.res_k[layer][b, :r].copy_(_dev.to_dev(residual_k, allow_bf16=False))
             self.res_v[layer][b, :r].copy_(_dev.to_dev(residual_v, allow_bf16=False))

@@ -395,3 +395,30 @@ def test_exact_kernel_geometries(H, hq, D, bits):
     for splits in (1, 5, 37):  # 37: splits of 16 tokens and empty ones
         out = store.attend(0, q, num_splits=splits, mode=1)
         assert np.abs(out.cpu().numpy() - want).max() <= 1e-5, f"splits {splits}"
+
+
+@pytest.mark.parametrize("where", ["mean", "scale"])
+def test_imported_cache_range_words(where):
+    """A TADAKV1 stream with a mean >= 2^15 (or a group scale >= 2^8) imported by deserialize_cache sets the
+    layer's range words like K1 does, so mode 0 attends it on the exact path (finite, equal to the oracle)."""
+    m = tk()
+    rng = np.random.default_rng(81 + len(where))
+    T, H, D, hq, bits = 300, 8, 128, 32, 8
+    k = rng.normal(size=(T, H, D))
+    v = rng.normal(size=(T, H, D))
+    if where == "mean":
+        v[:, :, 17] += 1e5
+    else:
+        v[:, 3, 17] = rng.choice([-1e6, 1e6], size=T)  # 8-bit group scale ~7e3 >= 2^8
+    k, v = orc.bf16_round(k.astype(np.float32)), orc.bf16_round(v.astype(np.float32))
+    st = orc.LayerState(H, D, bits, 128)
+    orc.append(st, k, v)
+    cache = m.deserialize_cache(orc.dump(st))
+    words = cache.store.range[0].tolist()
+    assert (words[0] >= 15) if where == "mean" else (words[1] >= 8), words
+    q = orc.bf16_round(rng.normal(size=(hq, D)).astype(np.float32))
+    want = orc.attend(q, st, hq)[0]
+    out = cache.store.attend(0, torch.from_numpy(q).cuda().unsqueeze(0), mode=0, out_dtype=torch.float32)[0]
+    out = out.cpu().numpy()
+    assert np.isfinite(out).all()
+    assert np.abs(out - want).max() <= 1e-5 * max(1.0, float(np.abs(want).max()))
