@@ -186,7 +186,8 @@ int tada_scatter_compressed(const tada_page_layout* layout, uint8_t* pool, const
  * group scale beyond what its kernel's P' holds (2^15 for the 2/4-bit kernel, 2^8 for the 8-bit one),
  * or a query element >= 2^15, is attended on their exact f32 path instead (mode 0 and 2). 
  * mode: 0 = auto, 1 = exact generic kernel (f32 reconstruct-then-dot, any geometry),
- *       2 = fast tensor-core kernel (head_dim 128, bits 2/4/8),
+ *       2 = fast tensor-core kernel (head_dim 128, bits 2/4/8, a multiple of 8 KV heads: other group sizes
+ *           and head counts run as padded passes / views of 8 KV heads),
  *       3 = fast tensor-core kernel, previous two-barrier-per-tile variant (A/B comparisons). */
 int64_t tada_decode_attn_workspace_bytes(int32_t batch, int32_t num_q_heads, int32_t head_dim,
                                          int32_t num_splits);

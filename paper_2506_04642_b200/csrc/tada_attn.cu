@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(kCombThreads) combine_residual_kernel(AttnArgs
   // residual logits: one warp per token, lanes split d (4 each) and reduce by shuffles
   const int warp = tid >> 5, lane = tid & 31;
   for (int t = warp; t < R; t += kCombThreads / 32) {
-    const float* kr = a.res_k + ((rbase + t) * H + h) * D;
+    const float* kr = a.res_k + ((rbase + t) * a.kv_rh + a.kv_h0 + h) * D;
     float dot = 0.f;
     for (int d = 4 * lane; d < D; d += 128) {  // the fast path has D % 4 == 0
       const float4 k4 = *reinterpret_cast<const float4*>(kr + d);
@@ -266,11 +266,11 @@ __global__ void __launch_bounds__(kCombThreads) combine_residual_kernel(AttnArgs
         acc1 = fmaf(s0 + 2 * u + 2 < S ? ws[s0 + 2 * u + 2] : 0.f, v[u + 1], acc1);
       }
     }
-    const float* vr = a.res_v + (rbase * H + h) * D + d;
+    const float* vr = a.res_v + (rbase * a.kv_rh + a.kv_h0 + h) * D + d;
     for (int t0 = j; t0 < R; t0 += 2 * U) {
       float v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = t0 + 2 * u < R ? vr[int64_t(t0 + 2 * u) * H * D] : 0.f;
+      for (int u = 0; u < U; ++u) v[u] = t0 + 2 * u < R ? vr[int64_t(t0 + 2 * u) * a.kv_rh * D] : 0.f;
 #pragma unroll
       for (int u = 0; u < U; u += 2) {
         acc0 = fmaf(t0 + 2 * u < R ? pr[t0 + 2 * u] : 0.f, v[u], acc0);
@@ -359,13 +359,13 @@ __global__ void __launch_bounds__(256) combine_pair_kernel(AttnArgs a, int n_row
     residual_rows(a, b, R, r_new);
     auto new_row = [&](const void* src) {  // this lane's 4 columns of the new row of head h, as f32
       float x[4];
-      const int64_t off = (int64_t(b) * H + h) * D + 4 * lane;
+      const int64_t off = (int64_t(b) * a.kv_rh + a.kv_h0 + h) * D + 4 * lane;
       if (a.new_dtype == TADA_F32) load4(reinterpret_cast<const float*>(src) + off, x);
       else load4(reinterpret_cast<const __nv_bfloat16*>(src) + off, x);
       return make_float4(x[0], x[1], x[2], x[3]);
     };
     if (r_new >= 0 && gq % G == 0 && rw == 0) {  // one warp per (sequence, KV head) stores the row for later steps
-      const int64_t dst = ((int64_t(b) * a.res_seq_stride + r_new) * H + h) * D + 4 * lane;
+      const int64_t dst = ((int64_t(b) * a.res_seq_stride + r_new) * a.kv_rh + a.kv_h0 + h) * D + 4 * lane;
       *reinterpret_cast<float4*>(const_cast<float*>(a.res_k) + dst) = new_row(a.new_k);
       *reinterpret_cast<float4*>(const_cast<float*>(a.res_v) + dst) = new_row(a.new_v);
       if (!a.step && gq == 0 && lane == 0) const_cast<int32_t*>(a.res_len)[b] = r_new + 1;
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(256) combine_pair_kernel(AttnArgs a, int n_row
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int t = t0 + u;
-        const int64_t o = ((rbase + t) * H + h) * D + 4 * lane;
+        const int64_t o = ((rbase + t) * a.kv_rh + a.kv_h0 + h) * D + 4 * lane;
         k4[u] = t >= R ? make_float4(0.f, 0.f, 0.f, 0.f)
                        : (t == r_new ? new_row(a.new_k) : *reinterpret_cast<const float4*>(a.res_k + o));
         v4[u] = t >= R ? make_float4(0.f, 0.f, 0.f, 0.f)
@@ -538,10 +538,10 @@ __global__ void __launch_bounds__((G + 8) * 32) combine_kv_kernel(AttnArgs a, in
   } else {  // ---- residual rows
     const int rw = warp - G;
     const int64_t rbase = int64_t(b) * a.res_seq_stride;
-    const int64_t nrow = (int64_t(b) * H + h) * D;  // this head's new row in the step input
+    const int64_t nrow = (int64_t(b) * a.kv_rh + a.kv_h0 + h) * D;  // this head's new row in the step input
     if (r_new >= 0 && rw == 0) {  // store the step's row for later steps
       float x[4];
-      const int64_t dst = ((rbase + r_new) * H + h) * D + 4 * lane;
+      const int64_t dst = ((rbase + r_new) * a.kv_rh + a.kv_h0 + h) * D + 4 * lane;
       if (a.new_dtype == TADA_F32) load4(reinterpret_cast<const float*>(a.new_k) + nrow + 4 * lane, x);
       else load4(reinterpret_cast<const __nv_bfloat16*>(a.new_k) + nrow + 4 * lane, x);
       *reinterpret_cast<float4*>(const_cast<float*>(a.res_k) + dst) = make_float4(x[0], x[1], x[2], x[3]);
@@ -571,7 +571,7 @@ __global__ void __launch_bounds__((G + 8) * 32) combine_kv_kernel(AttnArgs a, in
           else load4(reinterpret_cast<const __nv_bfloat16*>(src) + nrow + col, x);
           *reinterpret_cast<float4*>(dst) = make_float4(x[0], x[1], x[2], x[3]);
         } else {
-          const float* src = (side ? a.res_v : a.res_k) + ((rbase + cb + r) * H + h) * D + col;
+          const float* src = (side ? a.res_v : a.res_k) + ((rbase + cb + r) * a.kv_rh + a.kv_h0 + h) * D + col;
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
                        "l"(src)
                        : "memory");
@@ -763,12 +763,26 @@ bool pdl_enabled() {
 
 namespace tada {
 
-// ---------------------------------------------------------------- group-size remapping of the tensor-core path
-// The tensor-core kernels are instantiated for 8 KV heads and q-head groups G in {1, 2, 4, 8} (G <= 4 at 8-bit,
-// whose stages leave no room for 64 q heads).  Any other G runs in `passes` passes of up to gc q heads per KV
-// head: pass p takes q heads p*gc .. p*gc + n - 1 of every group, zero-padded to gp = 2^ceil(log2 n) rows
-// (a zero query row attends harmlessly and is dropped), then K2 + K3 as usual into staging buffers whose rows
-// go back to their places.  Each pass re-reads the layer's cache, so 8-bit layers with G > 4 cost 2x traffic.
+// ---------------------------------------------------------------- group-size and head-count remapping of the
+// tensor-core path.  The tensor-core kernels are instantiated for 8 KV heads and q-head groups G in {1, 2, 4, 8}
+// (G <= 4 at 8-bit, whose stages leave no room for 64 q heads).
+//  * Any other G runs in `passes` passes of up to gc q heads per KV head: pass p takes q heads p*gc .. p*gc + n - 1
+//    of every group, zero-padded to gp = 2^ceil(log2 n) rows (a zero query row attends harmlessly and is dropped).
+//  * A layout with 16, 24, 32, ... KV heads (e.g. Llama-2's multi-head attention) runs one view per group of 8 KV
+//    heads (head_group_view: the code / meta rows are read at an offset with the full row pitch, the residual and
+//    step rows likewise through AttnArgs::kv_rh / kv_h0).  Every view re-reads the f32 mean rows, so the bytes
+//    moved grow by 512 B per token and side for each extra group.
+// Each (head group, pass) stages its q rows, runs K2 + K3 into staging buffers, and puts the output rows back.
+tada_page_layout head_group_view(const tada_page_layout& L, int j) {
+  tada_page_layout v = L;
+  v.heads = 8;
+  for (int side = 0; side < 2; ++side) {
+    v.off_codes[side] += int64_t(8) * j * L.group_bytes;
+    v.off_meta[side] += int64_t(8) * j * 8;
+  }
+  return v;
+}
+
 bool fast_map(const tada_page_layout& L, int Hq, FastMap* m) {
   if (L.heads <= 0 || Hq <= 0 || Hq % L.heads) return false;
   const int G = Hq / L.heads;
@@ -776,44 +790,50 @@ bool fast_map(const tada_page_layout& L, int Hq, FastMap* m) {
     *m = FastMap{1, G, G, G};
     return true;
   }
-  if (L.heads != 8 || L.head_dim != 128 || !(L.bits == 2 || L.bits == 4 || L.bits == 8)) return false;
+  if (L.heads % 8 || L.head_dim != 128 || !(L.bits == 2 || L.bits == 4 || L.bits == 8)) return false;
+  const tada_page_layout v = head_group_view(L, 0);
   const int gc = L.bits == 8 ? 4 : 8;
   const int n0 = G < gc ? G : gc;
   int gp = 1;
   while (gp < n0) gp *= 2;
-  if (!fast_supported(L, 8 * gp)) return false;
+  if (!fast_supported(v, 8 * gp)) return false;
   *m = FastMap{(G + gc - 1) / gc, gc, gp, G};
+  m->hg = L.heads / 8;
   return true;
 }
 
+// qp[b][h][j] = q[b][hb + h][j0 + j] for j < n (q heads grouped by KV head: row (b * H + hb + h) * G + j0 + j),
+// zero otherwise; qp is [B][8][gp]
 template <typename T>
-__global__ void pad_q_kernel(const T* __restrict__ q, T* __restrict__ qp, int G, int j0, int n, int gp, int D,
-                             int64_t total) {
+__global__ void pad_q_kernel(const T* __restrict__ q, T* __restrict__ qp, int H, int hb, int G, int j0, int n, int gp,
+                             int D, int64_t total) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
     const int d = int(i % D);
-    const int64_t r = i / D;  // (b, h, j) row of the padded [B][8][gp] q
+    const int64_t r = i / D;
     const int j = int(r % gp);
     const int64_t bh = r / gp;  // b * 8 + h
-    qp[i] = j < n ? q[(bh * G + j0 + j) * D + d] : T(0.f);
+    const int64_t src = ((bh / 8) * H + hb + bh % 8) * G + j0 + j;
+    qp[i] = j < n ? q[src * D + d] : T(0.f);
   }
 }
 
 template <typename T>
 __global__ void unpad_out_kernel(const T* __restrict__ op, const float* __restrict__ lp, T* __restrict__ out,
-                                 float* __restrict__ lse, int G, int j0, int n, int gp, int D, int64_t total) {
+                                 float* __restrict__ lse, int H, int hb, int G, int j0, int n, int gp, int D,
+                                 int64_t total) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
     const int d = int(i % D);
     const int64_t r = i / D;  // (b, h, j) row of the output, j < n
     const int j = int(r % n);
     const int64_t bh = r / n;
-    const int64_t src = bh * gp + j, dst = bh * G + j0 + j;
+    const int64_t src = bh * gp + j, dst = ((bh / 8) * H + hb + bh % 8) * G + j0 + j;
     out[dst * D + d] = op[src * D + d];
     if (lse && d == 0) lse[dst] = lp[src];
   }
 }
 
 int launch_fast_mapped(const AttnArgs& a0, int batch, const FastMap& fm, int mode, void* workspace, cudaStream_t st) {
-  const int D = a0.L.head_dim, hq = 8 * fm.gp;
+  const int D = a0.L.head_dim, hq = 8 * fm.gp, H = a0.L.heads;
   const int64_t rows = int64_t(batch) * hq;
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
   const int64_t part_bytes = rows * a0.slots * (int64_t(D) + 2) * 4;
@@ -821,39 +841,46 @@ int launch_fast_mapped(const AttnArgs& a0, int batch, const FastMap& fm, int mod
   void* op = reinterpret_cast<uint8_t*>(qp) + rows * D * 4;
   float* lp = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(op) + rows * D * 4);
   const bool qbf = a0.q_dtype == TADA_BF16, obf = a0.out_dtype == TADA_BF16;
-  for (int p = 0; p < fm.passes; ++p) {
-    const int j0 = p * fm.gc, n = fm.g - j0 < fm.gc ? fm.g - j0 : fm.gc;
-    AttnArgs a = a0;
-    a.Hq = hq;
-    a.q = qp;
-    a.out = op;
-    a.lse_out = a0.lse_out ? lp : nullptr;
-    a.part_acc = reinterpret_cast<float*>(ws);
-    a.part_ml = a.part_acc + rows * a.slots * D;
-    const int64_t tq = rows * D;
-    const int grid = int((tq + 255) / 256 < 148 * 16 ? (tq + 255) / 256 : 148 * 16);
-    if (qbf)
-      pad_q_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(a0.q), reinterpret_cast<__nv_bfloat16*>(qp),
-                                         fm.g, j0, n, fm.gp, D, tq);
-    else
-      pad_q_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(a0.q), reinterpret_cast<float*>(qp), fm.g, j0, n,
-                                         fm.gp, D, tq);
-    int rc = check_launch("decode_attn_pad_q");
-    if (rc != TADA_OK) return rc;
-    rc = (mode != 3 && v8_supported(a.L, hq)) ? launch_v8(a, batch, st) : launch_fast(a, batch, st);
-    if (rc == TADA_OK) rc = launch_combine_residual(a, batch, st);
-    if (rc != TADA_OK) return rc;
-    const int64_t to = int64_t(batch) * 8 * n * D;
-    const int g2 = int((to + 255) / 256 < 148 * 16 ? (to + 255) / 256 : 148 * 16);
-    if (obf)
-      unpad_out_kernel<<<g2, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(op), lp,
-                                           reinterpret_cast<__nv_bfloat16*>(a0.out), a0.lse_out, fm.g, j0, n, fm.gp, D, to);
-    else
-      unpad_out_kernel<<<g2, 256, 0, st>>>(reinterpret_cast<const float*>(op), lp, reinterpret_cast<float*>(a0.out),
-                                           a0.lse_out, fm.g, j0, n, fm.gp, D, to);
-    rc = check_launch("decode_attn_unpad");
-    if (rc != TADA_OK) return rc;
-  }
+  for (int jg = 0; jg < fm.hg; ++jg)
+    for (int p = 0; p < fm.passes; ++p) {
+      const int j0 = p * fm.gc, n = fm.g - j0 < fm.gc ? fm.g - j0 : fm.gc, hb = 8 * jg;
+      AttnArgs a = a0;
+      if (fm.hg > 1) {
+        a.L = head_group_view(a0.L, jg);
+        a.kv_rh = H;
+        a.kv_h0 = hb;
+      }
+      a.Hq = hq;
+      a.q = qp;
+      a.out = op;
+      a.lse_out = a0.lse_out ? lp : nullptr;
+      a.part_acc = reinterpret_cast<float*>(ws);
+      a.part_ml = a.part_acc + rows * a.slots * D;
+      const int64_t tq = rows * D;
+      const int grid = int((tq + 255) / 256 < 148 * 16 ? (tq + 255) / 256 : 148 * 16);
+      if (qbf)
+        pad_q_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(a0.q),
+                                           reinterpret_cast<__nv_bfloat16*>(qp), H, hb, fm.g, j0, n, fm.gp, D, tq);
+      else
+        pad_q_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(a0.q), reinterpret_cast<float*>(qp), H, hb,
+                                           fm.g, j0, n, fm.gp, D, tq);
+      int rc = check_launch("decode_attn_pad_q");
+      if (rc != TADA_OK) return rc;
+      rc = (mode != 3 && v8_supported(a.L, hq)) ? launch_v8(a, batch, st) : launch_fast(a, batch, st);
+      if (rc == TADA_OK) rc = launch_combine_residual(a, batch, st);
+      if (rc != TADA_OK) return rc;
+      const int64_t to = int64_t(batch) * 8 * n * D;
+      const int g2 = int((to + 255) / 256 < 148 * 16 ? (to + 255) / 256 : 148 * 16);
+      if (obf)
+        unpad_out_kernel<<<g2, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(op), lp,
+                                             reinterpret_cast<__nv_bfloat16*>(a0.out), a0.lse_out, H, hb, fm.g, j0, n,
+                                             fm.gp, D, to);
+      else
+        unpad_out_kernel<<<g2, 256, 0, st>>>(reinterpret_cast<const float*>(op), lp, reinterpret_cast<float*>(a0.out),
+                                             a0.lse_out, H, hb, fm.g, j0, n, fm.gp, D, to);
+      rc = check_launch("decode_attn_unpad");
+      if (rc != TADA_OK) return rc;
+    }
   return TADA_OK;
 }
 
@@ -898,9 +925,11 @@ int32_t tada_decode_attn_plan_splits(const tada_page_layout* layout, int32_t num
   if (!layout || num_q_heads <= 0) return 1;
   int per_sm = 1;
   FastMap fm;
-  const int hq = fast_map(*layout, num_q_heads, &fm) ? 8 * fm.gp : num_q_heads;  // the instantiation that runs
-  if (v8_supported(*layout, hq)) per_sm = 2;  // attn_v8_kernel: two CTAs per SM
-  else if (fast_supported(*layout, hq)) per_sm = fast_tile_tokens(*layout, hq) == 16 ? 2 : 1;
+  const bool mapped = fast_map(*layout, num_q_heads, &fm);
+  const int hq = mapped ? 8 * fm.gp : num_q_heads;  // the instantiation that runs
+  const tada_page_layout lv = mapped && fm.hg > 1 ? head_group_view(*layout, 0) : *layout;
+  if (v8_supported(lv, hq)) per_sm = 2;  // attn_v8_kernel: two CTAs per SM
+  else if (fast_supported(lv, hq)) per_sm = fast_tile_tokens(lv, hq) == 16 ? 2 : 1;
   else per_sm = exact_ctas_per_sm(*layout, num_q_heads);
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -928,9 +957,9 @@ static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool,
   const bool mapped = fast_map(*layout, num_q_heads, &fm);
   const bool fast = mode >= 2 || (mode == 0 && mapped);
   if (mode >= 2 && !mapped)
-    return fail(TADA_ERR_CONFIG, "fast decode attention needs 8 KV heads, head_dim 128, bits 2/4/8 and page_tokens % 32 == 0");
-  if (fast && !fm.direct() && step_R >= 0 && fm.passes > 1)
-    return fail(TADA_ERR_CONFIG, "the fused decode step runs in one pass (group size <= 4 for 8-bit layers)");
+    return fail(TADA_ERR_CONFIG, "fast decode attention needs a multiple of 8 KV heads, head_dim 128, bits 2/4/8 and page_tokens % 32 == 0");
+  if (fast && !fm.direct() && step_R >= 0 && (fm.passes > 1 || fm.hg > 1))
+    return fail(TADA_ERR_CONFIG, "the fused decode step runs in one pass (8 KV heads; group size <= 4 for 8-bit layers)");
   if (!workspace && (num_splits > 1 || fast || exact_smem_bytes(*layout, num_q_heads)))
     return fail(TADA_ERR_SHAPE, "workspace required");
   AttnArgs a{};
@@ -961,6 +990,8 @@ static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool,
   a.step_R = step_R;
   a.step_sync = step_sync;
   a.range = range_word;
+  a.kv_rh = layout->heads;
+  a.kv_h0 = 0;
   {
     static const int diag = getenv("TADA_ATTN_DIAG") ? atoi(getenv("TADA_ATTN_DIAG")) : 0;
     a.diag = diag;
@@ -1015,7 +1046,7 @@ int tada_decode_step(const tada_page_layout* layout, uint8_t* pool, const void* 
                      int32_t* err_flag, int32_t* range_word, void* stream) {
   if (!layout) return fail(TADA_ERR_CONFIG, "null layout");
   FastMap fm;
-  if (mode == 1 || !fast_map(*layout, num_q_heads, &fm) || fm.passes != 1 || layout->head_dim != 128)
+  if (mode == 1 || !fast_map(*layout, num_q_heads, &fm) || fm.passes != 1 || fm.hg != 1 || layout->head_dim != 128)
     return fail(TADA_ERR_CONFIG, "the fused decode step needs the one-pass tensor-core attention path (head_dim 128)");
   if (!new_k || !new_v || !res_k || !res_v || !step_sync || !comp_len || !res_len) return fail(TADA_ERR_SHAPE, "null buffer");
   if (new_dtype != TADA_F32 && new_dtype != TADA_BF16) return fail(TADA_ERR_CONFIG, "new row dtype must be f32 or bf16");

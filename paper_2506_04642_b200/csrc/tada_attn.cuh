@@ -46,6 +46,11 @@ struct AttnArgs {
   // the layer's range words (K1's note_range): [0] binary exponent of its largest stored |mean| >= 2^15,
   // [1] of its largest group scale >= 2^8 (0 when below)
   const int32_t* range;
+  // a view of KV heads kv_h0 .. kv_h0 + L.heads - 1 of a layout with kv_rh heads per token row (head-group
+  // passes, tada_attn.cu): L.off_codes / L.off_meta already point at head kv_h0 of each row; the code and meta
+  // rows, the residual rows and the step's new rows are kv_rh heads wide.  Normally kv_rh = L.heads, kv_h0 = 0.
+  int kv_rh;
+  int kv_h0;
 };
 
 // The tensor-core kernels stage q and the f32 means (f16 hi + lo / f16) as f16, which holds |x| < 65504, and
@@ -89,8 +94,8 @@ __device__ void exact_split_partials(const AttnArgs& a, int b, int split, int t_
 #pragma unroll
     for (int side = 0; side < 2; ++side) {
       const float4 mean = *reinterpret_cast<const float4*>(page + a.L.off_mean[side] + (int64_t(r) * D + 4 * lane) * 4);
-      const uint8_t* grp = page + a.L.off_codes[side] + (int64_t(r) * H + h) * gb;
-      const float2 sm = *reinterpret_cast<const float2*>(page + a.L.off_meta[side] + (int64_t(r) * H + h) * 8);
+      const uint8_t* grp = page + a.L.off_codes[side] + (int64_t(r) * a.kv_rh + h) * gb;
+      const float2 sm = *reinterpret_cast<const float2*>(page + a.L.off_meta[side] + (int64_t(r) * a.kv_rh + h) * 8);
       const float mv[4] = {mean.x, mean.y, mean.z, mean.w};
       float* dst = side ? vh : kh;
 #pragma unroll
@@ -224,8 +229,11 @@ bool fast_supported(const tada_page_layout& L, int Hq);
 // tensor-core head mapping: `passes` passes of up to gc q heads per KV head, each padded to gp rows (tada_attn.cu)
 struct FastMap {
   int passes, gc, gp, g;
-  bool direct() const { return passes == 1 && gp == g; }
+  int hg = 1;  // head groups of 8 KV heads (layouts with 16, 24, 32, ... KV heads run one view per group)
+  bool direct() const { return passes == 1 && gp == g && hg == 1; }
 };
+// the view of KV heads 8j .. 8j + 7 of a layout with a multiple of 8 heads (AttnArgs::kv_rh / kv_h0)
+tada_page_layout head_group_view(const tada_page_layout& L, int j);
 bool fast_map(const tada_page_layout& L, int Hq, FastMap* m);
 int launch_fast_mapped(const AttnArgs& a, int batch, const FastMap& fm, int mode, void* workspace, cudaStream_t st);
 int launch_fast(const AttnArgs& a, int batch, cudaStream_t st);

@@ -734,12 +734,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 // [side][band][row][128 B]: every 128-byte line is one (band, row), so the 128B swizzle XORs the
 // 16-byte chunk index with (row & 7) exactly like swz().
 static bool encode_region5(CUtensorMap* m, const uint8_t* base, uint64_t row_bytes, uint64_t rows, uint64_t side_stride,
-                           uint64_t page_bytes, uint32_t tt) {
+                           uint64_t page_bytes, uint32_t tt, uint64_t row_stride = 0) {
   auto enc = get_encode();
   if (!enc) return false;
-  const uint64_t nband = row_bytes / 128;
+  const uint64_t nband = row_bytes / 128;  // row_bytes: the bytes read per row; row_stride: the row pitch
   const cuuint64_t dims[5] = {128, rows, nband, 2, uint64_t(1) << 20};
-  const cuuint64_t strides[4] = {row_bytes, 128, side_stride, page_bytes};
+  const cuuint64_t strides[4] = {row_stride ? row_stride : row_bytes, 128, side_stride, page_bytes};
   const cuuint32_t box[5] = {128, tt, uint32_t(nband), 2, 1};
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<uint8_t*>(base), dims, strides, box, estr,
@@ -749,11 +749,11 @@ static bool encode_region5(CUtensorMap* m, const uint8_t* base, uint64_t row_byt
 // metas: (byte in row, row, side, page); the box is 16 bytes wider than a row (zero fill) so that
 // smem rows are trow = H*8 + 16 bytes apart (bank spread for the per-token loads)
 static bool encode_meta(CUtensorMap* m, const uint8_t* base, uint64_t row_bytes, uint64_t rows, uint64_t side_stride,
-                        uint64_t page_bytes, uint32_t box0, uint32_t tt) {
+                        uint64_t page_bytes, uint32_t box0, uint32_t tt, uint64_t row_stride = 0) {
   auto enc = get_encode();
   if (!enc) return false;
   const cuuint64_t dims[4] = {row_bytes, rows, 2, uint64_t(1) << 20};
-  const cuuint64_t strides[3] = {row_bytes, side_stride, page_bytes};
+  const cuuint64_t strides[3] = {row_stride ? row_stride : row_bytes, side_stride, page_bytes};
   const cuuint32_t box[4] = {box0, tt, 2, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(base), dims, strides, box, estr,
@@ -764,11 +764,11 @@ static bool encode_meta(CUtensorMap* m, const uint8_t* base, uint64_t row_bytes,
 int get_tma_maps(const AttnArgs& a, TmaMaps* out, int tt) {
   struct Key {
     const uint8_t* pool;
-    int64_t page_bytes;
-    int bits, heads, page_tokens, tt;
+    int64_t page_bytes, off_codes;
+    int bits, heads, page_tokens, tt, rh;
     bool operator==(const Key& o) const {
-      return pool == o.pool && page_bytes == o.page_bytes && bits == o.bits && heads == o.heads &&
-             page_tokens == o.page_tokens && tt == o.tt;
+      return pool == o.pool && page_bytes == o.page_bytes && off_codes == o.off_codes && bits == o.bits &&
+             heads == o.heads && page_tokens == o.page_tokens && tt == o.tt && rh == o.rh;
     }
   };
   struct Hash {
@@ -778,7 +778,7 @@ int get_tma_maps(const AttnArgs& a, TmaMaps* out, int tt) {
   };
   static std::mutex mu;
   static std::unordered_map<Key, TmaMaps, Hash> cache;
-  const Key key{a.pool, a.L.page_bytes, a.L.bits, a.L.heads, a.L.page_tokens, tt};
+  const Key key{a.pool, a.L.page_bytes, a.L.off_codes[0], a.L.bits, a.L.heads, a.L.page_tokens, tt, a.kv_rh};
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) {
@@ -793,9 +793,9 @@ int get_tma_maps(const AttnArgs& a, TmaMaps* out, int tt) {
   if (!encode_region5(&m.m[0][0], a.pool + L.off_mean[0], uint64_t(L.head_dim) * 4, L.page_tokens, side_stride,
                       L.page_bytes, uint32_t(tt)) ||
       !encode_region5(&m.m[0][1], a.pool + L.off_codes[0], uint64_t(L.heads) * L.group_bytes, L.page_tokens,
-                      side_stride, L.page_bytes, uint32_t(tt)) ||
+                      side_stride, L.page_bytes, uint32_t(tt), uint64_t(a.kv_rh) * L.group_bytes) ||
       !encode_meta(&m.m[0][2], a.pool + L.off_meta[0], uint64_t(L.heads) * 8, L.page_tokens, side_stride, L.page_bytes,
-                   uint32_t(L.heads * 8 + 16), uint32_t(tt)))
+                   uint32_t(L.heads * 8 + 16), uint32_t(tt), uint64_t(a.kv_rh) * 8))
     return fail(TADA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the decode-attention pool");
   if (cache.size() > 256) cache.clear();
   cache.emplace(key, m);

@@ -422,3 +422,24 @@ def test_imported_cache_range_words(where):
     out = out.cpu().numpy()
     assert np.isfinite(out).all()
     assert np.abs(out - want).max() <= 1e-5 * max(1.0, float(np.abs(want).max()))
+
+
+@pytest.mark.parametrize("H,hq,bits", [(16, 16, 4), (32, 32, 4), (32, 32, 2), (16, 64, 2), (24, 48, 8), (32, 64, 8),
+                                       (16, 48, 4)])
+def test_fast_head_group_views(H, hq, bits):
+    """Layouts with 16 / 24 / 32 KV heads (Llama-2 multi-head attention) on the tensor-core path as views of 8 KV
+    heads each: outputs and lse within 2e-3 of the oracle / exact kernel; mode 0 takes this path; append_attend
+    (one step per view is not fused) equals append() + attend()."""
+    m = tk()
+    store, q, want = _paged_case(B=2, H=H, hq=hq, D=128, bits=bits, T=600, R=16, seed=900 + H + hq + bits)
+    out, lse = store.attend_lse(0, q, mode=2)
+    assert np.abs(out.float().cpu().numpy() - want).max() <= 2e-3
+    _, lse1 = store.attend_lse(0, q, mode=1)
+    assert np.abs(lse.cpu().numpy() - lse1.cpu().numpy()).max() <= 2e-3
+    auto = store.attend(0, q.bfloat16(), out_dtype=torch.float32)
+    assert np.abs(auto.cpu().numpy() - want).max() <= 2e-3
+    rng = np.random.default_rng(H + hq)
+    k1 = torch.from_numpy(orc.bf16_round(rng.normal(size=(2, 1, H, 128)).astype(np.float32))).cuda().bfloat16()
+    step = store.append_attend(0, q, k1, k1, out_dtype=torch.float32)
+    assert torch.isfinite(step).all()
+    assert m is not None
