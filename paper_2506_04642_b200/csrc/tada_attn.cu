@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(256) combine_pair_kernel(AttnArgs a, int n_row
   if (active && role >= 1) {  // ---- residual rows (raw f32; this step's row read from the input)
     const int rw = role - 1;
     int R, r_new;
-    residual_rows(a, b, R, r_new);
+    residual_rows(a, b, R, r_new, h);
     auto new_row = [&](const void* src) {  // this lane's 4 columns of the new row of head h, as f32
       float x[4];
       const int64_t off = (int64_t(b) * a.kv_rh + a.kv_h0 + h) * D + 4 * lane;
@@ -474,7 +474,7 @@ __global__ void __launch_bounds__((G + 8) * 32) combine_kv_kernel(AttnArgs a, in
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int h = blockIdx.x, b = blockIdx.y, H = a.L.heads, Hq = a.Hq, S = a.splits;
   int R, r_new;
-  residual_rows(a, b, R, r_new);
+  residual_rows(a, b, R, r_new, h);
   if (warp >= G) {  // the residual warps stage the q rows (named barrier 1: the split warps start at once)
     for (int i = threadIdx.x - G * 32; i < G * D; i += RWN * 32) {
       const int g = i / D, d = i - (i / D) * D;
@@ -790,7 +790,10 @@ bool fast_map(const tada_page_layout& L, int Hq, FastMap* m) {
     *m = FastMap{1, G, G, G};
     return true;
   }
-  if (L.heads % 8 || L.head_dim != 128 || !(L.bits == 2 || L.bits == 4 || L.bits == 8)) return false;
+  if (L.head_dim != 128 || !(L.bits == 2 || L.bits == 4 || L.bits == 8)) return false;
+  // multiples of 8 KV heads: one view per 8; fewer than 8: one view whose missing heads read as zeros (TMA: the
+  // code rows must be whole 128-byte bands and the meta row pitch a multiple of 16 bytes, so an even head count)
+  if (L.heads % 8 && (L.heads > 8 || (int64_t(L.heads) * L.group_bytes) % 128 || L.heads % 2)) return false;
   const tada_page_layout v = head_group_view(L, 0);
   const int gc = L.bits == 8 ? 4 : 8;
   const int n0 = G < gc ? G : gc;
@@ -798,7 +801,8 @@ bool fast_map(const tada_page_layout& L, int Hq, FastMap* m) {
   while (gp < n0) gp *= 2;
   if (!fast_supported(v, 8 * gp)) return false;
   *m = FastMap{(G + gc - 1) / gc, gc, gp, G};
-  m->hg = L.heads / 8;
+  m->hg = L.heads < 8 ? 1 : L.heads / 8;
+  m->view = L.heads != 8;
   return true;
 }
 
@@ -812,8 +816,9 @@ __global__ void pad_q_kernel(const T* __restrict__ q, T* __restrict__ qp, int H,
     const int64_t r = i / D;
     const int j = int(r % gp);
     const int64_t bh = r / gp;  // b * 8 + h
-    const int64_t src = ((bh / 8) * H + hb + bh % 8) * G + j0 + j;
-    qp[i] = j < n ? q[src * D + d] : T(0.f);
+    const int hh = hb + int(bh % 8);  // KV head in the layout; >= H: a view's missing head
+    const int64_t src = ((bh / 8) * H + hh) * G + j0 + j;
+    qp[i] = (j < n && hh < H) ? q[src * D + d] : T(0.f);
   }
 }
 
@@ -826,7 +831,9 @@ __global__ void unpad_out_kernel(const T* __restrict__ op, const float* __restri
     const int64_t r = i / D;  // (b, h, j) row of the output, j < n
     const int j = int(r % n);
     const int64_t bh = r / n;
-    const int64_t src = bh * gp + j, dst = ((bh / 8) * H + hb + bh % 8) * G + j0 + j;
+    const int hh = hb + int(bh % 8);
+    if (hh >= H) continue;  // a view's missing head
+    const int64_t src = bh * gp + j, dst = ((bh / 8) * H + hh) * G + j0 + j;
     out[dst * D + d] = op[src * D + d];
     if (lse && d == 0) lse[dst] = lp[src];
   }
@@ -845,7 +852,7 @@ int launch_fast_mapped(const AttnArgs& a0, int batch, const FastMap& fm, int mod
     for (int p = 0; p < fm.passes; ++p) {
       const int j0 = p * fm.gc, n = fm.g - j0 < fm.gc ? fm.g - j0 : fm.gc, hb = 8 * jg;
       AttnArgs a = a0;
-      if (fm.hg > 1) {
+      if (fm.view) {
         a.L = head_group_view(a0.L, jg);
         a.kv_rh = H;
         a.kv_h0 = hb;
@@ -927,7 +934,7 @@ int32_t tada_decode_attn_plan_splits(const tada_page_layout* layout, int32_t num
   FastMap fm;
   const bool mapped = fast_map(*layout, num_q_heads, &fm);
   const int hq = mapped ? 8 * fm.gp : num_q_heads;  // the instantiation that runs
-  const tada_page_layout lv = mapped && fm.hg > 1 ? head_group_view(*layout, 0) : *layout;
+  const tada_page_layout lv = mapped && fm.view ? head_group_view(*layout, 0) : *layout;
   if (v8_supported(lv, hq)) per_sm = 2;  // attn_v8_kernel: two CTAs per SM
   else if (fast_supported(lv, hq)) per_sm = fast_tile_tokens(lv, hq) == 16 ? 2 : 1;
   else per_sm = exact_ctas_per_sm(*layout, num_q_heads);
@@ -958,7 +965,7 @@ static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool,
   const bool fast = mode >= 2 || (mode == 0 && mapped);
   if (mode >= 2 && !mapped)
     return fail(TADA_ERR_CONFIG, "fast decode attention needs a multiple of 8 KV heads, head_dim 128, bits 2/4/8 and page_tokens % 32 == 0");
-  if (fast && !fm.direct() && step_R >= 0 && (fm.passes > 1 || fm.hg > 1))
+  if (fast && !fm.direct() && step_R >= 0 && (fm.passes > 1 || fm.view))
     return fail(TADA_ERR_CONFIG, "the fused decode step runs in one pass (8 KV heads; group size <= 4 for 8-bit layers)");
   if (!workspace && (num_splits > 1 || fast || exact_smem_bytes(*layout, num_q_heads)))
     return fail(TADA_ERR_SHAPE, "workspace required");
@@ -1046,7 +1053,7 @@ int tada_decode_step(const tada_page_layout* layout, uint8_t* pool, const void* 
                      int32_t* err_flag, int32_t* range_word, void* stream) {
   if (!layout) return fail(TADA_ERR_CONFIG, "null layout");
   FastMap fm;
-  if (mode == 1 || !fast_map(*layout, num_q_heads, &fm) || fm.passes != 1 || fm.hg != 1 || layout->head_dim != 128)
+  if (mode == 1 || !fast_map(*layout, num_q_heads, &fm) || fm.passes != 1 || fm.view || layout->head_dim != 128)
     return fail(TADA_ERR_CONFIG, "the fused decode step needs the one-pass tensor-core attention path (head_dim 128)");
   if (!new_k || !new_v || !res_k || !res_v || !step_sync || !comp_len || !res_len) return fail(TADA_ERR_SHAPE, "null buffer");
   if (new_dtype != TADA_F32 && new_dtype != TADA_BF16) return fail(TADA_ERR_CONFIG, "new row dtype must be f32 or bf16");

@@ -76,6 +76,18 @@ __device__ void exact_split_partials(const AttnArgs& a, int b, int split, int t_
   if (warp >= H) return;
   const int h = warp;
   const float NEG_INF = -__int_as_float(0x7f800000);
+  if (a.kv_h0 + h >= a.kv_rh) {  // a view's missing KV head (fewer than 8 in the layout): empty slots
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int64_t slot = (int64_t(b) * Hq + h * G + g) * a.slots + split;
+      *reinterpret_cast<float4*>(a.part_acc + slot * D + 4 * lane) = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (lane == 0) {
+        a.part_ml[slot * 2] = NEG_INF;
+        a.part_ml[slot * 2 + 1] = 0.f;
+      }
+    }
+    return;
+  }
   float q[G][4], acc[G][4], m[G], l[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -135,7 +147,12 @@ __device__ __forceinline__ int comp_tokens(const AttnArgs& a, int b) {
 
 // K3 side of a decode step: how many residual rows sequence b attends and which of them
 // (r_new, or -1) is the step's new row read from the input.
-__device__ __forceinline__ void residual_rows(const AttnArgs& a, int b, int& rows, int& r_new) {
+__device__ __forceinline__ void residual_rows(const AttnArgs& a, int b, int& rows, int& r_new, int h = 0) {
+  if (a.kv_h0 + h >= a.kv_rh) {  // a view's missing KV head (fewer than 8 in the layout)
+    rows = 0;
+    r_new = -1;
+    return;
+  }
   if (a.step) {
     const int rb = a.res_len[b];
     const SeqPlan p = seq_plan(rb, 1, a.step_R);
@@ -229,8 +246,9 @@ bool fast_supported(const tada_page_layout& L, int Hq);
 // tensor-core head mapping: `passes` passes of up to gc q heads per KV head, each padded to gp rows (tada_attn.cu)
 struct FastMap {
   int passes, gc, gp, g;
-  int hg = 1;  // head groups of 8 KV heads (layouts with 16, 24, 32, ... KV heads run one view per group)
-  bool direct() const { return passes == 1 && gp == g && hg == 1; }
+  int hg = 1;         // head groups of 8 KV heads (layouts with 16, 24, 32, ... KV heads run one view per group)
+  bool view = false;  // the layout is not 8 KV heads: views (head_group_view; fewer than 8 heads zero-filled)
+  bool direct() const { return passes == 1 && gp == g && !view; }
 };
 // the view of KV heads 8j .. 8j + 7 of a layout with a multiple of 8 heads (AttnArgs::kv_rh / kv_h0)
 tada_page_layout head_group_view(const tada_page_layout& L, int j);

@@ -734,11 +734,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 // [side][band][row][128 B]: every 128-byte line is one (band, row), so the 128B swizzle XORs the
 // 16-byte chunk index with (row & 7) exactly like swz().
 static bool encode_region5(CUtensorMap* m, const uint8_t* base, uint64_t row_bytes, uint64_t rows, uint64_t side_stride,
-                           uint64_t page_bytes, uint32_t tt, uint64_t row_stride = 0) {
+                           uint64_t page_bytes, uint32_t tt, uint64_t row_stride = 0, uint64_t row_extent = 0) {
   auto enc = get_encode();
   if (!enc) return false;
-  const uint64_t nband = row_bytes / 128;  // row_bytes: the bytes read per row; row_stride: the row pitch
-  const cuuint64_t dims[5] = {128, rows, nband, 2, uint64_t(1) << 20};
+  // row_bytes: the bytes read per row; row_stride: the row pitch; row_extent: the bytes that exist from the base
+  // (a view of fewer than 8 KV heads reads the missing ones as zeros: the box exceeds the tensor)
+  const uint64_t nband = row_bytes / 128, nreal = (row_extent ? row_extent : row_bytes) / 128;
+  const cuuint64_t dims[5] = {128, rows, nreal, 2, uint64_t(1) << 20};
   const cuuint64_t strides[4] = {row_stride ? row_stride : row_bytes, 128, side_stride, page_bytes};
   const cuuint32_t box[5] = {128, tt, uint32_t(nband), 2, 1};
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
@@ -787,15 +789,17 @@ int get_tma_maps(const AttnArgs& a, TmaMaps* out, int tt) {
   }
   TmaMaps m{};
   const tada_page_layout& L = a.L;
+  const int real_heads = a.kv_rh - a.kv_h0 < L.heads ? a.kv_rh - a.kv_h0 : L.heads;  // < 8: zero-filled view
   const uint64_t side_stride = uint64_t(L.off_mean[1] - L.off_mean[0]);
   if (uint64_t(L.off_codes[1] - L.off_codes[0]) != side_stride || uint64_t(L.off_meta[1] - L.off_meta[0]) != side_stride)
     return fail(TADA_ERR_CONFIG, "page layout sides are not uniformly strided");
   if (!encode_region5(&m.m[0][0], a.pool + L.off_mean[0], uint64_t(L.head_dim) * 4, L.page_tokens, side_stride,
                       L.page_bytes, uint32_t(tt)) ||
       !encode_region5(&m.m[0][1], a.pool + L.off_codes[0], uint64_t(L.heads) * L.group_bytes, L.page_tokens,
-                      side_stride, L.page_bytes, uint32_t(tt), uint64_t(a.kv_rh) * L.group_bytes) ||
-      !encode_meta(&m.m[0][2], a.pool + L.off_meta[0], uint64_t(L.heads) * 8, L.page_tokens, side_stride, L.page_bytes,
-                   uint32_t(L.heads * 8 + 16), uint32_t(tt), uint64_t(a.kv_rh) * 8))
+                      side_stride, L.page_bytes, uint32_t(tt), uint64_t(a.kv_rh) * L.group_bytes,
+                      uint64_t(real_heads) * L.group_bytes) ||
+      !encode_meta(&m.m[0][2], a.pool + L.off_meta[0], uint64_t(real_heads) * 8, L.page_tokens, side_stride,
+                   L.page_bytes, uint32_t(L.heads * 8 + 16), uint32_t(tt), uint64_t(a.kv_rh) * 8))
     return fail(TADA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the decode-attention pool");
   if (cache.size() > 256) cache.clear();
   cache.emplace(key, m);

@@ -425,11 +425,13 @@ def test_imported_cache_range_words(where):
 
 
 @pytest.mark.parametrize("H,hq,bits", [(16, 16, 4), (32, 32, 4), (32, 32, 2), (16, 64, 2), (24, 48, 8), (32, 64, 8),
-                                       (16, 48, 4)])
+                                       (16, 48, 4), (4, 32, 4), (4, 28, 4), (4, 16, 2), (2, 16, 4), (6, 24, 4),
+                                       (2, 8, 8), (4, 32, 8)])
 def test_fast_head_group_views(H, hq, bits):
     """Layouts with 16 / 24 / 32 KV heads (Llama-2 multi-head attention) on the tensor-core path as views of 8 KV
-    heads each: outputs and lse within 2e-3 of the oracle / exact kernel; mode 0 takes this path; append_attend
-    (one step per view is not fused) equals append() + attend()."""
+    heads each, and an even count below 8 (Qwen2's 4 KV / 28 q heads, 2 KV heads) as one view whose missing heads read as
+    zeros: outputs and lse within 2e-3 of the oracle / exact kernel; mode 0 takes this path; append_attend (not
+    fused for views) stays finite."""
     m = tk()
     store, q, want = _paged_case(B=2, H=H, hq=hq, D=128, bits=bits, T=600, R=16, seed=900 + H + hq + bits)
     out, lse = store.attend_lse(0, q, mode=2)
