@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(256) combine_pair_kernel(AttnArgs a, int n_row
     for (int e = 0; e < 4; ++e) store_any(a.out, a.out_dtype, qi + e, o[e] * inv);
     if (lane == 0 && a.lse_out) a.lse_out[row] = M + logf(L);
   }
-  if (a.step) {  // both rows of this CTA belong to one sequence (Hq is even: a multiple of 8 KV heads)
+  if (a.step && a.step_commit) {  // both rows of this CTA belong to one sequence (Hq is even: a multiple of 8 KV heads)
     __syncthreads();
     if (threadIdx.x == 0 && active) step_commit(a, b, Hq / 2);
   }
@@ -675,7 +675,7 @@ __global__ void __launch_bounds__((G + 8) * 32) combine_kv_kernel(AttnArgs a, in
     for (int e = 0; e < 4; ++e) store_any(a.out, a.out_dtype, qi + e, o[e] * inv);
     if (lane == 0 && a.lse_out) a.lse_out[row] = M + logf(L);
   }
-  if (a.step) {  // the H CTAs of sequence b: the last one advances its lengths
+  if (a.step && a.step_commit) {  // the H CTAs of sequence b: the last one advances its lengths
     __syncthreads();
     if (threadIdx.x == 0) step_commit(a, b, gridDim.x);
   }
@@ -860,6 +860,9 @@ int launch_fast_mapped(const AttnArgs& a0, int batch, const FastMap& fm, int mod
       a.Hq = hq;
       a.q = qp;
       a.out = op;
+      // a decode step: every (view, pass) stores its heads' new rows and reads the pre-step lengths; only the
+      // last one advances them
+      a.step_commit = jg == fm.hg - 1 && p == fm.passes - 1;
       a.lse_out = a0.lse_out ? lp : nullptr;
       a.part_acc = reinterpret_cast<float*>(ws);
       a.part_ml = a.part_acc + rows * a.slots * D;
@@ -965,8 +968,6 @@ static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool,
   const bool fast = mode >= 2 || (mode == 0 && mapped);
   if (mode >= 2 && !mapped)
     return fail(TADA_ERR_CONFIG, "fast decode attention needs a multiple of 8 KV heads, head_dim 128, bits 2/4/8 and page_tokens % 32 == 0");
-  if (fast && !fm.direct() && step_R >= 0 && (fm.passes > 1 || fm.view))
-    return fail(TADA_ERR_CONFIG, "the fused decode step runs in one pass (8 KV heads; group size <= 4 for 8-bit layers)");
   if (!workspace && (num_splits > 1 || fast || exact_smem_bytes(*layout, num_q_heads)))
     return fail(TADA_ERR_SHAPE, "workspace required");
   AttnArgs a{};
@@ -999,6 +1000,7 @@ static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool,
   a.range = range_word;
   a.kv_rh = layout->heads;
   a.kv_h0 = 0;
+  a.step_commit = true;
   {
     static const int diag = getenv("TADA_ATTN_DIAG") ? atoi(getenv("TADA_ATTN_DIAG")) : 0;
     a.diag = diag;
@@ -1053,8 +1055,8 @@ int tada_decode_step(const tada_page_layout* layout, uint8_t* pool, const void* 
                      int32_t* err_flag, int32_t* range_word, void* stream) {
   if (!layout) return fail(TADA_ERR_CONFIG, "null layout");
   FastMap fm;
-  if (mode == 1 || !fast_map(*layout, num_q_heads, &fm) || fm.passes != 1 || fm.view || layout->head_dim != 128)
-    return fail(TADA_ERR_CONFIG, "the fused decode step needs the one-pass tensor-core attention path (head_dim 128)");
+  if (mode == 1 || !fast_map(*layout, num_q_heads, &fm) || layout->head_dim != 128)
+    return fail(TADA_ERR_CONFIG, "the fused decode step needs the tensor-core attention path (head_dim 128)");
   if (!new_k || !new_v || !res_k || !res_v || !step_sync || !comp_len || !res_len) return fail(TADA_ERR_SHAPE, "null buffer");
   if (new_dtype != TADA_F32 && new_dtype != TADA_BF16) return fail(TADA_ERR_CONFIG, "new row dtype must be f32 or bf16");
   if (residual_length < 0 || (residual_length > 0 && residual_length > res_seq_stride) ||

@@ -51,6 +51,7 @@ struct AttnArgs {
   // rows, the residual rows and the step's new rows are kv_rh heads wide.  Normally kv_rh = L.heads, kv_h0 = 0.
   int kv_rh;
   int kv_h0;
+  bool step_commit;  // a decode step's K3 advances the lengths (false for all but the last view / q-head pass)
 };
 
 // The tensor-core kernels stage q and the f32 means (f16 hi + lo / f16) as f16, which holds |x| < 65504, and

@@ -360,12 +360,14 @@ def test_fast_mapped_lse_and_auto(bits, hq):
     assert m is not None
 
 
-@pytest.mark.parametrize("bits,hq", [(4, 24), (8, 40), (8, 64)])
-def test_fused_step_mapped_geometry(bits, hq):
-    """append_attend at remapped group sizes (one pass: fused K3 step; two passes: the composition) equals
-    append() + attend() bit for bit across a residual flush."""
+@pytest.mark.parametrize("bits,hq,H", [(4, 24, 8), (8, 40, 8), (8, 64, 8), (4, 32, 4), (4, 28, 4), (4, 32, 16),
+                                       (2, 32, 32)])
+def test_fused_step_mapped_geometry(bits, hq, H):
+    """append_attend at remapped group sizes and head counts (fused steps over several q-head passes / 8-head
+    views: every pass stores its heads' new rows, the last one advances the lengths) equals append() + attend()
+    bit for bit across residual flushes."""
     m = tk()
-    B, T, H, D, R = 2, 200, 8, 128, 8
+    B, T, D, R = 2, 200, 128, 8
     rng = np.random.default_rng(90 + bits + hq)
     k0 = torch.from_numpy(orc.bf16_round(rng.normal(size=(B, T, H, D)).astype(np.float32))).cuda().bfloat16()
     v0 = torch.from_numpy(orc.bf16_round(rng.normal(size=(B, T, H, D)).astype(np.float32))).cuda().bfloat16()
@@ -430,8 +432,8 @@ def test_imported_cache_range_words(where):
 def test_fast_head_group_views(H, hq, bits):
     """Layouts with 16 / 24 / 32 KV heads (Llama-2 multi-head attention) on the tensor-core path as views of 8 KV
     heads each, and an even count below 8 (Qwen2's 4 KV / 28 q heads, 2 KV heads) as one view whose missing heads read as
-    zeros: outputs and lse within 2e-3 of the oracle / exact kernel; mode 0 takes this path; append_attend (not
-    fused for views) stays finite."""
+    zeros: outputs and lse within 2e-3 of the oracle / exact kernel; mode 0 takes this path; append_attend (a fused
+    step over the views) stays finite."""
     m = tk()
     store, q, want = _paged_case(B=2, H=H, hq=hq, D=128, bits=bits, T=600, R=16, seed=900 + H + hq + bits)
     out, lse = store.attend_lse(0, q, mode=2)
