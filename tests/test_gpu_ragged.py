@@ -116,12 +116,13 @@ def test_ragged_append_rope_equals_composition():
                 assert torch.equal(x, y), (s, name)
 
 
-@pytest.mark.parametrize("hq", [32, 64])
-def test_decode_graph_replay_equals_eager(hq):
+@pytest.mark.parametrize("hq,H", [(32, 8), (64, 8), (28, 4), (32, 16), (24, 8)])
+def test_decode_graph_replay_equals_eager(hq, H):
     """A DecodeGraph captured once and replayed for 24 steps (two layers, plan (4, 2), R = 8: every sequence
-    flushes during replays, at different steps) == the same steps run eagerly through append_attend."""
+    flushes during replays, at different steps) == the same steps run eagerly through append_attend; also for
+    4 / 16 KV heads (8-head views) and a padded group size."""
     m = tk()
-    rng = np.random.default_rng(90 + hq)
+    rng = np.random.default_rng(90 + hq + H)
     lens = [20, 5, 33, 12]
     B, n, L, R = len(lens), max(lens), 2, 8
     k = torch.from_numpy(_rows(rng, B, n, H, D)).cuda().bfloat16()
