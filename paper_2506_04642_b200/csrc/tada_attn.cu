@@ -249,39 +249,41 @@ __global__ void __launch_bounds__(kCombThreads) combine_residual_kernel(AttnArgs
     lsum += w * ml[2 * s2 + 1];
   }
   const float L = block_reduce(lsum, red, false);  // its barrier also publishes pr / ws
-  // output: thread = (half j, d); each half takes every other slot and residual token
+  // output: thread = (half j, d); with D <= 128 each of two halves takes every other slot and residual token,
+  // with D up to 256 one half takes them all
+  const int NH = 2 * D <= kCombThreads ? 2 : 1;
   const int j = tid / D, d = tid - j * D;
-  if (j < 2) {
+  if (j < NH) {
     // the partial slots live in L2 (written by K2 just before): issue a batch of loads, then the FMAs
     constexpr int U = 8;
     const float* pa = a.part_acc + (int64_t(b) * Hq + gq) * a.slots * D + d;
     float acc0 = 0.f, acc1 = 0.f;
-    for (int s0 = j; s0 < S; s0 += 2 * U) {
+    for (int s0 = j; s0 < S; s0 += NH * U) {
       float v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = s0 + 2 * u < S ? pa[int64_t(s0 + 2 * u) * D] : 0.f;
+      for (int u = 0; u < U; ++u) v[u] = s0 + NH * u < S ? pa[int64_t(s0 + NH * u) * D] : 0.f;
 #pragma unroll
       for (int u = 0; u < U; u += 2) {
-        acc0 = fmaf(s0 + 2 * u < S ? ws[s0 + 2 * u] : 0.f, v[u], acc0);
-        acc1 = fmaf(s0 + 2 * u + 2 < S ? ws[s0 + 2 * u + 2] : 0.f, v[u + 1], acc1);
+        acc0 = fmaf(s0 + NH * u < S ? ws[s0 + NH * u] : 0.f, v[u], acc0);
+        acc1 = fmaf(s0 + NH * (u + 1) < S ? ws[s0 + NH * (u + 1)] : 0.f, v[u + 1], acc1);
       }
     }
     const float* vr = a.res_v + (rbase * a.kv_rh + a.kv_h0 + h) * D + d;
-    for (int t0 = j; t0 < R; t0 += 2 * U) {
+    for (int t0 = j; t0 < R; t0 += NH * U) {
       float v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = t0 + 2 * u < R ? vr[int64_t(t0 + 2 * u) * a.kv_rh * D] : 0.f;
+      for (int u = 0; u < U; ++u) v[u] = t0 + NH * u < R ? vr[int64_t(t0 + NH * u) * a.kv_rh * D] : 0.f;
 #pragma unroll
       for (int u = 0; u < U; u += 2) {
-        acc0 = fmaf(t0 + 2 * u < R ? pr[t0 + 2 * u] : 0.f, v[u], acc0);
-        acc1 = fmaf(t0 + 2 * u + 2 < R ? pr[t0 + 2 * u + 2] : 0.f, v[u + 1], acc1);
+        acc0 = fmaf(t0 + NH * u < R ? pr[t0 + NH * u] : 0.f, v[u], acc0);
+        acc1 = fmaf(t0 + NH * (u + 1) < R ? pr[t0 + NH * (u + 1)] : 0.f, v[u + 1], acc1);
       }
     }
     part[j * D + d] = acc0 + acc1;
   }
   __syncthreads();
   for (int dd = tid; dd < D; dd += kCombThreads) {
-    store_any(a.out, a.out_dtype, qi + dd, (part[dd] + part[D + dd]) / L);
+    store_any(a.out, a.out_dtype, qi + dd, (NH == 2 ? part[dd] + part[D + dd] : part[dd]) / L);
     if (dd == 0 && a.lse_out) a.lse_out[int64_t(b) * Hq + gq] = M + logf(L);
   }
 }

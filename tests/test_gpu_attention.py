@@ -387,10 +387,11 @@ def test_fused_step_mapped_geometry(bits, hq, H):
 
 
 @pytest.mark.parametrize("H,hq,D", [(8, 32, 128), (8, 8, 128), (8, 64, 128), (32, 32, 128), (16, 32, 128), (4, 32, 128),
-                                    (2, 16, 128), (1, 8, 128), (32, 64, 128), (8, 24, 64), (4, 4, 64), (16, 48, 64)])
+                                    (2, 16, 128), (1, 8, 128), (32, 64, 128), (8, 24, 64), (4, 4, 64), (16, 48, 64),
+                                    (8, 16, 256), (4, 16, 256), (8, 32, 32), (1, 4, 32)])
 @pytest.mark.parametrize("bits", [2, 4, 8, 16])
 def test_exact_kernel_geometries(H, hq, D, bits):
-    """The exact f32 kernel (mode 1: attn_exact2_kernel for head_dim 64 / 128) at MHA, GQA and MQA shapes and
+    """The exact f32 kernel (mode 1: attn_exact2_kernel for head_dim 32 / 64 / 128 / 256) at MHA, GQA and MQA shapes and
     every width, ragged tails and several splits: within the reference's 1e-5 streaming bar."""
     store, q, want = _paged_case(B=2, H=H, hq=hq, D=D, bits=bits, T=333, R=16, seed=700 + H + hq + D + bits,
                                  poison=True)
