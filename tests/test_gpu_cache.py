@@ -225,3 +225,31 @@ def test_deserialize_untrusted_residual_header():
     cache.append_tokens(k[7:], v[7:])
     orc.append(ref, k[7:], v[7:])
     assert m.serialize_cache(cache) == orc.dump(ref)
+
+
+@pytest.mark.parametrize("H,D", [(4, 256), (1, 64), (16, 128), (2, 32), (3, 96), (32, 128)])
+@pytest.mark.parametrize("bits", [2, 4, 8, 16])
+def test_append_other_geometries_bit_exact(H, D, bits):
+    """K1 (the generic quant_append_kernel off H=8/D=128; the fast kernel there) at other head counts and head
+    dims, bf16 and f32 inputs, with a residual flush: the TADAKV1 bytes equal the oracle's; decode attention
+    (mode 0) is within 1e-5 of the oracle where it runs exact and 2e-3 on the tensor-core views."""
+    import torch
+
+    m = tk()
+    rng = np.random.default_rng(1200 + H + D + bits)
+    T, R, hq = 150, 16, 2 * H
+    k = orc.bf16_round(rng.normal(size=(T, H, D)).astype(np.float32))
+    v = orc.bf16_round(rng.normal(size=(T, H, D)).astype(np.float32))
+    for dtype in (torch.bfloat16, torch.float32):
+        cache = m.CompressedLayerCache(H, D, bits, R)
+        cache.append_tokens(torch.from_numpy(k[:70]).cuda().to(dtype), torch.from_numpy(v[:70]).cuda().to(dtype))
+        cache.append_tokens(torch.from_numpy(k[70:]).cuda().to(dtype), torch.from_numpy(v[70:]).cuda().to(dtype))
+        st = orc.LayerState(H, D, bits, R)
+        orc.append(st, k, v)
+        assert m.serialize_cache(cache) == orc.dump(st), dtype
+    q = orc.bf16_round(rng.normal(size=(hq, D)).astype(np.float32))
+    want = orc.attend(q, st, hq)[0]
+    out = cache.store.attend(0, torch.from_numpy(q).cuda().unsqueeze(0), out_dtype=torch.float32)[0].cpu().numpy()
+    assert np.abs(out - want).max() <= 2e-3
+    exact = m.attend_streaming(q, cache, m.ModelConfig(1, hq, H, D, R, m.RopeParams(D), m.PrecisionPlan((bits,)))).output
+    assert np.abs(exact - want).max() <= 1e-5
