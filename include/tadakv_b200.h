@@ -245,6 +245,10 @@ int tada_decode_step(const tada_page_layout* layout, uint8_t* pool, const void* 
  * with >= 256 tokens per split. */
 int32_t tada_decode_attn_plan_splits(const tada_page_layout* layout, int32_t num_q_heads, int32_t batch,
                                      int64_t max_tokens);
+/* The same for the kernel a given mode runs (mode 1: the exact kernels, which also take splits down to 64
+ * tokens when 256-token splits would leave SMs idle, e.g. one sequence). */
+int32_t tada_decode_attn_plan_splits_mode(const tada_page_layout* layout, int32_t num_q_heads, int32_t batch,
+                                          int64_t max_tokens, int32_t mode);
 
 /* Suggested split count assuming one CTA per SM on a 148-SM B200 (geometry-agnostic). */
 int32_t tada_decode_attn_suggest_splits(int32_t batch, int64_t max_tokens, int32_t page_tokens);

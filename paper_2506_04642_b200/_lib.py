@@ -76,6 +76,7 @@ SIGNATURES = {
                                I32, P, F, I32, P, P, I32, I32, P, P, P]),
     "tada_decode_attn_suggest_splits": (I32, [I32, I64, I32]),
     "tada_decode_attn_plan_splits": (I32, [C.POINTER(PageLayout), I32, I32, I64]),
+    "tada_decode_attn_plan_splits_mode": (I32, [C.POINTER(PageLayout), I32, I32, I64, I32]),
 }
 
 _lib = None

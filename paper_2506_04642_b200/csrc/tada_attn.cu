@@ -903,17 +903,23 @@ using namespace tada;
 extern "C" {
 
 int64_t tada_decode_attn_workspace_bytes(int32_t batch, int32_t num_q_heads, int32_t head_dim, int32_t num_splits) {
-  // slots = splits + 1 (the tensor-core path puts the residual rows in an extra slot); a remapped group size
-  // (FastMap) runs with up to 2 * num_q_heads padded q heads and stages their q, outputs and lse here too
-  const int64_t direct = int64_t(batch) * num_q_heads * (num_splits + 1) * (int64_t(head_dim) + 2) * 4;
-  return 2 * direct + int64_t(batch) * 2 * num_q_heads * (2 * int64_t(head_dim) + 1) * 4 + 256;
+  // slots = splits + 1 (the tensor-core path puts the residual rows in an extra slot); a remapped layout or
+  // group size (FastMap) runs views of 8 KV heads x gp <= 8 padded q heads, i.e. <= 64 q rows per sequence, and
+  // stages their q, outputs and lse here too
+  const int64_t rows = int64_t(batch) * (num_q_heads > 64 ? num_q_heads : 64);
+  return rows * (num_splits + 1) * (int64_t(head_dim) + 2) * 4 + int64_t(batch) * 64 * (2 * int64_t(head_dim) + 1) * 4 +
+         256;
 }
 
 // Split count for `slots` concurrently resident CTAs: the fewest whole waves whose last wave is
 // >= 90% full, keeping >= 256 tokens per split (fewer, longer splits amortise the per-CTA q setup).
-static int32_t plan_splits(int64_t slots, int32_t batch, int64_t max_tokens) {
+static int32_t plan_splits(int64_t slots, int32_t batch, int64_t max_tokens, bool short_ok = false) {
   if (batch <= 0 || max_tokens <= 0) return 1;
-  const int64_t max_s = (max_tokens + 255) / 256;
+  // >= 256 tokens per split amortise the per-CTA q setup; for the exact kernel (short_ok), when that leaves SMs
+  // idle (small batches, short caches), splits go down to 64 tokens (the tensor-core path's K3 merges the
+  // splits of a head on one CTA, so more splits cost it more than they gain at small batches)
+  int64_t max_s = (max_tokens + 255) / 256;
+  if (short_ok && max_s * batch < slots) max_s = (max_tokens + 63) / 64;
   int64_t best = 1;
   for (int64_t waves = 1; waves <= 8; ++waves) {
     const int64_t s = waves * slots / batch;
@@ -932,20 +938,25 @@ int32_t tada_decode_attn_suggest_splits(int32_t batch, int64_t max_tokens, int32
   return plan_splits(148, batch, max_tokens);
 }
 
-int32_t tada_decode_attn_plan_splits(const tada_page_layout* layout, int32_t num_q_heads, int32_t batch,
-                                     int64_t max_tokens) {
+int32_t tada_decode_attn_plan_splits_mode(const tada_page_layout* layout, int32_t num_q_heads, int32_t batch,
+                                          int64_t max_tokens, int32_t mode) {
   if (!layout || num_q_heads <= 0) return 1;
   int per_sm = 1;
   FastMap fm;
-  const bool mapped = fast_map(*layout, num_q_heads, &fm);
+  const bool mapped = mode != 1 && fast_map(*layout, num_q_heads, &fm);  // else the exact kernels run
   const int hq = mapped ? 8 * fm.gp : num_q_heads;  // the instantiation that runs
   const tada_page_layout lv = mapped && fm.view ? head_group_view(*layout, 0) : *layout;
-  if (v8_supported(lv, hq)) per_sm = 2;  // attn_v8_kernel: two CTAs per SM
-  else if (fast_supported(lv, hq)) per_sm = fast_tile_tokens(lv, hq) == 16 ? 2 : 1;
+  if (mapped && v8_supported(lv, hq)) per_sm = 2;  // attn_v8_kernel: two CTAs per SM
+  else if (mapped && fast_supported(lv, hq)) per_sm = fast_tile_tokens(lv, hq) == 16 ? 2 : 1;
   else per_sm = exact_ctas_per_sm(*layout, num_q_heads);
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return plan_splits(int64_t(sms) * per_sm, batch, max_tokens);
+  return plan_splits(int64_t(sms) * per_sm, batch, max_tokens, !mapped);
+}
+
+int32_t tada_decode_attn_plan_splits(const tada_page_layout* layout, int32_t num_q_heads, int32_t batch,
+                                     int64_t max_tokens) {
+  return tada_decode_attn_plan_splits_mode(layout, num_q_heads, batch, max_tokens, 0);
 }
 
 static int decode_attn_impl(const tada_page_layout* layout, const uint8_t* pool, const void* q, int32_t q_dtype,

@@ -315,15 +315,15 @@ class PagedKVCache:
             self._ws = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
         return self._ws
 
-    def suggest_splits(self, layer: int, num_q_heads: int | None = None) -> int:
-        """Split-K factor for this layer's kernel (whole waves of resident CTAs on this device)."""
+    def suggest_splits(self, layer: int, num_q_heads: int | None = None, mode: int = 0) -> int:
+        """Split-K factor for this layer's kernel in ``mode`` (whole waves of resident CTAs on this device)."""
         from ._lib import load
 
         self._refresh()
         tokens = int((self.comp_host[layer] + self.res_host[layer]).max())
         if num_q_heads is None:
             return int(load().tada_decode_attn_suggest_splits(self.B, tokens, self.P))
-        return int(load().tada_decode_attn_plan_splits(self._layout_ptr(layer), num_q_heads, self.B, tokens))
+        return int(load().tada_decode_attn_plan_splits_mode(self._layout_ptr(layer), num_q_heads, self.B, tokens, mode))
 
     def attend(self, layer: int, q: torch.Tensor, out: torch.Tensor | None = None, out_dtype=torch.float32,
                num_splits: int | None = None, mode: int = 0, scale: float | None = None) -> torch.Tensor:
@@ -342,7 +342,7 @@ class PagedKVCache:
         if q.dtype not in (torch.float32, torch.bfloat16):
             q = q.float()
         q = q.contiguous()
-        splits = num_splits or self.suggest_splits(layer, hq)
+        splits = num_splits or self.suggest_splits(layer, hq, mode)
         ws = self.workspace(hq, splits)
         out = self._out(out, hq, out_dtype)
         sc = np.float32(1.0 / math.sqrt(self.D)) if scale is None else np.float32(scale)
@@ -391,7 +391,7 @@ class PagedKVCache:
             k1_rows = int(cnt_res.max()) if ncomp.any() else -1
             self._ensure_pages(max(1, int((self.comp_host[layer] + ncomp).max())))
             self._res_reserve(layer, int(res_after.max()))
-        splits = num_splits or self.suggest_splits(layer, hq)
+        splits = num_splits or self.suggest_splits(layer, hq, mode)
         ws = self.workspace(hq, splits)
         out = self._out(out, hq, out_dtype)
         sc = np.float32(1.0 / math.sqrt(self.D)) if scale is None else np.float32(scale)
@@ -427,7 +427,7 @@ class PagedKVCache:
         if q.dtype not in (torch.float32, torch.bfloat16):
             q = q.float()
         q = q.contiguous()
-        splits = num_splits or self.suggest_splits(layer, hq)
+        splits = num_splits or self.suggest_splits(layer, hq, mode)
         ws = self.workspace(hq, splits)
         out = torch.empty((self.B, hq, self.D), dtype=torch.float32, device=self.dev)
         lse = torch.empty((self.B, hq), dtype=torch.float32, device=self.dev)

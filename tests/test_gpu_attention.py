@@ -439,6 +439,8 @@ def test_fast_head_group_views(H, hq, bits):
     store, q, want = _paged_case(B=2, H=H, hq=hq, D=128, bits=bits, T=600, R=16, seed=900 + H + hq + bits)
     out, lse = store.attend_lse(0, q, mode=2)
     assert np.abs(out.float().cpu().numpy() - want).max() <= 2e-3
+    many = store.attend(0, q, mode=2, num_splits=37, out_dtype=torch.float32)  # the staging fits the workspace
+    assert np.abs(many.cpu().numpy() - want).max() <= 2e-3
     _, lse1 = store.attend_lse(0, q, mode=1)
     assert np.abs(lse.cpu().numpy() - lse1.cpu().numpy()).max() <= 2e-3
     auto = store.attend(0, q.bfloat16(), out_dtype=torch.float32)

@@ -41,7 +41,7 @@ def main():
             store.append(layer, k, v)
     q = torch.randn((B, args.hq, D), generator=g, device="cuda").bfloat16()
     out = torch.empty((B, args.hq, D), dtype=torch.bfloat16, device="cuda")
-    splits = args.splits or store.suggest_splits(0, args.hq)
+    splits = args.splits or store.suggest_splits(0, args.hq, args.mode)
     for i in range(3):
         store.attend(i % args.layers, q, out=out, num_splits=splits, mode=args.mode)
     torch.cuda.synchronize()
