@@ -83,8 +83,10 @@ def _attend(q, layer, cfg, return_scores, splits):
 
 
 def attend_naive(q, layer: CompressedLayerCache, cfg: ModelConfig, return_scores: bool = False) -> AttentionOutput:
-    """Single-position attention over the whole cache, one pass (attention.py:66-91)."""
-    return _attend(q, layer, cfg, return_scores, splits=1)
+    """Single-position attention over the whole cache (attention.py:66-91).  The reference does one pass; the
+    device runs the same exact kernel split-K like attend_streaming (only the f32 summation order differs, well
+    inside the reference's own 1e-5 streaming-vs-naive bar), so a long cache is not one CTA's work."""
+    return _attend(q, layer, cfg, return_scores, splits=None)
 
 
 def attend_streaming(q, layer: CompressedLayerCache, cfg: ModelConfig, block: BlockSpec = BlockSpec(),
