@@ -32,6 +32,7 @@ constexpr int NTHR = 256;
 struct Plan {
   int tt;  // tokens per tile (16)
   int H, G, Hq, gb, gt, nqc, upt, RS, CRS, QS, PS;
+  int gs;  // q rows per KV head in shared memory: G, or G padded to gt (G in 3, 5, 6, 7) with zero rows
   int sb;  // bytes per stage; stage st starts at st * sb
   int off_km, off_vm, off_kc, off_vc, off_kx, off_vx;  // within a stage
   int off_q, off_s, off_p, off_corr, off_ml, total;
@@ -50,6 +51,12 @@ inline bool plan(const tada_page_layout& L, int Hq, Plan* out) {
   p.gt = 1;  // q heads per unit: the largest power of two <= 8 dividing G
   while (p.gt < 8 && p.G % (2 * p.gt) == 0) p.gt *= 2;
   p.nqc = p.G / p.gt;
+  p.gs = p.G;
+  if (p.G < 8 && p.gt != p.G) {  // G in 3, 5, 6, 7: one unit of gt = 4 / 8 rows per KV head, the extra rows zero
+    p.gt = p.G <= 4 ? 4 : 8;
+    p.nqc = 1;
+    p.gs = p.gt;
+  }
   const int units = p.H * p.nqc * (D / 4);
   p.upt = (units + NTHR - 1) / NTHR;
   if (p.upt == 3) p.upt = 4;
@@ -75,11 +82,12 @@ inline bool plan(const tada_page_layout& L, int Hq, Plan* out) {
     p.off_vx = take(TT * p.H * 8);
     p.sb = off;
     off = 2 * p.sb;
-    p.off_q = take(Hq * p.QS * 4);
-    p.off_s = take(Hq * p.PS * 4);  // scores, then the weights P in place
+    const int hqs = p.H * p.gs;  // q rows in shared memory
+    p.off_q = take(hqs * p.QS * 4);
+    p.off_s = take(hqs * p.PS * 4);  // scores, then the weights P in place
     p.off_p = p.off_s;
-    p.off_corr = take(Hq * 4);
-    p.off_ml = take(Hq * 8);
+    p.off_corr = take(hqs * 4);
+    p.off_ml = take(hqs * 8);
     p.total = off;
     if (p.total <= 220 * 1024) {
       *out = p;
@@ -164,13 +172,19 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
   const int C = comp_tokens(a, b);
   int t_begin, t_end;
   split_range(C, a.splits, split, TT, t_begin, t_end);
-  for (int i = tid; i < Hq * D; i += NTHR) {
-    const int64_t qi = int64_t(b) * Hq * D + i;
+  const int gs = pl.gs, hqs = H * gs;  // shared-memory q rows: row h * gs + j is q head h * G + j (j < G), else 0
+  for (int i = tid; i < hqs * D; i += NTHR) {
+    const int r = i / D, dd = i - r * D, j = r % gs;
+    if (j >= G) {
+      qs[r * pl.QS + dd + (dd >= D / 2 ? 4 : 0)] = 0.f;
+      continue;
+    }
+    const int64_t qi = (int64_t(b) * Hq + (r / gs) * G + j) * D + dd;
     const int g = i / D, d = i - g * D;
     qs[g * pl.QS + d + (d >= D / 2 ? 4 : 0)] = a.q_dtype == TADA_F32 ? reinterpret_cast<const float*>(a.q)[qi]
                                                                     : to_f32(reinterpret_cast<const __nv_bfloat16*>(a.q)[qi]);
   }
-  for (int g = tid; g < Hq; g += NTHR) ml[g] = make_float2(NEG_INF, 0.f);
+  for (int g = tid; g < hqs; g += NTHR) ml[g] = make_float2(NEG_INF, 0.f);
   const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
   const int pshift = (P & (P - 1)) == 0 ? __ffs(P) - 1 : -1;
 
@@ -225,7 +239,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
 
     // ---- phase 1: lane = (token, column half), warp = (KV head, q chunk); the halves meet by one shuffle
     for (int u = warp; u < H * nqc; u += NTHR / 32) {
-      const int h = u / nqc, g0 = h * G + (u - h * nqc) * GT;
+      const int h = u / nqc, g0 = h * gs + (u - h * nqc) * GT;  // shared-memory row of the unit's first q head
       const int t = lane & (TT - 1), dh = (lane / TT) * (D / 2);
       const float* mrow = km + t * pl.RS;
       const uint8_t* crow = kc + t * pl.CRS + h * gb;
@@ -303,7 +317,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
       const int u = tid + NTHR * i;
       if (u >= H * nqc * (D / 4)) continue;
       const int hq = u / (D / 4), c = u - hq * (D / 4);
-      const int h = hq / nqc, g0 = h * G + (hq - h * nqc) * GT, d0 = 4 * c;
+      const int h = hq / nqc, g0 = h * gs + (hq - h * nqc) * GT, d0 = 4 * c;
 #pragma unroll
       for (int g = 0; g < GT; ++g) {
         const float cf = corr[g0 + g];
@@ -368,17 +382,19 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
     const int u = tid + NTHR * i;
     if (u >= H * nqc * (D / 4)) continue;
     const int hq = u / (D / 4), c = u - hq * (D / 4);
-    const int h = hq / nqc, g0 = h * G + (hq - h * nqc) * GT;
+    const int h = hq / nqc, qc0 = (hq - h * nqc) * GT;
 #pragma unroll
     for (int g = 0; g < GT; ++g) {
-      const int64_t slot = (int64_t(b) * Hq + g0 + g) * a.slots + split;
+      if (qc0 + g >= G) continue;  // a zero padding row
+      const int64_t slot = (int64_t(b) * Hq + h * G + qc0 + g) * a.slots + split;
       *reinterpret_cast<float4*>(a.part_acc + slot * D + 4 * c) =
           make_float4(acc[i][g][0].x, acc[i][g][0].y, acc[i][g][1].x, acc[i][g][1].y);
     }
   }
-  for (int g = tid; g < Hq; g += NTHR) {
-    const int64_t slot = (int64_t(b) * Hq + g) * a.slots + split;
-    const float2 m = ml[g];
+  for (int r = tid; r < hqs; r += NTHR) {
+    if (r % gs >= G) continue;  // a zero padding row
+    const int64_t slot = (int64_t(b) * Hq + (r / gs) * G + r % gs) * a.slots + split;
+    const float2 m = ml[r];
     a.part_ml[slot * 2] = m.y > 0.f ? m.x : NEG_INF;
     a.part_ml[slot * 2 + 1] = m.y;
   }

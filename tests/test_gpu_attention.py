@@ -388,7 +388,8 @@ def test_fused_step_mapped_geometry(bits, hq, H):
 
 @pytest.mark.parametrize("H,hq,D", [(8, 32, 128), (8, 8, 128), (8, 64, 128), (32, 32, 128), (16, 32, 128), (4, 32, 128),
                                     (2, 16, 128), (1, 8, 128), (32, 64, 128), (8, 24, 64), (4, 4, 64), (16, 48, 64),
-                                    (8, 16, 256), (4, 16, 256), (8, 32, 32), (1, 4, 32)])
+                                    (8, 16, 256), (4, 16, 256), (8, 32, 32), (1, 4, 32), (8, 24, 128), (4, 28, 128),
+                                    (8, 40, 128), (2, 12, 64)])
 @pytest.mark.parametrize("bits", [2, 4, 8, 16])
 def test_exact_kernel_geometries(H, hq, D, bits):
     """The exact f32 kernel (mode 1: attn_exact2_kernel for head_dim 32 / 64 / 128 / 256) at MHA, GQA and MQA shapes and
