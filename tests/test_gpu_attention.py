@@ -451,3 +451,12 @@ def test_fast_head_group_views(H, hq, bits):
     step = store.append_attend(0, q, k1, k1, out_dtype=torch.float32)
     assert torch.isfinite(step).all()
     assert m is not None
+
+
+@pytest.mark.parametrize("H,hq,bits,page_tokens", [(4, 28, 4, 32), (16, 32, 2, 128), (8, 24, 8, 32), (2, 16, 4, 256)])
+def test_views_and_padding_other_page_sizes(H, hq, bits, page_tokens):
+    """The remapped tensor-core paths (8-head views, padded group sizes) with 32 / 128 / 256-token pages."""
+    store, q, want = _paged_case(B=3, H=H, hq=hq, D=128, bits=bits, T=500, R=16, seed=1300 + H + hq + page_tokens,
+                                 page_tokens=page_tokens)
+    out = store.attend(0, q, mode=2, out_dtype=torch.float32)
+    assert np.abs(out.cpu().numpy() - want).max() <= 2e-3
