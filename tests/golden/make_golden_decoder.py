@@ -11,7 +11,7 @@ the weights with oracle.tada_oracle.toy_weights and check those hashes first).
 
 Cases: AC3 (test_acceptance.py:129-143: 4 layers, 8 q / 2 kv heads, D=16, all-residual R=256, 2-bit
 plan) and compressed decoding with R=4 at widths 2 and 4 and a mixed plan, plus a wider GQA model
-(Hq=16, H=8, D=128) that exercises the fused RoPE append.
+(Hq=16, H=8, D=128) that exercises the fused RoPE append, and 4 / 16 KV-head models (Qwen2-style and MHA).
 """
 
 from __future__ import annotations
@@ -39,6 +39,9 @@ CASES = [
     ("r4b4", 4, 8, 2, 16, 256, 7, [5, 9, 200, 31, 77], 40, [4, 4, 4, 4], 4),
     ("mixed", 4, 8, 2, 16, 256, 11, [1, 2, 3, 4, 5, 6, 7, 8, 9], 32, [8, 4, 2, 4], 8),
     ("wide", 2, 16, 8, 128, 512, 3, [17, 400, 3, 99], 24, [4, 2], 16),
+    # round 2: KV head counts other than 8 on the tensor-core path (Qwen2-style 4 KV / 28 q heads; 16-head MHA)
+    ("qwen", 2, 28, 4, 128, 512, 5, [9, 300, 41, 7, 120], 24, [4, 2], 16),
+    ("mha16", 2, 16, 16, 128, 512, 6, [2, 77, 301], 24, [2, 4], 16),
 ]
 
 
