@@ -33,6 +33,7 @@ struct Plan {
   int tt;  // tokens per tile (16)
   int H, G, Hq, gb, gt, nqc, upt, RS, CRS, QS, PS;
   int gs;  // q rows per KV head in shared memory: G, or G padded to gt (G in 3, 5, 6, 7) with zero rows
+  int cshift;  // log2 of the 16-byte chunks per code row when a power of two, else -1 (tile staging, below)
   int sb;  // bytes per stage; stage st starts at st * sb
   int off_km, off_vm, off_kc, off_vc, off_kx, off_vx;  // within a stage
   int off_q, off_s, off_p, off_corr, off_ml, total;
@@ -63,6 +64,9 @@ inline bool plan(const tada_page_layout& L, int Hq, Plan* out) {
   if (p.upt > 4 || p.upt * p.gt > 8) return false;
   p.RS = D + 4;                 // lane-per-row float4 reads: 8 lanes hit 8 distinct 16-byte bank groups
   p.CRS = p.H * p.gb + 16;      // ... and the code rows likewise
+  p.cshift = -1;
+  for (int c = (p.H * p.gb) / 16, k = 0; k < 16; ++k)
+    if (c == (1 << k)) p.cshift = k;
   p.QS = D + 4;  // the upper half of a q row sits 4 floats further: the two column halves of phase 1 differ in bank
   for (int tt = 16; tt >= 16; tt /= 2) {
     const int TT = tt;
@@ -188,8 +192,36 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
   const int32_t* pt = a.page_table + int64_t(b) * a.pt_stride;
   const int pshift = (P & (P - 1)) == 0 ? __ffs(P) - 1 : -1;
 
-  // ---- staging of tile [t0, t0 + TT) into stage st (cp.async; tokens past t_end are not loaded): warp per
-  // (side, token row), lanes over the row's 16-byte chunks
+  // ---- staging of tile [t0, t0 + TT) into stage st (cp.async; tokens past t_end are not loaded).
+  // Tiles start at multiples of TT (split_range), so with page_tokens a multiple of TT a tile's rows are
+  // consecutive rows of one page and each block (means, codes, metas) is one contiguous run: the CTA copies
+  // it as a flat range of 16-byte chunks, one page-table read per tile (`tile_page`, read one tile ahead).
+  // Otherwise: warp per (side, token row), lanes over the row's 16-byte chunks.
+  const bool flat = pshift >= 0 && P % TT == 0 && pl.cshift >= 0;
+  auto stage_flat = [&](int t0, int st, int32_t page_id) {
+    const int nv = min(TT, t_end - t0);
+    uint8_t* sb = smem + st * pl.sb;
+    const int row0 = t0 & (P - 1);
+    const uint8_t* page = a.pool + int64_t(page_id) * a.L.page_bytes;
+    constexpr int MC = D / 4, MS = MC == 8 ? 3 : MC == 16 ? 4 : MC == 32 ? 5 : 6;  // 16-byte chunks per mean row
+    const int cs = pl.cshift, nm = nv * H / 2;  // metas: H * 8 bytes per row
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const float* msrc = reinterpret_cast<const float*>(page + a.L.off_mean[side]) + int64_t(row0) * D;
+      float* mdst = reinterpret_cast<float*>(sb + (side ? pl.off_vm : pl.off_km));
+      for (int j = tid; j < (nv << MS); j += NTHR) cp16(mdst + (j >> MS) * pl.RS + 4 * (j & (MC - 1)), msrc + 4 * j);
+      const uint8_t* csrc = page + a.L.off_codes[side] + int64_t(row0) * H * gb;
+      uint8_t* cdst = sb + (side ? pl.off_vc : pl.off_kc);
+      for (int j = tid; j < (nv << cs); j += NTHR)
+        cp16(cdst + (j >> cs) * pl.CRS + 16 * (j & ((1 << cs) - 1)), csrc + 16 * j);
+      const uint8_t* xsrc = page + a.L.off_meta[side] + int64_t(row0) * H * 8;
+      uint8_t* xdst = sb + (side ? pl.off_vx : pl.off_kx);
+      for (int j = tid; j < nm; j += NTHR) cp16(xdst + 16 * j, xsrc + 16 * j);
+      if ((nv * H) & 1 && tid == NTHR - 1) cp8(xdst + 16 * nm, xsrc + 16 * nm);  // odd H, partial tile
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto tile_page = [&](int t0) { return t0 < t_end ? pt[t0 >> pshift] : 0; };
   auto stage = [&](int t0, int st) {
     const int nv = min(TT, t_end - t0);
     uint8_t* sb = smem + st * pl.sb;
@@ -218,12 +250,25 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
 #pragma unroll
     for (int g = 0; g < GT; ++g) acc[i][g][0] = acc[i][g][1] = make_float2(0.f, 0.f);
 
-  if (t_begin < t_end) stage(t_begin, 0);
+  int32_t next_page = 0;  // page of the tile after the one being staged (flat staging)
+  if (t_begin < t_end) {
+    if (flat) {
+      stage_flat(t_begin, 0, tile_page(t_begin));
+      next_page = tile_page(t_begin + TT);
+    } else {
+      stage(t_begin, 0);
+    }
+  }
   int st = 0;
   for (int t0 = t_begin; t0 < t_end; t0 += TT, st ^= 1) {
     const int nv = min(TT, t_end - t0);
     if (t0 + TT < t_end) {
-      stage(t0 + TT, st ^ 1);
+      if (flat) {
+        stage_flat(t0 + TT, st ^ 1, next_page);
+        next_page = tile_page(t0 + 2 * TT);
+      } else {
+        stage(t0 + TT, st ^ 1);
+      }
       asm volatile("cp.async.wait_group 1;" ::: "memory");
     } else {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
