@@ -12,3 +12,7 @@ run --bits 4 --hq 8 --heads 8 --dim 64 --mode 0
 run --bits 8 --hq 64 --mode 0
 run --bits 4 --hq 32 --heads 16 --mode 0 --batch 8
 run --bits 4 --hq 32 --heads 4 --mode 0
+run --bits 4 --hq 28 --heads 4 --mode 0
+run --bits 4 --hq 16 --heads 8 --dim 256 --mode 1
+run --bits 4 --hq 32 --batch 1 --mode 1
+run --bits 4 --hq 16 --heads 16 --dim 64 --mode 1 --batch 8
