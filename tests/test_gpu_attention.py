@@ -401,6 +401,20 @@ def test_exact_kernel_geometries(H, hq, D, bits):
         assert np.abs(out.cpu().numpy() - want).max() <= 1e-5, f"splits {splits}"
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("H,hq,D", [(1, 8, 128), (1, 4, 32), (3, 12, 128), (1, 16, 64)])
+@pytest.mark.parametrize("bits", [2, 4, 8])
+def test_exact_kernel_odd_lengths(H, hq, D, bits):
+    """Odd compressed lengths (residual 7) with odd KV head counts: the exact kernel's flat tile staging copies the
+    metas of a partial tile as 16-byte chunks plus one 8-byte tail."""
+    store, q, want = _paged_case(B=2, H=H, hq=hq, D=D, bits=bits, T=333, R=7, seed=900 + H + hq + D + bits,
+                                 poison=True)
+    assert all(store.lengths(0, b)[0] % 2 == 1 for b in range(2)), store.lengths(0)
+    for splits in (1, 5, 37):
+        out = store.attend(0, q, num_splits=splits, mode=1)
+        assert np.abs(out.cpu().numpy() - want).max() <= 1e-5, f"splits {splits}"
+
+
 @pytest.mark.parametrize("where", ["mean", "scale"])
 def test_imported_cache_range_words(where):
     """A TADAKV1 stream with a mean >= 2^15 (or a group scale >= 2^8) imported by deserialize_cache sets the

@@ -13,7 +13,10 @@ for tool in memcheck racecheck; do
   run $tool "--bits 2 --hq 32 --heads 32 --mode 1"
   run $tool "--bits 8 --hq 16 --heads 16 --dim 64 --mode 1"
   run $tool "--bits 16 --hq 24 --heads 4 --dim 64 --mode 1"
+  run $tool "--bits 4 --hq 8 --heads 1 --mode 1 --tokens 301 --residual 5"
+  run $tool "--bits 2 --hq 12 --heads 3 --mode 1 --tokens 299 --residual 7"
 done
 run synccheck "--bits 4 --hq 32"
 run synccheck "--bits 4 --hq 32 --mode 1"
 run initcheck "--bits 4 --hq 24"
+run initcheck "--bits 4 --hq 8 --heads 1 --mode 1 --tokens 301 --residual 5"

@@ -20,8 +20,10 @@ def main():
     ap.add_argument("--mode", type=int, default=2)
     ap.add_argument("--heads", type=int, default=8)
     ap.add_argument("--dim", type=int, default=128)
+    ap.add_argument("--tokens", type=int, default=300)
+    ap.add_argument("--residual", type=int, default=8, help="odd values give odd compressed lengths")
     args = ap.parse_args()
-    B, T, H, D, R = 2, 300, args.heads, args.dim, 8
+    B, T, H, D, R = 2, args.tokens, args.heads, args.dim, args.residual
     rng = np.random.default_rng(1)
     k = torch.from_numpy(rng.normal(size=(B, T, H, D)).astype(np.float32)).cuda().bfloat16()
     v = torch.from_numpy(rng.normal(size=(B, T, H, D)).astype(np.float32)).cuda().bfloat16()
