@@ -167,6 +167,7 @@ __device__ __forceinline__ void recon4(float4 m, uint32_t w, float4 dev4, float2
 template <int BITS, int D, int GT, int UPT, int TT>
 __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan pl) {
   constexpr int CPW = BITS == 16 ? 1 : 32 / BITS;  // codes per 32-bit word
+  constexpr int RS = D + 4, QS = D + 4, PS = TT + 4;  // = plan()'s row strides, as immediates
   extern __shared__ __align__(128) uint8_t smem[];
   const int H = pl.H, G = pl.G, Hq = pl.Hq, gb = pl.gb, P = a.L.page_tokens, nqc = pl.nqc;
   const int b = blockIdx.y, split = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -184,12 +185,12 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
   for (int i = tid; i < hqs * D; i += NTHR) {
     const int r = i / D, dd = i - r * D, j = r % gs;
     if (j >= G) {
-      qs[r * pl.QS + dd + (dd >= D / 2 ? 4 : 0)] = 0.f;
+      qs[r * QS + dd + (dd >= D / 2 ? 4 : 0)] = 0.f;
       continue;
     }
     const int64_t qi = (int64_t(b) * Hq + (r / gs) * G + j) * D + dd;
     const int g = i / D, d = i - g * D;
-    qs[g * pl.QS + d + (d >= D / 2 ? 4 : 0)] = a.q_dtype == TADA_F32 ? reinterpret_cast<const float*>(a.q)[qi]
+    qs[g * QS + d + (d >= D / 2 ? 4 : 0)] = a.q_dtype == TADA_F32 ? reinterpret_cast<const float*>(a.q)[qi]
                                                                     : to_f32(reinterpret_cast<const __nv_bfloat16*>(a.q)[qi]);
   }
   for (int g = tid; g < hqs; g += NTHR) ml[g] = make_float2(NEG_INF, 0.f);
@@ -219,10 +220,10 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
 #pragma unroll
         for (int k = 0; k < (TT << MS) / NTHR; ++k) {
           const int j = tid + k * NTHR;
-          cp16(mdst + (j >> MS) * pl.RS + 4 * (j & (MC - 1)), msrc + 4 * j);
+          cp16(mdst + (j >> MS) * RS + 4 * (j & (MC - 1)), msrc + 4 * j);
         }
       } else {
-        for (int j = tid; j < (nv << MS); j += NTHR) cp16(mdst + (j >> MS) * pl.RS + 4 * (j & (MC - 1)), msrc + 4 * j);
+        for (int j = tid; j < (nv << MS); j += NTHR) cp16(mdst + (j >> MS) * RS + 4 * (j & (MC - 1)), msrc + 4 * j);
       }
       for (int j = tid; j < (nv << cs); j += NTHR)
         cp16(cdst + (j >> cs) * pl.CRS + 16 * (j & ((1 << cs) - 1)), csrc + 16 * j);
@@ -243,7 +244,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
       const uint8_t* page = a.pool + int64_t(pt[pg]) * a.L.page_bytes;
       const int row = tok - pg * P;
       const float* msrc = reinterpret_cast<const float*>(page + a.L.off_mean[side]) + int64_t(row) * D;
-      float* mdst = reinterpret_cast<float*>(sb + (side ? pl.off_vm : pl.off_km)) + t * pl.RS;
+      float* mdst = reinterpret_cast<float*>(sb + (side ? pl.off_vm : pl.off_km)) + t * RS;
       for (int c = lane; c < D / 4; c += 32) cp16(mdst + 4 * c, msrc + 4 * c);
       const uint8_t* csrc = page + a.L.off_codes[side] + int64_t(row) * H * gb;
       uint8_t* cdst = sb + (side ? pl.off_vc : pl.off_kc) + t * pl.CRS;
@@ -298,7 +299,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
     for (int u = warp; u < H * nqc; u += NTHR / 32) {
       const int h = u / nqc, g0 = h * gs + (u - h * nqc) * GT;  // shared-memory row of the unit's first q head
       const int t = lane & (TT - 1), dh = (lane / TT) * (D / 2);
-      const float* mrow = km + t * pl.RS;
+      const float* mrow = km + t * RS;
       const uint8_t* crow = kc + t * pl.CRS + h * gb;
       const float2 sm = kx[t * H + h];
       const float* qrow = qs + (dh ? 4 : 0);
@@ -325,7 +326,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
           recon4<BITS>(m, w, dev4, sm, k01, k23);
 #pragma unroll
           for (int g = 0; g < GT; ++g) {
-            const float4 q4 = *reinterpret_cast<const float4*>(qrow + (g0 + g) * pl.QS + d + e);
+            const float4 q4 = *reinterpret_cast<const float4*>(qrow + (g0 + g) * QS + d + e);
             z2[g] = __ffma2_rn(make_float2(q4.x, q4.y), k01, z2[g]);
             z2[g] = __ffma2_rn(make_float2(q4.z, q4.w), k23, z2[g]);
           }
@@ -358,7 +359,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
         for (int g = 0; g < GT; ++g) ls[g] += __shfl_xor_sync(0xffffffffu, ls[g], o);
 #pragma unroll
       for (int g = 0; g < GT; ++g) {
-        if (lane < TT) S[(g0 + g) * pl.PS + lane] = pe[g];
+        if (lane < TT) S[(g0 + g) * PS + lane] = pe[g];
         if (lane == 0) {
           const float2 m0 = ml[g0 + g];
           const float cf = expf(m0.x - mx[g]);
@@ -384,9 +385,9 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
       const uint8_t* ccol = vc + h * gb + (BITS == 16 ? 16 * c : c * BITS / 2);
       const float* mcol = vm + d0;
       const float2* xcol = vx + h;
-      const float* srow = S + g0 * pl.PS;
+      const float* srow = S + g0 * PS;
       auto token = [&](int t, const float (&pw)[GT]) {
-        const float4 m = *reinterpret_cast<const float4*>(mcol + t * pl.RS);
+        const float4 m = *reinterpret_cast<const float4*>(mcol + t * RS);
         float4 dev4 = make_float4(0.f, 0.f, 0.f, 0.f);
         uint32_t w = 0;
         const uint8_t* cp = ccol + t * pl.CRS;
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
         for (int t = 0; t < TT; t += 4) {
           float4 w4[GT];
 #pragma unroll
-          for (int g = 0; g < GT; ++g) w4[g] = *reinterpret_cast<const float4*>(srow + g * pl.PS + t);
+          for (int g = 0; g < GT; ++g) w4[g] = *reinterpret_cast<const float4*>(srow + g * PS + t);
           float pw[GT];
 #pragma unroll
           for (int g = 0; g < GT; ++g) pw[g] = w4[g].x;
@@ -426,7 +427,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
         for (int t = 0; t < nv; ++t) {
           float pw[GT];
 #pragma unroll
-          for (int g = 0; g < GT; ++g) pw[g] = srow[g * pl.PS + t];
+          for (int g = 0; g < GT; ++g) pw[g] = srow[g * PS + t];
           token(t, pw);
         }
       }
