@@ -7,7 +7,9 @@
 // reference's f32(f64 min + code * f64 scale) (SURVEY §8a "Dequant").
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdlib>
+#include <mutex>
 #include <string>
 
 #include "tada_attn.cuh"
@@ -450,7 +452,7 @@ __global__ void __launch_bounds__(256) combine_pair_kernel(AttnArgs a, int n_row
   }
   if (a.step && a.step_commit) {  // both rows of this CTA belong to one sequence (Hq is even: a multiple of 8 KV heads)
     __syncthreads();
-    if (threadIdx.x == 0 && active) step_commit(a, b, Hq / 2);
+    if (threadIdx.x == 0 && active) step_commit(a, b, Hq / 2 * (a.commit_units > 1 ? a.commit_units : 1));
   }
 }
 
@@ -679,7 +681,7 @@ __global__ void __launch_bounds__((G + 8) * 32) combine_kv_kernel(AttnArgs a, in
   }
   if (a.step && a.step_commit) {  // the H CTAs of sequence b: the last one advances its lengths
     __syncthreads();
-    if (threadIdx.x == 0) step_commit(a, b, gridDim.x);
+    if (threadIdx.x == 0) step_commit(a, b, gridDim.x * (a.commit_units > 1 ? a.commit_units : 1));
   }
 }
 
@@ -775,6 +777,7 @@ namespace tada {
 //    step rows likewise through AttnArgs::kv_rh / kv_h0).  Every view re-reads the f32 mean rows, so the bytes
 //    moved grow by 512 B per token and side for each extra group.
 // Each (head group, pass) stages its q rows, runs K2 + K3 into staging buffers, and puts the output rows back.
+constexpr int kMaxUnits = 8;  // concurrent (view, pass) launches (launch_fast_mapped)
 tada_page_layout head_group_view(const tada_page_layout& L, int j) {
   tada_page_layout v = L;
   v.heads = 8;
@@ -841,58 +844,131 @@ __global__ void unpad_out_kernel(const T* __restrict__ op, const float* __restri
   }
 }
 
+// Auxiliary streams of the current device for concurrent (view, pass) launches (created once, never freed).
+struct AuxStreams {
+  cudaStream_t s[kMaxUnits];
+  cudaEvent_t fork, join[kMaxUnits];
+  bool ok = false;
+};
+static AuxStreams* aux_streams() {
+  static std::mutex mu;
+  static AuxStreams per_dev[16];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  AuxStreams& x = per_dev[dev];
+  if (!x.ok) {
+    bool good = cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; good && i < kMaxUnits; ++i)
+      good = cudaStreamCreateWithFlags(&x.s[i], cudaStreamNonBlocking) == cudaSuccess &&
+             cudaEventCreateWithFlags(&x.join[i], cudaEventDisableTiming) == cudaSuccess;
+    if (!good) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    x.ok = true;
+  }
+  return &x;
+}
+
 int launch_fast_mapped(const AttnArgs& a0, int batch, const FastMap& fm, int mode, void* workspace, cudaStream_t st) {
   const int D = a0.L.head_dim, hq = 8 * fm.gp, H = a0.L.heads;
   const int64_t rows = int64_t(batch) * hq;
-  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
-  const int64_t part_bytes = rows * a0.slots * (int64_t(D) + 2) * 4;
-  void* qp = ws + (part_bytes + 255) / 256 * 256;
-  void* op = reinterpret_cast<uint8_t*>(qp) + rows * D * 4;
-  float* lp = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(op) + rows * D * 4);
   const bool qbf = a0.q_dtype == TADA_BF16, obf = a0.out_dtype == TADA_BF16;
-  for (int jg = 0; jg < fm.hg; ++jg)
-    for (int p = 0; p < fm.passes; ++p) {
-      const int j0 = p * fm.gc, n = fm.g - j0 < fm.gc ? fm.g - j0 : fm.gc, hb = 8 * jg;
-      AttnArgs a = a0;
-      if (fm.view) {
-        a.L = head_group_view(a0.L, jg);
-        a.kv_rh = H;
-        a.kv_h0 = hb;
-      }
-      a.Hq = hq;
-      a.q = qp;
-      a.out = op;
-      // a decode step: every (view, pass) stores its heads' new rows and reads the pre-step lengths; only the
-      // last one advances them
-      a.step_commit = jg == fm.hg - 1 && p == fm.passes - 1;
-      a.lse_out = a0.lse_out ? lp : nullptr;
-      a.part_acc = reinterpret_cast<float*>(ws);
-      a.part_ml = a.part_acc + rows * a.slots * D;
+  auto al = [](int64_t x) { return (x + 255) / 256 * 256; };
+  // one (view, pass) unit: pad its q rows, K2 + K3 into its staging buffers, put its output rows back
+  auto run_unit = [&](int jg, int p, uint8_t* ws, int splits, int commit_units, bool commit,
+                      cudaStream_t s) {
+    const int j0 = p * fm.gc, n = fm.g - j0 < fm.gc ? fm.g - j0 : fm.gc, hb = 8 * jg;
+    const int64_t part_bytes = rows * splits * (int64_t(D) + 2) * 4;
+    void* qp = ws + al(part_bytes);
+    void* op = reinterpret_cast<uint8_t*>(qp) + rows * D * 4;
+    float* lp = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(op) + rows * D * 4);
+    AttnArgs a = a0;
+    if (fm.view) {
+      a.L = head_group_view(a0.L, jg);
+      a.kv_rh = H;
+      a.kv_h0 = hb;
+    }
+    a.Hq = hq;
+    a.q = qp;
+    a.out = op;
+    a.splits = a.slots = splits;
+    a.step_commit = commit;
+    a.commit_units = commit_units;
+    a.lse_out = a0.lse_out ? lp : nullptr;
+    a.part_acc = reinterpret_cast<float*>(ws);
+    a.part_ml = a.part_acc + rows * a.slots * D;
+    int rc = TADA_OK;
+    {
       const int64_t tq = rows * D;
       const int grid = int((tq + 255) / 256 < 148 * 16 ? (tq + 255) / 256 : 148 * 16);
       if (qbf)
-        pad_q_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(a0.q),
-                                           reinterpret_cast<__nv_bfloat16*>(qp), H, hb, fm.g, j0, n, fm.gp, D, tq);
+        pad_q_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(a0.q),
+                                          reinterpret_cast<__nv_bfloat16*>(qp), H, hb, fm.g, j0, n, fm.gp, D, tq);
       else
-        pad_q_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(a0.q), reinterpret_cast<float*>(qp), H, hb,
-                                           fm.g, j0, n, fm.gp, D, tq);
-      int rc = check_launch("decode_attn_pad_q");
+        pad_q_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const float*>(a0.q), reinterpret_cast<float*>(qp), H, hb,
+                                          fm.g, j0, n, fm.gp, D, tq);
+      rc = check_launch("decode_attn_pad_q");
       if (rc != TADA_OK) return rc;
-      rc = (mode != 3 && v8_supported(a.L, hq)) ? launch_v8(a, batch, st) : launch_fast(a, batch, st);
-      if (rc == TADA_OK) rc = launch_combine_residual(a, batch, st);
-      if (rc != TADA_OK) return rc;
+    }
+    rc = (mode != 3 && v8_supported(a.L, hq)) ? launch_v8(a, batch, s) : launch_fast(a, batch, s);
+    if (rc == TADA_OK) rc = launch_combine_residual(a, batch, s);
+    if (rc != TADA_OK) return rc;
+    {
       const int64_t to = int64_t(batch) * 8 * n * D;
       const int g2 = int((to + 255) / 256 < 148 * 16 ? (to + 255) / 256 : 148 * 16);
       if (obf)
-        unpad_out_kernel<<<g2, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(op), lp,
-                                             reinterpret_cast<__nv_bfloat16*>(a0.out), a0.lse_out, H, hb, fm.g, j0, n,
-                                             fm.gp, D, to);
+        unpad_out_kernel<<<g2, 256, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(op), lp,
+                                            reinterpret_cast<__nv_bfloat16*>(a0.out), a0.lse_out, H, hb, fm.g, j0, n,
+                                            fm.gp, D, to);
       else
-        unpad_out_kernel<<<g2, 256, 0, st>>>(reinterpret_cast<const float*>(op), lp, reinterpret_cast<float*>(a0.out),
-                                             a0.lse_out, H, hb, fm.g, j0, n, fm.gp, D, to);
+        unpad_out_kernel<<<g2, 256, 0, s>>>(reinterpret_cast<const float*>(op), lp, reinterpret_cast<float*>(a0.out),
+                                            a0.lse_out, H, hb, fm.g, j0, n, fm.gp, D, to);
       rc = check_launch("decode_attn_unpad");
-      if (rc != TADA_OK) return rc;
     }
+    return rc;
+  };
+  const int units = fm.hg * fm.passes;
+  // Concurrent units: every (view, pass) re-reads the f32 mean rows (views) or the whole tile (q-head passes),
+  // and each unit's K3, q padding and output copy leave the GPU partly idle between K2s.  The units run on
+  // auxiliary streams, so one unit's K2 overlaps the previous one's tail and K3, and units reading the same
+  // token ranges at nearly the same time share bytes through L2.  Measured (tools/attn_bench.py, mode 0):
+  // two units with half the splits each, MHA 16 KV heads 4-bit 4015 -> 4543 GB/s, 8-bit 4412 -> 4846;
+  // more units keep the full split count (divided, their start skew left one unit running alone at the end:
+  // 32 KV heads B=16 3728 -> 2180; undivided 3937, and 2708 -> 3281 at B=4).  Needs the units' buffers to
+  // fit the documented workspace and the auxiliary streams to exist before a graph capture.
+  static const int conc_env = getenv("TADA_MAPPED_CONCURRENT") ? atoi(getenv("TADA_MAPPED_CONCURRENT")) : 1;
+  const int splits_u = units == 2 ? a0.splits / 2 : a0.splits;
+  const int64_t unit_bytes = al(rows * splits_u * (int64_t(D) + 2) * 4) + 2 * rows * D * 4 + al(rows * 4);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cap);
+  static std::atomic<bool> made{false};
+  AuxStreams* aux = nullptr;
+  if (conc_env && units > 1 && units <= kMaxUnits && splits_u >= 1 &&
+      units * unit_bytes <= tada_decode_attn_workspace_bytes(batch, a0.Hq, D, a0.splits) &&
+      (cap == cudaStreamCaptureStatusNone || made.load())) {
+    aux = aux_streams();
+    if (aux) made.store(true);
+  }
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  if (!aux) {  // one unit after another on the caller's stream; only the last one advances a step's lengths
+    for (int jg = 0; jg < fm.hg; ++jg)
+      for (int p = 0; p < fm.passes; ++p) {
+        const int rc = run_unit(jg, p, ws, a0.splits, 1, jg == fm.hg - 1 && p == fm.passes - 1, st);
+        if (rc != TADA_OK) return rc;
+      }
+    return TADA_OK;
+  }
+  if (cudaEventRecord(aux->fork, st) != cudaSuccess) return fail(TADA_ERR_CUDA, "decode_attn: fork event");
+  for (int u = 0; u < units; ++u) {
+    if (cudaStreamWaitEvent(aux->s[u], aux->fork, 0) != cudaSuccess) return fail(TADA_ERR_CUDA, "decode_attn: fork");
+    // every unit's K3 counts towards the step's arrivals: the last CTA of all units advances the lengths
+    const int rc = run_unit(u / fm.passes, u % fm.passes, ws + u * unit_bytes, splits_u, units, true, aux->s[u]);
+    if (rc != TADA_OK) return rc;
+    if (cudaEventRecord(aux->join[u], aux->s[u]) != cudaSuccess || cudaStreamWaitEvent(st, aux->join[u], 0) != cudaSuccess)
+      return fail(TADA_ERR_CUDA, "decode_attn: join");
+  }
   return TADA_OK;
 }
 

@@ -52,6 +52,7 @@ struct AttnArgs {
   int kv_rh;
   int kv_h0;
   bool step_commit;  // a decode step's K3 advances the lengths (false for all but the last view / q-head pass)
+  int commit_units;  // > 1: that many concurrent (view, pass) launches share the step's arrival counters
 };
 
 // The tensor-core kernels stage q and the f32 means (f16 hi + lo / f16) as f16, which holds |x| < 65504, and
