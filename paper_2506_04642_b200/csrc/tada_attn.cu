@@ -960,6 +960,10 @@ int launch_fast_mapped(const AttnArgs& a0, int batch, const FastMap& fm, int mod
       }
     return TADA_OK;
   }
+  // the fork / join events and streams are shared by every caller on this device: issue under a lock so that
+  // two host threads cannot interleave their records and waits
+  static std::mutex issue_mu;
+  std::lock_guard<std::mutex> lock(issue_mu);
   if (cudaEventRecord(aux->fork, st) != cudaSuccess) return fail(TADA_ERR_CUDA, "decode_attn: fork event");
   for (int u = 0; u < units; ++u) {
     if (cudaStreamWaitEvent(aux->s[u], aux->fork, 0) != cudaSuccess) return fail(TADA_ERR_CUDA, "decode_attn: fork");
