@@ -116,13 +116,20 @@ def test_ragged_append_rope_equals_composition():
                 assert torch.equal(x, y), (s, name)
 
 
-@pytest.mark.parametrize("hq,H", [(32, 8), (64, 8), (28, 4), (32, 16), (24, 8)])
-def test_decode_graph_replay_equals_eager(hq, H):
+@pytest.mark.parametrize("hq,H,splits", [(32, 8, None), (64, 8, None), (28, 4, None), (32, 16, None), (24, 8, None),
+                                          (32, 16, 4), (32, 32, 3)])
+def test_decode_graph_replay_equals_eager(hq, H, splits):
     """A DecodeGraph captured once and replayed for 24 steps (two layers, plan (4, 2), R = 8: every sequence
     flushes during replays, at different steps) == the same steps run eagerly through append_attend; also for
-    4 / 16 KV heads (8-head views) and a padded group size."""
+    4 / 16 / 32 KV heads (8-head views) and a padded group size.  With explicit splits the 16 / 32-head views
+    run as concurrent units on auxiliary streams (launch_fast_mapped), captured into the graph too."""
     m = tk()
     rng = np.random.default_rng(90 + hq + H)
+    if splits:  # an eager call first, so the auxiliary streams exist before the capture
+        warm = m.PagedKVCache(1, H, D, (4,), 8, batch=2, page_tokens=64, max_tokens=128)
+        warm.append(0, torch.zeros(2, 40, H, D, device="cuda", dtype=torch.bfloat16),
+                    torch.zeros(2, 40, H, D, device="cuda", dtype=torch.bfloat16))
+        warm.attend(0, torch.zeros(2, hq, D, device="cuda", dtype=torch.bfloat16), num_splits=4)
     lens = [20, 5, 33, 12]
     B, n, L, R = len(lens), max(lens), 2, 8
     k = torch.from_numpy(_rows(rng, B, n, H, D)).cuda().bfloat16()
@@ -132,7 +139,7 @@ def test_decode_graph_replay_equals_eager(hq, H):
         for layer in range(L):
             st.append(layer, k, v, lengths=lens)
     eager, graphed = stores
-    g = m.DecodeGraph(graphed, hq)
+    g = m.DecodeGraph(graphed, hq, num_splits={4: splits, 2: splits} if splits else None)
     for step in range(24):
         q = torch.from_numpy(_rows(rng, L, B, hq, D)).cuda().bfloat16()
         kn = torch.from_numpy(_rows(rng, L, B, 1, H, D)).cuda().bfloat16()
