@@ -113,12 +113,6 @@ def mean_center(x):
     return (mean, dev) if is_t else (_dev.host(mean), _dev.host(dev))
 
 
-def _finite_or_raise(*ts) -> None:
-    for t in ts:
-        if t.numel() and not bool(torch.isfinite(t).all()):
-            raise DataError("cannot quantize non-finite values")
-
-
 class CompressedLayerCache:
     """One layer's compressed KV state in HBM (cache.py:114-213), single writer."""
 
@@ -163,8 +157,8 @@ class CompressedLayerCache:
             return
         if v.dtype != k.dtype:
             k, v = k.float(), v.float()
-        _finite_or_raise(k, v)  # raise before mutation, like the reference
-        self.store.append(0, k.unsqueeze(0), v.unsqueeze(0))
+        # a non-finite row that K1 compresses raises DataError with the cache unchanged (one flag read, no pre-pass)
+        self.store.append_checked(0, k.unsqueeze(0), v.unsqueeze(0))
 
     # --- reference attributes, exported from the paged layout -------------------------------------------
     def _export(self) -> dict:

@@ -294,6 +294,32 @@ class PagedKVCache:
         if self.err.raised():
             raise DataError("cannot quantize non-finite values")
 
+    def append_checked(self, layer: int, k: torch.Tensor, v: torch.Tensor, rope=None) -> None:
+        """:meth:`append` (or :meth:`append_rope` with ``rope = (pos, n_pos, params)``) that raises DataError
+        and leaves the layer unchanged when a kernel saw a non-finite row — the drop-in ``append_tokens``
+        contract (cache.py:154-180) without a pre-pass over the input.  K1 flags the rows it compresses; on a
+        flag the lengths (device and host) and the residual rows a flush overwrote are restored.  Rows that
+        only enter the residual buffer are not inspected, like the reference, which raises when they flush."""
+        self._refresh()
+        comp, res = self.comp_host[layer].copy(), self.res_host[layer].copy()
+        r = int(res.max())
+        saved = None
+        if self.R > 0 and r > 0:  # a flush rewrites residual rows [0, r_after) in place
+            saved = (self.res_k[layer][:, :r].clone(), self.res_v[layer][:, :r].clone())
+        if rope is None:
+            self.append(layer, k, v)
+        else:
+            self.append_rope(layer, k, v, *rope)
+        if not self.err.raised():
+            return
+        self.comp_len[layer].copy_(torch.from_numpy(comp.astype(np.int32)))
+        self.res_len[layer].copy_(torch.from_numpy(res.astype(np.int32)))
+        self.comp_host[layer], self.res_host[layer] = comp, res
+        if saved is not None:
+            self.res_k[layer][:, :r].copy_(saved[0])
+            self.res_v[layer][:, :r].copy_(saved[1])
+        raise DataError("cannot quantize non-finite values")
+
     # ------------------------------------------------------------------ attention (K2 + K3)
     def _out(self, out, hq: int, out_dtype) -> torch.Tensor:
         """The caller's output buffer, validated (the kernels write B*Hq*D elements to it), or a new one."""

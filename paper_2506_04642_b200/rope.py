@@ -19,7 +19,7 @@ import torch
 
 from . import _dev
 from ._lib import call
-from .cache import CompressedLayerCache, RopeParams, _finite_or_raise
+from .cache import CompressedLayerCache, RopeParams
 from .errors import DataError, ShapeError
 
 F32 = np.float32
@@ -118,8 +118,8 @@ def append_rope(cache: CompressedLayerCache, k_pre_rope, v_new, positions, rope:
         return
     if v.dtype != k.dtype:
         k, v = k.float(), v.float()
-    _finite_or_raise(k, v)  # rotation keeps finite rows finite: raise before mutation, like the reference
-    cache.store.append_rope(0, k.unsqueeze(0), v.unsqueeze(0), pos.unsqueeze(0), top, rope)
+    # non-finite rows that K1 compresses raise DataError with the cache unchanged (PagedKVCache.append_checked)
+    cache.store.append_checked(0, k.unsqueeze(0), v.unsqueeze(0), rope=(pos.unsqueeze(0), top, rope))
 
 
 def append_fused(cache: CompressedLayerCache, k_pre_rope, x_norm, w_v, positions, rope: RopeParams) -> None:

@@ -128,6 +128,48 @@ def test_outlier_regime_and_errors():
     assert m.serialize_cache(cache) == before  # no mutation on error
 
 
+@pytest.mark.parametrize("bits,R", [(4, 16), (2, 5), (8, 0)])
+def test_nonfinite_flush_leaves_cache_unchanged(bits, R):
+    """append_tokens with a non-finite row that K1 compresses raises DataError and restores the lengths and
+    the residual rows the flush overwrote (no input pre-pass); the cache keeps working afterwards (oracle)."""
+    m = tk()
+    rng = np.random.default_rng(11 + bits)
+    x = rng.standard_normal((3 * max(R, 1) + 3, 8, 128)).astype(np.float32)
+    y = rng.standard_normal(x.shape).astype(np.float32)
+    cache = m.CompressedLayerCache(8, 128, bits, R)
+    ref = orc.LayerState(8, 128, bits, R)
+    head = max(R - 2, 1)  # leaves a residual (R > 0) so the failing append's flush would overwrite it
+    cache.append_tokens(x[:head], y[:head])
+    orc.append(ref, x[:head], y[:head])
+    before = m.serialize_cache(cache)
+    for side in (0, 1):
+        bad = [x[head:head + R + 4].copy(), y[head:head + R + 4].copy()]
+        bad[side][1, 5, 9] = np.inf if side else np.nan
+        with pytest.raises(m.DataError):
+            cache.append_tokens(*bad)
+        assert m.serialize_cache(cache) == before
+        assert cache.total_tokens == head
+    cache.append_tokens(x[head:], y[head:])
+    orc.append(ref, x[head:], y[head:])
+    assert m.serialize_cache(cache) == orc.dump(ref)
+
+
+def test_nonfinite_residual_row_raises_at_its_flush():
+    """Like the reference, a non-finite row that only enters the residual buffer is accepted; the append
+    whose flush compresses it raises DataError and leaves the cache as it was before that append."""
+    m = tk()
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((24, 8, 128)).astype(np.float32)
+    x[2, 1, 3] = np.nan
+    cache = m.CompressedLayerCache(8, 128, 4, 8)
+    cache.append_tokens(x[:4], x[:4])  # 4 raw rows, one of them non-finite: no flush, no error
+    assert cache.total_tokens == 4
+    before = m.serialize_cache(cache)
+    with pytest.raises(m.DataError):
+        cache.append_tokens(x[4:12], x[4:12])  # flushes the first 8 rows
+    assert m.serialize_cache(cache) == before
+
+
 @pytest.mark.parametrize("plan", [(8, 4, 2, 16), (4, 4, 4, 4)])
 def test_paged_multilayer_batched_vs_oracle(plan):
     """PagedKVCache: B sequences x L layers, shuffled pages, mixed widths; each (layer, seq) == oracle."""
