@@ -386,10 +386,12 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
         sh<uint4>(smem, pl.off_qi + (warp * 4 + s) * 512 + lane * 16) = make_uint4(qA[s][0], qA[s][1], qA[s][2], qA[s][3]);
   }
   // QK mean A fragments of every piece, lane-major: [quarter qd][mt][ks][lane]; q rows 16mt + r (+8),
-  // k-step ks slots (2c, 2c+1 | 2c+8, 2c+9) <-> d = 32qd + 16ks + 4c + (0, 1 | 2, 3)
+  // k-step ks slots (2c, 2c+1 | 2c+8, 2c+9) <-> d = 32qd + 16(ks ^ (c & 1)) + 4c + (0, 1 | 2, 3): odd quads take
+  // the other half of the kmean row first, so each 8-lane phase of the kmean LDS.128 (rows r, r + 1 under the
+  // 128-B swizzle) covers 8 distinct 16-B chunks (16ks + 4c made it a 2-way bank conflict)
   for (int f = warp; f < 4 * MT * 2; f += NW) {
     const int qd2 = f / (MT * 2), mt = (f >> 1) % MT, ks = f & 1;
-    const __half* r0 = q16 + (16 * mt + r) * D + 32 * qd2 + 16 * ks + 4 * c;
+    const __half* r0 = q16 + (16 * mt + r) * D + 32 * qd2 + 16 * (ks ^ (c & 1)) + 4 * c;
     const __half* r1 = r0 + 8 * D;
     sh<uint4>(smem, pl.off_qa + f * 512 + lane * 16) =
         make_uint4(*reinterpret_cast<const uint32_t*>(r0), *reinterpret_cast<const uint32_t*>(r1),
@@ -418,8 +420,8 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
 
   // ---------------------------------------------------------------- per-thread shared offsets
   const int qd = warp & 3, oct = warp >> 2;
-  const int oX0 = qd * BAND + swz(8 * oct + r, 16 * c);  // kmean, stage-relative
-  const int oX1 = qd * BAND + swz(8 * oct + r, 64 + 16 * c);
+  const int oX0 = qd * BAND + swz(8 * oct + r, 64 * (c & 1) + 16 * c);  // kmean, stage-relative (k-step 0)
+  const int oX1 = qd * BAND + swz(8 * oct + r, 64 * (~c & 1) + 16 * c);  // k-step 1
   const int oQA = pl.off_qa + qd * (MT * 2 * 512) + lane * 16;
   const int oQI = pl.off_qi + warp * 4 * 512 + lane * 16;
   const int oSW = pl.off_sm + qd * PLANE + (r * TT + ((8 * oct + 2 * c) ^ (8 * ((r >> 1) & 1)))) * 4;
