@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(TT * 16, TT == 16 ? 2 : 1) attn_fast_kernel(At
     if (QA_SMEM) {  // pack every piece's fragments once: (kq, mt, ks) by the warps, lane-major
       for (int f = warp; f < NKQ * MT * KS; f += NW) {
         const int kq2 = f / (MT * KS), mt = (f / KS) % MT, ks = f % KS;
-        const __half* r0 = q16 + (16 * mt + r) * D + 16 * (KS * kq2 + ks) + 4 * c;
+        const __half* r0 = q16 + (16 * mt + r) * D + 16 * ((KS * kq2 + ks) ^ (c & 1)) + 4 * c;  // see the kmean load
         const __half* r1 = r0 + 8 * D;
         qa_s[f * 32 + lane] = make_uint4(*reinterpret_cast<const uint32_t*>(r0), *reinterpret_cast<const uint32_t*>(r1),
                                          *reinterpret_cast<const uint32_t*>(r0 + 2),
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(TT * 16, TT == 16 ? 2 : 1) attn_fast_kernel(At
       for (int mt = 0; mt < (QA_SMEM ? 1 : MT); ++mt)
 #pragma unroll
         for (int ks = 0; ks < (QA_SMEM ? 1 : KS); ++ks) {
-          const __half* r0 = q16 + (16 * mt + r) * D + 16 * ((KS * kq + ks) & 7) + 4 * c;
+          const __half* r0 = q16 + (16 * mt + r) * D + 16 * (((KS * kq + ks) & 7) ^ (c & 1)) + 4 * c;
           const __half* r1 = r0 + 8 * D;
           qa[mt][ks][0] = *reinterpret_cast<const uint32_t*>(r0);
           qa[mt][ks][1] = *reinterpret_cast<const uint32_t*>(r1);
@@ -338,7 +338,8 @@ __global__ void __launch_bounds__(TT * 16, TT == 16 ? 2 : 1) attn_fast_kernel(At
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
         const int s = KS * kq + ks;
-        const float4 x = *reinterpret_cast<const float4*>(kmean + (s >> 1) * BAND + swz(tok, 64 * (s & 1) + 16 * c));
+        // odd thread quads take chunk s ^ 1: an 8-lane phase (rows r, r + 1) then reads 8 distinct 16-B chunks
+        const float4 x = *reinterpret_cast<const float4*>(kmean + (s >> 1) * BAND + swz(tok, 64 * ((s ^ c) & 1) + 16 * c));
         uint32_t h0, l0, h1, l1;
         split_h2(x.x, x.y, h0, l0);
         split_h2(x.z, x.w, h1, l1);
