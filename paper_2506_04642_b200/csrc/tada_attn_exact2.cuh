@@ -229,8 +229,15 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
         cp16(cdst + (j >> cs) * pl.CRS + 16 * (j & ((1 << cs) - 1)), csrc + 16 * j);
       const uint8_t* xsrc = page + a.L.off_meta[side] + int64_t(row0) * H * 8;
       uint8_t* xdst = sb + (side ? pl.off_vx : pl.off_kx);
-      for (int j = tid; j < nm; j += NTHR) cp16(xdst + 16 * j, xsrc + 16 * j);
-      if ((nv * H) & 1 && tid == NTHR - 1) cp8(xdst + 16 * nm, xsrc + 16 * nm);  // odd H, partial tile
+      if (side == 0) {  // key metas transposed to [head][token]: phase 1's 16 token lanes read 128 contiguous bytes
+        for (int j = tid; j < H * TT; j += NTHR) {
+          const int h = j / TT, t = j - h * TT;
+          if (t < nv) cp8(xdst + 8 * j, xsrc + 8 * (t * H + h));
+        }
+      } else {  // value metas stay [token][head] (phase 2 broadcasts one per warp)
+        for (int j = tid; j < nm; j += NTHR) cp16(xdst + 16 * j, xsrc + 16 * j);
+        if ((nv * H) & 1 && tid == NTHR - 1) cp8(xdst + 16 * nm, xsrc + 16 * nm);  // odd H, partial tile
+      }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
@@ -250,8 +257,10 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
       uint8_t* cdst = sb + (side ? pl.off_vc : pl.off_kc) + t * pl.CRS;
       for (int c = lane; c < H * gb / 16; c += 32) cp16(cdst + 16 * c, csrc + 16 * c);
       const uint8_t* xsrc = page + a.L.off_meta[side] + int64_t(row) * H * 8;
-      uint8_t* xdst = sb + (side ? pl.off_vx : pl.off_kx) + t * H * 8;
-      for (int h = lane; h < H; h += 32) cp8(xdst + 8 * h, xsrc + 8 * h);
+      if (side == 0)  // key metas [head][token] (see stage_flat)
+        for (int h = lane; h < H; h += 32) cp8(sb + pl.off_kx + 8 * (h * TT + t), xsrc + 8 * h);
+      else
+        for (int h = lane; h < H; h += 32) cp8(sb + pl.off_vx + 8 * (t * H + h), xsrc + 8 * h);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
@@ -301,7 +310,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
       const int t = lane & (TT - 1), dh = (lane / TT) * (D / 2);
       const float* mrow = km + t * RS;
       const uint8_t* crow = kc + t * pl.CRS + h * gb;
-      const float2 sm = kx[t * H + h];
+      const float2 sm = kx[h * TT + t];
       const float* qrow = qs + (dh ? 4 : 0);
       float2 z2[GT];
 #pragma unroll
