@@ -304,19 +304,26 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
     const float2* kx = reinterpret_cast<const float2*>(sbase + pl.off_kx);
     const float2* vx = reinterpret_cast<const float2*>(sbase + pl.off_vx);
 
-    // ---- phase 1: lane = (token, column half), warp = (KV head, q chunk); the halves meet by one shuffle
+    // ---- phase 1: lane = (token, column half), warp = (KV head, q chunk); the halves meet by one shuffle.
+    // 2/4-bit (ILV): lane = 2 token + half and the halves interleave 16-column blocks (half hf takes blocks
+    // hf, hf + 2, ...), so the code loads of one phase hit distinct banks (the contiguous halves, lane = token +
+    // 16 half, put rows t and t + 8 of a 16-byte-padded code row on the same bank: 2-way at 4-bit, 4-way at 2-bit).
+    constexpr bool ILV = BITS == 2 || BITS == 4;
+    constexpr int HX = ILV ? 1 : TT;  // lane distance between the two halves of a token
     for (int u = warp; u < H * nqc; u += NTHR / 32) {
       const int h = u / nqc, g0 = h * gs + (u - h * nqc) * GT;  // shared-memory row of the unit's first q head
-      const int t = lane & (TT - 1), dh = (lane / TT) * (D / 2);
+      const int t = ILV ? lane >> 1 : lane & (TT - 1), hf = ILV ? lane & 1 : lane / TT;
       const float* mrow = km + t * RS;
       const uint8_t* crow = kc + t * pl.CRS + h * gb;
       const float2 sm = kx[h * TT + t];
-      const float* qrow = qs + (dh ? 4 : 0);
       float2 z2[GT];
 #pragma unroll
       for (int g = 0; g < GT; ++g) z2[g] = make_float2(0.f, 0.f);
 #pragma unroll kEx2Unroll
-      for (int d = dh; d < dh + D / 2; d += 16) {
+      for (int i = 0; i < D / 32; ++i) {
+        const int d = ILV ? 16 * hf + 32 * i : hf * (D / 2) + 16 * i;
+        // q columns >= D/2 sit 4 floats further in their row (staging above)
+        const float* qrow = qs + (d >= D / 2 ? 4 : 0);
         uint4 w4 = make_uint4(0, 0, 0, 0);  // the 16 codes of columns d .. d + 15 (BITS < 16)
         if (BITS == 2) w4.x = *reinterpret_cast<const uint32_t*>(crow + d / 4);
         if (BITS == 4) *reinterpret_cast<uint2*>(&w4) = *reinterpret_cast<const uint2*>(crow + d / 2);
@@ -342,20 +349,20 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
         }
       }
       // online softmax of the unit's q heads over the tile, in the same warp (attention.py:139-147): the two
-      // column halves hold the same sums after the shuffle, so lanes t and t + TT agree; P goes to shared memory
+      // column halves hold the same sums after the shuffle, so both lanes of a token agree; P goes to shared memory
       // (the GT reductions interleaved: independent shuffle chains; 16-lane butterflies, the halves being equal)
       float zz[GT], mx[GT], pe[GT], ls[GT];
 #pragma unroll
       for (int g = 0; g < GT; ++g) {
         float z = z2[g].x + z2[g].y;
-        z += __shfl_xor_sync(0xffffffffu, z, TT);
+        z += __shfl_xor_sync(0xffffffffu, z, HX);
         zz[g] = t < nv ? __fmul_rn(z, a.scale) : NEG_INF;
         mx[g] = zz[g];
       }
 #pragma unroll
       for (int o = TT / 2; o > 0; o >>= 1)
 #pragma unroll
-        for (int g = 0; g < GT; ++g) mx[g] = fmaxf(mx[g], __shfl_xor_sync(0xffffffffu, mx[g], o));
+        for (int g = 0; g < GT; ++g) mx[g] = fmaxf(mx[g], __shfl_xor_sync(0xffffffffu, mx[g], ILV ? 2 * o : o));
 #pragma unroll
       for (int g = 0; g < GT; ++g) {
         mx[g] = fmaxf(ml[g0 + g].x, mx[g]);
@@ -365,10 +372,10 @@ __global__ void __launch_bounds__(NTHR, 2) attn_exact2_kernel(AttnArgs a, Plan p
 #pragma unroll
       for (int o = TT / 2; o > 0; o >>= 1)
 #pragma unroll
-        for (int g = 0; g < GT; ++g) ls[g] += __shfl_xor_sync(0xffffffffu, ls[g], o);
+        for (int g = 0; g < GT; ++g) ls[g] += __shfl_xor_sync(0xffffffffu, ls[g], ILV ? 2 * o : o);
 #pragma unroll
       for (int g = 0; g < GT; ++g) {
-        if (lane < TT) S[(g0 + g) * PS + lane] = pe[g];
+        if (hf == 0) S[(g0 + g) * PS + t] = pe[g];
         if (lane == 0) {
           const float2 m0 = ml[g0 + g];
           const float cf = expf(m0.x - mx[g]);
