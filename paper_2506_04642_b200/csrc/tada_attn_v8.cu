@@ -54,6 +54,9 @@ constexpr int kBudget = 113 * 1024;  // two CTAs per SM
 #ifndef TADA_V8_ACHAINS
 #define TADA_V8_ACHAINS 0
 #endif
+#ifndef TADA_V8_AC2_B2
+#define TADA_V8_AC2_B2 0  // two QK-mean accumulation chains at 2-bit too (measured: one chain +1% there)
+#endif
 #ifndef TADA_V8_QTM
 #define TADA_V8_QTM 2  // IMMA q fragments in TMEM: 0 where shared memory has no room, 1 at Hq=64, 2 always
 #endif
@@ -531,7 +534,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
       tmem_wait_ld();
     }
     // MT (or 2 MT) independent accumulation chains, interleaved so no MMA waits on the previous one
-    constexpr bool AC2 = TADA_V8_ACHAINS == 2 || (TADA_V8_ACHAINS == 0 && MT <= 2);
+    constexpr bool AC2 = TADA_V8_ACHAINS == 2 || (TADA_V8_ACHAINS == 0 && MT <= 2 && (BITS != 2 || TADA_V8_AC2_B2));
     [[maybe_unused]] float acc2[AC2 ? MT : 1][4];
     if constexpr (AC2)
 #pragma unroll
