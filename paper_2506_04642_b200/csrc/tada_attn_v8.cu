@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(NTHR, 2) attn_v8_kernel(AttnArgs a, const __gr
         wb[4 % NWD] = p3.x; wb[5 % NWD] = p3.y; wb[6 % NWD] = p3.z; wb[7 % NWD] = p3.w;
       }
       // rows r: hi . code, rows r + 8: lo . code; q_fx . code / sq = 256 hi + lo (exact, |.| < 2^31)
-      constexpr int NIC = TADA_V8_ICHAINS ? TADA_V8_ICHAINS : (BITS == 2 && MT <= 2 ? 2 : 1);
+      constexpr int NIC = TADA_V8_ICHAINS ? TADA_V8_ICHAINS : 1;  // 2 chains measured -3% at 2-bit Hq=32 (one QK-mean chain)
       int acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
       float qf[QTM ? 16 : 1];
       if constexpr (QTM) {
